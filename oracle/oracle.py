@@ -67,12 +67,29 @@ class OracleError(RuntimeError):
     pass
 
 
+class OracleInputError(OracleError):
+    """commdet::input_error"""
+
+
+class OracleInvalidArgument(OracleError, ValueError):
+    """std::invalid_argument"""
+
+
+class OracleDomainError(OracleError, ValueError):
+    """std::domain_error"""
+
+
+class OracleOutOfRange(OracleError, IndexError):
+    """std::out_of_range"""
+
+
 _CODES = {-1: "input_error", -2: "invalid_argument", -3: "domain_error", -4: "out_of_range", -5: "ENOMEM"}
+_EXC = {-1: OracleInputError, -2: OracleInvalidArgument, -3: OracleDomainError, -4: OracleOutOfRange}
 
 
 def _check(rc):
     if rc < 0:
-        raise OracleError(_CODES.get(rc, f"error {rc}"))
+        raise _EXC.get(rc, OracleError)(_CODES.get(rc, f"error {rc}"))
     return rc
 
 
@@ -176,7 +193,7 @@ def ref():
 def _rcheck(rc):
     if rc != 0:
         msg = ref().ref_last_error().decode(errors="replace")
-        raise OracleError(f"{_CODES.get(rc, 'error')}: {msg}")
+        raise _EXC.get(rc, OracleError)(f"{_CODES.get(rc, 'error')}: {msg}")
 
 
 # --------------------------------------------------------------------------- #
@@ -384,7 +401,10 @@ def djb2(data: bytes) -> int:
 
 
 def combine_hashed(solutions):
+    """H/ensemble.hpp:86-107 incl. check_ensemble_lengths (:33-39)."""
     sols = [_i32(s) for s in solutions]
+    if not sols or any(len(s) != len(sols[0]) for s in sols):
+        raise OracleInvalidArgument("empty ensemble or partitions of different lengths")
     n = len(sols[0])
     ptrs = (C.c_void_p * len(sols))(*[s.ctypes.data for s in sols])
     out = np.zeros(n, np.int32)

@@ -1,0 +1,311 @@
+// common.cuh -- context, device buffers, launch accounting and device
+// utilities shared by every kernel file of libcommdet_cuda.so (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "commdet_cuda.h"
+
+namespace cdk {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+struct Error : std::runtime_error {
+    cd_status code;
+    Error(cd_status c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(cd_status c, const std::string &m) { throw Error(c, m); }
+
+#define CD_CUDA(x)                                                                                   \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            ::cdk::fail(e_ == cudaErrorMemoryAllocation ? CD_ENOMEM : CD_ECUDA,                      \
+                        std::string(#x) + ": " + cudaGetErrorString(e_));                            \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// context
+// ---------------------------------------------------------------------------
+struct KStat {
+    int64_t launches = 0;
+    double total_ms = 0.0;
+    double bytes = 0.0;
+    double items = 0.0;
+};
+
+struct PendingEvent {
+    std::string name;
+    cudaEvent_t a, b;
+};
+
+}  // namespace cdk
+
+struct cd_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaMemPool_t pool = nullptr;
+    int num_sms = 148;
+    size_t smem_optin = 0;
+    bool profiling = false;
+    int64_t launches = 0;
+    std::map<std::string, cdk::KStat> stats;
+    std::vector<cdk::PendingEvent> pending;
+    std::vector<cudaEvent_t> free_events;
+    // small pinned staging area for scalar read-backs
+    int64_t *pinned = nullptr;
+    // device counters: [0..31] general purpose (see cdk::Ctr)
+    int64_t *dctr = nullptr;
+};
+
+namespace cdk {
+
+enum Ctr : int {
+    CTR_LIST0 = 0,   // 0..7  per-bin worklist counts (int32 packed in int64 slots)
+    CTR_MOVES = 8,   // moves in the current bucket
+    CTR_TOTAL = 9,   // moves accumulated (iteration / pass)
+    CTR_FLAG = 10,   // error flag
+    CTR_AUX = 11,    // scratch
+    CTR_NODES = 12,  // nodes evaluated (stats)
+    CTR_ENTRIES = 13,  // entries scanned (stats)
+    CTR_COUNT = 32
+};
+
+// ---------------------------------------------------------------------------
+// device buffers (stream-ordered pool allocations on the context stream)
+// ---------------------------------------------------------------------------
+template <class T>
+struct DBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    cudaStream_t s = nullptr;
+
+    DBuf() = default;
+    DBuf(cd_ctx *ctx, size_t count) { alloc(ctx, count); }
+    DBuf(const DBuf &) = delete;
+    DBuf &operator=(const DBuf &) = delete;
+    DBuf(DBuf &&o) noexcept : p(o.p), n(o.n), s(o.s) { o.p = nullptr; o.n = 0; }
+    DBuf &operator=(DBuf &&o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p; n = o.n; s = o.s;
+            o.p = nullptr; o.n = 0;
+        }
+        return *this;
+    }
+    ~DBuf() { release(); }
+
+    void alloc(cd_ctx *ctx, size_t count) {
+        release();
+        s = ctx->stream;
+        n = count;
+        if (count) {
+            cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), count * sizeof(T), s);
+            if (e != cudaSuccess) {
+                p = nullptr;
+                n = 0;
+                cudaGetLastError();
+                fail(CD_ENOMEM, "device allocation of " + std::to_string(count * sizeof(T)) + " bytes failed");
+            }
+        }
+    }
+    void release() {
+        if (p)
+            cudaFreeAsync(p, s);
+        p = nullptr;
+        n = 0;
+    }
+    void zero() {
+        if (p)
+            CD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+    }
+    void fill_bytes(int v) {
+        if (p)
+            CD_CUDA(cudaMemsetAsync(p, v, n * sizeof(T), s));
+    }
+    T *get() const { return p; }
+    size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------------------
+// launch accounting
+// ---------------------------------------------------------------------------
+cudaEvent_t ctx_event(cd_ctx *ctx);
+void ctx_flush_stats(cd_ctx *ctx);  // resolves pending events (after sync)
+void ctx_sync(cd_ctx *ctx);
+int64_t read_counter(cd_ctx *ctx, int idx);  // syncs
+void read_counters(cd_ctx *ctx, int first, int count, int64_t *out);  // syncs
+
+struct LaunchScope {
+    cd_ctx *ctx;
+    const char *name;
+    cudaEvent_t a = nullptr;
+    LaunchScope(cd_ctx *c, const char *nm) : ctx(c), name(nm) {
+        ctx->launches++;
+        if (ctx->profiling) {
+            a = ctx_event(ctx);
+            cudaEventRecord(a, ctx->stream);
+        }
+    }
+    ~LaunchScope() {
+        if (ctx->profiling) {
+            cudaEvent_t b = ctx_event(ctx);
+            cudaEventRecord(b, ctx->stream);
+            ctx->pending.push_back({name, a, b});
+        }
+    }
+};
+
+inline void check_launch(const char *name) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess)
+        fail(CD_ECUDA, std::string("launch of ") + name + ": " + cudaGetErrorString(e));
+}
+
+// LAUNCH(ctx, "family", kernel, grid, block, smem)(args...)
+#define CD_LAUNCH(ctx, family, kernel, grid, block, smem, ...)                                       \
+    do {                                                                                             \
+        ::cdk::LaunchScope ls_((ctx), (family));                                                     \
+        kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                            \
+        ::cdk::check_launch(family);                                                                 \
+    } while (0)
+
+inline void add_stat_work(cd_ctx *ctx, const char *family, double bytes, double items) {
+    auto &s = ctx->stats[family];
+    s.bytes += bytes;
+    s.items += items;
+}
+
+inline int grid_for(int64_t items, int per_block, int cap_blocks) {
+    int64_t g = (items + per_block - 1) / per_block;
+    if (g < 1)
+        g = 1;
+    if (g > cap_blocks)
+        g = cap_blocks;
+    return static_cast<int>(g);
+}
+
+// ---------------------------------------------------------------------------
+// host <-> device argument handling: every ABI array may be host or device
+// ---------------------------------------------------------------------------
+bool is_device_ptr(const void *p);
+
+template <class T>
+struct InArr {
+    const T *d = nullptr;
+    DBuf<T> own;
+    InArr(cd_ctx *ctx, const T *p, size_t count) {
+        if (!p || count == 0) {
+            d = p;
+            return;
+        }
+        if (is_device_ptr(p)) {
+            d = p;
+        } else {
+            own.alloc(ctx, count);
+            CD_CUDA(cudaMemcpyAsync(own.p, p, count * sizeof(T), cudaMemcpyHostToDevice, ctx->stream));
+            d = own.p;
+        }
+    }
+};
+
+template <class T>
+struct OutArr {
+    T *host = nullptr;
+    T *d = nullptr;
+    DBuf<T> own;
+    size_t count = 0;
+    cd_ctx *ctx;
+    OutArr(cd_ctx *c, T *p, size_t cnt) : ctx(c), count(cnt) {
+        if (!p || cnt == 0) {
+            d = p;
+            return;
+        }
+        if (is_device_ptr(p)) {
+            d = p;
+        } else {
+            host = p;
+            own.alloc(ctx, cnt);
+            d = own.p;
+        }
+    }
+    void finish() {
+        if (host && count)
+            CD_CUDA(cudaMemcpyAsync(host, d, count * sizeof(T), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// device utilities
+// ---------------------------------------------------------------------------
+constexpr int32_t EMPTY_KEY = -1;
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+}
+
+// Bucket schedule shared by every driver (ported in oracle/commdet_oracle.c:
+// cdo_bucket_key / cdo_bucket_of).
+__host__ __device__ __forceinline__ uint64_t bucket_key(uint64_t seed, uint64_t salt) {
+    return splitmix64(seed ^ splitmix64(salt ^ 0xb5ad4eceda1ce2a9ULL));
+}
+__host__ __device__ __forceinline__ int32_t bucket_of(uint64_t key, int32_t u, int32_t buckets) {
+    return static_cast<int32_t>(static_cast<uint32_t>(splitmix64(key ^ static_cast<uint64_t>(static_cast<uint32_t>(u))) >> 32) %
+                                static_cast<uint32_t>(buckets));
+}
+
+__device__ __forceinline__ uint32_t hash_slot(int32_t key, uint32_t mask) {
+    return (static_cast<uint32_t>(key) * 0x9E3779B1u) & mask;
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// warp-aggregated append: returns the slot for this lane (only lanes with
+// pred == true get a valid slot).
+__device__ __forceinline__ int32_t warp_append(int32_t *counter, bool pred) {
+    const uint32_t mask = __ballot_sync(0xffffffffu, pred);
+    if (!mask)
+        return -1;
+    const int leader = __ffs(mask) - 1;
+    int32_t base = 0;
+    if (lane_id() == leader)
+        base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return base + __popc(mask & lanemask_lt());
+}
+
+inline uint64_t next_pow2(uint64_t x) {
+    uint64_t p = 1;
+    while (p < x)
+        p <<= 1;
+    return p;
+}
+
+}  // namespace cdk

@@ -1,0 +1,304 @@
+// detect.cu -- device drivers: PLP (H/plp.hpp:67-149), move phase
+// (H/louvain.hpp:65-141), PLM / PLMR recursion (H/louvain.hpp:237-301) and
+// EPP (H/ensemble.hpp:111-199).
+//
+// Update order: every PLP iteration / PLM pass is
+// split into `buckets` sub-sweeps by bucket_of(bucket_key(seed, salt), u);
+// each sub-sweep evaluates its nodes against frozen labels and its moves are
+// applied before the next sub-sweep.  This is the deterministic stand-in for
+// the reference's racy in-place OpenMP updates (H/plp.hpp:127-130,
+// H/louvain.hpp:120-126); a pure Jacobi sweep oscillates (SURVEY.md finding 2).
+// oracle/commdet_oracle.c (cdo_*_bucketed) ports this order exactly.
+#include <chrono>
+
+#include "detect.cuh"
+
+namespace cdk {
+
+DevTimer::DevTimer(cd_ctx *c) : ctx(c) {
+    CD_CUDA(cudaEventCreate(&a));
+    CD_CUDA(cudaEventCreate(&b));
+}
+DevTimer::~DevTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+}
+void DevTimer::start() { CD_CUDA(cudaEventRecord(a, ctx->stream)); }
+double DevTimer::stop_ms() {
+    CD_CUDA(cudaEventRecord(b, ctx->stream));
+    CD_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    CD_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+__global__ void k_count_diff(int64_t n, const int32_t *a, const int32_t *b, unsigned long long *cnt) {
+    unsigned long long c = 0;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        c += a[i] != b[i];
+    c = warp_sum(c);
+    if (lane_id() == 0 && c)
+        atomicAdd(cnt, c);
+}
+
+// ---------------------------------------------------------------------------
+// PLP
+// ---------------------------------------------------------------------------
+void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32_t *initial, int32_t *labels,
+                 Report rep) {
+    const int64_t n = g->n;
+    const int64_t theta = cfg.theta >= 0 ? cfg.theta : std::max<int64_t>(1, n / 100000);  // H/plp.hpp:24-28
+    const int K = cfg.buckets > 0 ? cfg.buckets : 4;
+    if (initial)
+        CD_CUDA(cudaMemcpyAsync(labels, initial, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+        iota_dev(ctx, labels, n);
+    DBuf<uint8_t> active(ctx, std::max<int64_t>(n, 1));
+    active.fill_bytes(1);
+    SweepState st;
+    sweep_init(ctx, g, st);
+    DevTimer it(ctx);
+    int64_t updated = n, iter = 0;
+    while (updated > theta && iter < cfg.max_iterations) {  // H/plp.hpp:98
+        it.start();
+        sweep_reset_total(st);
+        const uint64_t key = bucket_key(cfg.seed, static_cast<uint64_t>(iter));
+        for (int b = 0; b < K; ++b) {
+            SweepCall c;
+            c.mode = MODE_PLP;
+            c.z = labels;
+            c.active = active.p;
+            c.key = key;
+            c.bucket = b;
+            c.buckets = K;
+            sweep_bucket(st, c);
+        }
+        updated = sweep_read_total(st);
+        rep.iteration(updated, it.stop_ms());
+        ++iter;
+    }
+}
+
+int64_t plp_sweep_sync_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z_in, int32_t *z_out) {
+    const int64_t n = g->n;
+    if (n == 0)
+        return 0;
+    CD_CUDA(cudaMemcpyAsync(z_out, z_in, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
+    SweepState st;
+    sweep_init(ctx, g, st);
+    SweepCall c;
+    c.mode = MODE_PLP;
+    c.z = const_cast<int32_t *>(z_in);
+    c.buckets = 1;
+    c.dense_best = z_out;
+    sweep_bucket(st, c);
+    DBuf<unsigned long long> cnt(ctx, 1);
+    cnt.zero();
+    CD_LAUNCH(ctx, "count_diff", k_count_diff, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z_in,
+              static_cast<const int32_t *>(z_out), cnt.p);
+    unsigned long long h = 0;
+    CD_CUDA(cudaMemcpyAsync(&h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return static_cast<int64_t>(h);
+}
+
+// ---------------------------------------------------------------------------
+// Louvain
+// ---------------------------------------------------------------------------
+__global__ void k_fill_gain0(int64_t n, const int32_t *z, int32_t *best, double *gain) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        best[i] = z[i];
+        if (gain)
+            gain[i] = 0.0;
+    }
+}
+
+void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vols, double gamma, int32_t *best,
+                   double *gain) {
+    const int64_t n = g->n;
+    if (n == 0)
+        return;
+    CD_LAUNCH(ctx, "move_eval", k_fill_gain0, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z, best, gain);
+    if (g->total == 0.0)
+        return;
+    SweepState st;
+    sweep_init(ctx, g, st);
+    SweepCall c;
+    c.mode = MODE_PLM;
+    c.z = const_cast<int32_t *>(z);
+    c.vols = const_cast<double *>(vols);
+    c.gamma = gamma;
+    c.buckets = 1;
+    c.dense_best = best;
+    c.dense_gain = gain;
+    sweep_bucket(st, c);
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt) {
+    const int64_t n = g->n;
+    if (n == 0 || g->total == 0.0)  // H/louvain.hpp:67-68
+        return false;
+    const int K = cfg.buckets > 0 ? cfg.buckets : 4;
+    const int64_t theta = cfg.move_theta >= 0 ? cfg.move_theta : n / 100000;
+    DBuf<double> vols(ctx, n);
+    DBuf<int32_t> csize(ctx, n);
+    community_volumes_sizes_dev(ctx, g, z, vols.p, csize.p, n);  // H/louvain.hpp:75
+    SweepState st;
+    sweep_init(ctx, g, st);
+    bool changed = false;
+    for (int64_t pass = 0; pass < cfg.max_move_iterations; ++pass) {
+        sweep_reset_total(st);
+        const uint64_t key = bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass));
+        for (int b = 0; b < K; ++b) {
+            SweepCall c;
+            c.mode = MODE_PLM;
+            c.z = z;
+            c.vols = vols.p;
+            c.csize = csize.p;
+            c.gamma = cfg.gamma;
+            c.guard = cfg.singleton_guard;
+            c.key = key;
+            c.bucket = b;
+            c.buckets = K;
+            sweep_bucket(st, c);
+        }
+        const int64_t moved = sweep_read_total(st);
+        if (moved == 0)  // H/louvain.hpp:136-137
+            break;
+        changed = true;
+        if (moved <= theta)
+            break;
+    }
+    return changed;
+}
+
+// H/louvain.hpp:237-267
+static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg, int64_t level, int32_t *z,
+                            Report rep) {
+    const int64_t n = g->n;
+    iota_dev(ctx, z, n);  // singleton_partition (:242)
+    DevTimer t(ctx);
+    t.start();
+    const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0));
+    const double mv = t.stop_ms();
+    if (auto *L = rep.level(level)) {
+        L->move_ms += mv;
+        L->nodes = n;
+        L->entries = g->D;
+    }
+    if (changed && level + 1 < cfg.max_levels) {  // :247
+        DBuf<int32_t> zc(ctx, std::max<int64_t>(n, 1));
+        const int64_t k = compact_dev(ctx, n, z, n, zc.p);  // :248
+        if (k < n) {                                        // :249
+            t.start();
+            cd_graph *coarse = coarsen_dev(ctx, g, zc.p, k);  // :251
+            const double cm = t.stop_ms();
+            if (auto *L = rep.level(level))
+                L->coarsen_ms += cm;
+            try {
+                DBuf<int32_t> zcoarse(ctx, std::max<int64_t>(k, 1));
+                louvain_recurse(ctx, coarse, cfg, level + 1, zcoarse.p, rep);  // :255
+                prolong_dev(ctx, k, zcoarse.p, n, zc.p, z);                     // :256
+            } catch (...) {
+                delete coarse;
+                throw;
+            }
+            delete coarse;
+            if (cfg.refine) {  // PLMR :258-263
+                t.start();
+                move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 1));
+                const double rm = t.stop_ms();
+                if (auto *L = rep.level(level))
+                    L->refine_ms += rm;
+            }
+        }
+    }
+}
+
+int64_t louvain_run_dev(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg, int32_t *z, Report rep) {
+    if (g->total == 0.0)
+        fail(CD_EDOMAIN, "Louvain requires positive total edge weight");  // H/louvain.hpp:271-272
+    DBuf<int32_t> tmp(ctx, std::max<int64_t>(g->n, 1));
+    louvain_recurse(ctx, g, cfg, 0, tmp.p, rep);
+    return compact_dev(ctx, g->n, tmp.p, std::max<int64_t>(g->n, 1), z);  // :278
+}
+
+// ---------------------------------------------------------------------------
+// EPP
+// ---------------------------------------------------------------------------
+int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep) {
+    if (cfg.ensemble_size < 1)
+        fail(CD_EINVAL, "ensemble size must be >= 1");  // H/ensemble.hpp:113-114
+    if (g->total == 0.0)
+        fail(CD_EDOMAIN, "EPP requires positive total edge weight");  // :115-116
+    const int64_t n = g->n, b = cfg.ensemble_size;
+    DevTimer t(ctx);
+    // bases (:152-161): seed + i
+    t.start();
+    DBuf<int32_t> bases(ctx, std::max<int64_t>(n * b, 1));
+    for (int64_t i = 0; i < b; ++i) {
+        int32_t *zi = bases.p + i * n;
+        if (cfg.base == CD_ALGO_PLP) {
+            cd_plp_config pc = cfg.base_plp;
+            pc.seed = cfg.seed + static_cast<uint64_t>(i);
+            plp_run_dev(ctx, g, pc, nullptr, zi, Report{nullptr});
+        } else {
+            cd_louvain_config lc = cfg.final_louvain;
+            lc.seed = cfg.seed + static_cast<uint64_t>(i);
+            lc.refine = cfg.base == CD_ALGO_PLMR;
+            louvain_run_dev(ctx, g, lc, zi, Report{nullptr});
+        }
+    }
+    const double base_ms = t.stop_ms();
+    // combine (:163-165)
+    t.start();
+    std::vector<const int32_t *> hp(b);
+    for (int64_t i = 0; i < b; ++i)
+        hp[i] = bases.p + i * n;
+    DBuf<const int32_t *> dp(ctx, b);
+    CD_CUDA(cudaMemcpyAsync(dp.p, hp.data(), b * sizeof(int32_t *), cudaMemcpyHostToDevice, ctx->stream));
+    DBuf<int32_t> core(ctx, std::max<int64_t>(n, 1));
+    const int64_t k = combine_hashed_dev(ctx, b, n, dp.p, core.p);
+    const double combine_ms = t.stop_ms();
+    // coarsen (:167-169)
+    t.start();
+    cd_graph *coarse = coarsen_dev(ctx, g, core.p, k);
+    const double coarsen_ms = t.stop_ms();
+    double final_ms = 0.0;
+    try {
+        // final solver (:171-191), seed = cfg.seed
+        t.start();
+        DBuf<int32_t> zc(ctx, std::max<int64_t>(k, 1));
+        if (cfg.final_algo == CD_ALGO_PLP) {
+            cd_plp_config pc = cfg.base_plp;
+            pc.seed = cfg.seed;
+            plp_run_dev(ctx, coarse, pc, nullptr, zc.p, Report{nullptr});
+        } else {
+            cd_louvain_config fc = cfg.final_louvain;
+            fc.seed = cfg.seed;
+            fc.refine = cfg.final_algo == CD_ALGO_PLMR;
+            louvain_run_dev(ctx, coarse, fc, zc.p, Report{nullptr});
+        }
+        final_ms = t.stop_ms();
+        // prolong + compact (:193)
+        DBuf<int32_t> fine(ctx, std::max<int64_t>(n, 1));
+        prolong_dev(ctx, k, zc.p, n, core.p, fine.p);
+        const int64_t kk = compact_dev(ctx, n, fine.p, std::max<int64_t>(k, 1), z);
+        delete coarse;
+        if (rep.r) {
+            rep.r->base_ms = base_ms;
+            rep.r->combine_ms = combine_ms;
+            rep.r->coarsen_ms = coarsen_ms;
+            rep.r->final_ms = final_ms;
+        }
+        return kk;
+    } catch (...) {
+        delete coarse;
+        throw;
+    }
+}
+
+}  // namespace cdk

@@ -1,0 +1,334 @@
+// graph.cu -- device CSR construction (Graph::from_edges, H/graph.hpp:48-81),
+// finalize (H/graph.hpp:229-255), validation and the degree-tier work
+// decomposition used by the sweep / move kernels.
+#include "rows.cuh"
+
+namespace cdk {
+
+// ---------------------------------------------------------------------------
+// finalize: vol(u) = sum w + loop (loop twice), loop(u), m, w(E), max degree
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off, const int32_t *col,
+                                                  const float *w, double *vol, double *loop, int64_t *acc_i,
+                                                  double *acc_d) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    int64_t m_loc = 0, maxdeg = 0, iso = 0;
+    double tot_loc = 0.0;
+    for (int64_t u = gw; u < n; u += nw) {
+        const int64_t s = off[u], e = off[u + 1];
+        double vs = 0.0, lp = 0.0, up = 0.0;
+        int64_t cnt = 0;
+        for (int64_t i = s + lane; i < e; i += 32) {
+            const int32_t v = col[i];
+            const double wt = w ? static_cast<double>(w[i]) : 1.0;
+            vs += wt;
+            if (v == u) {
+                lp += wt;
+                up += wt;
+                ++cnt;
+            } else if (v > u) {
+                up += wt;
+                ++cnt;
+            }
+        }
+        vs = warp_sum(vs);
+        lp = warp_sum(lp);
+        up = warp_sum(up);
+        cnt = warp_sum(cnt);
+        if (lane == 0) {
+            vol[u] = vs + lp;
+            loop[u] = lp;
+        }
+        m_loc += cnt;
+        tot_loc += up;
+        maxdeg = max(maxdeg, e - s);
+        iso += (e == s);
+    }
+    if (lane == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[0]), static_cast<unsigned long long>(m_loc));
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[1]), static_cast<unsigned long long>(maxdeg));
+        atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[2]), static_cast<unsigned long long>(iso));
+        atomicAdd(acc_d, tot_loc);
+    }
+}
+
+void graph_finalize(cd_ctx *ctx, cd_graph *g) {
+    g->vol.alloc(ctx, std::max<int64_t>(g->n, 1));
+    g->loop.alloc(ctx, std::max<int64_t>(g->n, 1));
+    DBuf<int64_t> acc_i(ctx, 3);
+    DBuf<double> acc_d(ctx, 1);
+    acc_i.zero();
+    acc_d.zero();
+    if (g->n > 0)
+        CD_LAUNCH(ctx, "finalize", k_finalize, grid_for(g->n, 8, ctx->num_sms * 16), 256, 0, g->n,
+                  static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                  static_cast<const float *>(g->weighted ? g->w.p : nullptr), g->vol.p, g->loop.p, acc_i.p, acc_d.p);
+    int64_t hi[3];
+    double hd;
+    CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&hd, acc_d.p, sizeof(hd), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    g->m = hi[0];
+    g->max_degree = hi[1];
+    g->isolated = hi[2];
+    g->total = hd;
+    g->binned = false;
+}
+
+// ---------------------------------------------------------------------------
+// builder from canonical or arbitrary pairs (device arrays)
+// ---------------------------------------------------------------------------
+__global__ void k_pair_degree(int64_t m, const int32_t *u, const int32_t *v, int32_t *deg) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t a = u[i], b = v[i];
+        atomicAdd(&deg[a], 1);
+        if (a != b)
+            atomicAdd(&deg[b], 1);
+    }
+}
+
+__global__ void k_pair_scatter(int64_t m, const int32_t *u, const int32_t *v, const float *w, int64_t *cursor,
+                               int32_t *rk, float *rw) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t a = u[i], b = v[i];
+        const float wt = w ? w[i] : 1.0f;
+        int64_t p = static_cast<int64_t>(atomicAdd(reinterpret_cast<unsigned long long *>(&cursor[a]), 1ULL));
+        rk[p] = b;
+        if (rw)
+            rw[p] = wt;
+        if (a != b) {
+            p = static_cast<int64_t>(atomicAdd(reinterpret_cast<unsigned long long *>(&cursor[b]), 1ULL));
+            rk[p] = a;
+            if (rw)
+                rw[p] = wt;
+        }
+    }
+}
+
+struct DegGen {
+    const int32_t *deg;
+    __device__ int64_t operator()(int64_t i) const { return deg[i]; }
+};
+
+cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, const int32_t *v, const float *w,
+                           DupMode mode) {
+    DBuf<int32_t> deg(ctx, std::max<int64_t>(n, 1));
+    deg.zero();
+    const int blocks = ctx->num_sms * 8;
+    if (m > 0)
+        CD_LAUNCH(ctx, "build", k_pair_degree, grid_for(m, 256, blocks), 256, 0, m, u, v, deg.p);
+    DBuf<int64_t> fpre(ctx, n + 1);
+    exclusive_scan<int64_t>(ctx, n, DegGen{deg.p}, fpre.p, fpre.p + n);
+    int64_t F = 0;
+    CD_CUDA(cudaMemcpyAsync(&F, fpre.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    deg.release();
+    DBuf<int32_t> rk(ctx, std::max<int64_t>(F, 1));
+    DBuf<float> rw;
+    const bool weighted = (w != nullptr) && mode != DUP_ONE;
+    if (weighted)
+        rw.alloc(ctx, std::max<int64_t>(F, 1));
+    {
+        DBuf<int64_t> cursor(ctx, n + 1);
+        CD_CUDA(cudaMemcpyAsync(cursor.p, fpre.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
+        if (m > 0)
+            CD_LAUNCH(ctx, "build", k_pair_scatter, grid_for(m, 256, blocks), 256, 0, m, u, v,
+                      weighted ? w : static_cast<const float *>(nullptr), cursor.p, rk.p, weighted ? rw.p : nullptr);
+    }
+    auto *g = new cd_graph();
+    g->ctx = ctx;
+    g->n = n;
+    g->weighted = weighted;
+    bool dup = false;
+    try {
+        SrcFlat src{fpre.p, rk.p, weighted ? rw.p : nullptr};
+        g->D = run_row_engine(ctx, src, n, fpre.p, F, std::max<int64_t>(n, 1), mode, weighted, g->off, g->col, g->w,
+                              &dup, "build");
+        if (dup && mode == DUP_ERROR)
+            fail(CD_EINPUT, "duplicate edge");
+        graph_finalize(ctx, g);
+    } catch (...) {
+        delete g;
+        throw;
+    }
+    return g;
+}
+
+// ---------------------------------------------------------------------------
+// validation of an input CSR (ranges, strictly ascending rows, weights > 0)
+// ---------------------------------------------------------------------------
+__global__ void k_validate_csr(int64_t n, int64_t D, const int64_t *off, const int32_t *col, const float *w,
+                               int64_t *flag) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t u = gw; u < n; u += nw) {
+        const int64_t s = off[u], e = off[u + 1];
+        bool bad = (s > e) || (s < 0) || (e > D);
+        if (u == 0 && s != 0)
+            bad = true;
+        if (u == n - 1 && e != D)
+            bad = true;
+        if (!bad) {
+            for (int64_t i = s + lane; i < e; i += 32) {
+                const int32_t c = col[i];
+                if (c < 0 || c >= n)
+                    bad = true;
+                if (i > s && col[i - 1] >= c)
+                    bad = true;
+                if (w && !(w[i] > 0.0f))
+                    bad = true;
+            }
+        }
+        if (__any_sync(0xffffffffu, bad) && lane == 0)
+            flag[0] = 1;
+    }
+}
+
+void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D) {
+    if (n == 0)
+        return;
+    DBuf<int64_t> flag(ctx, 1);
+    flag.zero();
+    CD_LAUNCH(ctx, "validate", k_validate_csr, grid_for(n, 8, ctx->num_sms * 16), 256, 0, n, D, off, col, w, flag.p);
+    int64_t h = 0;
+    CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h)
+        fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
+}
+
+// ---------------------------------------------------------------------------
+// degree tiers and hub tables
+// ---------------------------------------------------------------------------
+__global__ void k_tiers(int64_t n, const int64_t *off, uint8_t *tier, unsigned long long *counts) {
+    __shared__ unsigned int sc[NUM_TIERS];
+    if (threadIdx.x < NUM_TIERS)
+        sc[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int t = tier_of_degree(off[u + 1] - off[u]);
+        tier[u] = static_cast<uint8_t>(t);
+        if (t != TIER_NONE)
+            atomicAdd(&sc[t], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < NUM_TIERS && sc[threadIdx.x])
+        atomicAdd(&counts[threadIdx.x], static_cast<unsigned long long>(sc[threadIdx.x]));
+}
+
+__global__ void k_collect_hubs(int64_t n, const uint8_t *tier, int32_t *hubs, int32_t *count) {
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
+         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t u = base + threadIdx.x;
+        const bool is = u < n && tier[u] == TIER_HUB;
+        const int32_t pos = warp_append(count, is);
+        if (is)
+            hubs[pos] = static_cast<int32_t>(u);
+    }
+}
+
+struct HubCapGen {
+    const int32_t *hubs;
+    const int64_t *off;
+    __device__ int64_t operator()(int64_t h) const {
+        const int64_t d = off[hubs[h] + 1] - off[hubs[h]];
+        int64_t c = 64;
+        while (c < 2 * d)
+            c <<= 1;
+        return c;
+    }
+};
+struct HubChunkGen {
+    const int32_t *hubs;
+    const int64_t *off;
+    __device__ int64_t operator()(int64_t h) const {
+        const int64_t d = off[hubs[h] + 1] - off[hubs[h]];
+        return (d + HUB_CHUNK - 1) / HUB_CHUNK;
+    }
+};
+
+__global__ void k_hub_chunks(int64_t nh, const int32_t *hubs, const int64_t *off, const int64_t *tab,
+                             const int64_t *chunk_pre, int32_t *mask, int32_t *chunk_hub, int32_t *chunk_part) {
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int64_t d = off[hubs[h] + 1] - off[hubs[h]];
+        int64_t c = 64;
+        while (c < 2 * d)
+            c <<= 1;
+        if (threadIdx.x == 0)
+            mask[h] = static_cast<int32_t>(c - 1);
+        const int64_t nch = (d + HUB_CHUNK - 1) / HUB_CHUNK;
+        for (int64_t k = threadIdx.x; k < nch; k += blockDim.x) {
+            chunk_hub[chunk_pre[h] + k] = static_cast<int32_t>(h);
+            chunk_part[chunk_pre[h] + k] = static_cast<int32_t>(k);
+        }
+    }
+    (void)tab;
+}
+
+void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
+    if (g->binned)
+        return;
+    const int64_t n = g->n;
+    g->tier.alloc(ctx, std::max<int64_t>(n, 1));
+    DBuf<unsigned long long> counts(ctx, NUM_TIERS);
+    counts.zero();
+    if (n > 0)
+        CD_LAUNCH(ctx, "bins", k_tiers, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
+                  static_cast<const int64_t *>(g->off.p), g->tier.p, counts.p);
+    unsigned long long hc[NUM_TIERS];
+    CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t s = 0;
+    for (int t = 0; t < NUM_TIERS; ++t)
+        g->tier_nodes[t] = static_cast<int64_t>(hc[t]);
+    for (int t = 0; t < NUM_LIST_TIERS; ++t) {
+        g->tier_start[t] = s;
+        s += g->tier_nodes[t];
+    }
+    g->tier_start[NUM_LIST_TIERS] = s;
+    g->lists.alloc(ctx, std::max<int64_t>(s, 1));
+    // hubs
+    g->n_hubs = g->tier_nodes[TIER_HUB];
+    g->n_hub_chunks = 0;
+    g->hub_slots = 0;
+    if (g->n_hubs > 0) {
+        const int64_t nh = g->n_hubs;
+        g->hubs.alloc(ctx, nh);
+        DBuf<int32_t> cnt(ctx, 1);
+        cnt.zero();
+        CD_LAUNCH(ctx, "bins", k_collect_hubs, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
+                  static_cast<const uint8_t *>(g->tier.p), g->hubs.p, cnt.p);
+        g->hub_tab.alloc(ctx, nh + 1);
+        DBuf<int64_t> chunk_pre(ctx, nh + 1);
+        exclusive_scan<int64_t>(ctx, nh, HubCapGen{g->hubs.p, g->off.p}, g->hub_tab.p, g->hub_tab.p + nh);
+        exclusive_scan<int64_t>(ctx, nh, HubChunkGen{g->hubs.p, g->off.p}, chunk_pre.p, chunk_pre.p + nh);
+        int64_t tot[2];
+        CD_CUDA(cudaMemcpyAsync(&tot[0], g->hub_tab.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaMemcpyAsync(&tot[1], chunk_pre.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        g->hub_slots = tot[0];
+        g->n_hub_chunks = tot[1];
+        g->hub_mask.alloc(ctx, nh);
+        g->chunk_hub.alloc(ctx, g->n_hub_chunks);
+        g->chunk_part.alloc(ctx, g->n_hub_chunks);
+        CD_LAUNCH(ctx, "bins", k_hub_chunks, grid_for(nh, 1, ctx->num_sms * 4), 128, 0, nh,
+                  static_cast<const int32_t *>(g->hubs.p), static_cast<const int64_t *>(g->off.p),
+                  static_cast<const int64_t *>(g->hub_tab.p), static_cast<const int64_t *>(chunk_pre.p),
+                  g->hub_mask.p, g->chunk_hub.p, g->chunk_part.p);
+        g->hub_keys.alloc(ctx, g->hub_slots);
+        g->hub_vals.alloc(ctx, g->hub_slots);
+        g->hub_aux.alloc(ctx, nh);
+        g->hub_keys.fill_bytes(0xff);
+        g->hub_vals.zero();
+        g->hub_aux.zero();
+    }
+    g->binned = true;
+}
+
+}  // namespace cdk

@@ -1,0 +1,113 @@
+// graph.cuh -- device-resident CSR graph (the reference's Graph,
+// H/graph.hpp:38-272, laid out for HBM) and its work decomposition.
+//
+// HBM layout per graph (n nodes, D directed entries):
+//   off  int64[n+1]   row offsets (int64: C5 has D ~ 8.5e9)
+//   col  int32[D]     neighbour ids, rows strictly ascending (H/graph.hpp:177)
+//   w    fp32[D]      only for weighted graphs (unweighted => 1.0 implied)
+//   vol  fp64[n]      weighted degree, self-loop twice (H/graph.hpp:240-243)
+//   loop fp64[n]      self-loop weight
+// Work decomposition (built once per graph, lazily):
+//   tier  uint8[n]    degree tier of each node (255 = isolated)
+//   hubs  int32[H]    nodes of the hub tier, with a global hash region each
+#pragma once
+
+#include "common.cuh"
+
+namespace cdk {
+
+// Degree tiers of the sweep / move kernels.
+enum Tier : int {
+    TIER_G8 = 0,     // deg <= 8      : 8 lanes per node (4 nodes / warp)
+    TIER_G16 = 1,    // deg <= 16     : 16 lanes per node
+    TIER_G32 = 2,    // deg <= 32     : one warp per node, one pass
+    TIER_WARP = 3,   // deg <= 256    : one warp per node, per-warp smem hash
+    TIER_BLOCK = 4,  // deg <= 4096   : one block per node, block smem hash
+    TIER_HUB = 5,    // deg >  4096   : multi-block per node, global hash
+    NUM_TIERS = 6,
+    NUM_LIST_TIERS = 5,
+    TIER_NONE = 255
+};
+constexpr int64_t TIER_MAX_DEG[NUM_LIST_TIERS] = {8, 16, 32, 256, 4096};
+constexpr int WARP_TABLE_CAP = 512;    // per-warp smem hash slots (>= 2*256)
+constexpr int BLOCK_TABLE_CAP = 8192;  // block smem hash slots (>= 2*4096)
+constexpr int HUB_CHUNK = 4096;        // entries per hub chunk block
+
+__host__ __device__ inline int tier_of_degree(int64_t d) {
+    if (d <= 0)
+        return TIER_NONE;
+    if (d <= 8)
+        return TIER_G8;
+    if (d <= 16)
+        return TIER_G16;
+    if (d <= 32)
+        return TIER_G32;
+    if (d <= 256)
+        return TIER_WARP;
+    if (d <= 4096)
+        return TIER_BLOCK;
+    return TIER_HUB;
+}
+
+}  // namespace cdk
+
+struct cd_graph {
+    cd_ctx *ctx = nullptr;
+    int64_t n = 0, D = 0, m = 0;
+    double total = 0.0;
+    bool weighted = false;
+    int64_t max_degree = 0, isolated = 0;
+    cdk::DBuf<int64_t> off;
+    cdk::DBuf<int32_t> col;
+    cdk::DBuf<float> w;
+    cdk::DBuf<double> vol, loop;
+
+    // work decomposition
+    bool binned = false;
+    cdk::DBuf<uint8_t> tier;
+    int64_t tier_nodes[cdk::NUM_TIERS] = {0, 0, 0, 0, 0, 0};
+    int64_t tier_start[cdk::NUM_LIST_TIERS + 1] = {0, 0, 0, 0, 0, 0};  // list capacity offsets
+    cdk::DBuf<int32_t> lists;  // per-bucket worklists, sized sum of list-tier nodes
+    // hub tier: static chunk grid and hash regions
+    int64_t n_hubs = 0, n_hub_chunks = 0, hub_slots = 0;
+    cdk::DBuf<int32_t> hubs;        // [n_hubs] node ids
+    cdk::DBuf<int64_t> hub_tab;     // [n_hubs] table offset
+    cdk::DBuf<int32_t> hub_mask;    // [n_hubs] capacity - 1
+    cdk::DBuf<int32_t> chunk_hub;   // [n_hub_chunks]
+    cdk::DBuf<int32_t> chunk_part;  // [n_hub_chunks] chunk index within hub
+    cdk::DBuf<int32_t> hub_keys;    // [hub_slots] EMPTY when free
+    cdk::DBuf<double> hub_vals;     // [hub_slots]
+    cdk::DBuf<double> hub_aux;      // [n_hubs] per-hub w(u, C) accumulator (PLM)
+};
+
+namespace cdk {
+
+// Duplicate handling of the row engine (H/graph.hpp:178-194).
+enum DupMode : int { DUP_ERROR = 0, DUP_SUM = 1, DUP_ONE = 2 };
+
+// graph.cu
+void graph_finalize(cd_ctx *ctx, cd_graph *g);  // vol, loop, m, total, max degree
+void graph_ensure_bins(cd_ctx *ctx, cd_graph *g);
+cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, const int32_t *v, const float *w,
+                           DupMode mode);  // device arrays; symmetrises
+void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D);
+
+// quality.cu
+void community_volumes_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, double *vols, int64_t ub);
+// vols and sizes without range checks (driver-internal labels, always < ub)
+void community_volumes_sizes_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, double *vols, int32_t *csize,
+                                 int64_t ub);
+void modularity_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub, double gamma, double *q,
+                    double *cov);
+
+// partition.cu
+int64_t max_label_dev(cd_ctx *ctx, int64_t n, const int32_t *z);  // max+1 (>= 1); -1 if a label < 0
+int64_t compact_dev(cd_ctx *ctx, int64_t n, const int32_t *z, int64_t ub, int32_t *out);
+void prolong_dev(cd_ctx *ctx, int64_t nc, const int32_t *zc, int64_t n, const int32_t *pi, int32_t *out);
+int64_t combine_hashed_dev(cd_ctx *ctx, int64_t b, int64_t n, const int32_t *const *sols_dev, int32_t *out);
+void iota_dev(cd_ctx *ctx, int32_t *z, int64_t n);
+
+// coarsen.cu
+cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc);
+
+}  // namespace cdk

@@ -1,0 +1,720 @@
+// sweep.cu -- degree-tiered evaluation kernels shared by PLP and PLM.
+//
+//   PLP (H/plp.hpp:111-126): tally neighbour labels incl. the self-loop,
+//        best = argmax weight, ties -> smallest label.
+//   PLM (H/louvain.hpp:95-120): tally neighbour communities excl. the
+//        self-loop, delta(d) = (aff[d]-w_c)/w(E) + g(vol_c - vols[d])vol_u/(2w(E)^2),
+//        best = argmax delta with ties -> smallest d, move iff delta > 0.
+//
+// Tiers (graph.cuh): G8/G16/G32 one pass with __match_any_sync, lanes grouped
+// 8/16/32 per node; WARP per-warp smem hash; BLOCK block smem hash; HUB
+// multi-block insert into a global hash + per-hub finalize.  Every tally sum
+// is exact (int counts or fp64 of fp32 weights), so the decision does not
+// depend on the summation order and equals the sequential reference's.
+#include "sweep.cuh"
+
+#include <cmath>
+
+namespace cdk {
+
+struct SweepParams {
+    const int64_t *off;
+    const int32_t *col;
+    const float *w;
+    const double *vol;
+    const uint8_t *tier;
+    const int32_t *z;
+    uint8_t *active;
+    const double *vols;
+    const int32_t *csize;
+    double gamma, inv_total, inv_sq2;
+    int guard;
+    uint64_t key;
+    int bucket, buckets;
+    const int32_t *lists;
+    int64_t list_start[NUM_LIST_TIERS];
+    int32_t *cnt;  // [0..4] tier counts, [5] moves
+    int32_t *mv_node, *mv_label;
+    int32_t *dense_best;
+    double *dense_gain;
+    unsigned long long *stats;
+    // hub tier
+    const int32_t *hubs;
+    const int64_t *hub_tab;
+    const int32_t *hub_mask;
+    const int32_t *chunk_hub;
+    const int32_t *chunk_part;
+    int32_t *hub_keys;
+    double *hub_vals;
+    double *hub_aux;
+    int64_t n_hubs;
+};
+
+__device__ __forceinline__ double plm_delta(double aff_d, double w_c, double vol_c, double vols_d, double vol_u,
+                                            const SweepParams &P) {
+    // (aff[d] - w_c) * inv_total + gamma * (vol_c - vols[d]) * vol_u * inv_sq2
+    // evaluated exactly as the reference's left-to-right double expression
+    // (no FMA contraction): H/louvain.hpp:111-112.
+    const double t1 = __dmul_rn(__dsub_rn(aff_d, w_c), P.inv_total);
+    const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(P.gamma, __dsub_rn(vol_c, vols_d)), vol_u), P.inv_sq2);
+    return __dadd_rn(t1, t2);
+}
+
+__device__ __forceinline__ bool better(double a, int32_t ka, double b, int32_t kb) {
+    return a > b || (a == b && ka < kb);
+}
+
+template <int WIDTH>
+__device__ __forceinline__ void argmax_xor(double &v, int32_t &k) {
+#pragma unroll
+    for (int o = WIDTH / 2; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int32_t ok = __shfl_xor_sync(0xffffffffu, k, o);
+        if (better(ov, ok, v, k)) {
+            v = ov;
+            k = ok;
+        }
+    }
+}
+
+template <int WIDTH>
+__device__ __forceinline__ double sum_xor(double v) {
+#pragma unroll
+    for (int o = WIDTH / 2; o > 0; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Group aggregation: returns leader flag and the group's count / weight sum.
+template <bool W>
+__device__ __forceinline__ bool aggregate(int32_t key, double w, bool valid, uint32_t gmask, double *scratch,
+                                          double &val) {
+    const int lane = lane_id();
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    const uint32_t peers = __match_any_sync(0xffffffffu, key) & vmask & gmask;
+    const bool leader = valid && ((__ffs(peers) - 1) == lane);
+    if (W) {
+        scratch[lane] = w;
+        __syncwarp();
+        double s = 0.0;
+        if (leader)
+            for (uint32_t m = peers; m; m &= m - 1)
+                s += scratch[__ffs(m) - 1];
+        __syncwarp();
+        val = s;
+    } else {
+        val = static_cast<double>(__popc(peers));
+    }
+    return leader;
+}
+
+template <class V>
+__device__ __forceinline__ void tinsert(int32_t *keys, V *vals, uint32_t mask, int32_t key, V w) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
+        if (old == EMPTY_KEY || old == key) {
+            atomicAdd(&vals[s], w);
+            return;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// Applies one decision.  Must be reached by all lanes of the warp (the move
+// append is warp-aggregated); only lanes with `act` carry a decision.
+template <int MODE>
+__device__ __forceinline__ void decide(const SweepParams &P, bool act, int32_t u, int32_t cur, int32_t best,
+                                       double val) {
+    bool moved = false;
+    if (act) {
+        if (MODE == MODE_PLP) {
+            moved = best != cur;
+        } else {
+            moved = best != INT32_MAX && best != cur && val > 0.0;
+            if (moved && P.guard && P.csize && P.csize[cur] == 1 && P.csize[best] == 1 && best > cur)
+                moved = false;
+        }
+    }
+    if (P.dense_best) {
+        if (act) {
+            P.dense_best[u] = moved ? best : cur;
+            if (P.dense_gain)
+                P.dense_gain[u] = (moved && MODE == MODE_PLM) ? val : 0.0;
+        }
+        return;
+    }
+    const int32_t pos = warp_append(&P.cnt[5], moved);
+    if (moved) {
+        P.mv_node[pos] = u;
+        P.mv_label[pos] = best;
+    }
+    if (MODE == MODE_PLP && act && !moved && P.active)
+        P.active[u] = 0;
+}
+
+__device__ __forceinline__ void flush_stats(const SweepParams &P, unsigned long long nodes,
+                                            unsigned long long entries) {
+    nodes = warp_sum(nodes);
+    entries = warp_sum(entries);
+    if (lane_id() == 0 && (nodes | entries)) {
+        atomicAdd(&P.stats[0], nodes);
+        atomicAdd(&P.stats[1], entries);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tiers G8 / G16 / G32: one entry per lane, G lanes per node
+// ---------------------------------------------------------------------------
+template <int G, int MODE, bool W>
+__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
+    __shared__ double scratch[8][32];
+    constexpr int NPW = 32 / G;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int sub = lane / G, k = lane % G;
+    const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
+    const int32_t *list = P.lists + P.list_start[tier];
+    const int64_t count = P.cnt[tier];
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long st_n = 0, st_e = 0;
+    for (int64_t base = gw * NPW; base < count; base += nw * NPW) {
+        const int64_t idx = base + sub;
+        const bool has = idx < count;
+        const int32_t u = has ? list[idx] : 0;
+        int64_t s = 0, d = 0;
+        if (has) {
+            s = P.off[u];
+            d = P.off[u + 1] - s;
+        }
+        bool valid = has && k < d;
+        const int32_t v = valid ? P.col[s + k] : 0;
+        const double wt = (W && valid) ? static_cast<double>(P.w[s + k]) : 1.0;
+        if (MODE == MODE_PLM)
+            valid = valid && v != u;
+        const int32_t key = valid ? P.z[v] : 0;
+        double agg;
+        const bool leader = aggregate<W>(key, wt, valid, gmask, scratch[wid], agg);
+        const int32_t cur = has ? P.z[u] : 0;
+        double cv;
+        int32_t ck;
+        if (MODE == MODE_PLP) {
+            cv = leader ? agg : -1.0;
+            ck = leader ? key : INT32_MAX;
+        } else {
+            const double wc = sum_xor<G>((valid && key == cur) ? wt : 0.0);
+            if (leader && key != cur) {
+                const double vol_u = P.vol[u];
+                const double vol_c = __dsub_rn(P.vols[cur], vol_u);
+                cv = plm_delta(agg, wc, vol_c, P.vols[key], vol_u, P);
+                ck = key;
+            } else {
+                cv = -INFINITY;
+                ck = INT32_MAX;
+            }
+        }
+        argmax_xor<G>(cv, ck);
+        const bool act = has && k == 0;
+        decide<MODE>(P, act, u, cur, ck, cv);
+        if (act) {
+            ++st_n;
+            st_e += static_cast<unsigned long long>(d);
+        }
+    }
+    flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
+// tier WARP: one warp per node, per-warp smem hash (cap <= 512)
+// ---------------------------------------------------------------------------
+constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
+
+template <int MODE, bool W>
+__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
+    using V = typename std::conditional<W, double, unsigned int>::type;
+    __shared__ double scratch[4][32];
+    __shared__ int32_t skeys[4][SW_WARP_CAP];
+    __shared__ V svals[4][SW_WARP_CAP];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    int32_t *keys = skeys[wid];
+    V *vals = svals[wid];
+    const int32_t *list = P.lists + P.list_start[TIER_WARP];
+    const int64_t count = P.cnt[TIER_WARP];
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long st_n = 0, st_e = 0;
+    for (int64_t i = gw; i < count; i += nw) {
+        const int32_t u = list[i];
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        uint32_t cap = 64;
+        while (cap < 2 * (e - s))
+            cap <<= 1;
+        for (uint32_t t = lane; t < cap; t += 32) {
+            keys[t] = EMPTY_KEY;
+            vals[t] = V(0);
+        }
+        __syncwarp();
+        const int32_t cur = P.z[u];
+        double wc = 0.0;
+        for (int64_t f = s; f < e; f += 32) {
+            bool valid = f + lane < e;
+            const int32_t v = valid ? P.col[f + lane] : 0;
+            const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+            if (MODE == MODE_PLM)
+                valid = valid && v != u;
+            const int32_t key = valid ? P.z[v] : 0;
+            if (MODE == MODE_PLM && valid && key == cur)
+                wc += wt;
+            double agg;
+            if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
+                tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
+        }
+        __syncwarp();
+        if (MODE == MODE_PLM)
+            wc = warp_sum(wc);
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        int32_t ck = INT32_MAX;
+        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+        for (uint32_t t = lane; t < cap; t += 32) {
+            const int32_t key = keys[t];
+            if (key == EMPTY_KEY)
+                continue;
+            double val;
+            if (MODE == MODE_PLP) {
+                val = static_cast<double>(vals[t]);
+            } else {
+                if (key == cur)
+                    continue;
+                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+            }
+            if (better(val, key, cv, ck)) {
+                cv = val;
+                ck = key;
+            }
+        }
+        argmax_xor<32>(cv, ck);
+        decide<MODE>(P, lane == 0, u, cur, ck, cv);
+        if (lane == 0) {
+            ++st_n;
+            st_e += static_cast<unsigned long long>(e - s);
+        }
+        __syncwarp();
+    }
+    flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
+// tier BLOCK: one block per node, block smem hash (cap <= 8192)
+// ---------------------------------------------------------------------------
+template <int MODE, bool W>
+__global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
+    using V = typename std::conditional<W, double, unsigned int>::type;
+    extern __shared__ unsigned char smem_raw[];
+    V *vals = reinterpret_cast<V *>(smem_raw);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + BLOCK_TABLE_CAP);
+    __shared__ double scratch[8][32];
+    __shared__ double red_v[8];
+    __shared__ int32_t red_k[8];
+    __shared__ double red_wc[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int32_t *list = P.lists + P.list_start[TIER_BLOCK];
+    const int64_t count = P.cnt[TIER_BLOCK];
+    unsigned long long st_n = 0, st_e = 0;
+    for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const int32_t u = list[i];
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        uint32_t cap = 64;
+        while (cap < 2 * (e - s))
+            cap <<= 1;
+        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+            keys[t] = EMPTY_KEY;
+            vals[t] = V(0);
+        }
+        __syncthreads();
+        const int32_t cur = P.z[u];
+        double wc = 0.0;
+        for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
+            bool valid = f + lane < e;
+            const int32_t v = valid ? P.col[f + lane] : 0;
+            const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+            if (MODE == MODE_PLM)
+                valid = valid && v != u;
+            const int32_t key = valid ? P.z[v] : 0;
+            if (MODE == MODE_PLM && valid && key == cur)
+                wc += wt;
+            double agg;
+            if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
+                tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
+        }
+        if (MODE == MODE_PLM) {
+            wc = warp_sum(wc);
+            if (lane == 0)
+                red_wc[wid] = wc;
+        }
+        __syncthreads();
+        if (MODE == MODE_PLM) {
+            wc = 0.0;
+            for (int q = 0; q < 8; ++q)
+                wc += red_wc[q];
+        }
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        int32_t ck = INT32_MAX;
+        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+            const int32_t key = keys[t];
+            if (key == EMPTY_KEY)
+                continue;
+            double val;
+            if (MODE == MODE_PLP) {
+                val = static_cast<double>(vals[t]);
+            } else {
+                if (key == cur)
+                    continue;
+                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+            }
+            if (better(val, key, cv, ck)) {
+                cv = val;
+                ck = key;
+            }
+        }
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cv = lane < 8 ? red_v[lane] : -INFINITY;
+            ck = lane < 8 ? red_k[lane] : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(e - s);
+            }
+        }
+        __syncthreads();
+    }
+    if (wid == 0)
+        flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
+// tier HUB: chunk blocks insert into a per-hub global hash, then finalize
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool hub_selected(const SweepParams &P, int32_t u) {
+    if (P.buckets > 1 && bucket_of(P.key, u, P.buckets) != P.bucket)
+        return false;
+    if (P.active && !P.active[u])
+        return false;
+    return true;
+}
+
+template <int MODE, bool W>
+__global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
+    __shared__ double scratch[8][32];
+    __shared__ double red_wc[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int32_t h = P.chunk_hub[blockIdx.x];
+    const int32_t u = P.hubs[h];
+    if (!hub_selected(P, u))
+        return;
+    const int64_t s0 = P.off[u], e0 = P.off[u + 1];
+    const int64_t s = s0 + static_cast<int64_t>(P.chunk_part[blockIdx.x]) * HUB_CHUNK;
+    const int64_t e = min(e0, s + HUB_CHUNK);
+    int32_t *keys = P.hub_keys + P.hub_tab[h];
+    double *vals = P.hub_vals + P.hub_tab[h];
+    const uint32_t mask = static_cast<uint32_t>(P.hub_mask[h]);
+    const int32_t cur = P.z[u];
+    double wc = 0.0;
+    for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
+        bool valid = f + lane < e;
+        const int32_t v = valid ? P.col[f + lane] : 0;
+        const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+        if (MODE == MODE_PLM)
+            valid = valid && v != u;
+        const int32_t key = valid ? P.z[v] : 0;
+        if (MODE == MODE_PLM && valid && key == cur)
+            wc += wt;
+        double agg;
+        if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
+            tinsert<double>(keys, vals, mask, key, agg);
+    }
+    if (MODE == MODE_PLM) {
+        wc = warp_sum(wc);
+        if (lane == 0)
+            red_wc[wid] = wc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q)
+                t += red_wc[q];
+            if (t != 0.0)
+                atomicAdd(&P.hub_aux[h], t);
+        }
+    }
+    if (threadIdx.x == 0)
+        atomicAdd(&P.stats[1], static_cast<unsigned long long>(e - s));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
+    __shared__ double red_v[16];
+    __shared__ int32_t red_k[16];
+    const int lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
+        const int32_t u = P.hubs[h];
+        if (!hub_selected(P, u))
+            continue;
+        int32_t *keys = P.hub_keys + P.hub_tab[h];
+        double *vals = P.hub_vals + P.hub_tab[h];
+        const int64_t cap = static_cast<int64_t>(P.hub_mask[h]) + 1;
+        const int32_t cur = P.z[u];
+        const double wc = (MODE == MODE_PLM) ? P.hub_aux[h] : 0.0;
+        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        int32_t ck = INT32_MAX;
+        for (int64_t t = threadIdx.x; t < cap; t += blockDim.x) {
+            const int32_t key = keys[t];
+            if (key == EMPTY_KEY)
+                continue;
+            const double a = vals[t];
+            keys[t] = EMPTY_KEY;
+            vals[t] = 0.0;
+            double val;
+            if (MODE == MODE_PLP) {
+                val = a;
+            } else {
+                if (key == cur)
+                    continue;
+                val = plm_delta(a, wc, vol_c, P.vols[key], vol_u, P);
+            }
+            if (better(val, key, cv, ck)) {
+                cv = val;
+                ck = key;
+            }
+        }
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cv = lane < nwarps ? red_v[lane] : -INFINITY;
+            ck = lane < nwarps ? red_k[lane] : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                if (MODE == MODE_PLM)
+                    P.hub_aux[h] = 0.0;
+                atomicAdd(&P.stats[0], 1ULL);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// selection and apply
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_select(int64_t n, SweepParams P) {
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
+         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t u = base + threadIdx.x;
+        int t = TIER_NONE;
+        if (u < n) {
+            t = P.tier[u];
+            if (t < NUM_LIST_TIERS) {
+                if (P.active && !P.active[u])
+                    t = TIER_NONE;
+                else if (P.buckets > 1 && bucket_of(P.key, static_cast<int32_t>(u), P.buckets) != P.bucket)
+                    t = TIER_NONE;
+            } else {
+                t = TIER_NONE;
+            }
+        }
+        if (__ballot_sync(0xffffffffu, t != TIER_NONE) == 0)
+            continue;
+#pragma unroll
+        for (int q = 0; q < NUM_LIST_TIERS; ++q) {
+            const int32_t pos = warp_append(&P.cnt[q], t == q);
+            if (t == q)
+                const_cast<int32_t *>(P.lists)[P.list_start[q] + pos] = static_cast<int32_t>(u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const int32_t *mv_label,
+                                                   const int32_t *cnt, int32_t *z, uint8_t *active,
+                                                   const int64_t *off, const int32_t *col, long long *total) {
+    const int64_t count = cnt[5];
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
+    for (int64_t i = gw; i < count; i += nw) {
+        const int32_t u = mv_node[i];
+        if (lane == 0)
+            z[u] = mv_label[i];
+        if (active)
+            for (int64_t e = off[u] + lane; e < off[u + 1]; e += 32)
+                active[col[e]] = 1;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const int32_t *mv_label,
+                                                   const int32_t *cnt, int32_t *z, double *vols, int32_t *csize,
+                                                   const double *vol, long long *total) {
+    const int64_t count = cnt[5];
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int32_t u = mv_node[i], d = mv_label[i];
+        const int32_t c = z[u];
+        z[u] = d;
+        const double vu = vol[u];
+        atomicAdd(&vols[c], -vu);
+        atomicAdd(&vols[d], vu);
+        if (csize) {
+            atomicSub(&csize[c], 1);
+            atomicAdd(&csize[d], 1);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+void sweep_init(cd_ctx *ctx, cd_graph *g, SweepState &st) {
+    graph_ensure_bins(ctx, g);
+    st.ctx = ctx;
+    st.g = g;
+    st.cnt.alloc(ctx, 8);
+    st.mv_node.alloc(ctx, std::max<int64_t>(g->n, 1));
+    st.mv_label.alloc(ctx, std::max<int64_t>(g->n, 1));
+    st.stats.alloc(ctx, 4);
+    st.stats.zero();
+    st.total.alloc(ctx, 1);
+    st.total.zero();
+}
+
+template <int MODE, bool W>
+static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, const char *fam) {
+    const int sms = ctx->num_sms;
+    if (g->tier_nodes[TIER_G8])
+        CD_LAUNCH(ctx, fam, (k_sweep_direct<8, MODE, W>), sms * 8, 256, 0, P, int(TIER_G8));
+    if (g->tier_nodes[TIER_G16])
+        CD_LAUNCH(ctx, fam, (k_sweep_direct<16, MODE, W>), sms * 8, 256, 0, P, int(TIER_G16));
+    if (g->tier_nodes[TIER_G32])
+        CD_LAUNCH(ctx, fam, (k_sweep_direct<32, MODE, W>), sms * 8, 256, 0, P, int(TIER_G32));
+    if (g->tier_nodes[TIER_WARP])
+        CD_LAUNCH(ctx, fam, (k_sweep_warp<MODE, W>), sms * 8, 128, 0, P);
+    if (g->tier_nodes[TIER_BLOCK]) {
+        using V = typename std::conditional<W, double, unsigned int>::type;
+        const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
+        static bool attr_set = false;
+        if (!attr_set) {
+            CD_CUDA(cudaFuncSetAttribute(k_sweep_block<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            attr_set = true;
+        }
+        const int64_t nb = std::min<int64_t>(g->tier_nodes[TIER_BLOCK], sms * 2);
+        CD_LAUNCH(ctx, fam, (k_sweep_block<MODE, W>), static_cast<int>(nb), 256, smem, P);
+    }
+    if (g->n_hubs) {
+        CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
+        CD_LAUNCH(ctx, fam, (k_sweep_hub_final<MODE>), static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 4)), 512, 0,
+                  P);
+    }
+}
+
+void sweep_bucket(SweepState &st, const SweepCall &c) {
+    cd_ctx *ctx = st.ctx;
+    cd_graph *g = st.g;
+    SweepParams P;
+    P.off = g->off.p;
+    P.col = g->col.p;
+    P.w = g->weighted ? g->w.p : nullptr;
+    P.vol = g->vol.p;
+    P.tier = g->tier.p;
+    P.z = c.z;
+    P.active = c.active;
+    P.vols = c.vols;
+    P.csize = c.csize;
+    P.gamma = c.gamma;
+    P.inv_total = g->total > 0 ? 1.0 / g->total : 0.0;
+    P.inv_sq2 = g->total > 0 ? 1.0 / (2.0 * g->total * g->total) : 0.0;
+    P.guard = c.guard;
+    P.key = c.key;
+    P.bucket = c.bucket;
+    P.buckets = c.buckets;
+    P.lists = g->lists.p;
+    for (int t = 0; t < NUM_LIST_TIERS; ++t)
+        P.list_start[t] = g->tier_start[t];
+    P.cnt = st.cnt.p;
+    P.mv_node = st.mv_node.p;
+    P.mv_label = st.mv_label.p;
+    P.dense_best = c.dense_best;
+    P.dense_gain = c.dense_gain;
+    P.stats = st.stats.p;
+    P.hubs = g->hubs.p;
+    P.hub_tab = g->hub_tab.p;
+    P.hub_mask = g->hub_mask.p;
+    P.chunk_hub = g->chunk_hub.p;
+    P.chunk_part = g->chunk_part.p;
+    P.hub_keys = g->hub_keys.p;
+    P.hub_vals = g->hub_vals.p;
+    P.hub_aux = g->hub_aux.p;
+    P.n_hubs = g->n_hubs;
+
+    const int sms = ctx->num_sms;
+    const bool plp = c.mode == MODE_PLP;
+    const char *fam = plp ? "plp_sweep" : "plm_move";
+    CD_CUDA(cudaMemsetAsync(st.cnt.p, 0, 8 * sizeof(int32_t), ctx->stream));
+    if (g->n > 0)
+        CD_LAUNCH(ctx, plp ? "plp_select" : "plm_select", k_select, grid_for(g->n, 256, sms * 8), 256, 0, g->n, P);
+    if (plp) {
+        if (g->weighted)
+            launch_tiers<MODE_PLP, true>(ctx, g, P, fam);
+        else
+            launch_tiers<MODE_PLP, false>(ctx, g, P, fam);
+    } else {
+        if (g->weighted)
+            launch_tiers<MODE_PLM, true>(ctx, g, P, fam);
+        else
+            launch_tiers<MODE_PLM, false>(ctx, g, P, fam);
+    }
+    if (c.dense_best)
+        return;
+    if (plp)
+        CD_LAUNCH(ctx, "plp_apply", k_apply_plp, sms * 4, 256, 0, static_cast<const int32_t *>(st.mv_node.p),
+                  static_cast<const int32_t *>(st.mv_label.p), static_cast<const int32_t *>(st.cnt.p), c.z, c.active,
+                  static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), st.total.p);
+    else
+        CD_LAUNCH(ctx, "plm_apply", k_apply_plm, sms * 4, 256, 0, static_cast<const int32_t *>(st.mv_node.p),
+                  static_cast<const int32_t *>(st.mv_label.p), static_cast<const int32_t *>(st.cnt.p), c.z, c.vols,
+                  c.csize, static_cast<const double *>(g->vol.p), st.total.p);
+}
+
+int64_t sweep_read_total(SweepState &st) {
+    long long h = 0;
+    CD_CUDA(cudaMemcpyAsync(&h, st.total.p, sizeof(h), cudaMemcpyDeviceToHost, st.ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(st.ctx->stream));
+    return h;
+}
+
+void sweep_reset_total(SweepState &st) { st.total.zero(); }
+
+void sweep_read_stats(SweepState &st, unsigned long long *out4) {
+    CD_CUDA(cudaMemcpyAsync(out4, st.stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                            st.ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(st.ctx->stream));
+}
+
+}  // namespace cdk
