@@ -33,10 +33,11 @@ def assert_csr_equal(dev_g, og, weights_exact=True):
         np.testing.assert_array_equal(w, og.w)
     else:
         np.testing.assert_allclose(w, og.w, rtol=REL_W)
-    np.testing.assert_allclose(c["vol"], og.vol, rtol=1e-12)
-    np.testing.assert_allclose(c["loop"], og.loop, rtol=1e-12)
+    rel = 1e-12 if weights_exact else REL_W
+    np.testing.assert_allclose(c["vol"], og.vol, rtol=rel)
+    np.testing.assert_allclose(c["loop"], og.loop, rtol=rel)
     assert dev_g.edge_count() == og.m
-    assert dev_g.total_edge_weight() == pytest.approx(og.total, rel=1e-12)
+    assert dev_g.total_edge_weight() == pytest.approx(og.total, rel=rel)
 
 
 # ---------------------------------------------------------------------------
@@ -64,8 +65,9 @@ def test_golden_builder_sweep_modularity_coarsen(golden, dev, ctx, oracle):
         cc = cg.csr()
         assert np.array_equal(cc["off"], arr[f"{k}_coff"]) and np.array_equal(cc["col"], arr[f"{k}_ccol"])
         np.testing.assert_allclose(cc["w"], arr[f"{k}_cw"], rtol=REL_W)
-        np.testing.assert_allclose(cc["vol"], arr[f"{k}_cvol"], rtol=1e-12)
-        assert cg.edge_count() == c["cm"] and cg.total_edge_weight() == pytest.approx(c["ctotal"], rel=1e-12)
+        # coarse weights are stored as fp32 (one rounding), so vol follows them
+        np.testing.assert_allclose(cc["vol"], arr[f"{k}_cvol"], rtol=REL_W)
+        assert cg.edge_count() == c["cm"] and cg.total_edge_weight() == pytest.approx(c["ctotal"], rel=REL_W)
         assert np.array_equal(pi, arr[f"{k}_zc"])
 
 
@@ -149,7 +151,8 @@ def test_modularity_move_eval_coarsen_rmat(dev, ctx, oracle, rmat18, weighted):
     cg, pi = dev.coarsen(g, zc)
     ocg = oracle.coarsen(og, zc)
     assert_csr_equal(cg, ocg, weights_exact=False)
-    assert dev.modularity(cg, np.arange(k, dtype=np.int32)) == pytest.approx(q_ref, rel=1e-9)
+    # the coarse graph carries fp32-rounded weights: Q agrees to ~1e-7
+    assert dev.modularity(cg, np.arange(k, dtype=np.int32)) == pytest.approx(q_ref, rel=REL_Q)
 
 
 def test_modularity_vs_reference_flooded_partition(dev, ctx, ref, rmat18):
