@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 community-detection hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl b200|reference]
+
+One "step" = one complete detector run (the reference's RunReport.total_ms
+region, H/louvain.hpp:277-279) over one synthetic graph resident in HBM.
+Metric: edges/s = m (undirected edges, the reference CLI bench's
+edge_count(), P/tools/commdet.cpp:241-245) / step time.  Default workload =
+BASELINE.json configs[1]: PLM (gamma 1) on the LFR-shaped n=1e6 graph.
+
+value      device time (CUDA events on the library stream), graph + output in HBM,
+           L2 flushed (256 MiB write) before every timed step.
+e2e        the same metric through the public C ABI with HOST buffers: pinned
+           host CSR -> cd_graph_from_csr (H2D + validation + finalize) ->
+           cd_louvain_run with a host output (D2H of the labels).
+roofline   dominant kernel family (per-launch CUDA events on a profiled pass of
+           the same workload), algorithmic bytes per DESIGN.md's byte model vs
+           MEASURED_PEAKS.json hbm_gbs.
+cpu_baseline  the unmodified reference (oracle/_ref) on identical bytes (the C
+           port of the generator), all host threads, rank 0 at N=1.
+--impl reference  the reference arm: the same metric from oracle/_ref only.
+Multi-GPU (torchrun): one replica per rank ("replicas", weak scaling); value =
+all ranks' edges / max-over-ranks time.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PLP/PLM edges/sec at 1/2/4/8 B200, % HBM roofline; modularity vs CPU ref"
+
+LFR_C2 = dict(n=1_000_000, tau1=2.0, avg_degree=20.0, max_degree=200, tau2=1.0, min_community=20,
+              max_community=1000, mu=0.3)
+
+WORKLOADS = {
+    # BASELINE.json configs[1] -- the headline (fits one GPU)
+    "c2_lfr_plm": dict(gen="lfr", algo="plm", seed=1,
+                       desc="PLM gamma=1 on LFR-shaped n=1e6 (tau1=2, mean 20, max 200, tau2=1, [20,1000], mu=0.3)"),
+    "c1_planted_plp": dict(gen="planted", algo="plp", seed=1,
+                           desc="PLP on planted partition n=1e5, k=1000, p_in=0.1, p_out=2/99900"),
+    "c1_planted_plm": dict(gen="planted", algo="plm", seed=1, desc="PLM on config-1 planted graph"),
+    "c3_rmat24_plp": dict(gen="rmat", scale=24, weighted=False, algo="plp", seed=1,
+                          desc="PLP on R-MAT scale 24 ef 16 (0.57,0.19,0.19,0.05)"),
+    "c3_rmat24_plm": dict(gen="rmat", scale=24, weighted=False, algo="plm", seed=1,
+                          desc="PLM on R-MAT scale 24 ef 16"),
+    "c4_rmat22w_plmr": dict(gen="rmat", scale=22, weighted=True, algo="plmr", seed=1,
+                            desc="PLMR on weighted R-MAT scale 22 ef 16"),
+    "c4_rmat22w_epp": dict(gen="rmat", scale=22, weighted=True, algo="epp", seed=1,
+                           desc="EPP(4,PLP,PLMR) on weighted R-MAT scale 22 ef 16"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0, help="bound on the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=open(self.path, "w"),
+                                         stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        with open(self.path) as f:
+            for line in f:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 8:
+                    try:
+                        rows.append((float(p[0]), float(p[1]), p[4:8]))
+                    except ValueError:
+                        pass
+        os.unlink(self.path)
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def make_device_graph(P, ctx, wl):
+    if wl["gen"] == "lfr":
+        g, _ = P.generate_lfr(seed=wl["seed"], ctx=ctx, **LFR_C2)
+    elif wl["gen"] == "planted":
+        g, _ = P.generate_planted(100000, 1000, 0.1, 2 / 99900, wl["seed"], ctx=ctx)
+    else:
+        g = P.generate_rmat(wl["scale"], 16, 0.57, 0.19, 0.19, weighted=wl["weighted"], seed=wl["seed"], ctx=ctx)
+    return g
+
+
+def make_oracle_graph(O, wl):
+    """The identical graph through the C port / the reference generator."""
+    if wl["gen"] == "lfr":
+        return O.generate_lfr(seed=wl["seed"], **LFR_C2)[0]
+    if wl["gen"] == "planted":
+        rg, _ = O.RefGraph.planted(100000, 1000, 0.1, 2 / 99900, wl["seed"], workers=0)
+        return rg.csr()
+    return O.generate_rmat(wl["scale"], 16, 0.57, 0.19, 0.19, weighted=wl["weighted"], seed=wl["seed"])
+
+
+def run_device(P, g, algo, out, report=False):
+    if algo == "plp":
+        return P.run_plp(g, P.PlpConfig(), out=out, report=report)
+    if algo == "plm":
+        return P.run_louvain(g, P.LouvainConfig(refine=False), out=out, report=report)
+    if algo == "plmr":
+        return P.run_louvain(g, P.LouvainConfig(refine=True), out=out, report=report)
+    return P.run_epp(g, P.EnsembleConfig(), out=out)
+
+
+def run_reference(O, rg, algo, workers):
+    if algo == "plp":
+        return rg.run_plp(workers=workers)[1]
+    if algo == "plm":
+        return rg.run_louvain(refine=False, workers=workers)[1]
+    if algo == "plmr":
+        return rg.run_louvain(refine=True, workers=workers)[1]
+    return rg.run_epp(workers=workers)[1]
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def bench_reference(args, wl):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcommdet_ref.so not built"}))
+        return 0
+    og = make_oracle_graph(O, wl)
+    rg = O.RefGraph.from_csr(og)
+    threads = cpu_threads()
+    for _ in range(args.warmup):
+        run_reference(O, rg, wl["algo"], threads)
+    times, qs = [], []
+    for _ in range(args.steps):
+        rep = run_reference(O, rg, wl["algo"], threads)
+        times.append(rep["total_ms"] / 1e3)
+        qs.append(rep["modularity"])
+    total = sum(times)
+    value = og.m * args.steps / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "desc": wl["desc"], "m": og.m, "n": og.n,
+                   "modularity": statistics.median(qs), "parallelism": "openmp"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"{args.steps} complete runs of the reference {wl['algo']} (oracle/_ref, "
+                                   f"OMP workers={threads}) on the identical graph"},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def bench_b200(args, wl):
+    import numpy as np
+    import torch
+
+    import paper_1304_4453_b200 as P
+
+    world, rank, local = dist_env()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    ctx = P.Context(local)
+    g = make_device_graph(P, ctx, wl)
+    n, m = g.node_count(), g.edge_count()
+    out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{local}")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
+
+    def step():
+        run_device(P, g, wl["algo"], out, report=False)
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    # ---- timed region ------------------------------------------------------------
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # evict L2 (256 MiB > 126 MB) outside the timed step
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    launches = ctx.launch_count() - launches0
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+    if dist:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    value = world * m * args.steps / (total_ms / 1e3)
+
+    # ---- quality of the run (modularity vs the CPU reference below) --------------
+    z, rep = run_device(P, g, wl["algo"], None, report=True)
+    quality = {"modularity": rep.modularity, "communities": rep.community_count,
+               "levels": len(rep.levels), "iterations": len(rep.iterations)}
+
+    # ---- roofline: profiled pass of the same workload ---------------------------
+    ctx.reset_stats()
+    ctx.set_profiling(True)
+    prof_steps = max(1, min(3, args.steps))
+    for _ in range(prof_steps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        step()
+    ctx.set_profiling(False)
+    stats = ctx.kernel_stats()
+    fam = "plp_sweep" if wl["algo"] == "plp" else ("plm_move" if wl["algo"] in ("plm", "plmr") else None)
+    if fam is None or fam not in stats:
+        fam = max(stats, key=lambda k: stats[k]["total_ms"])
+    s = stats[fam]
+    peak, peak_kind = measured_peak()
+    achieved = s["bytes"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 and s["bytes"] > 0 else None
+    prof_total = sum(v["total_ms"] for v in stats.values())
+    roofline = {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": (achieved / peak) if achieved else None, "traffic": None,
+                "peak_kind": peak_kind, "bytes_per_launch": s["bytes"] / max(s["launches"], 1),
+                "avg_launch_ms": s["total_ms"] / max(s["launches"], 1), "launches": s["launches"] // prof_steps,
+                "share_of_step": s["total_ms"] / prof_total if prof_total else None,
+                "families_ms_per_step": {k: round(v["total_ms"] / prof_steps, 4) for k, v in
+                                         sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])[:8]}}
+    prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof_path):
+        with open(prof_path) as f:
+            ps = json.load(f).get(args.workload, {}).get(fam)
+        if ps and ps.get("dram_bytes_per_launch"):
+            roofline["traffic"] = ps["dram_bytes_per_launch"]
+
+    # ---- end to end through the C ABI with host buffers ----------------------------
+    c = g.csr()
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+    h_off, h_col = pin(c["off"]), pin(c["col"])
+    h_w = pin(c["w"]) if c["w"] is not None else None
+    h_out = torch.empty(max(n, 1), dtype=torch.int32).pin_memory().numpy()
+    e2e_ms = 0.0
+    e2e_steps = max(1, min(args.steps, 5))
+    for i in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        gh = P.Graph.from_csr(n, h_off, h_col, h_w, ctx=ctx)
+        run_device(P, gh, wl["algo"], h_out, report=False)
+        e1.record(stream)
+        e1.synchronize()
+        if i > 0:  # first iteration is a warm-up
+            e2e_ms += e0.elapsed_time(e1)
+        del gh
+    e2e_ms /= e2e_steps
+    h2d = h_off.nbytes + h_col.nbytes + (h_w.nbytes if h_w is not None else 0)
+    e2e = {"value": world * m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(4 * n), "ms_per_step": e2e_ms}
+
+    # ---- CPU baseline: the reference on identical bytes (rank 0, N = 1) -----------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            if O.ref_available():
+                og = make_oracle_graph(O, wl)
+                assert og.m == m and np.array_equal(og.col, c["col"]), "oracle graph differs from device graph"
+                rg = O.RefGraph.from_csr(og)
+                threads = cpu_threads()
+                ts, qs = [], []
+                t0 = time.time()
+                while len(ts) < 3 and (not ts or time.time() - t0 < args.cpu_sample_s):
+                    r = run_reference(O, rg, wl["algo"], threads)
+                    ts.append(r["total_ms"] / 1e3)
+                    qs.append(r["modularity"])
+                cpu = {"value": m / statistics.median(ts), "unit": "edges/s", "cores": threads, "kind": "reference",
+                       "sample": f"{len(ts)} complete reference {wl['algo']} runs (oracle/_ref, OMP workers="
+                                 f"{threads}) on the identical graph, median total_ms"}
+                quality["ref_modularity"] = statistics.median(qs)
+                quality["abs_diff"] = abs(quality["modularity"] - quality["ref_modularity"])
+        except Exception as exc:  # the baseline is reported, never the target
+            cpu = {"value": None, "unit": "edges/s", "cores": cpu_threads(), "kind": "reference",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic",
+            "config": {"workload": args.workload, "desc": wl["desc"], "n": n, "m": m, "entries": g.entries,
+                       "algo": wl["algo"], "seed": wl["seed"], "parallelism": "replicas" if world > 1 else "1gpu",
+                       "l2": "flushed (256 MiB write) before every timed step",
+                       "quality": quality},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return bench_reference(args, wl)
+    return bench_b200(args, wl)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -560,7 +560,7 @@ def _trim(g, arr):
 # ---------------------------------------------------------------------------
 # detectors
 # ---------------------------------------------------------------------------
-def run_plp(g: Graph, cfg: PlpConfig = None, initial=None, out=None):
+def run_plp(g: Graph, cfg: PlpConfig = None, initial=None, out=None, report=True):
     """run_plp (H/plp.hpp:67-149).  Returns (labels, RunReport); labels are raw
     (not compacted).  ``out`` may be a preallocated int32 CUDA tensor."""
     cfg = cfg or PlpConfig()
@@ -570,17 +570,19 @@ def run_plp(g: Graph, cfg: PlpConfig = None, initial=None, out=None):
     labels, lp = _labels_out(g, out)
     rep = _Report()
     c = cfg._c()
-    _check(load_library().cd_plp_run(g.ctx.h, g.h, C.byref(c), pi, lp, C.byref(rep)))
-    return _trim(g, labels), RunReport._from(rep)
+    _check(load_library().cd_plp_run(g.ctx.h, g.h, C.byref(c), pi, lp, C.byref(rep) if report else None))
+    return _trim(g, labels), (RunReport._from(rep) if report else None)
 
 
-def run_louvain(g: Graph, cfg: LouvainConfig = None, out=None):
+def run_louvain(g: Graph, cfg: LouvainConfig = None, out=None, report=True):
+    """run_plm / run_plmr by cfg.refine.  report=False skips the quality
+    evaluation (the reference's total_ms excludes it too) and returns None."""
     cfg = cfg or LouvainConfig()
     z, zp = _labels_out(g, out)
     rep = _Report()
     c = cfg._c()
-    _check(load_library().cd_louvain_run(g.ctx.h, g.h, C.byref(c), zp, C.byref(rep)))
-    return _trim(g, z), RunReport._from(rep)
+    _check(load_library().cd_louvain_run(g.ctx.h, g.h, C.byref(c), zp, C.byref(rep) if report else None))
+    return _trim(g, z), (RunReport._from(rep) if report else None)
 
 
 def run_plm(g: Graph, cfg: LouvainConfig = None, out=None):

@@ -171,6 +171,8 @@ cd_status cd_ctx_create(int device, cd_ctx **out) {
         CD_CUDA(cudaGetDeviceProperties(&prop, device));
         ctx->num_sms = prop.multiProcessorCount;
         ctx->smem_optin = prop.sharedMemPerBlockOptin;
+        CD_CUDA(cudaMalloc(reinterpret_cast<void **>(&ctx->dstats), DSTATS * sizeof(unsigned long long)));
+        CD_CUDA(cudaMemset(ctx->dstats, 0, DSTATS * sizeof(unsigned long long)));
         *out = ctx;
         return CD_OK;
     } catch (const ::cdk::Error &e) {
@@ -199,6 +201,8 @@ cd_status cd_ctx_destroy(cd_ctx *ctx) {
     }
     for (auto e : ctx->free_events)
         cudaEventDestroy(e);
+    if (ctx->dstats)
+        cudaFree(ctx->dstats);
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return CD_OK;
@@ -215,13 +219,31 @@ cd_status cd_ctx_set_profiling(cd_ctx *ctx, int enabled) {
 }
 
 cd_status cd_ctx_reset_stats(cd_ctx *ctx) {
-    CD_GUARD(ctx, CD_REQUIRE(ctx, CD_EINVAL, "null context"); ctx_flush_stats(ctx); ctx->stats.clear())
+    CD_GUARD(ctx, CD_REQUIRE(ctx, CD_EINVAL, "null context"); ctx_flush_stats(ctx); ctx->stats.clear();
+             CD_CUDA(cudaMemsetAsync(ctx->dstats, 0, DSTATS * sizeof(unsigned long long), ctx->stream));
+             ctx_sync(ctx))
 }
 
 cd_status cd_ctx_kernel_stats(cd_ctx *ctx, cd_kernel_stat *out, int32_t capacity, int32_t *count) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && count, CD_EINVAL, "null argument");
         ctx_flush_stats(ctx);
+        // algorithmic bytes of the sweep families (DESIGN.md byte model):
+        //   plp_sweep: 17 B / evaluated node + (8 + 4W) B / entry
+        //   plm_move:  24 B / evaluated node + (8 + 4W) B / entry
+        unsigned long long ds[DSTATS];
+        CD_CUDA(cudaMemcpyAsync(ds, ctx->dstats, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
+        ctx_sync(ctx);
+        if (ctx->stats.count("plp_sweep")) {
+            auto &s = ctx->stats["plp_sweep"];
+            s.items = static_cast<double>(ds[1] + ds[2]);
+            s.bytes = 17.0 * ds[0] + 8.0 * ds[1] + 12.0 * ds[2];
+        }
+        if (ctx->stats.count("plm_move")) {
+            auto &s = ctx->stats["plm_move"];
+            s.items = static_cast<double>(ds[4] + ds[5]);
+            s.bytes = 24.0 * ds[3] + 8.0 * ds[4] + 12.0 * ds[5];
+        }
         int32_t i = 0;
         for (auto &kv : ctx->stats) {
             if (out && i < capacity) {

@@ -64,22 +64,15 @@ struct cd_ctx {
     std::vector<cudaEvent_t> free_events;
     // small pinned staging area for scalar read-backs
     int64_t *pinned = nullptr;
-    // device counters: [0..31] general purpose (see cdk::Ctr)
-    int64_t *dctr = nullptr;
+    // device work counters of the sweep families (algorithmic-byte model):
+    // [0] plp nodes, [1] plp entries (unweighted), [2] plp entries (weighted),
+    // [3] plm nodes, [4] plm entries (unweighted), [5] plm entries (weighted)
+    unsigned long long *dstats = nullptr;
 };
 
 namespace cdk {
 
-enum Ctr : int {
-    CTR_LIST0 = 0,   // 0..7  per-bin worklist counts (int32 packed in int64 slots)
-    CTR_MOVES = 8,   // moves in the current bucket
-    CTR_TOTAL = 9,   // moves accumulated (iteration / pass)
-    CTR_FLAG = 10,   // error flag
-    CTR_AUX = 11,    // scratch
-    CTR_NODES = 12,  // nodes evaluated (stats)
-    CTR_ENTRIES = 13,  // entries scanned (stats)
-    CTR_COUNT = 32
-};
+constexpr int DSTATS = 8;
 
 // ---------------------------------------------------------------------------
 // device buffers (stream-ordered pool allocations on the context stream)

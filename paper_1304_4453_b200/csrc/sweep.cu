@@ -153,13 +153,14 @@ __device__ __forceinline__ void decide(const SweepParams &P, bool act, int32_t u
         P.active[u] = 0;
 }
 
+// stats layout per mode: [0] nodes, [1] entries unweighted, [2] entries weighted
 __device__ __forceinline__ void flush_stats(const SweepParams &P, unsigned long long nodes,
                                             unsigned long long entries) {
     nodes = warp_sum(nodes);
     entries = warp_sum(entries);
     if (lane_id() == 0 && (nodes | entries)) {
         atomicAdd(&P.stats[0], nodes);
-        atomicAdd(&P.stats[1], entries);
+        atomicAdd(&P.stats[P.w ? 2 : 1], entries);
     }
 }
 
@@ -456,7 +457,7 @@ __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
         }
     }
     if (threadIdx.x == 0)
-        atomicAdd(&P.stats[1], static_cast<unsigned long long>(e - s));
+        atomicAdd(&P.stats[P.w ? 2 : 1], static_cast<unsigned long long>(e - s));
 }
 
 template <int MODE>
@@ -598,8 +599,6 @@ void sweep_init(cd_ctx *ctx, cd_graph *g, SweepState &st) {
     st.cnt.alloc(ctx, 8);
     st.mv_node.alloc(ctx, std::max<int64_t>(g->n, 1));
     st.mv_label.alloc(ctx, std::max<int64_t>(g->n, 1));
-    st.stats.alloc(ctx, 4);
-    st.stats.zero();
     st.total.alloc(ctx, 1);
     st.total.zero();
 }
@@ -662,7 +661,7 @@ void sweep_bucket(SweepState &st, const SweepCall &c) {
     P.mv_label = st.mv_label.p;
     P.dense_best = c.dense_best;
     P.dense_gain = c.dense_gain;
-    P.stats = st.stats.p;
+    P.stats = ctx->dstats + (c.mode == MODE_PLP ? 0 : 3);
     P.hubs = g->hubs.p;
     P.hub_tab = g->hub_tab.p;
     P.hub_mask = g->hub_mask.p;
@@ -710,11 +709,5 @@ int64_t sweep_read_total(SweepState &st) {
 }
 
 void sweep_reset_total(SweepState &st) { st.total.zero(); }
-
-void sweep_read_stats(SweepState &st, unsigned long long *out4) {
-    CD_CUDA(cudaMemcpyAsync(out4, st.stats.p, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                            st.ctx->stream));
-    CD_CUDA(cudaStreamSynchronize(st.ctx->stream));
-}
 
 }  // namespace cdk

@@ -14,7 +14,6 @@ struct SweepState {
     DBuf<int32_t> cnt;         // [8]: per-tier list counts [0..4], [5] moves
     DBuf<int32_t> mv_node;     // [n]
     DBuf<int32_t> mv_label;    // [n]
-    DBuf<unsigned long long> stats;  // [4]: nodes, entries (evaluated), moves, spare
     DBuf<long long> total;     // [1] moves accumulated since last reset
 };
 
@@ -42,6 +41,5 @@ void sweep_bucket(SweepState &st, const SweepCall &c);
 // host read of the accumulated move counter (syncs) and reset
 int64_t sweep_read_total(SweepState &st);
 void sweep_reset_total(SweepState &st);
-void sweep_read_stats(SweepState &st, unsigned long long *out4);
 
 }  // namespace cdk
