@@ -282,7 +282,9 @@ def bench_b200(args, wl):
     # ---- quality of the run (modularity vs the CPU reference below) --------------
     z, rep = run_device(P, g, wl["algo"], None, report=True)
     quality = {"modularity": rep.modularity, "communities": rep.community_count,
-               "levels": len(rep.levels), "iterations": len(rep.iterations)}
+               "levels": [{k: (round(v, 3) if isinstance(v, float) else v) for k, v in l.items()}
+                          for l in rep.levels],
+               "iterations": len(rep.iterations), "run_ms": rep.total_ms}
 
     # ---- roofline: profiled pass of the same workload ---------------------------
     ctx.reset_stats()
@@ -300,7 +302,8 @@ def bench_b200(args, wl):
     s = stats[fam]
     peak, peak_kind = measured_peak()
     achieved = s["bytes"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 and s["bytes"] > 0 else None
-    prof_total = sum(v["total_ms"] for v in stats.values())
+    # "plp_sweep" / "plm_move" aggregate their per-tier ".g8/.warp/..." entries
+    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in ("plp_sweep", "plm_move"))
     roofline = {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "peak_kind": peak_kind, "bytes_per_launch": s["bytes"] / max(s["launches"], 1),

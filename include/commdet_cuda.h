@@ -76,6 +76,7 @@ typedef struct cd_louvain_config {
     int32_t singleton_guard; /* device: singleton->singleton only to smaller id */
     int64_t move_theta;      /* device: stop a move phase once a pass moves <= this;
                                 <0: floor(n/100000) of the level's graph     */
+    double move_tol;         /* device: ... or <= move_tol * n (0 disables)  */
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */
@@ -99,7 +100,8 @@ typedef struct cd_iteration_record {
 } cd_iteration_record;
 typedef struct cd_level_record {
     double move_ms, coarsen_ms, refine_ms;
-    int64_t nodes, entries;
+    int64_t nodes, entries;   /* the level's graph                        */
+    int64_t passes, moves;    /* move phase (+ refinement) passes and moves */
 } cd_level_record;
 typedef struct cd_report {
     char algorithm[16];

@@ -1244,7 +1244,9 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
     const double total = g->total;
     const double inv_total = 1.0 / total;
     const double inv_sq2 = 1.0 / (2.0 * total * total);
-    const int64_t theta = cfg->move_theta >= 0 ? cfg->move_theta : n / 100000;
+    int64_t theta = cfg->move_theta >= 0 ? cfg->move_theta : n / 100000;
+    if ((int64_t)(cfg->move_tol * (double)n) > theta)
+        theta = (int64_t)(cfg->move_tol * (double)n);
     double *vols = (double *)malloc(sizeof(double) * (size_t)ub);
     int32_t *csize = (int32_t *)calloc((size_t)ub, sizeof(int32_t));
     cdo_community_volumes(g, z, ub, vols);

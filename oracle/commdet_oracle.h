@@ -134,6 +134,7 @@ typedef struct {
     int32_t refine;
     int32_t singleton_guard;
     int64_t move_theta; /* <0: floor(n/100000) per level */
+    double move_tol;    /* stop also once a pass moves <= move_tol * n */
 } cdo_louvain_config;
 
 /* bucket key / id: the order every device driver uses. */

@@ -80,7 +80,7 @@ class _PlpConfig(C.Structure):
 class _LouvainConfig(C.Structure):
     _fields_ = [("gamma", C.c_double), ("max_move_iterations", C.c_int64), ("max_levels", C.c_int64),
                 ("seed", C.c_uint64), ("workers", C.c_int32), ("refine", C.c_int32), ("buckets", C.c_int32),
-                ("singleton_guard", C.c_int32), ("move_theta", C.c_int64)]
+                ("singleton_guard", C.c_int32), ("move_theta", C.c_int64), ("move_tol", C.c_double)]
 
 
 class _EnsembleConfig(C.Structure):
@@ -95,7 +95,7 @@ class _IterRec(C.Structure):
 
 class _LevelRec(C.Structure):
     _fields_ = [("move_ms", C.c_double), ("coarsen_ms", C.c_double), ("refine_ms", C.c_double),
-                ("nodes", C.c_int64), ("entries", C.c_int64)]
+                ("nodes", C.c_int64), ("entries", C.c_int64), ("passes", C.c_int64), ("moves", C.c_int64)]
 
 
 class _Report(C.Structure):
@@ -481,10 +481,12 @@ class LouvainConfig:
     buckets: int = 4
     singleton_guard: bool = True
     move_theta: int = -1
+    move_tol: float = 1e-3
 
     def _c(self):
         return _LouvainConfig(self.gamma, self.max_move_iterations, self.max_levels, self.seed, self.workers,
-                              int(self.refine), self.buckets, int(self.singleton_guard), self.move_theta)
+                              int(self.refine), self.buckets, int(self.singleton_guard), self.move_theta,
+                              self.move_tol)
 
 
 @dataclass
@@ -525,7 +527,8 @@ class RunReport:
         its = [dict(updated=r.iterations[i].updated, ms=r.iterations[i].ms)
                for i in range(min(r.n_iterations, 1024))]
         lvs = [dict(move_ms=r.levels[i].move_ms, coarsen_ms=r.levels[i].coarsen_ms,
-                    refine_ms=r.levels[i].refine_ms, nodes=r.levels[i].nodes, entries=r.levels[i].entries)
+                    refine_ms=r.levels[i].refine_ms, nodes=r.levels[i].nodes, entries=r.levels[i].entries,
+                    passes=r.levels[i].passes, moves=r.levels[i].moves)
                for i in range(min(r.n_levels, 64))]
         return cls(r.algorithm.decode(), r.workers, r.seed, r.total_ms, r.modularity, r.coverage,
                    r.community_count, its, lvs, r.base_ms, r.combine_ms, r.coarsen_ms, r.final_ms,

@@ -2,6 +2,7 @@
 // point validates like the reference function it replaces, moves host
 // arguments in / out and maps C++ errors to cd_status codes.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -139,6 +140,7 @@ void cd_louvain_config_default(cd_louvain_config *c) {
     c->buckets = 4;
     c->singleton_guard = 1;
     c->move_theta = -1;
+    c->move_tol = 1e-3;  // stop a level's passes below 0.1% movers
 }
 
 void cd_ensemble_config_default(cd_ensemble_config *c) {
@@ -171,6 +173,7 @@ cd_status cd_ctx_create(int device, cd_ctx **out) {
         CD_CUDA(cudaGetDeviceProperties(&prop, device));
         ctx->num_sms = prop.multiProcessorCount;
         ctx->smem_optin = prop.sharedMemPerBlockOptin;
+        ctx->use_graphs = std::getenv("CD_NO_GRAPHS") == nullptr;
         CD_CUDA(cudaMalloc(reinterpret_cast<void **>(&ctx->dstats), DSTATS * sizeof(unsigned long long)));
         CD_CUDA(cudaMemset(ctx->dstats, 0, DSTATS * sizeof(unsigned long long)));
         *out = ctx;
@@ -234,6 +237,20 @@ cd_status cd_ctx_kernel_stats(cd_ctx *ctx, cd_kernel_stat *out, int32_t capacity
         unsigned long long ds[DSTATS];
         CD_CUDA(cudaMemcpyAsync(ds, ctx->dstats, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
         ctx_sync(ctx);
+        // aggregate the per-tier families ("plm_move.warp", ...) into "plm_move"
+        for (const char *agg : {"plp_sweep", "plm_move"}) {
+            KStat tot;
+            bool any = false;
+            const std::string pre = std::string(agg) + ".";
+            for (auto &kv : ctx->stats)
+                if (kv.first.compare(0, pre.size(), pre) == 0) {
+                    tot.launches += kv.second.launches;
+                    tot.total_ms += kv.second.total_ms;
+                    any = true;
+                }
+            if (any)
+                ctx->stats[agg] = tot;
+        }
         if (ctx->stats.count("plp_sweep")) {
             auto &s = ctx->stats["plp_sweep"];
             s.items = static_cast<double>(ds[1] + ds[2]);

@@ -68,6 +68,13 @@ struct cd_ctx {
     // [0] plp nodes, [1] plp entries (unweighted), [2] plp entries (weighted),
     // [3] plm nodes, [4] plm entries (unweighted), [5] plm entries (weighted)
     unsigned long long *dstats = nullptr;
+    // side streams + events used to capture independent kernels as parallel
+    // branches of a CUDA graph
+    static constexpr int NSIDE = 6;
+    cudaStream_t side[NSIDE] = {};
+    cudaEvent_t fork_ev = nullptr;
+    cudaEvent_t join_ev[NSIDE] = {};
+    bool use_graphs = true;
 };
 
 namespace cdk {
@@ -170,6 +177,14 @@ inline void check_launch(const char *name) {
     do {                                                                                             \
         ::cdk::LaunchScope ls_((ctx), (family));                                                     \
         kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);                            \
+        ::cdk::check_launch(family);                                                                 \
+    } while (0)
+
+// same on an explicit stream (graph capture branches; never profiled)
+#define CD_LAUNCH_S(ctx, strm, family, kernel, grid, block, smem, ...)                               \
+    do {                                                                                             \
+        (ctx)->launches++;                                                                           \
+        kernel<<<(grid), (block), (smem), (strm)>>>(__VA_ARGS__);                                   \
         ::cdk::check_launch(family);                                                                 \
     } while (0)
 

@@ -10,6 +10,8 @@
 // H/louvain.hpp:120-126); a pure Jacobi sweep oscillates (SURVEY.md finding 2).
 // oracle/commdet_oracle.c (cdo_*_bucketed) ports this order exactly.
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 
 #include "detect.cuh"
 
@@ -56,25 +58,18 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
         iota_dev(ctx, labels, n);
     DBuf<uint8_t> active(ctx, std::max<int64_t>(n, 1));
     active.fill_bytes(1);
-    SweepState st;
-    sweep_init(ctx, g, st);
+    SweepCall c;
+    c.mode = MODE_PLP;
+    c.z = labels;
+    c.active = active.p;
+    c.buckets = K;
+    Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
     int64_t updated = n, iter = 0;
     while (updated > theta && iter < cfg.max_iterations) {  // H/plp.hpp:98
         it.start();
-        sweep_reset_total(st);
-        const uint64_t key = bucket_key(cfg.seed, static_cast<uint64_t>(iter));
-        for (int b = 0; b < K; ++b) {
-            SweepCall c;
-            c.mode = MODE_PLP;
-            c.z = labels;
-            c.active = active.p;
-            c.key = key;
-            c.bucket = b;
-            c.buckets = K;
-            sweep_bucket(st, c);
-        }
-        updated = sweep_read_total(st);
+        sw.pass(bucket_key(cfg.seed, static_cast<uint64_t>(iter)));
+        updated = sw.take_moves();
         rep.iteration(updated, it.stop_ms());
         ++iter;
     }
@@ -85,14 +80,15 @@ int64_t plp_sweep_sync_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z_in, int32_
     if (n == 0)
         return 0;
     CD_CUDA(cudaMemcpyAsync(z_out, z_in, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, ctx->stream));
-    SweepState st;
-    sweep_init(ctx, g, st);
     SweepCall c;
     c.mode = MODE_PLP;
     c.z = const_cast<int32_t *>(z_in);
     c.buckets = 1;
     c.dense_best = z_out;
-    sweep_bucket(st, c);
+    {
+        Sweeper sw(ctx, g, c);
+        sw.pass(0);
+    }
     DBuf<unsigned long long> cnt(ctx, 1);
     cnt.zero();
     CD_LAUNCH(ctx, "count_diff", k_count_diff, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z_in,
@@ -123,8 +119,6 @@ void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vol
     CD_LAUNCH(ctx, "move_eval", k_fill_gain0, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z, best, gain);
     if (g->total == 0.0)
         return;
-    SweepState st;
-    sweep_init(ctx, g, st);
     SweepCall c;
     c.mode = MODE_PLM;
     c.z = const_cast<int32_t *>(z);
@@ -133,39 +127,45 @@ void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vol
     c.buckets = 1;
     c.dense_best = best;
     c.dense_gain = gain;
-    sweep_bucket(st, c);
+    {
+        Sweeper sw(ctx, g, c);
+        sw.pass(0);
+    }
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
-bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt) {
+bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt,
+                    int64_t *passes, int64_t *moves) {
     const int64_t n = g->n;
     if (n == 0 || g->total == 0.0)  // H/louvain.hpp:67-68
         return false;
     const int K = cfg.buckets > 0 ? cfg.buckets : 4;
-    const int64_t theta = cfg.move_theta >= 0 ? cfg.move_theta : n / 100000;
+    const int64_t theta = std::max<int64_t>(cfg.move_theta >= 0 ? cfg.move_theta : n / 100000,
+                                            static_cast<int64_t>(cfg.move_tol * static_cast<double>(n)));
     DBuf<double> vols(ctx, n);
     DBuf<int32_t> csize(ctx, n);
     community_volumes_sizes_dev(ctx, g, z, vols.p, csize.p, n);  // H/louvain.hpp:75
-    SweepState st;
-    sweep_init(ctx, g, st);
+    SweepCall c;
+    c.mode = MODE_PLM;
+    c.z = z;
+    c.vols = vols.p;
+    c.csize = csize.p;
+    c.gamma = cfg.gamma;
+    c.guard = cfg.singleton_guard;
+    c.buckets = K;
+    Sweeper sw(ctx, g, c);
     bool changed = false;
+    static const bool trace = std::getenv("CD_TRACE") != nullptr;
     for (int64_t pass = 0; pass < cfg.max_move_iterations; ++pass) {
-        sweep_reset_total(st);
-        const uint64_t key = bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass));
-        for (int b = 0; b < K; ++b) {
-            SweepCall c;
-            c.mode = MODE_PLM;
-            c.z = z;
-            c.vols = vols.p;
-            c.csize = csize.p;
-            c.gamma = cfg.gamma;
-            c.guard = cfg.singleton_guard;
-            c.key = key;
-            c.bucket = b;
-            c.buckets = K;
-            sweep_bucket(st, c);
-        }
-        const int64_t moved = sweep_read_total(st);
+        sw.pass(bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass)));
+        const int64_t moved = sw.take_moves();
+        if (trace)
+            std::fprintf(stderr, "[cd] move n=%lld D=%lld pass=%lld moved=%lld\n", static_cast<long long>(n),
+                         static_cast<long long>(g->D), static_cast<long long>(pass), static_cast<long long>(moved));
+        if (passes)
+            ++*passes;
+        if (moves)
+            *moves += moved;
         if (moved == 0)  // H/louvain.hpp:136-137
             break;
         changed = true;
@@ -182,12 +182,15 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
     iota_dev(ctx, z, n);  // singleton_partition (:242)
     DevTimer t(ctx);
     t.start();
-    const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0));
+    int64_t passes = 0, moves = 0;
+    const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0), &passes, &moves);
     const double mv = t.stop_ms();
     if (auto *L = rep.level(level)) {
         L->move_ms += mv;
         L->nodes = n;
         L->entries = g->D;
+        L->passes += passes;
+        L->moves += moves;
     }
     if (changed && level + 1 < cfg.max_levels) {  // :247
         DBuf<int32_t> zc(ctx, std::max<int64_t>(n, 1));
@@ -209,10 +212,14 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
             delete coarse;
             if (cfg.refine) {  // PLMR :258-263
                 t.start();
-                move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 1));
+                int64_t rp = 0, rmv = 0;
+                move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 1), &rp, &rmv);
                 const double rm = t.stop_ms();
-                if (auto *L = rep.level(level))
+                if (auto *L = rep.level(level)) {
                     L->refine_ms += rm;
+                    L->passes += rp;
+                    L->moves += rmv;
+                }
             }
         }
     }

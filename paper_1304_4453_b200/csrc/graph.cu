@@ -222,15 +222,17 @@ __global__ void k_tiers(int64_t n, const int64_t *off, uint8_t *tier, unsigned l
         atomicAdd(&counts[threadIdx.x], static_cast<unsigned long long>(sc[threadIdx.x]));
 }
 
-__global__ void k_collect_hubs(int64_t n, const uint8_t *tier, int32_t *hubs, int32_t *count) {
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
-         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t u = base + threadIdx.x;
-        const bool is = u < n && tier[u] == TIER_HUB;
-        const int32_t pos = warp_append(count, is);
-        if (is)
-            hubs[pos] = static_cast<int32_t>(u);
-    }
+struct TierFlag {
+    const uint8_t *tier;
+    int t;
+    __device__ int32_t operator()(int64_t u) const { return tier[u] == t ? 1 : 0; }
+};
+
+__global__ void k_tier_scatter(int64_t n, const uint8_t *tier, int t, const int32_t *rank, int32_t *out) {
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        if (tier[u] == t)
+            out[rank[u]] = static_cast<int32_t>(u);
 }
 
 struct HubCapGen {
@@ -285,29 +287,36 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
     int64_t s = 0;
-    for (int t = 0; t < NUM_TIERS; ++t)
+    for (int t = 0; t < NUM_TIERS; ++t) {
         g->tier_nodes[t] = static_cast<int64_t>(hc[t]);
-    for (int t = 0; t < NUM_LIST_TIERS; ++t) {
         g->tier_start[t] = s;
         s += g->tier_nodes[t];
     }
-    g->tier_start[NUM_LIST_TIERS] = s;
-    g->lists.alloc(ctx, std::max<int64_t>(s, 1));
+    g->tier_start[NUM_TIERS] = s;
+    g->tlist.alloc(ctx, std::max<int64_t>(s, 1));
+    {
+        // stable partition by tier: rank within tier = exclusive scan of flags
+        DBuf<int32_t> rank(ctx, n + 1);
+        for (int t = 0; t < NUM_TIERS; ++t) {
+            if (!g->tier_nodes[t])
+                continue;
+            exclusive_scan<int32_t>(ctx, n, TierFlag{g->tier.p, t}, rank.p, rank.p + n);
+            CD_LAUNCH(ctx, "bins", k_tier_scatter, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
+                      static_cast<const uint8_t *>(g->tier.p), t, static_cast<const int32_t *>(rank.p),
+                      g->tlist.p + g->tier_start[t]);
+        }
+    }
     // hubs
     g->n_hubs = g->tier_nodes[TIER_HUB];
     g->n_hub_chunks = 0;
     g->hub_slots = 0;
+    g->hubs = g->tlist.p + g->tier_start[TIER_HUB];
     if (g->n_hubs > 0) {
         const int64_t nh = g->n_hubs;
-        g->hubs.alloc(ctx, nh);
-        DBuf<int32_t> cnt(ctx, 1);
-        cnt.zero();
-        CD_LAUNCH(ctx, "bins", k_collect_hubs, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
-                  static_cast<const uint8_t *>(g->tier.p), g->hubs.p, cnt.p);
         g->hub_tab.alloc(ctx, nh + 1);
         DBuf<int64_t> chunk_pre(ctx, nh + 1);
-        exclusive_scan<int64_t>(ctx, nh, HubCapGen{g->hubs.p, g->off.p}, g->hub_tab.p, g->hub_tab.p + nh);
-        exclusive_scan<int64_t>(ctx, nh, HubChunkGen{g->hubs.p, g->off.p}, chunk_pre.p, chunk_pre.p + nh);
+        exclusive_scan<int64_t>(ctx, nh, HubCapGen{g->hubs, g->off.p}, g->hub_tab.p, g->hub_tab.p + nh);
+        exclusive_scan<int64_t>(ctx, nh, HubChunkGen{g->hubs, g->off.p}, chunk_pre.p, chunk_pre.p + nh);
         int64_t tot[2];
         CD_CUDA(cudaMemcpyAsync(&tot[0], g->hub_tab.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
         CD_CUDA(cudaMemcpyAsync(&tot[1], chunk_pre.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
@@ -318,7 +327,7 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
         g->chunk_hub.alloc(ctx, g->n_hub_chunks);
         g->chunk_part.alloc(ctx, g->n_hub_chunks);
         CD_LAUNCH(ctx, "bins", k_hub_chunks, grid_for(nh, 1, ctx->num_sms * 4), 128, 0, nh,
-                  static_cast<const int32_t *>(g->hubs.p), static_cast<const int64_t *>(g->off.p),
+                  static_cast<const int32_t *>(g->hubs), static_cast<const int64_t *>(g->off.p),
                   static_cast<const int64_t *>(g->hub_tab.p), static_cast<const int64_t *>(chunk_pre.p),
                   g->hub_mask.p, g->chunk_hub.p, g->chunk_part.p);
         g->hub_keys.alloc(ctx, g->hub_slots);

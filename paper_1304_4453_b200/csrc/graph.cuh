@@ -62,15 +62,16 @@ struct cd_graph {
     cdk::DBuf<float> w;
     cdk::DBuf<double> vol, loop;
 
-    // work decomposition
+    // work decomposition: every non-isolated node listed once, grouped by
+    // tier, ascending id within a tier (stable partition by scan)
     bool binned = false;
     cdk::DBuf<uint8_t> tier;
     int64_t tier_nodes[cdk::NUM_TIERS] = {0, 0, 0, 0, 0, 0};
-    int64_t tier_start[cdk::NUM_LIST_TIERS + 1] = {0, 0, 0, 0, 0, 0};  // list capacity offsets
-    cdk::DBuf<int32_t> lists;  // per-bucket worklists, sized sum of list-tier nodes
-    // hub tier: static chunk grid and hash regions
+    int64_t tier_start[cdk::NUM_TIERS + 1] = {0, 0, 0, 0, 0, 0, 0};
+    cdk::DBuf<int32_t> tlist;  // [tier_start[NUM_TIERS]]
+    // hub tier: static chunk grid and hash regions; hubs = tlist + tier_start[TIER_HUB]
     int64_t n_hubs = 0, n_hub_chunks = 0, hub_slots = 0;
-    cdk::DBuf<int32_t> hubs;        // [n_hubs] node ids
+    const int32_t *hubs = nullptr;  // [n_hubs] node ids (view into tlist)
     cdk::DBuf<int64_t> hub_tab;     // [n_hubs] table offset
     cdk::DBuf<int32_t> hub_mask;    // [n_hubs] capacity - 1
     cdk::DBuf<int32_t> chunk_hub;   // [n_hub_chunks]

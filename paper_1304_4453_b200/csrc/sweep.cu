@@ -11,6 +11,10 @@
 // multi-block insert into a global hash + per-hub finalize.  Every tally sum
 // is exact (int counts or fp64 of fp32 weights), so the decision does not
 // depend on the summation order and equals the sequential reference's.
+//
+// Selection (bucket of this sub-sweep, PLP active flag) is done inline: each
+// warp loads 32 candidates of its tier's static list, ballots the selected
+// ones and processes them -- no worklist kernel, no global atomics.
 #include "sweep.cuh"
 
 #include <cmath>
@@ -22,18 +26,17 @@ struct SweepParams {
     const int32_t *col;
     const float *w;
     const double *vol;
-    const uint8_t *tier;
     const int32_t *z;
     uint8_t *active;
     const double *vols;
     const int32_t *csize;
     double gamma, inv_total, inv_sq2;
     int guard;
-    uint64_t key;
+    const unsigned long long *keyp;  // bucket key of the current pass (device)
     int bucket, buckets;
-    const int32_t *lists;
-    int64_t list_start[NUM_LIST_TIERS];
-    int32_t *cnt;  // [0..4] tier counts, [5] moves
+    const int32_t *tlist;
+    int64_t tstart[NUM_TIERS + 1];
+    int32_t *mv_count;  // moves of this bucket
     int32_t *mv_node, *mv_label;
     int32_t *dense_best;
     double *dense_gain;
@@ -85,7 +88,8 @@ __device__ __forceinline__ double sum_xor(double v) {
     return v;
 }
 
-// Group aggregation: returns leader flag and the group's count / weight sum.
+// Group aggregation: returns leader flag and the group's count / weight sum
+// (weights summed in lane order by the leader).
 template <bool W>
 __device__ __forceinline__ bool aggregate(int32_t key, double w, bool valid, uint32_t gmask, double *scratch,
                                           double &val) {
@@ -121,6 +125,16 @@ __device__ __forceinline__ void tinsert(int32_t *keys, V *vals, uint32_t mask, i
     }
 }
 
+__device__ __forceinline__ bool selected(const SweepParams &P, unsigned long long key, int32_t u) {
+    if (P.buckets > 1 && bucket_of(key, u, P.buckets) != P.bucket)
+        return false;
+    return !P.active || P.active[u];
+}
+
+__device__ __forceinline__ unsigned long long load_key(const SweepParams &P) {
+    return P.buckets > 1 ? *P.keyp : 0ULL;
+}
+
 // Applies one decision.  Must be reached by all lanes of the warp (the move
 // append is warp-aggregated); only lanes with `act` carry a decision.
 template <int MODE>
@@ -144,7 +158,7 @@ __device__ __forceinline__ void decide(const SweepParams &P, bool act, int32_t u
         }
         return;
     }
-    const int32_t pos = warp_append(&P.cnt[5], moved);
+    const int32_t pos = warp_append(P.mv_count, moved);
     if (moved) {
         P.mv_node[pos] = u;
         P.mv_label[pos] = best;
@@ -174,61 +188,73 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int sub = lane / G, k = lane % G;
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
-    const int32_t *list = P.lists + P.list_start[tier];
-    const int64_t count = P.cnt[tier];
+    const int32_t *list = P.tlist + P.tstart[tier];
+    const int64_t count = P.tstart[tier + 1] - P.tstart[tier];
+    const unsigned long long bkey = load_key(P);
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
-    for (int64_t base = gw * NPW; base < count; base += nw * NPW) {
-        const int64_t idx = base + sub;
-        const bool has = idx < count;
-        const int32_t u = has ? list[idx] : 0;
-        int64_t s = 0, d = 0;
-        if (has) {
-            s = P.off[u];
-            d = P.off[u + 1] - s;
-        }
-        bool valid = has && k < d;
-        const int32_t v = valid ? P.col[s + k] : 0;
-        const double wt = (W && valid) ? static_cast<double>(P.w[s + k]) : 1.0;
-        if (MODE == MODE_PLM)
-            valid = valid && v != u;
-        const int32_t key = valid ? P.z[v] : 0;
-        double agg;
-        const bool leader = aggregate<W>(key, wt, valid, gmask, scratch[wid], agg);
-        const int32_t cur = has ? P.z[u] : 0;
-        double cv;
-        int32_t ck;
-        if (MODE == MODE_PLP) {
-            cv = leader ? agg : -1.0;
-            ck = leader ? key : INT32_MAX;
-        } else {
-            const double wc = sum_xor<G>((valid && key == cur) ? wt : 0.0);
-            if (leader && key != cur) {
-                const double vol_u = P.vol[u];
-                const double vol_c = __dsub_rn(P.vols[cur], vol_u);
-                cv = plm_delta(agg, wc, vol_c, P.vols[key], vol_u, P);
-                ck = key;
-            } else {
-                cv = -INFINITY;
-                ck = INT32_MAX;
+    for (int64_t base = gw * 32; base < count; base += nw * 32) {
+        const bool in = base + lane < count;
+        const int32_t cand = in ? list[base + lane] : 0;
+        uint32_t selmask = __ballot_sync(0xffffffffu, in && selected(P, bkey, cand));
+        while (selmask) {
+            const uint32_t pos = __fns(selmask, 0, sub + 1);
+            const bool has = pos < 32;
+            const int32_t u = __shfl_sync(0xffffffffu, cand, has ? pos : 0);
+#pragma unroll
+            for (int q = 0; q < NPW; ++q)
+                selmask &= selmask - 1;
+            int64_t s = 0, d = 0;
+            if (has) {
+                s = P.off[u];
+                d = P.off[u + 1] - s;
             }
-        }
-        argmax_xor<G>(cv, ck);
-        const bool act = has && k == 0;
-        decide<MODE>(P, act, u, cur, ck, cv);
-        if (act) {
-            ++st_n;
-            st_e += static_cast<unsigned long long>(d);
+            bool valid = has && k < d;
+            const int32_t v = valid ? P.col[s + k] : 0;
+            const double wt = (W && valid) ? static_cast<double>(P.w[s + k]) : 1.0;
+            if (MODE == MODE_PLM)
+                valid = valid && v != u;
+            const int32_t key = valid ? P.z[v] : 0;
+            double agg;
+            const bool leader = aggregate<W>(key, wt, valid, gmask, scratch[wid], agg);
+            const int32_t cur = has ? P.z[u] : 0;
+            double cv;
+            int32_t ck;
+            if (MODE == MODE_PLP) {
+                cv = leader ? agg : -1.0;
+                ck = leader ? key : INT32_MAX;
+            } else {
+                const double wc = sum_xor<G>((valid && key == cur) ? wt : 0.0);
+                if (leader && key != cur) {
+                    const double vol_u = P.vol[u];
+                    const double vol_c = __dsub_rn(P.vols[cur], vol_u);
+                    cv = plm_delta(agg, wc, vol_c, P.vols[key], vol_u, P);
+                    ck = key;
+                } else {
+                    cv = -INFINITY;
+                    ck = INT32_MAX;
+                }
+            }
+            argmax_xor<G>(cv, ck);
+            const bool act = has && k == 0;
+            decide<MODE>(P, act, u, cur, ck, cv);
+            if (act) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(d);
+            }
         }
     }
     flush_stats(P, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
-// tier WARP: one warp per node, per-warp smem hash (cap <= 512)
+// tier WARP: one warp per node (deg <= 256), per-warp smem hash (cap <= 512).
+// All of a row's neighbour ids, then all labels, are loaded up front (8 per
+// lane) so a node costs two rounds of memory latency, not deg/32.
 // ---------------------------------------------------------------------------
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
+constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
 template <int MODE, bool W>
 __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
@@ -239,74 +265,93 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     int32_t *keys = skeys[wid];
     V *vals = svals[wid];
-    const int32_t *list = P.lists + P.list_start[TIER_WARP];
-    const int64_t count = P.cnt[TIER_WARP];
+    const int32_t *list = P.tlist + P.tstart[TIER_WARP];
+    const int64_t count = P.tstart[TIER_WARP + 1] - P.tstart[TIER_WARP];
+    const unsigned long long bkey = load_key(P);
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
-    for (int64_t i = gw; i < count; i += nw) {
-        const int32_t u = list[i];
-        const int64_t s = P.off[u], e = P.off[u + 1];
-        uint32_t cap = 64;
-        while (cap < 2 * (e - s))
-            cap <<= 1;
-        for (uint32_t t = lane; t < cap; t += 32) {
-            keys[t] = EMPTY_KEY;
-            vals[t] = V(0);
-        }
-        __syncwarp();
-        const int32_t cur = P.z[u];
-        double wc = 0.0;
-        for (int64_t f = s; f < e; f += 32) {
-            bool valid = f + lane < e;
-            const int32_t v = valid ? P.col[f + lane] : 0;
-            const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+    for (int64_t base = gw * 32; base < count; base += nw * 32) {
+        const bool in = base + lane < count;
+        const int32_t cand = in ? list[base + lane] : 0;
+        uint32_t selmask = __ballot_sync(0xffffffffu, in && selected(P, bkey, cand));
+        while (selmask) {
+            const int32_t u = __shfl_sync(0xffffffffu, cand, __ffs(selmask) - 1);
+            selmask &= selmask - 1;
+            const int64_t s = P.off[u], e = P.off[u + 1];
+            uint32_t cap = 64;
+            while (cap < 2 * (e - s))
+                cap <<= 1;
+            for (uint32_t t = lane; t < cap; t += 32) {
+                keys[t] = EMPTY_KEY;
+                vals[t] = V(0);
+            }
+            const int32_t cur = P.z[u];
+            int32_t vv[SW_WARP_ITEMS], kk[SW_WARP_ITEMS];
+            float ww[SW_WARP_ITEMS];
+#pragma unroll
+            for (int c = 0; c < SW_WARP_ITEMS; ++c) {
+                const int64_t f = s + c * 32 + lane;
+                vv[c] = f < e ? P.col[f] : -1;
+                ww[c] = (W && f < e) ? P.w[f] : 1.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < SW_WARP_ITEMS; ++c)
+                kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+            __syncwarp();
+            double wc = 0.0;
+#pragma unroll
+            for (int c = 0; c < SW_WARP_ITEMS; ++c) {
+                if (s + c * 32 >= e)
+                    break;
+                bool valid = vv[c] >= 0;
+                if (MODE == MODE_PLM)
+                    valid = valid && vv[c] != u;
+                const double wt = static_cast<double>(ww[c]);
+                if (MODE == MODE_PLM && valid && kk[c] == cur)
+                    wc += wt;
+                double agg;
+                if (aggregate<W>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                    tinsert<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg));
+            }
+            __syncwarp();
             if (MODE == MODE_PLM)
-                valid = valid && v != u;
-            const int32_t key = valid ? P.z[v] : 0;
-            if (MODE == MODE_PLM && valid && key == cur)
-                wc += wt;
-            double agg;
-            if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
-                tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
-        }
-        __syncwarp();
-        if (MODE == MODE_PLM)
-            wc = warp_sum(wc);
-        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
-        int32_t ck = INT32_MAX;
-        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-        for (uint32_t t = lane; t < cap; t += 32) {
-            const int32_t key = keys[t];
-            if (key == EMPTY_KEY)
-                continue;
-            double val;
-            if (MODE == MODE_PLP) {
-                val = static_cast<double>(vals[t]);
-            } else {
-                if (key == cur)
+                wc = warp_sum(wc);
+            double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+            int32_t ck = INT32_MAX;
+            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+            for (uint32_t t = lane; t < cap; t += 32) {
+                const int32_t key = keys[t];
+                if (key == EMPTY_KEY)
                     continue;
-                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+                double val;
+                if (MODE == MODE_PLP) {
+                    val = static_cast<double>(vals[t]);
+                } else {
+                    if (key == cur)
+                        continue;
+                    val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+                }
+                if (better(val, key, cv, ck)) {
+                    cv = val;
+                    ck = key;
+                }
             }
-            if (better(val, key, cv, ck)) {
-                cv = val;
-                ck = key;
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(e - s);
             }
+            __syncwarp();
         }
-        argmax_xor<32>(cv, ck);
-        decide<MODE>(P, lane == 0, u, cur, ck, cv);
-        if (lane == 0) {
-            ++st_n;
-            st_e += static_cast<unsigned long long>(e - s);
-        }
-        __syncwarp();
     }
     flush_stats(P, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
-// tier BLOCK: one block per node, block smem hash (cap <= 8192)
+// tier BLOCK: one block per node (deg <= 4096), block smem hash (cap <= 8192)
 // ---------------------------------------------------------------------------
 template <int MODE, bool W>
 __global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
@@ -319,84 +364,90 @@ __global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
     __shared__ int32_t red_k[8];
     __shared__ double red_wc[8];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int32_t *list = P.lists + P.list_start[TIER_BLOCK];
-    const int64_t count = P.cnt[TIER_BLOCK];
+    const int32_t *list = P.tlist + P.tstart[TIER_BLOCK];
+    const int64_t count = P.tstart[TIER_BLOCK + 1] - P.tstart[TIER_BLOCK];
+    const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
+    // one candidate per block iteration; unselected candidates cost one load
     for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
         const int32_t u = list[i];
-        const int64_t s = P.off[u], e = P.off[u + 1];
-        uint32_t cap = 64;
-        while (cap < 2 * (e - s))
-            cap <<= 1;
-        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
-            keys[t] = EMPTY_KEY;
-            vals[t] = V(0);
-        }
-        __syncthreads();
-        const int32_t cur = P.z[u];
-        double wc = 0.0;
-        for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
-            bool valid = f + lane < e;
-            const int32_t v = valid ? P.col[f + lane] : 0;
-            const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
-            if (MODE == MODE_PLM)
-                valid = valid && v != u;
-            const int32_t key = valid ? P.z[v] : 0;
-            if (MODE == MODE_PLM && valid && key == cur)
-                wc += wt;
-            double agg;
-            if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
-                tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
-        }
-        if (MODE == MODE_PLM) {
-            wc = warp_sum(wc);
-            if (lane == 0)
-                red_wc[wid] = wc;
-        }
-        __syncthreads();
-        if (MODE == MODE_PLM) {
-            wc = 0.0;
-            for (int q = 0; q < 8; ++q)
-                wc += red_wc[q];
-        }
-        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
-        int32_t ck = INT32_MAX;
-        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
-            const int32_t key = keys[t];
-            if (key == EMPTY_KEY)
-                continue;
-            double val;
-            if (MODE == MODE_PLP) {
-                val = static_cast<double>(vals[t]);
-            } else {
-                if (key == cur)
+        if (!selected(P, bkey, u))
+            continue;
+        {
+            const int64_t s = P.off[u], e = P.off[u + 1];
+            uint32_t cap = 64;
+            while (cap < 2 * (e - s))
+                cap <<= 1;
+            for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+                keys[t] = EMPTY_KEY;
+                vals[t] = V(0);
+            }
+            __syncthreads();
+            const int32_t cur = P.z[u];
+            double wc = 0.0;
+            for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
+                bool valid = f + lane < e;
+                const int32_t v = valid ? P.col[f + lane] : 0;
+                const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+                if (MODE == MODE_PLM)
+                    valid = valid && v != u;
+                const int32_t key = valid ? P.z[v] : 0;
+                if (MODE == MODE_PLM && valid && key == cur)
+                    wc += wt;
+                double agg;
+                if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
+                    tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
+            }
+            if (MODE == MODE_PLM) {
+                wc = warp_sum(wc);
+                if (lane == 0)
+                    red_wc[wid] = wc;
+            }
+            __syncthreads();
+            if (MODE == MODE_PLM) {
+                wc = 0.0;
+                for (int q = 0; q < 8; ++q)
+                    wc += red_wc[q];
+            }
+            double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+            int32_t ck = INT32_MAX;
+            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+            for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+                const int32_t key = keys[t];
+                if (key == EMPTY_KEY)
                     continue;
-                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+                double val;
+                if (MODE == MODE_PLP) {
+                    val = static_cast<double>(vals[t]);
+                } else {
+                    if (key == cur)
+                        continue;
+                    val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+                }
+                if (better(val, key, cv, ck)) {
+                    cv = val;
+                    ck = key;
+                }
             }
-            if (better(val, key, cv, ck)) {
-                cv = val;
-                ck = key;
-            }
-        }
-        argmax_xor<32>(cv, ck);
-        if (lane == 0) {
-            red_v[wid] = cv;
-            red_k[wid] = ck;
-        }
-        __syncthreads();
-        if (wid == 0) {
-            cv = lane < 8 ? red_v[lane] : -INFINITY;
-            ck = lane < 8 ? red_k[lane] : INT32_MAX;
             argmax_xor<32>(cv, ck);
-            decide<MODE>(P, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
-                ++st_n;
-                st_e += static_cast<unsigned long long>(e - s);
+                red_v[wid] = cv;
+                red_k[wid] = ck;
             }
+            __syncthreads();
+            if (wid == 0) {
+                cv = lane < 8 ? red_v[lane] : -INFINITY;
+                ck = lane < 8 ? red_k[lane] : INT32_MAX;
+                argmax_xor<32>(cv, ck);
+                decide<MODE>(P, lane == 0, u, cur, ck, cv);
+                if (lane == 0) {
+                    ++st_n;
+                    st_e += static_cast<unsigned long long>(e - s);
+                }
+            }
+            __syncthreads();
         }
-        __syncthreads();
     }
     if (wid == 0)
         flush_stats(P, st_n, st_e);
@@ -405,14 +456,6 @@ __global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
 // ---------------------------------------------------------------------------
 // tier HUB: chunk blocks insert into a per-hub global hash, then finalize
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool hub_selected(const SweepParams &P, int32_t u) {
-    if (P.buckets > 1 && bucket_of(P.key, u, P.buckets) != P.bucket)
-        return false;
-    if (P.active && !P.active[u])
-        return false;
-    return true;
-}
-
 template <int MODE, bool W>
 __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
     __shared__ double scratch[8][32];
@@ -420,7 +463,7 @@ __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int32_t h = P.chunk_hub[blockIdx.x];
     const int32_t u = P.hubs[h];
-    if (!hub_selected(P, u))
+    if (!selected(P, load_key(P), u))
         return;
     const int64_t s0 = P.off[u], e0 = P.off[u + 1];
     const int64_t s = s0 + static_cast<int64_t>(P.chunk_part[blockIdx.x]) * HUB_CHUNK;
@@ -465,9 +508,10 @@ __global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
     __shared__ double red_v[16];
     __shared__ int32_t red_k[16];
     const int lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+    const unsigned long long bkey = load_key(P);
     for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
         const int32_t u = P.hubs[h];
-        if (!hub_selected(P, u))
+        if (!selected(P, bkey, u))
             continue;
         int32_t *keys = P.hub_keys + P.hub_tab[h];
         double *vals = P.hub_vals + P.hub_tab[h];
@@ -520,39 +564,12 @@ __global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// selection and apply
+// apply: the bucket's moves become visible to the next sub-sweep
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_select(int64_t n, SweepParams P) {
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < n;
-         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t u = base + threadIdx.x;
-        int t = TIER_NONE;
-        if (u < n) {
-            t = P.tier[u];
-            if (t < NUM_LIST_TIERS) {
-                if (P.active && !P.active[u])
-                    t = TIER_NONE;
-                else if (P.buckets > 1 && bucket_of(P.key, static_cast<int32_t>(u), P.buckets) != P.bucket)
-                    t = TIER_NONE;
-            } else {
-                t = TIER_NONE;
-            }
-        }
-        if (__ballot_sync(0xffffffffu, t != TIER_NONE) == 0)
-            continue;
-#pragma unroll
-        for (int q = 0; q < NUM_LIST_TIERS; ++q) {
-            const int32_t pos = warp_append(&P.cnt[q], t == q);
-            if (t == q)
-                const_cast<int32_t *>(P.lists)[P.list_start[q] + pos] = static_cast<int32_t>(u);
-        }
-    }
-}
-
 __global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const int32_t *mv_label,
-                                                   const int32_t *cnt, int32_t *z, uint8_t *active,
+                                                   const int32_t *mv_count, int32_t *z, uint8_t *active,
                                                    const int64_t *off, const int32_t *col, long long *total) {
-    const int64_t count = cnt[5];
+    const int64_t count = *mv_count;
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -562,16 +579,16 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const
         const int32_t u = mv_node[i];
         if (lane == 0)
             z[u] = mv_label[i];
-        if (active)
+        if (active)  // H/plp.hpp:127-130: a changed node activates its neighbours
             for (int64_t e = off[u] + lane; e < off[u + 1]; e += 32)
                 active[col[e]] = 1;
     }
 }
 
 __global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const int32_t *mv_label,
-                                                   const int32_t *cnt, int32_t *z, double *vols, int32_t *csize,
+                                                   const int32_t *mv_count, int32_t *z, double *vols, int32_t *csize,
                                                    const double *vol, long long *total) {
-    const int64_t count = cnt[5];
+    const int64_t count = *mv_count;
     if (blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
@@ -579,7 +596,7 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const
         const int32_t u = mv_node[i], d = mv_label[i];
         const int32_t c = z[u];
         z[u] = d;
-        const double vu = vol[u];
+        const double vu = vol[u];  // H/louvain.hpp:121-125
         atomicAdd(&vols[c], -vu);
         atomicAdd(&vols[d], vu);
         if (csize) {
@@ -592,29 +609,91 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-void sweep_init(cd_ctx *ctx, cd_graph *g, SweepState &st) {
+static void ensure_side_streams(cd_ctx *ctx) {
+    if (ctx->fork_ev)
+        return;
+    for (int i = 0; i < cd_ctx::NSIDE; ++i) {
+        CD_CUDA(cudaStreamCreateWithFlags(&ctx->side[i], cudaStreamNonBlocking));
+        CD_CUDA(cudaEventCreateWithFlags(&ctx->join_ev[i], cudaEventDisableTiming));
+    }
+    CD_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+}
+
+Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g), c_(c) {
     graph_ensure_bins(ctx, g);
-    st.ctx = ctx;
-    st.g = g;
-    st.cnt.alloc(ctx, 8);
-    st.mv_node.alloc(ctx, std::max<int64_t>(g->n, 1));
-    st.mv_label.alloc(ctx, std::max<int64_t>(g->n, 1));
-    st.total.alloc(ctx, 1);
-    st.total.zero();
+    cnt_.alloc(ctx, 8);
+    mv_node_.alloc(ctx, std::max<int64_t>(g->n, 1));
+    mv_label_.alloc(ctx, std::max<int64_t>(g->n, 1));
+    total_.alloc(ctx, 1);
+    total_.zero();
+    key_.alloc(ctx, 1);
+    key_.zero();
+    if (c_.buckets < 1)
+        c_.buckets = 1;
+    if (c_.buckets > 8)
+        fail(CD_EINVAL, "at most 8 buckets per pass");
+}
+
+Sweeper::~Sweeper() {
+    if (exec_)
+        cudaGraphExecDestroy(exec_);
+    if (graph_)
+        cudaGraphDestroy(graph_);
 }
 
 template <int MODE, bool W>
-static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, const char *fam) {
+static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool capture, int &branch) {
     const int sms = ctx->num_sms;
-    if (g->tier_nodes[TIER_G8])
-        CD_LAUNCH(ctx, fam, (k_sweep_direct<8, MODE, W>), sms * 8, 256, 0, P, int(TIER_G8));
-    if (g->tier_nodes[TIER_G16])
-        CD_LAUNCH(ctx, fam, (k_sweep_direct<16, MODE, W>), sms * 8, 256, 0, P, int(TIER_G16));
-    if (g->tier_nodes[TIER_G32])
-        CD_LAUNCH(ctx, fam, (k_sweep_direct<32, MODE, W>), sms * 8, 256, 0, P, int(TIER_G32));
-    if (g->tier_nodes[TIER_WARP])
-        CD_LAUNCH(ctx, fam, (k_sweep_warp<MODE, W>), sms * 8, 128, 0, P);
+    // per-tier profiler families; cd_ctx_kernel_stats aggregates "plp_sweep.*"
+    // and "plm_move.*" into the family the roofline reports
+    static const char *names[2][6] = {
+        {"plp_sweep.g8", "plp_sweep.g16", "plp_sweep.g32", "plp_sweep.warp", "plp_sweep.block", "plp_sweep.hub"},
+        {"plm_move.g8", "plm_move.g16", "plm_move.g32", "plm_move.warp", "plm_move.block", "plm_move.hub"}};
+    const char *fam = names[MODE][0];
+    auto go = [&](auto launch) {
+        if (capture) {
+            cudaStream_t s = ctx->side[branch];
+            CD_CUDA(cudaStreamWaitEvent(s, ctx->fork_ev, 0));
+            launch(s);
+            CD_CUDA(cudaEventRecord(ctx->join_ev[branch], s));
+            ++branch;
+        } else {
+            launch(static_cast<cudaStream_t>(nullptr));
+        }
+    };
+    // grid sizes: enough warps to cover the tier list once, capped at a full wave
+    auto warps_grid = [&](int64_t nodes, int threads) {
+        const int64_t warps = (nodes + 31) / 32;
+        return grid_for(warps, threads / 32, sms * (2048 / threads));
+    };
+#define CD_TIER_LAUNCH(KERNEL, GRID, BLOCK, SMEM, ...)                                               \
+    go([&](cudaStream_t s) {                                                                         \
+        if (s)                                                                                       \
+            CD_LAUNCH_S(ctx, s, fam, KERNEL, GRID, BLOCK, SMEM, __VA_ARGS__);                        \
+        else                                                                                         \
+            CD_LAUNCH(ctx, fam, KERNEL, GRID, BLOCK, SMEM, __VA_ARGS__);                             \
+    })
+    if (g->tier_nodes[TIER_G8]) {
+        fam = names[MODE][TIER_G8];
+        CD_TIER_LAUNCH((k_sweep_direct<8, MODE, W>), warps_grid(g->tier_nodes[TIER_G8], 256), 256, 0, P,
+                       int(TIER_G8));
+    }
+    if (g->tier_nodes[TIER_G16]) {
+        fam = names[MODE][TIER_G16];
+        CD_TIER_LAUNCH((k_sweep_direct<16, MODE, W>), warps_grid(g->tier_nodes[TIER_G16], 256), 256, 0, P,
+                       int(TIER_G16));
+    }
+    if (g->tier_nodes[TIER_G32]) {
+        fam = names[MODE][TIER_G32];
+        CD_TIER_LAUNCH((k_sweep_direct<32, MODE, W>), warps_grid(g->tier_nodes[TIER_G32], 256), 256, 0, P,
+                       int(TIER_G32));
+    }
+    if (g->tier_nodes[TIER_WARP]) {
+        fam = names[MODE][TIER_WARP];
+        CD_TIER_LAUNCH((k_sweep_warp<MODE, W>), warps_grid(g->tier_nodes[TIER_WARP], 128), 128, 0, P);
+    }
     if (g->tier_nodes[TIER_BLOCK]) {
+        fam = names[MODE][TIER_BLOCK];
         using V = typename std::conditional<W, double, unsigned int>::type;
         const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
         static bool attr_set = false;
@@ -623,46 +702,52 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, const c
                                          static_cast<int>(smem)));
             attr_set = true;
         }
-        const int64_t nb = std::min<int64_t>(g->tier_nodes[TIER_BLOCK], sms * 2);
-        CD_LAUNCH(ctx, fam, (k_sweep_block<MODE, W>), static_cast<int>(nb), 256, smem, P);
+        const int nb = grid_for(g->tier_nodes[TIER_BLOCK], 1, sms * (W ? 2 : 3));
+        CD_TIER_LAUNCH((k_sweep_block<MODE, W>), nb, 256, smem, P);
     }
     if (g->n_hubs) {
-        CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
-        CD_LAUNCH(ctx, fam, (k_sweep_hub_final<MODE>), static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 4)), 512, 0,
-                  P);
+        fam = names[MODE][TIER_HUB];
+        const int nf = static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 4));
+        go([&](cudaStream_t s) {
+            if (s) {
+                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
+                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
+            } else {
+                CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
+                CD_LAUNCH(ctx, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
+            }
+        });
     }
+#undef CD_TIER_LAUNCH
 }
 
-void sweep_bucket(SweepState &st, const SweepCall &c) {
-    cd_ctx *ctx = st.ctx;
-    cd_graph *g = st.g;
+void Sweeper::enqueue(bool capture) {
+    cd_ctx *ctx = ctx_;
+    cd_graph *g = g_;
     SweepParams P;
     P.off = g->off.p;
     P.col = g->col.p;
     P.w = g->weighted ? g->w.p : nullptr;
     P.vol = g->vol.p;
-    P.tier = g->tier.p;
-    P.z = c.z;
-    P.active = c.active;
-    P.vols = c.vols;
-    P.csize = c.csize;
-    P.gamma = c.gamma;
+    P.z = c_.z;
+    P.active = c_.active;
+    P.vols = c_.vols;
+    P.csize = c_.csize;
+    P.gamma = c_.gamma;
     P.inv_total = g->total > 0 ? 1.0 / g->total : 0.0;
     P.inv_sq2 = g->total > 0 ? 1.0 / (2.0 * g->total * g->total) : 0.0;
-    P.guard = c.guard;
-    P.key = c.key;
-    P.bucket = c.bucket;
-    P.buckets = c.buckets;
-    P.lists = g->lists.p;
-    for (int t = 0; t < NUM_LIST_TIERS; ++t)
-        P.list_start[t] = g->tier_start[t];
-    P.cnt = st.cnt.p;
-    P.mv_node = st.mv_node.p;
-    P.mv_label = st.mv_label.p;
-    P.dense_best = c.dense_best;
-    P.dense_gain = c.dense_gain;
-    P.stats = ctx->dstats + (c.mode == MODE_PLP ? 0 : 3);
-    P.hubs = g->hubs.p;
+    P.guard = c_.guard;
+    P.keyp = key_.p;
+    P.buckets = c_.buckets;
+    P.tlist = g->tlist.p;
+    for (int t = 0; t <= NUM_TIERS; ++t)
+        P.tstart[t] = g->tier_start[t];
+    P.mv_node = mv_node_.p;
+    P.mv_label = mv_label_.p;
+    P.dense_best = c_.dense_best;
+    P.dense_gain = c_.dense_gain;
+    P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : 3);
+    P.hubs = g->hubs;
     P.hub_tab = g->hub_tab.p;
     P.hub_mask = g->hub_mask.p;
     P.chunk_hub = g->chunk_hub.p;
@@ -671,43 +756,80 @@ void sweep_bucket(SweepState &st, const SweepCall &c) {
     P.hub_vals = g->hub_vals.p;
     P.hub_aux = g->hub_aux.p;
     P.n_hubs = g->n_hubs;
-
     const int sms = ctx->num_sms;
-    const bool plp = c.mode == MODE_PLP;
-    const char *fam = plp ? "plp_sweep" : "plm_move";
-    CD_CUDA(cudaMemsetAsync(st.cnt.p, 0, 8 * sizeof(int32_t), ctx->stream));
-    if (g->n > 0)
-        CD_LAUNCH(ctx, plp ? "plp_select" : "plm_select", k_select, grid_for(g->n, 256, sms * 8), 256, 0, g->n, P);
-    if (plp) {
-        if (g->weighted)
-            launch_tiers<MODE_PLP, true>(ctx, g, P, fam);
+    const bool plp = c_.mode == MODE_PLP;
+    if (!c_.dense_best)
+        CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
+    for (int b = 0; b < c_.buckets; ++b) {
+        P.bucket = b;
+        P.mv_count = cnt_.p + b;
+        int branch = 0;
+        if (capture)
+            CD_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
+        if (plp) {
+            if (g->weighted)
+                launch_tiers<MODE_PLP, true>(ctx, g, P, capture, branch);
+            else
+                launch_tiers<MODE_PLP, false>(ctx, g, P, capture, branch);
+        } else {
+            if (g->weighted)
+                launch_tiers<MODE_PLM, true>(ctx, g, P, capture, branch);
+            else
+                launch_tiers<MODE_PLM, false>(ctx, g, P, capture, branch);
+        }
+        for (int i = 0; i < branch; ++i)
+            CD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[i], 0));
+        if (c_.dense_best)
+            continue;
+        const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, sms * 4));
+        if (plp)
+            CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0,
+                      static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
+                      static_cast<const int32_t *>(cnt_.p + b), c_.z, c_.active,
+                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), total_.p);
         else
-            launch_tiers<MODE_PLP, false>(ctx, g, P, fam);
-    } else {
-        if (g->weighted)
-            launch_tiers<MODE_PLM, true>(ctx, g, P, fam);
-        else
-            launch_tiers<MODE_PLM, false>(ctx, g, P, fam);
+            CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0,
+                      static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
+                      static_cast<const int32_t *>(cnt_.p + b), c_.z, c_.vols, c_.csize,
+                      static_cast<const double *>(g->vol.p), total_.p);
     }
-    if (c.dense_best)
-        return;
-    if (plp)
-        CD_LAUNCH(ctx, "plp_apply", k_apply_plp, sms * 4, 256, 0, static_cast<const int32_t *>(st.mv_node.p),
-                  static_cast<const int32_t *>(st.mv_label.p), static_cast<const int32_t *>(st.cnt.p), c.z, c.active,
-                  static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), st.total.p);
-    else
-        CD_LAUNCH(ctx, "plm_apply", k_apply_plm, sms * 4, 256, 0, static_cast<const int32_t *>(st.mv_node.p),
-                  static_cast<const int32_t *>(st.mv_label.p), static_cast<const int32_t *>(st.cnt.p), c.z, c.vols,
-                  c.csize, static_cast<const double *>(g->vol.p), st.total.p);
 }
 
-int64_t sweep_read_total(SweepState &st) {
+void Sweeper::pass(uint64_t key) {
+    unsigned long long k = key;
+    CD_CUDA(cudaMemcpyAsync(key_.p, &k, sizeof(k), cudaMemcpyHostToDevice, ctx_->stream));
+    if (ctx_->profiling || !ctx_->use_graphs) {
+        enqueue(false);
+        return;
+    }
+    if (!exec_) {
+        ensure_side_streams(ctx_);
+        const int64_t l0 = ctx_->launches;
+        CD_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
+        try {
+            enqueue(true);
+        } catch (...) {
+            cudaGraph_t gtmp = nullptr;
+            cudaStreamEndCapture(ctx_->stream, &gtmp);
+            if (gtmp)
+                cudaGraphDestroy(gtmp);
+            throw;
+        }
+        CD_CUDA(cudaStreamEndCapture(ctx_->stream, &graph_));
+        CD_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
+        kernels_per_pass_ = ctx_->launches - l0;
+        ctx_->launches = l0;
+    }
+    CD_CUDA(cudaGraphLaunch(exec_, ctx_->stream));
+    ctx_->launches += kernels_per_pass_;
+}
+
+int64_t Sweeper::take_moves() {
     long long h = 0;
-    CD_CUDA(cudaMemcpyAsync(&h, st.total.p, sizeof(h), cudaMemcpyDeviceToHost, st.ctx->stream));
-    CD_CUDA(cudaStreamSynchronize(st.ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&h, total_.p, sizeof(h), cudaMemcpyDeviceToHost, ctx_->stream));
+    CD_CUDA(cudaMemsetAsync(total_.p, 0, sizeof(long long), ctx_->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx_->stream));
     return h;
 }
-
-void sweep_reset_total(SweepState &st) { st.total.zero(); }
 
 }  // namespace cdk

@@ -8,21 +8,7 @@ namespace cdk {
 
 enum SweepMode : int { MODE_PLP = 0, MODE_PLM = 1 };
 
-struct SweepState {
-    cd_ctx *ctx = nullptr;
-    cd_graph *g = nullptr;
-    DBuf<int32_t> cnt;         // [8]: per-tier list counts [0..4], [5] moves
-    DBuf<int32_t> mv_node;     // [n]
-    DBuf<int32_t> mv_label;    // [n]
-    DBuf<long long> total;     // [1] moves accumulated since last reset
-};
-
-void sweep_init(cd_ctx *ctx, cd_graph *g, SweepState &st);
-
-// One bucket sub-sweep: every selected node (tier list, bucket, active) is
-// evaluated against the frozen labels z; the decisions are then applied to z
-// (PLP: and neighbours activated; PLM: vols / csize moved).  With dense_best
-// set, decisions are written densely instead and nothing is applied.
+// Fixed for the lifetime of a Sweeper (one PLP run / one move phase).
 struct SweepCall {
     int mode = MODE_PLP;
     int32_t *z = nullptr;
@@ -31,15 +17,38 @@ struct SweepCall {
     int32_t *csize = nullptr;    // PLM community sizes (singleton guard; nullable)
     double gamma = 1.0;
     int guard = 0;
-    uint64_t key = 0;
-    int bucket = 0, buckets = 1;
-    int32_t *dense_best = nullptr;
+    int buckets = 1;
+    int32_t *dense_best = nullptr;  // evaluation only: write decisions densely, apply nothing
     double *dense_gain = nullptr;
 };
-void sweep_bucket(SweepState &st, const SweepCall &c);
 
-// host read of the accumulated move counter (syncs) and reset
-int64_t sweep_read_total(SweepState &st);
-void sweep_reset_total(SweepState &st);
+// One iteration / pass = `buckets` sub-sweeps.  Each sub-sweep evaluates the
+// selected nodes of every degree tier against the frozen labels (the tier
+// kernels run as parallel branches) and then applies its moves.  After the
+// first pass the launch sequence is replayed from a CUDA graph; the bucket key
+// lives in device memory so the graph is reusable.
+class Sweeper {
+  public:
+    Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c);
+    ~Sweeper();
+    Sweeper(const Sweeper &) = delete;
+    Sweeper &operator=(const Sweeper &) = delete;
+
+    void pass(uint64_t key);   // enqueue one full pass with this bucket key
+    int64_t take_moves();      // moves since the last call (syncs)
+
+  private:
+    void enqueue(bool capture);
+    cd_ctx *ctx_;
+    cd_graph *g_;
+    SweepCall c_;
+    DBuf<int32_t> cnt_;     // [8]: [b] moves of bucket b
+    DBuf<int32_t> mv_node_, mv_label_;
+    DBuf<long long> total_;
+    DBuf<unsigned long long> key_;
+    cudaGraph_t graph_ = nullptr;
+    cudaGraphExec_t exec_ = nullptr;
+    int64_t kernels_per_pass_ = 0;
+};
 
 }  // namespace cdk

@@ -1,0 +1,37 @@
+"""Single-workload driver for ncu captures (profiles/README.md).
+
+    python tools/prof_run.py [--workload c2_lfr_plm] [--runs 2]
+
+Generates the bench workload on cuda:0 and runs the detector `runs` times
+(the first is a warm-up).  Prints one line with the per-level report.
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+import paper_1304_4453_b200 as P  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--runs", type=int, default=2)
+    ap.add_argument("--no-graphs", action="store_true")
+    a = ap.parse_args()
+    wl = bench.WORKLOADS[a.workload]
+    ctx = P.Context(0)
+    g = bench.make_device_graph(P, ctx, wl)
+    for i in range(a.runs):
+        z, rep = bench.run_device(P, g, wl["algo"], None, report=True)
+        print(a.workload, "run", i, "m", g.edge_count(), "Q", round(rep.modularity, 6), "k", rep.community_count,
+              "ms", round(rep.total_ms, 3),
+              "levels", [(l["nodes"], l["passes"], round(l["move_ms"], 2), round(l["coarsen_ms"], 2))
+                         for l in rep.levels], "iters", len(rep.iterations), flush=True)
+
+
+if __name__ == "__main__":
+    main()
