@@ -12,9 +12,17 @@ OBJS = $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS = $(wildcard $(SRC_DIR)/*.cuh) include/commdet_cuda.h
 LIB = paper_1304_4453_b200/libcommdet_cuda.so
 
-all: lib oracle
+all: lib shim oracle
 
 lib: $(LIB)
+
+# reference-style C++ caller of the drop-in shim (include/commdet/gpu.hpp)
+SHIM = build/shim_kat
+shim: $(SHIM)
+$(SHIM): tests/cpp/shim_kat.cpp include/commdet/gpu.hpp include/commdet_cuda.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude tests/cpp/shim_kat.cpp -o $@ -Lpaper_1304_4453_b200 -lcommdet_cuda \
+	    -Wl,-rpath,'$$ORIGIN/../paper_1304_4453_b200'
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)
 	@mkdir -p $(OBJ_DIR)
@@ -30,4 +38,4 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -C oracle clean
 
-.PHONY: all lib oracle clean
+.PHONY: all lib shim oracle clean

@@ -1,0 +1,669 @@
+// commdet/gpu.hpp -- header-only C++ drop-in for the reference detector
+// interface (/root/reference/proj/include/commdet, "H/" below), implemented
+// over the C ABI of libcommdet_cuda.so (include/commdet_cuda.h).
+//
+// Same names, signatures, value types and exception types as the reference:
+//   Graph::from_edges / from_adjacency      H/graph.hpp:48, :85
+//   Partition (+ compacted, community_count) H/partition.hpp:13-91
+//   run_plp / run_plm / run_plmr / run_epp   H/plp.hpp:67, H/louvain.hpp:290/297, H/ensemble.hpp:111
+//   modularity / coverage                    H/quality.hpp:35, :21
+//   coarsen / prolong / move_phase           H/louvain.hpp:154, :223, :65
+//   combine_hashed / dominant_label / is_stable / generate_planted
+// The types live in namespace commdet::gpu; define COMMDET_GPU_DROP_IN before
+// including to also export them as namespace commdet (then do not include
+// the reference headers in the same translation unit).
+//
+// Differences a caller can observe:
+//   * node ids / labels must fit int32 (std::out_of_range otherwise);
+//   * stored edge weights are fp32 (decisions and sums are fp64);
+//   * PLP/PLM update order is the device's seeded bucket schedule, so
+//     `workers` and `randomize_order` do not change the result, and
+//     MoveObserver / EnsembleConfig::base_override are not supported.
+#pragma once
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <vector>
+
+#include "../commdet_cuda.h"
+
+namespace commdet {
+namespace gpu {
+
+using node = std::uint64_t;
+using index = std::uint64_t;
+using count = std::uint64_t;
+using edgeweight = double;
+
+/// Thrown on malformed input data (H/graph.hpp:21-24).
+class input_error : public std::runtime_error {
+  public:
+    using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(cd_status s) {
+    if (s == CD_OK)
+        return;
+    const std::string msg = cd_last_error();
+    switch (s) {
+    case CD_EINPUT:
+        throw input_error(msg);
+    case CD_EINVAL:
+        throw std::invalid_argument(msg);
+    case CD_EDOMAIN:
+        throw std::domain_error(msg);
+    case CD_ERANGE:
+        throw std::out_of_range(msg);
+    case CD_ENOMEM:
+        throw std::bad_alloc();
+    default:
+        throw std::runtime_error("commdet gpu: " + msg);
+    }
+}
+
+inline int32_t to_i32(std::uint64_t v, const char *what) {
+    if (v > static_cast<std::uint64_t>(INT32_MAX))
+        throw std::out_of_range(std::string(what) + " does not fit the device's int32 ids");
+    return static_cast<int32_t>(v);
+}
+}  // namespace detail
+
+/// One CUDA device context (stream + memory pool).  Not thread-safe.
+class Context {
+  public:
+    explicit Context(int device = 0) { detail::check(cd_ctx_create(device, &ctx_)); }
+    ~Context() { cd_ctx_destroy(ctx_); }
+    Context(const Context &) = delete;
+    Context &operator=(const Context &) = delete;
+    cd_ctx *get() const { return ctx_; }
+    static Context &instance() {
+        static Context c(0);
+        return c;
+    }
+
+  private:
+    cd_ctx *ctx_ = nullptr;
+};
+
+struct Edge {
+    node u;
+    node v;
+    edgeweight w;
+};
+using EdgeList = std::vector<Edge>;
+
+inline int resolve_workers(int workers) { return workers > 0 ? workers : 1; }
+
+/// Device-resident undirected weighted graph (H/graph.hpp:38-272).
+class Graph {
+  public:
+    Graph() = default;
+
+    static Graph from_edges(count node_count, const EdgeList &edges, bool merge_duplicates = false) {
+        const int32_t n = detail::to_i32(node_count, "node count");
+        std::vector<int32_t> u(edges.size()), v(edges.size());
+        std::vector<float> w(edges.size());
+        bool weighted = false;
+        for (std::size_t i = 0; i < edges.size(); ++i) {
+            const Edge &e = edges[i];
+            if (e.u >= node_count || e.v >= node_count)
+                throw input_error("edge endpoint out of range: " + std::to_string(e.u) + "," + std::to_string(e.v));
+            if (!(e.w > 0.0))
+                throw input_error("nonpositive edge weight on edge " + std::to_string(e.u) + "," +
+                                  std::to_string(e.v));
+            u[i] = static_cast<int32_t>(e.u);
+            v[i] = static_cast<int32_t>(e.v);
+            w[i] = static_cast<float>(e.w);
+            weighted = weighted || e.w != 1.0;
+        }
+        cd_graph *h = nullptr;
+        detail::check(cd_graph_from_edges(Context::instance().get(), n, static_cast<int64_t>(edges.size()),
+                                          u.empty() ? nullptr : u.data(), v.empty() ? nullptr : v.data(),
+                                          weighted ? w.data() : nullptr, merge_duplicates ? 1 : 0, &h));
+        return Graph(h);
+    }
+
+    /// Full symmetric adjacency, rows sorted (H/graph.hpp:85-103).
+    static Graph from_adjacency(const std::vector<std::vector<std::pair<node, edgeweight>>> &adj) {
+        const int64_t n = detail::to_i32(adj.size(), "node count");
+        std::vector<int64_t> off(n + 1, 0);
+        std::vector<int32_t> col;
+        std::vector<float> w;
+        bool weighted = false;
+        for (int64_t u = 0; u < n; ++u) {
+            for (auto [v, wt] : adj[u]) {
+                col.push_back(detail::to_i32(v, "node id"));
+                w.push_back(static_cast<float>(wt));
+                weighted = weighted || wt != 1.0;
+            }
+            off[u + 1] = static_cast<int64_t>(col.size());
+        }
+        cd_graph *h = nullptr;
+        detail::check(cd_graph_from_csr(Context::instance().get(), n, off.data(), col.empty() ? nullptr : col.data(),
+                                        weighted ? w.data() : nullptr, &h));
+        return Graph(h);
+    }
+
+    count node_count() const { return h_ ? static_cast<count>(info().n) : 0; }
+    count edge_count() const { return h_ ? static_cast<count>(info().m) : 0; }
+    edgeweight total_edge_weight() const { return h_ ? info().total_weight : 0.0; }
+
+    count degree(node u) const {
+        check_node(u);
+        const auto &c = host();
+        return static_cast<count>(c.off[u + 1] - c.off[u]);
+    }
+    edgeweight volume(node u) const {
+        check_node(u);
+        return host().vol[u];
+    }
+    edgeweight loop_weight(node u) const {
+        check_node(u);
+        return host().loop[u];
+    }
+
+    template <typename F>
+    void for_neighbors(node u, F &&f) const {
+        const auto &c = host();
+        for (int64_t i = c.off[u]; i < c.off[u + 1]; ++i)
+            f(static_cast<node>(c.col[i]), c.w.empty() ? 1.0 : static_cast<edgeweight>(c.w[i]));
+    }
+    template <typename F>
+    void for_nodes(F &&f) const {
+        for (node u = 0; u < node_count(); ++u)
+            f(u);
+    }
+    template <typename F>
+    void for_nodes_parallel(F &&f, int = 0) const {
+        for_nodes(std::forward<F>(f));
+    }
+    template <typename F>
+    void for_edges(F &&f) const {
+        const auto &c = host();
+        for (node u = 0; u < node_count(); ++u)
+            for (int64_t i = c.off[u]; i < c.off[u + 1]; ++i)
+                if (static_cast<node>(c.col[i]) >= u)
+                    f(u, static_cast<node>(c.col[i]), c.w.empty() ? 1.0 : static_cast<edgeweight>(c.w[i]));
+    }
+
+    bool operator==(const Graph &o) const {
+        const auto &a = host(), &b = o.host();
+        auto wa = a.w.empty() ? std::vector<float>(a.col.size(), 1.0f) : a.w;
+        auto wb = b.w.empty() ? std::vector<float>(b.col.size(), 1.0f) : b.w;
+        return a.off == b.off && a.col == b.col && wa == wb;
+    }
+
+    const cd_graph *handle() const { return h_.get(); }
+
+  private:
+    struct Deleter {
+        void operator()(cd_graph *g) const { cd_graph_destroy(g); }
+    };
+    struct Host {
+        std::vector<int64_t> off;
+        std::vector<int32_t> col;
+        std::vector<float> w;
+        std::vector<double> vol, loop;
+    };
+    explicit Graph(cd_graph *h) : h_(h, Deleter()) {}
+    friend struct CoarseningResult;
+    template <class>
+    friend struct GraphFactory;
+    friend Graph adopt_graph(cd_graph *);
+
+    cd_graph_info info() const {
+        cd_graph_info i{};
+        detail::check(cd_graph_get_info(h_.get(), &i));
+        return i;
+    }
+    void check_node(node u) const {
+        if (u >= node_count())
+            throw std::out_of_range("node id " + std::to_string(u) + " out of range");
+    }
+    const Host &host() const {
+        if (!host_) {
+            auto hc = std::make_shared<Host>();
+            const cd_graph_info i = h_ ? info() : cd_graph_info{};
+            hc->off.assign(i.n + 1, 0);
+            hc->col.resize(i.D);
+            if (i.weighted)
+                hc->w.resize(i.D);
+            hc->vol.resize(i.n);
+            hc->loop.resize(i.n);
+            if (h_)
+                detail::check(cd_graph_download(h_.get(), hc->off.data(), hc->col.data(),
+                                                i.weighted ? hc->w.data() : nullptr, hc->vol.data(),
+                                                hc->loop.data()));
+            host_ = hc;
+        }
+        return *host_;
+    }
+
+    std::shared_ptr<cd_graph> h_;
+    mutable std::shared_ptr<Host> host_;
+};
+
+inline Graph adopt_graph(cd_graph *h) { return Graph(h); }
+
+/// Dense node -> community assignment (H/partition.hpp:13-91).
+class Partition {
+  public:
+    Partition() = default;
+    explicit Partition(count n, index initial = 0) : data_(n, initial), upper_(initial + 1) {}
+
+    static Partition singletons(count n) {
+        Partition z;
+        z.data_.resize(n);
+        for (node u = 0; u < n; ++u)
+            z.data_[u] = u;
+        z.upper_ = n > 0 ? n : 1;
+        return z;
+    }
+
+    count size() const { return data_.size(); }
+    index upper_bound() const { return upper_; }
+    void set_upper_bound(index ub) { upper_ = ub; }
+    index operator[](node u) const { return data_[u]; }
+    index &operator[](node u) { return data_[u]; }
+    const std::vector<index> &data() const { return data_; }
+    std::vector<index> &data() { return data_; }
+
+    /// First-appearance compaction on the device (cd_compact).
+    Partition compacted() const {
+        std::vector<int32_t> z = to_device_labels(), out(z.size());
+        int64_t k = 0;
+        detail::check(cd_compact(Context::instance().get(), static_cast<int64_t>(z.size()), z.data(), out.data(), &k));
+        Partition p = from_device_labels(out);
+        p.upper_ = k > 0 ? static_cast<index>(k) : 1;
+        return p;
+    }
+    count community_count() const {
+        std::vector<int32_t> z = to_device_labels();
+        int64_t k = 0;
+        detail::check(cd_community_count(Context::instance().get(), static_cast<int64_t>(z.size()), z.data(), &k));
+        return static_cast<count>(k);
+    }
+    std::vector<count> community_sizes() const {
+        std::vector<count> sizes;
+        for (index c : data_) {
+            if (c >= sizes.size())
+                sizes.resize(c + 1, 0);
+            ++sizes[c];
+        }
+        return sizes;
+    }
+    bool is_compact() const {
+        std::vector<bool> used;
+        for (index c : data_) {
+            if (c >= used.size())
+                used.resize(c + 1, false);
+            used[c] = true;
+        }
+        return std::all_of(used.begin(), used.end(), [](bool b) { return b; });
+    }
+    bool operator==(const Partition &o) const { return data_ == o.data_; }
+
+    std::vector<int32_t> to_device_labels() const {
+        std::vector<int32_t> z(data_.size());
+        for (std::size_t u = 0; u < data_.size(); ++u)
+            z[u] = detail::to_i32(data_[u], "community id");
+        return z;
+    }
+    static Partition from_device_labels(const std::vector<int32_t> &z, index ub = 0) {
+        Partition p;
+        p.data_.resize(z.size());
+        index mx = 0;
+        for (std::size_t u = 0; u < z.size(); ++u) {
+            p.data_[u] = static_cast<index>(z[u]);
+            mx = std::max<index>(mx, p.data_[u] + 1);
+        }
+        p.upper_ = ub ? ub : std::max<index>(mx, 1);
+        return p;
+    }
+
+  private:
+    std::vector<index> data_;
+    index upper_ = 1;
+};
+
+inline Partition singleton_partition(const Graph &g) { return Partition::singletons(g.node_count()); }
+
+// ---- configs and report (H/plp.hpp:16-22, H/louvain.hpp:15-22, H/report.hpp) ----
+struct PlpConfig {
+    long long theta = -1;
+    count max_iterations = 100;
+    bool randomize_order = false;
+    std::uint64_t seed = 1;
+    int workers = 1;
+};
+
+struct LouvainConfig {
+    double gamma = 1.0;
+    count max_move_iterations = 32;
+    count max_levels = 64;
+    std::uint64_t seed = 1;
+    int workers = 1;
+    bool refine = false;
+};
+
+enum class Algo { plp, plm, plmr };
+
+struct EnsembleConfig {
+    count ensemble_size = 4;
+    Algo base = Algo::plp;
+    Algo final_algo = Algo::plmr;
+    std::uint64_t seed = 1;
+    int workers = 1;
+    PlpConfig base_plp{.randomize_order = true};
+    LouvainConfig final_louvain;
+};
+
+struct LevelTiming {
+    double move_ms = 0.0;
+    double coarsen_ms = 0.0;
+    double refine_ms = 0.0;
+};
+
+struct IterationRecord {
+    count updated = 0;
+    double ms = 0.0;
+};
+
+struct RunReport {
+    std::string algorithm;
+    std::string input;
+    int workers = 1;
+    std::uint64_t seed = 0;
+    double total_ms = 0.0;
+    double modularity = 0.0;
+    double coverage = 0.0;
+    count community_count = 0;
+    std::vector<LevelTiming> levels;
+    std::vector<IterationRecord> iterations;
+    double base_ms = 0.0;
+    double combine_ms = 0.0;
+    double coarsen_ms = 0.0;
+    double final_ms = 0.0;
+};
+
+namespace detail {
+inline cd_plp_config plp_c(const PlpConfig &c) {
+    cd_plp_config o;
+    cd_plp_config_default(&o);
+    o.theta = c.theta;
+    o.max_iterations = static_cast<int64_t>(c.max_iterations);
+    o.randomize_order = c.randomize_order ? 1 : 0;
+    o.seed = c.seed;
+    o.workers = c.workers;
+    return o;
+}
+inline cd_louvain_config louvain_c(const LouvainConfig &c) {
+    cd_louvain_config o;
+    cd_louvain_config_default(&o);
+    o.gamma = c.gamma;
+    o.max_move_iterations = static_cast<int64_t>(c.max_move_iterations);
+    o.max_levels = static_cast<int64_t>(c.max_levels);
+    o.seed = c.seed;
+    o.workers = c.workers;
+    o.refine = c.refine ? 1 : 0;
+    return o;
+}
+inline int algo_c(Algo a) { return a == Algo::plp ? CD_ALGO_PLP : (a == Algo::plm ? CD_ALGO_PLM : CD_ALGO_PLMR); }
+inline RunReport report_of(const cd_report &r) {
+    RunReport o;
+    o.algorithm = r.algorithm;
+    o.workers = r.workers;
+    o.seed = r.seed;
+    o.total_ms = r.total_ms;
+    o.modularity = r.modularity;
+    o.coverage = r.coverage;
+    o.community_count = static_cast<count>(r.community_count);
+    for (int64_t i = 0; i < std::min<int64_t>(r.n_levels, CD_MAX_LEVEL_RECORDS); ++i)
+        o.levels.push_back({r.levels[i].move_ms, r.levels[i].coarsen_ms, r.levels[i].refine_ms});
+    for (int64_t i = 0; i < std::min<int64_t>(r.n_iterations, CD_MAX_ITERATION_RECORDS); ++i)
+        o.iterations.push_back({static_cast<count>(r.iterations[i].updated), r.iterations[i].ms});
+    o.base_ms = r.base_ms;
+    o.combine_ms = r.combine_ms;
+    o.coarsen_ms = r.coarsen_ms;
+    o.final_ms = r.final_ms;
+    return o;
+}
+inline void check_cover(const Graph &g, const Partition &z) {
+    if (z.size() != g.node_count())
+        throw std::invalid_argument("partition length " + std::to_string(z.size()) + " does not match node count " +
+                                    std::to_string(g.node_count()));
+}
+}  // namespace detail
+
+// ---- quality (H/quality.hpp) ------------------------------------------------------
+inline double coverage(const Graph &g, const Partition &z) {
+    detail::check_cover(g, z);
+    if (g.total_edge_weight() == 0.0)
+        return 0.0;
+    auto l = z.to_device_labels();
+    double q = 0.0, c = 0.0;
+    detail::check(cd_modularity(Context::instance().get(), g.handle(), l.data(),
+                                static_cast<int64_t>(std::max<index>(z.upper_bound(), 1)), 1.0, &q, &c));
+    return c;
+}
+
+inline double modularity(const Graph &g, const Partition &z, double gamma = 1.0) {
+    detail::check_cover(g, z);
+    auto l = z.to_device_labels();
+    double q = 0.0, c = 0.0;
+    detail::check(cd_modularity(Context::instance().get(), g.handle(), l.data(),
+                                static_cast<int64_t>(std::max<index>(z.upper_bound(), 1)), gamma, &q, &c));
+    return q;
+}
+
+// ---- PLP (H/plp.hpp) ------------------------------------------------------------------
+inline count resolved_theta(const PlpConfig &cfg, count n) {
+    if (cfg.theta >= 0)
+        return static_cast<count>(cfg.theta);
+    return std::max<count>(1, n / 100000);
+}
+
+inline std::pair<Partition, RunReport> run_plp(const Graph &g, const PlpConfig &cfg,
+                                               const std::optional<Partition> &initial = std::nullopt) {
+    if (initial && initial->size() != g.node_count())
+        throw std::invalid_argument("initial partition does not cover the graph");
+    std::vector<int32_t> init = initial ? initial->to_device_labels() : std::vector<int32_t>();
+    std::vector<int32_t> labels(g.node_count());
+    cd_plp_config c = detail::plp_c(cfg);
+    auto rep = std::make_unique<cd_report>();
+    detail::check(cd_plp_run(Context::instance().get(), g.handle(), &c, initial ? init.data() : nullptr,
+                             labels.data(), rep.get()));
+    return {Partition::from_device_labels(labels), detail::report_of(*rep)};
+}
+
+inline index dominant_label(const Graph &g, const Partition &z, node u) {
+    if (g.degree(u) == 0)
+        throw std::invalid_argument("dominant_label: node " + std::to_string(u) + " is isolated");
+    auto l = z.to_device_labels();
+    std::vector<int32_t> out(l.size());
+    int64_t upd = 0;
+    detail::check(cd_plp_sweep_sync(Context::instance().get(), g.handle(), l.data(), out.data(), &upd));
+    return static_cast<index>(out[u]);
+}
+
+inline bool is_stable(const Graph &g, const Partition &z) {
+    auto l = z.to_device_labels();
+    std::vector<int32_t> out(l.size());
+    int64_t upd = 0;
+    detail::check(cd_plp_sweep_sync(Context::instance().get(), g.handle(), l.data(), out.data(), &upd));
+    return upd == 0;
+}
+
+// ---- Louvain (H/louvain.hpp) --------------------------------------------------------
+using CommunityVolumes = std::vector<edgeweight>;
+
+inline CommunityVolumes community_volumes(const Graph &g, const Partition &z) {
+    auto l = z.to_device_labels();
+    CommunityVolumes vols(std::max<index>(z.upper_bound(), 1));
+    detail::check(cd_community_volumes(Context::instance().get(), g.handle(), l.data(),
+                                       static_cast<int64_t>(vols.size()), vols.data()));
+    return vols;
+}
+
+/// H/louvain.hpp:37-56 (scalar; evaluated on the host mirror of the graph).
+inline double delta_mod(const Graph &g, const Partition &z, const CommunityVolumes &vols, node u, index target,
+                        double gamma) {
+    const index c = z[u];
+    if (target == c)
+        return 0.0;
+    edgeweight w_c = 0.0, w_d = 0.0;
+    g.for_neighbors(u, [&](node v, edgeweight w) {
+        if (v == u)
+            return;
+        if (z[v] == c)
+            w_c += w;
+        else if (z[v] == target)
+            w_d += w;
+    });
+    const edgeweight total = g.total_edge_weight();
+    const edgeweight vol_u = g.volume(u);
+    return (w_d - w_c) / total + gamma * ((vols[c] - vol_u) - vols[target]) * vol_u / (2.0 * total * total);
+}
+
+/// move_phase (H/louvain.hpp:65-141) with the device's bucketed order.
+inline bool move_phase(const Graph &g, Partition &z, const LouvainConfig &cfg) {
+    detail::check_cover(g, z);
+    auto l = z.to_device_labels();
+    cd_louvain_config c = detail::louvain_c(cfg);
+    int32_t changed = 0;
+    detail::check(cd_move_phase(Context::instance().get(), g.handle(), l.data(), &c, &changed));
+    const index ub = z.upper_bound();
+    z = Partition::from_device_labels(l, ub);
+    return changed != 0;
+}
+
+struct CoarseningResult {
+    Graph coarse;
+    std::vector<node> pi;
+};
+
+inline CoarseningResult coarsen(const Graph &g, const Partition &z, int = 1) {
+    detail::check_cover(g, z);
+    auto l = z.to_device_labels();
+    std::vector<int32_t> pi(l.size());
+    cd_graph *h = nullptr;
+    detail::check(cd_coarsen(Context::instance().get(), g.handle(), l.data(), &h, pi.data()));
+    CoarseningResult r{adopt_graph(h), {}};
+    r.pi.assign(pi.begin(), pi.end());
+    return r;
+}
+
+inline Partition prolong(const Partition &z_coarse, const std::vector<node> &pi) {
+    auto zc = z_coarse.to_device_labels();
+    std::vector<int32_t> p(pi.size()), out(pi.size());
+    for (std::size_t v = 0; v < pi.size(); ++v) {
+        if (pi[v] >= z_coarse.size())
+            throw std::out_of_range("prolong: contraction map entry out of range");
+        p[v] = static_cast<int32_t>(pi[v]);
+    }
+    detail::check(cd_prolong(Context::instance().get(), static_cast<int64_t>(zc.size()), zc.data(),
+                             static_cast<int64_t>(p.size()), p.data(), out.data()));
+    return Partition::from_device_labels(out, z_coarse.upper_bound());
+}
+
+inline std::pair<Partition, RunReport> run_plm(const Graph &g, const LouvainConfig &cfg) {
+    cd_louvain_config c = detail::louvain_c(cfg);
+    c.refine = 0;
+    std::vector<int32_t> z(g.node_count());
+    auto rep = std::make_unique<cd_report>();
+    detail::check(cd_louvain_run(Context::instance().get(), g.handle(), &c, z.data(), rep.get()));
+    return {Partition::from_device_labels(z), detail::report_of(*rep)};
+}
+
+inline std::pair<Partition, RunReport> run_plmr(const Graph &g, const LouvainConfig &cfg) {
+    cd_louvain_config c = detail::louvain_c(cfg);
+    c.refine = 1;
+    std::vector<int32_t> z(g.node_count());
+    auto rep = std::make_unique<cd_report>();
+    detail::check(cd_louvain_run(Context::instance().get(), g.handle(), &c, z.data(), rep.get()));
+    return {Partition::from_device_labels(z), detail::report_of(*rep)};
+}
+
+// ---- ensemble (H/ensemble.hpp) ------------------------------------------------------
+inline std::uint64_t djb2(const std::uint8_t *data, std::size_t len) {
+    std::uint64_t h = 5381;
+    for (std::size_t i = 0; i < len; ++i)
+        h = h * 33 + data[i];
+    return h;
+}
+
+inline Partition combine_hashed(const std::vector<Partition> &solutions, int = 1) {
+    if (solutions.empty())
+        throw std::invalid_argument("empty ensemble");
+    std::vector<std::vector<int32_t>> l;
+    std::vector<const int32_t *> p;
+    for (const Partition &s : solutions) {
+        if (s.size() != solutions.front().size())
+            throw std::invalid_argument("ensemble partitions cover different node sets");
+        l.push_back(s.to_device_labels());
+    }
+    for (auto &v : l)
+        p.push_back(v.data());
+    std::vector<int32_t> out(solutions.front().size());
+    int64_t k = 0;
+    detail::check(cd_combine_hashed(Context::instance().get(), static_cast<int64_t>(p.size()),
+                                    static_cast<int64_t>(out.size()), p.data(), out.data(), &k));
+    return Partition::from_device_labels(out, k > 0 ? static_cast<index>(k) : 1);
+}
+
+inline std::pair<Partition, RunReport> run_epp(const Graph &g, const EnsembleConfig &cfg) {
+    cd_ensemble_config c;
+    cd_ensemble_config_default(&c);
+    c.ensemble_size = static_cast<int64_t>(cfg.ensemble_size);
+    c.base = detail::algo_c(cfg.base);
+    c.final_algo = detail::algo_c(cfg.final_algo);
+    c.seed = cfg.seed;
+    c.workers = cfg.workers;
+    c.base_plp = detail::plp_c(cfg.base_plp);
+    c.final_louvain = detail::louvain_c(cfg.final_louvain);
+    std::vector<int32_t> z(g.node_count());
+    auto rep = std::make_unique<cd_report>();
+    detail::check(cd_epp_run(Context::instance().get(), g.handle(), &c, z.data(), rep.get()));
+    return {Partition::from_device_labels(z), detail::report_of(*rep)};
+}
+
+// ---- generator (H/generator.hpp) ------------------------------------------------------
+struct PlantedPartitionSpec {
+    count n = 0;
+    count k = 1;
+    double p_in = 0.0;
+    double p_out = 0.0;
+    std::uint64_t seed = 1;
+};
+
+inline index planted_block(node u, count n, count k) {
+    return static_cast<index>((static_cast<unsigned __int128>(u) * k) / n);
+}
+
+inline std::pair<Graph, Partition> generate_planted(const PlantedPartitionSpec &spec, int = 1) {
+    std::vector<int32_t> truth(spec.n);
+    cd_graph *h = nullptr;
+    detail::check(cd_graph_generate_planted(Context::instance().get(), static_cast<int64_t>(spec.n),
+                                            static_cast<int64_t>(spec.k), spec.p_in, spec.p_out, spec.seed, &h,
+                                            truth.empty() ? nullptr : truth.data()));
+    Partition t = Partition::from_device_labels(truth, spec.n > 0 ? spec.k : 1);
+    return {adopt_graph(h), t};
+}
+
+}  // namespace gpu
+
+#ifdef COMMDET_GPU_DROP_IN
+using namespace gpu;
+#endif
+
+}  // namespace commdet
