@@ -88,8 +88,9 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
     cg->weighted = true;
     try {
         SrcCoarsen src{moff.p, mem.p, mpre.p, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, z};
-        cg->D = run_row_engine(ctx, src, nc, fpre.p, g->D, std::max<int64_t>(nc, 1), DUP_SUM, true, cg->off, cg->col,
-                               cg->w, nullptr, "coarsen");
+        bool want_w = true;
+        cg->D = run_row_engine(ctx, src, nc, fpre.p, g->D, std::max<int64_t>(nc, 1), DUP_SUM, want_w, cg->off,
+                               cg->col, cg->w, nullptr, "coarsen");
         graph_finalize(ctx, cg);
     } catch (...) {
         delete cg;

@@ -146,10 +146,12 @@ cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, 
     bool dup = false;
     try {
         SrcFlat src{fpre.p, rk.p, weighted ? rw.p : nullptr};
-        g->D = run_row_engine(ctx, src, n, fpre.p, F, std::max<int64_t>(n, 1), mode, weighted, g->off, g->col, g->w,
+        bool want_w = weighted;
+        g->D = run_row_engine(ctx, src, n, fpre.p, F, std::max<int64_t>(n, 1), mode, want_w, g->off, g->col, g->w,
                               &dup, "build");
         if (dup && mode == DUP_ERROR)
-            fail(CD_EINPUT, "duplicate edge");
+            fail(CD_EINPUT, "duplicate edge");  // H/graph.hpp:178-181
+        g->weighted = want_w;
         graph_finalize(ctx, g);
     } catch (...) {
         delete g;

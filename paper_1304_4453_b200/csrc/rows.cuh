@@ -191,7 +191,7 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_direct(Src src, const
             const int rank = __popc(lm & lanemask_lt());
             out.tkey[f0 + rank] = k;
             out.tval[f0 + rank] = mode == DUP_ONE ? 1.0 : sum;
-            if (mode == DUP_ERROR && cnt > 1)
+            if (cnt > 1)
                 out.flag[0] = 1;
         }
         if (lane == 0)
@@ -253,7 +253,7 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
                 const int64_t pos = f0 + base + __popc(bm & lanemask_lt());
                 out.tkey[pos] = keys[s];
                 out.tval[pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (mode == DUP_ERROR && cnts[s] > 1)
+                if (cnts[s] > 1)
                     out.flag[0] = 1;
             }
             base += __popc(bm);
@@ -314,7 +314,7 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (mode == DUP_ERROR && cnts[s] > 1)
+                if (cnts[s] > 1)
                     out.flag[0] = 1;
             }
         }
@@ -394,7 +394,7 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const in
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (mode == DUP_ERROR && cnts[s] > 1)
+                if (cnts[s] > 1)
                     out.flag[0] = 1;
             }
         }
@@ -637,11 +637,11 @@ static __global__ void k_cap_from_prefix(int64_t m, const int64_t *pre, const in
 }
 
 // Runs the engine.  fpre: device [nrows+1] source prefix.  Produces off2
-// ([nrows+1]), col ([D2]) and w ([D2], if want_w).  Returns D2.  Sets
-// *dup (host) when DUP_ERROR saw a duplicate.
+// ([nrows+1]), col ([D2]) and w ([D2], if want_w; DUP_SUM turns want_w on
+// when duplicates were merged).  Returns D2.  *dup (host) = duplicates seen.
 template <class Src>
 int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t *fpre, int64_t F_total,
-                       int64_t key_bound, DupMode mode, bool want_w, DBuf<int64_t> &off2, DBuf<int32_t> &col,
+                       int64_t key_bound, DupMode mode, bool &want_w, DBuf<int64_t> &off2, DBuf<int32_t> &col,
                        DBuf<float> &wout, bool *dup, const char *family) {
     off2.alloc(ctx, nrows + 1);
     if (nrows == 0) {
@@ -718,6 +718,9 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         *dup = hflag != 0;
     if (mode == DUP_ERROR && hflag)
         return D2;
+    // merged duplicates of an unweighted input carry summed weights
+    if (mode == DUP_SUM && hflag)
+        want_w = true;
     col.alloc(ctx, std::max<int64_t>(D2, 1));
     if (want_w)
         wout.alloc(ctx, std::max<int64_t>(D2, 1));

@@ -159,6 +159,8 @@ def kat_graph_errors(B):
             B.graph(n, edges)
     c = B.csr(B.graph(2, [(0, 1, 1), (1, 0, 1)], merge=True))  # merge (:49-54)
     assert c["m"] == 1 and c["total"] == 2.0 and c["vol"][0] == 2.0
+    c = B.csr(B.graph(2, [(0, 1), (1, 0)], merge=True))  # unweighted input: merged weight 2
+    assert c["m"] == 1 and c["total"] == 2.0 and c["vol"][0] == 2.0
 
 
 def kat_graph_random_invariants(B):
