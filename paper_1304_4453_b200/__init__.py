@@ -147,7 +147,8 @@ def load_library():
     global _lib
     if _lib is not None:
         return _lib
-    path = library_path()
+    # COMMDET_CUDA_LIB: an alternative build of the same library (A/B timing)
+    path = os.environ.get("COMMDET_CUDA_LIB") or library_path()
     if not os.path.exists(path):
         raise CommdetError(f"{path} is missing: build it with `make lib` (or __graft_entry__.build())")
     L = C.CDLL(path)

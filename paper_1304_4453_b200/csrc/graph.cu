@@ -15,7 +15,8 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off,
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     int64_t m_loc = 0, maxdeg = 0, iso = 0;
-    double tot_loc = 0.0;
+    double tot_loc = 0.0, maxvol = 0.0;
+    bool frac = false;
     for (int64_t u = gw; u < n; u += nw) {
         const int64_t s = off[u], e = off[u + 1];
         double vs = 0.0, lp = 0.0, up = 0.0;
@@ -23,6 +24,7 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off,
         for (int64_t i = s + lane; i < e; i += 32) {
             const int32_t v = col[i];
             const double wt = w ? static_cast<double>(w[i]) : 1.0;
+            frac |= wt != floor(wt);
             vs += wt;
             if (v == u) {
                 lp += wt;
@@ -44,12 +46,18 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off,
         m_loc += cnt;
         tot_loc += up;
         maxdeg = max(maxdeg, e - s);
+        maxvol = fmax(maxvol, vs + lp);
         iso += (e == s);
     }
+    const bool any_frac = __any_sync(0xffffffffu, frac);
     if (lane == 0) {
         atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[0]), static_cast<unsigned long long>(m_loc));
         atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[1]), static_cast<unsigned long long>(maxdeg));
         atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[2]), static_cast<unsigned long long>(iso));
+        if (any_frac)
+            atomicOr(reinterpret_cast<unsigned long long *>(&acc_i[3]), 1ULL);
+        // vol >= 0: the bit pattern of a non-negative double orders like its value
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[4]), static_cast<unsigned long long>(__double_as_longlong(maxvol)));
         atomicAdd(acc_d, tot_loc);
     }
 }
@@ -57,7 +65,7 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off,
 void graph_finalize(cd_ctx *ctx, cd_graph *g) {
     g->vol.alloc(ctx, std::max<int64_t>(g->n, 1));
     g->loop.alloc(ctx, std::max<int64_t>(g->n, 1));
-    DBuf<int64_t> acc_i(ctx, 3);
+    DBuf<int64_t> acc_i(ctx, 5);
     DBuf<double> acc_d(ctx, 1);
     acc_i.zero();
     acc_d.zero();
@@ -65,7 +73,7 @@ void graph_finalize(cd_ctx *ctx, cd_graph *g) {
         CD_LAUNCH(ctx, "finalize", k_finalize, grid_for(g->n, 8, ctx->num_sms * 16), 256, 0, g->n,
                   static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
                   static_cast<const float *>(g->weighted ? g->w.p : nullptr), g->vol.p, g->loop.p, acc_i.p, acc_d.p);
-    int64_t hi[3];
+    int64_t hi[5];
     double hd;
     CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaMemcpyAsync(&hd, acc_d.p, sizeof(hd), cudaMemcpyDeviceToHost, ctx->stream));
@@ -73,6 +81,9 @@ void graph_finalize(cd_ctx *ctx, cd_graph *g) {
     g->m = hi[0];
     g->max_degree = hi[1];
     g->isolated = hi[2];
+    std::memcpy(&g->max_vol, &hi[4], sizeof(double));
+    // exact integer tallies when every weight is integral and sums fit
+    g->int_weights = hi[3] == 0 && g->max_vol < 2147483648.0;
     g->total = hd;
     g->binned = false;
 }

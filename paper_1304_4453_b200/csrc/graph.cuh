@@ -18,20 +18,20 @@ namespace cdk {
 
 // Degree tiers of the sweep / move kernels.
 enum Tier : int {
-    TIER_G8 = 0,     // deg <= 8      : 8 lanes per node (4 nodes / warp)
-    TIER_G16 = 1,    // deg <= 16     : 16 lanes per node
-    TIER_G32 = 2,    // deg <= 32     : one warp per node, one pass
-    TIER_WARP = 3,   // deg <= 256    : one warp per node, per-warp smem hash
-    TIER_BLOCK = 4,  // deg <= 4096   : one block per node, block smem hash
-    TIER_HUB = 5,    // deg >  4096   : multi-block per node, global hash
-    NUM_TIERS = 6,
-    NUM_LIST_TIERS = 5,
+    TIER_G8 = 0,      // deg <= 8      : 8 lanes per node (4 nodes / warp)
+    TIER_G16 = 1,     // deg <= 16     : 16 lanes per node
+    TIER_G32 = 2,     // deg <= 32     : one warp per node, one pass
+    TIER_WARP = 3,    // deg <= 256    : one warp per node, per-warp smem hash
+    TIER_BLOCK = 4,   // deg <= 1024   : one block per node, 2048-slot smem hash
+    TIER_BLOCK2 = 5,  // deg <= 4096   : one block per node, 8192-slot smem hash
+    TIER_HUB = 6,     // deg >  4096   : multi-block per node, global hash
+    NUM_TIERS = 7,
     TIER_NONE = 255
 };
-constexpr int64_t TIER_MAX_DEG[NUM_LIST_TIERS] = {8, 16, 32, 256, 4096};
-constexpr int WARP_TABLE_CAP = 512;    // per-warp smem hash slots (>= 2*256)
-constexpr int BLOCK_TABLE_CAP = 8192;  // block smem hash slots (>= 2*4096)
-constexpr int HUB_CHUNK = 4096;        // entries per hub chunk block
+constexpr int WARP_TABLE_CAP = 512;     // per-warp smem hash slots (>= 2*256)
+constexpr int BLOCK_TABLE_CAP = 2048;   // >= 2*1024
+constexpr int BLOCK2_TABLE_CAP = 8192;  // >= 2*4096
+constexpr int HUB_CHUNK = 4096;         // entries per hub chunk block
 
 __host__ __device__ inline int tier_of_degree(int64_t d) {
     if (d <= 0)
@@ -44,10 +44,17 @@ __host__ __device__ inline int tier_of_degree(int64_t d) {
         return TIER_G32;
     if (d <= 256)
         return TIER_WARP;
-    if (d <= 4096)
+    if (d <= 1024)
         return TIER_BLOCK;
+    if (d <= 4096)
+        return TIER_BLOCK2;
     return TIER_HUB;
 }
+
+// Tally value class of a graph: 0 unweighted (counts), 1 integral weights
+// whose row sums fit uint32 (exact integer tallies, native smem atomics),
+// 2 general fp32 weights (fp64 tallies).
+enum ValueClass : int { VC_COUNT = 0, VC_INT = 1, VC_REAL = 2 };
 
 }  // namespace cdk
 
@@ -56,6 +63,8 @@ struct cd_graph {
     int64_t n = 0, D = 0, m = 0;
     double total = 0.0;
     bool weighted = false;
+    bool int_weights = false;  // every weight integral and max vol < 2^31 (finalize)
+    double max_vol = 0.0;
     int64_t max_degree = 0, isolated = 0;
     cdk::DBuf<int64_t> off;
     cdk::DBuf<int32_t> col;
@@ -66,8 +75,8 @@ struct cd_graph {
     // tier, ascending id within a tier (stable partition by scan)
     bool binned = false;
     cdk::DBuf<uint8_t> tier;
-    int64_t tier_nodes[cdk::NUM_TIERS] = {0, 0, 0, 0, 0, 0};
-    int64_t tier_start[cdk::NUM_TIERS + 1] = {0, 0, 0, 0, 0, 0, 0};
+    int64_t tier_nodes[cdk::NUM_TIERS] = {};
+    int64_t tier_start[cdk::NUM_TIERS + 1] = {};
     cdk::DBuf<int32_t> tlist;  // [tier_start[NUM_TIERS]]
     // hub tier: static chunk grid and hash regions; hubs = tlist + tier_start[TIER_HUB]
     int64_t n_hubs = 0, n_hub_chunks = 0, hub_slots = 0;

@@ -163,7 +163,7 @@ struct EngineOut {
     int32_t *tkey;   // [F_total] reduced keys (row r at fpre[r])
     double *tval;    // [F_total]
     int64_t *deg2;   // [nrows] distinct count
-    int64_t *flag;   // duplicate flag (DUP_ERROR)
+    int64_t *flag;   // duplicates seen (nullptr: not tracked); written once
 };
 
 // ---- reduce kernels -------------------------------------------------------
@@ -191,8 +191,8 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_direct(Src src, const
             const int rank = __popc(lm & lanemask_lt());
             out.tkey[f0 + rank] = k;
             out.tval[f0 + rank] = mode == DUP_ONE ? 1.0 : sum;
-            if (cnt > 1)
-                out.flag[0] = 1;
+            if (cnt > 1 && out.flag && !*out.flag)
+                *out.flag = 1;
         }
         if (lane == 0)
             out.deg2[r] = __popc(lm);
@@ -253,8 +253,8 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
                 const int64_t pos = f0 + base + __popc(bm & lanemask_lt());
                 out.tkey[pos] = keys[s];
                 out.tval[pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1)
-                    out.flag[0] = 1;
+                if (cnts[s] > 1 && out.flag && !*out.flag)
+                    *out.flag = 1;
             }
             base += __popc(bm);
         }
@@ -314,8 +314,8 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1)
-                    out.flag[0] = 1;
+                if (cnts[s] > 1 && out.flag && !*out.flag)
+                    *out.flag = 1;
             }
         }
         __syncthreads();
@@ -394,8 +394,8 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const in
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1)
-                    out.flag[0] = 1;
+                if (cnts[s] > 1 && out.flag && !*out.flag)
+                    *out.flag = 1;
             }
         }
         __syncthreads();
@@ -668,7 +668,10 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
     int32_t hc[8];
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
-    EngineOut eo{tkey.p, tval.p, deg2.p, flag.p};
+    // duplicates matter only for the builder (error / unweighted merge); in a
+    // contraction every row is full of them
+    const bool track = mode == DUP_ERROR || (mode == DUP_SUM && !want_w);
+    EngineOut eo{tkey.p, tval.p, deg2.p, track ? flag.p : nullptr};
     const int sms = ctx->num_sms;
     if (hc[0])
         CD_LAUNCH(ctx, family, (k_eng_reduce_direct<Src>), grid_for(hc[0], 8, sms * 8), 256, 0, src, fpre, L[0],

@@ -7,10 +7,11 @@
 //        best = argmax delta with ties -> smallest d, move iff delta > 0.
 //
 // Tiers (graph.cuh): G8/G16/G32 one pass with __match_any_sync, lanes grouped
-// 8/16/32 per node; WARP per-warp smem hash; BLOCK block smem hash; HUB
-// multi-block insert into a global hash + per-hub finalize.  Every tally sum
-// is exact (int counts or fp64 of fp32 weights), so the decision does not
-// depend on the summation order and equals the sequential reference's.
+// 8/16/32 per node; WARP per-warp smem hash; BLOCK / BLOCK2 block smem hash
+// (2048 / 8192 slots); HUB multi-block insert into a global hash + per-hub
+// finalize.  Every tally is exact (integer counts / integral weights in
+// uint32, general weights in fp64), so the decision does not depend on the
+// summation order and equals the sequential reference's.
 //
 // Selection (bucket of this sub-sweep, PLP active flag) is done inline: each
 // warp loads 32 candidates of its tier's static list, ballots the selected
@@ -53,6 +54,9 @@ struct SweepParams {
     int64_t n_hubs;
 };
 
+template <int VC>
+using TallyT = typename std::conditional<VC == VC_REAL, double, unsigned int>::type;
+
 __device__ __forceinline__ double plm_delta(double aff_d, double w_c, double vol_c, double vols_d, double vol_u,
                                             const SweepParams &P) {
     // (aff[d] - w_c) * inv_total + gamma * (vol_c - vols[d]) * vol_u * inv_sq2
@@ -90,14 +94,14 @@ __device__ __forceinline__ double sum_xor(double v) {
 
 // Group aggregation: returns leader flag and the group's count / weight sum
 // (weights summed in lane order by the leader).
-template <bool W>
+template <int VC>
 __device__ __forceinline__ bool aggregate(int32_t key, double w, bool valid, uint32_t gmask, double *scratch,
                                           double &val) {
     const int lane = lane_id();
     const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
     const uint32_t peers = __match_any_sync(0xffffffffu, key) & vmask & gmask;
     const bool leader = valid && ((__ffs(peers) - 1) == lane);
-    if (W) {
+    if (VC != VC_COUNT) {
         scratch[lane] = w;
         __syncwarp();
         double s = 0.0;
@@ -123,6 +127,11 @@ __device__ __forceinline__ void tinsert(int32_t *keys, V *vals, uint32_t mask, i
         }
         s = (s + 1) & mask;
     }
+}
+
+template <int VC>
+__device__ __forceinline__ double load_w(const SweepParams &P, int64_t f, bool valid) {
+    return (VC != VC_COUNT && valid) ? static_cast<double>(P.w[f]) : 1.0;
 }
 
 __device__ __forceinline__ bool selected(const SweepParams &P, unsigned long long key, int32_t u) {
@@ -181,8 +190,8 @@ __device__ __forceinline__ void flush_stats(const SweepParams &P, unsigned long 
 // ---------------------------------------------------------------------------
 // tiers G8 / G16 / G32: one entry per lane, G lanes per node
 // ---------------------------------------------------------------------------
-template <int G, int MODE, bool W>
-__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
+template <int G, int MODE, int VC>
+__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, int chunk) {
     __shared__ double scratch[8][32];
     constexpr int NPW = 32 / G;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
@@ -194,8 +203,10 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
-    for (int64_t base = gw * 32; base < count; base += nw * 32) {
-        const bool in = base + lane < count;
+    // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
+    // many of them, so the tail of a sub-sweep stays occupied
+    for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
+        const bool in = lane < chunk && base + lane < count;
         const int32_t cand = in ? list[base + lane] : 0;
         uint32_t selmask = __ballot_sync(0xffffffffu, in && selected(P, bkey, cand));
         while (selmask) {
@@ -212,12 +223,12 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
             }
             bool valid = has && k < d;
             const int32_t v = valid ? P.col[s + k] : 0;
-            const double wt = (W && valid) ? static_cast<double>(P.w[s + k]) : 1.0;
+            const double wt = load_w<VC>(P, s + k, valid);
             if (MODE == MODE_PLM)
                 valid = valid && v != u;
             const int32_t key = valid ? P.z[v] : 0;
             double agg;
-            const bool leader = aggregate<W>(key, wt, valid, gmask, scratch[wid], agg);
+            const bool leader = aggregate<VC>(key, wt, valid, gmask, scratch[wid], agg);
             const int32_t cur = has ? P.z[u] : 0;
             double cv;
             int32_t ck;
@@ -256,9 +267,9 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier) {
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
-template <int MODE, bool W>
-__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
-    using V = typename std::conditional<W, double, unsigned int>::type;
+template <int MODE, int VC>
+__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
+    using V = TallyT<VC>;
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][SW_WARP_CAP];
     __shared__ V svals[4][SW_WARP_CAP];
@@ -271,8 +282,10 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
-    for (int64_t base = gw * 32; base < count; base += nw * 32) {
-        const bool in = base + lane < count;
+    // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
+    // many of them, so the tail of a sub-sweep stays occupied
+    for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
+        const bool in = lane < chunk && base + lane < count;
         const int32_t cand = in ? list[base + lane] : 0;
         uint32_t selmask = __ballot_sync(0xffffffffu, in && selected(P, bkey, cand));
         while (selmask) {
@@ -293,7 +306,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
             for (int c = 0; c < SW_WARP_ITEMS; ++c) {
                 const int64_t f = s + c * 32 + lane;
                 vv[c] = f < e ? P.col[f] : -1;
-                ww[c] = (W && f < e) ? P.w[f] : 1.0f;
+                ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
             }
 #pragma unroll
             for (int c = 0; c < SW_WARP_ITEMS; ++c)
@@ -311,7 +324,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
                 if (MODE == MODE_PLM && valid && kk[c] == cur)
                     wc += wt;
                 double agg;
-                if (aggregate<W>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
                     tinsert<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg));
             }
             __syncwarp();
@@ -351,21 +364,26 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P) {
 }
 
 // ---------------------------------------------------------------------------
-// tier BLOCK: one block per node (deg <= 4096), block smem hash (cap <= 8192)
+// tiers BLOCK / BLOCK2: one block per node, block smem hash of CAP slots.
+// Entry and slot loops are unrolled 4-wide so each thread keeps 4
+// independent global loads in flight.
 // ---------------------------------------------------------------------------
-template <int MODE, bool W>
-__global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
-    using V = typename std::conditional<W, double, unsigned int>::type;
+constexpr int SW_BLOCK_THREADS = 256;
+constexpr int SW_ILP = 4;
+
+template <int MODE, int VC, int CAP, int TIER>
+__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
+    using V = TallyT<VC>;
     extern __shared__ unsigned char smem_raw[];
     V *vals = reinterpret_cast<V *>(smem_raw);
-    int32_t *keys = reinterpret_cast<int32_t *>(vals + BLOCK_TABLE_CAP);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
     __shared__ double scratch[8][32];
     __shared__ double red_v[8];
     __shared__ int32_t red_k[8];
     __shared__ double red_wc[8];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int32_t *list = P.tlist + P.tstart[TIER_BLOCK];
-    const int64_t count = P.tstart[TIER_BLOCK + 1] - P.tstart[TIER_BLOCK];
+    const int32_t *list = P.tlist + P.tstart[TIER];
+    const int64_t count = P.tstart[TIER + 1] - P.tstart[TIER];
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     // one candidate per block iteration; unselected candidates cost one load
@@ -373,81 +391,108 @@ __global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
         const int32_t u = list[i];
         if (!selected(P, bkey, u))
             continue;
-        {
-            const int64_t s = P.off[u], e = P.off[u + 1];
-            uint32_t cap = 64;
-            while (cap < 2 * (e - s))
-                cap <<= 1;
-            for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
-                keys[t] = EMPTY_KEY;
-                vals[t] = V(0);
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        const int32_t cur = P.z[u];
+        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+        uint32_t cap = 64;
+        while (cap < 2 * (e - s))
+            cap <<= 1;
+        for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
+            keys[t] = EMPTY_KEY;
+            vals[t] = V(0);
+        }
+        __syncthreads();
+        double wc = 0.0;
+        for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
+            int32_t vv[SW_ILP], kk[SW_ILP];
+            float ww[SW_ILP];
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                const int64_t f = f0 + c * 32 + lane;
+                vv[c] = f < e ? P.col[f] : -1;
+                ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
             }
-            __syncthreads();
-            const int32_t cur = P.z[u];
-            double wc = 0.0;
-            for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
-                bool valid = f + lane < e;
-                const int32_t v = valid ? P.col[f + lane] : 0;
-                const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c)
+                kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                bool valid = vv[c] >= 0;
                 if (MODE == MODE_PLM)
-                    valid = valid && v != u;
-                const int32_t key = valid ? P.z[v] : 0;
-                if (MODE == MODE_PLM && valid && key == cur)
+                    valid = valid && vv[c] != u;
+                const double wt = static_cast<double>(ww[c]);
+                if (MODE == MODE_PLM && valid && kk[c] == cur)
                     wc += wt;
                 double agg;
-                if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
-                    tinsert<V>(keys, vals, cap - 1, key, static_cast<V>(agg));
+                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                    tinsert<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg));
+            }
+        }
+        const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
+        if (MODE == MODE_PLM) {
+            wc = warp_sum(wc);
+            if (lane == 0)
+                red_wc[wid] = wc;
+        }
+        __syncthreads();
+        if (MODE == MODE_PLM) {
+            wc = 0.0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                wc += red_wc[q];
+        }
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        int32_t ck = INT32_MAX;
+        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
+        for (uint32_t t0 = threadIdx.x; t0 < cap; t0 += SW_BLOCK_THREADS * SW_ILP) {
+            int32_t key[SW_ILP];
+            double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                const uint32_t t = t0 + c * SW_BLOCK_THREADS;
+                key[c] = t < cap ? keys[t] : EMPTY_KEY;
+                aff[c] = t < cap ? static_cast<double>(vals[t]) : 0.0;
             }
             if (MODE == MODE_PLM) {
-                wc = warp_sum(wc);
-                if (lane == 0)
-                    red_wc[wid] = wc;
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c)
+                    vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
             }
-            __syncthreads();
-            if (MODE == MODE_PLM) {
-                wc = 0.0;
-                for (int q = 0; q < 8; ++q)
-                    wc += red_wc[q];
-            }
-            double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
-            int32_t ck = INT32_MAX;
-            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-            for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
-                const int32_t key = keys[t];
-                if (key == EMPTY_KEY)
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                if (key[c] == EMPTY_KEY)
                     continue;
                 double val;
                 if (MODE == MODE_PLP) {
-                    val = static_cast<double>(vals[t]);
+                    val = aff[c];
                 } else {
-                    if (key == cur)
+                    if (key[c] == cur)
                         continue;
-                    val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+                    val = plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
                 }
-                if (better(val, key, cv, ck)) {
+                if (better(val, key[c], cv, ck)) {
                     cv = val;
-                    ck = key;
+                    ck = key[c];
                 }
             }
-            argmax_xor<32>(cv, ck);
-            if (lane == 0) {
-                red_v[wid] = cv;
-                red_k[wid] = ck;
-            }
-            __syncthreads();
-            if (wid == 0) {
-                cv = lane < 8 ? red_v[lane] : -INFINITY;
-                ck = lane < 8 ? red_k[lane] : INT32_MAX;
-                argmax_xor<32>(cv, ck);
-                decide<MODE>(P, lane == 0, u, cur, ck, cv);
-                if (lane == 0) {
-                    ++st_n;
-                    st_e += static_cast<unsigned long long>(e - s);
-                }
-            }
-            __syncthreads();
         }
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cv = lane < 8 ? red_v[lane] : -INFINITY;
+            ck = lane < 8 ? red_k[lane] : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(e - s);
+            }
+        }
+        __syncthreads();
     }
     if (wid == 0)
         flush_stats(P, st_n, st_e);
@@ -456,7 +501,7 @@ __global__ void __launch_bounds__(256) k_sweep_block(SweepParams P) {
 // ---------------------------------------------------------------------------
 // tier HUB: chunk blocks insert into a per-hub global hash, then finalize
 // ---------------------------------------------------------------------------
-template <int MODE, bool W>
+template <int MODE, int VC>
 __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
     __shared__ double scratch[8][32];
     __shared__ double red_wc[8];
@@ -473,18 +518,30 @@ __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
     const uint32_t mask = static_cast<uint32_t>(P.hub_mask[h]);
     const int32_t cur = P.z[u];
     double wc = 0.0;
-    for (int64_t f = s + wid * 32; f < e; f += blockDim.x) {
-        bool valid = f + lane < e;
-        const int32_t v = valid ? P.col[f + lane] : 0;
-        const double wt = (W && valid) ? static_cast<double>(P.w[f + lane]) : 1.0;
-        if (MODE == MODE_PLM)
-            valid = valid && v != u;
-        const int32_t key = valid ? P.z[v] : 0;
-        if (MODE == MODE_PLM && valid && key == cur)
-            wc += wt;
-        double agg;
-        if (aggregate<W>(key, wt, valid, 0xffffffffu, scratch[wid], agg))
-            tinsert<double>(keys, vals, mask, key, agg);
+    for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += 256 * SW_ILP) {
+        int32_t vv[SW_ILP], kk[SW_ILP];
+        float ww[SW_ILP];
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            const int64_t f = f0 + c * 32 + lane;
+            vv[c] = f < e ? P.col[f] : -1;
+            ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c)
+            kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            bool valid = vv[c] >= 0;
+            if (MODE == MODE_PLM)
+                valid = valid && vv[c] != u;
+            const double wt = static_cast<double>(ww[c]);
+            if (MODE == MODE_PLM && valid && kk[c] == cur)
+                wc += wt;
+            double agg;
+            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                tinsert<double>(keys, vals, mask, kk[c], agg);
+        }
     }
     if (MODE == MODE_PLM) {
         wc = warp_sum(wc);
@@ -641,14 +698,37 @@ Sweeper::~Sweeper() {
         cudaGraphDestroy(graph_);
 }
 
-template <int MODE, bool W>
+template <class K>
+static void set_smem(K kernel, size_t bytes) {
+    CD_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+}
+
+// resident blocks per SM of a kernel (occupancy API, cached per kernel)
+template <class K>
+static int resident_blocks(K kernel, int threads, size_t smem) {
+    static std::map<const void *, int> cache;
+    const void *key = reinterpret_cast<const void *>(kernel);
+    auto it = cache.find(key);
+    if (it != cache.end())
+        return it->second;
+    int b = 0;
+    CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem));
+    b = b > 0 ? b : 1;
+    cache[key] = b;
+    return b;
+}
+
+template <int MODE, int VC>
 static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool capture, int &branch) {
+    using V = TallyT<VC>;
     const int sms = ctx->num_sms;
     // per-tier profiler families; cd_ctx_kernel_stats aggregates "plp_sweep.*"
     // and "plm_move.*" into the family the roofline reports
-    static const char *names[2][6] = {
-        {"plp_sweep.g8", "plp_sweep.g16", "plp_sweep.g32", "plp_sweep.warp", "plp_sweep.block", "plp_sweep.hub"},
-        {"plm_move.g8", "plm_move.g16", "plm_move.g32", "plm_move.warp", "plm_move.block", "plm_move.hub"}};
+    static const char *names[2][NUM_TIERS] = {
+        {"plp_sweep.g8", "plp_sweep.g16", "plp_sweep.g32", "plp_sweep.warp", "plp_sweep.block", "plp_sweep.block2",
+         "plp_sweep.hub"},
+        {"plm_move.g8", "plm_move.g16", "plm_move.g32", "plm_move.warp", "plm_move.block", "plm_move.block2",
+         "plm_move.hub"}};
     const char *fam = names[MODE][0];
     auto go = [&](auto launch) {
         if (capture) {
@@ -661,10 +741,15 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             launch(static_cast<cudaStream_t>(nullptr));
         }
     };
-    // grid sizes: enough warps to cover the tier list once, capped at a full wave
-    auto warps_grid = [&](int64_t nodes, int threads) {
-        const int64_t warps = (nodes + 31) / 32;
-        return grid_for(warps, threads / 32, sms * (2048 / threads));
+    // candidates per warp: about two rounds of work per warp (a round serves
+    // 32/G nodes; a bucket selects 1/buckets of the candidates)
+    auto chunk_for = [&](int npw) { return static_cast<int>(std::min<int64_t>(32, 2LL * npw * P.buckets)); };
+    // grid: one resident wave (grid-stride over the chunks), fewer blocks if
+    // the tier list is short
+    auto wave = [&](auto kernel, int threads, size_t smem) { return sms * resident_blocks(kernel, threads, smem); };
+    auto warps_grid_k = [&](auto kernel, int64_t nodes, int threads, int chunk) {
+        const int64_t warps = (nodes + chunk - 1) / chunk;
+        return grid_for(warps, threads / 32, wave(kernel, threads, 0));
     };
 #define CD_TIER_LAUNCH(KERNEL, GRID, BLOCK, SMEM, ...)                                               \
     go([&](cudaStream_t s) {                                                                         \
@@ -675,50 +760,78 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     })
     if (g->tier_nodes[TIER_G8]) {
         fam = names[MODE][TIER_G8];
-        CD_TIER_LAUNCH((k_sweep_direct<8, MODE, W>), warps_grid(g->tier_nodes[TIER_G8], 256), 256, 0, P,
-                       int(TIER_G8));
+        const int ch = chunk_for(4);
+        auto kfn = k_sweep_direct<8, MODE, VC>;
+        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G8], 256, ch);
+        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G8), ch);
     }
     if (g->tier_nodes[TIER_G16]) {
         fam = names[MODE][TIER_G16];
-        CD_TIER_LAUNCH((k_sweep_direct<16, MODE, W>), warps_grid(g->tier_nodes[TIER_G16], 256), 256, 0, P,
-                       int(TIER_G16));
+        const int ch = chunk_for(2);
+        auto kfn = k_sweep_direct<16, MODE, VC>;
+        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G16], 256, ch);
+        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16), ch);
     }
     if (g->tier_nodes[TIER_G32]) {
         fam = names[MODE][TIER_G32];
-        CD_TIER_LAUNCH((k_sweep_direct<32, MODE, W>), warps_grid(g->tier_nodes[TIER_G32], 256), 256, 0, P,
-                       int(TIER_G32));
+        const int ch = chunk_for(1);
+        auto kfn = k_sweep_direct<32, MODE, VC>;
+        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G32], 256, ch);
+        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G32), ch);
     }
     if (g->tier_nodes[TIER_WARP]) {
         fam = names[MODE][TIER_WARP];
-        CD_TIER_LAUNCH((k_sweep_warp<MODE, W>), warps_grid(g->tier_nodes[TIER_WARP], 128), 128, 0, P);
+        const int ch = chunk_for(1);
+        auto kfn = k_sweep_warp<MODE, VC>;
+        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_WARP], 128, ch);
+        CD_TIER_LAUNCH(kfn, grid, 128, 0, P, ch);
     }
     if (g->tier_nodes[TIER_BLOCK]) {
         fam = names[MODE][TIER_BLOCK];
-        using V = typename std::conditional<W, double, unsigned int>::type;
         const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
-        static bool attr_set = false;
-        if (!attr_set) {
-            CD_CUDA(cudaFuncSetAttribute(k_sweep_block<MODE, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-            attr_set = true;
+        static bool attr = false;
+        if (!attr) {
+            set_smem(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>, smem);
+            attr = true;
         }
-        const int nb = grid_for(g->tier_nodes[TIER_BLOCK], 1, sms * (W ? 2 : 3));
-        CD_TIER_LAUNCH((k_sweep_block<MODE, W>), nb, 256, smem, P);
+        const int nb = grid_for(g->tier_nodes[TIER_BLOCK], 1, sms * 8);
+        CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), nb, SW_BLOCK_THREADS, smem, P);
+    }
+    if (g->tier_nodes[TIER_BLOCK2]) {
+        fam = names[MODE][TIER_BLOCK2];
+        const size_t smem = size_t(BLOCK2_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
+        static bool attr2 = false;
+        if (!attr2) {
+            set_smem(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>, smem);
+            attr2 = true;
+        }
+        const int nb = grid_for(g->tier_nodes[TIER_BLOCK2], 1, sms * (VC == VC_REAL ? 2 : 3));
+        CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
     }
     if (g->n_hubs) {
         fam = names[MODE][TIER_HUB];
         const int nf = static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 4));
         go([&](cudaStream_t s) {
             if (s) {
-                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
+                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_insert<MODE, VC>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
                 CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
             } else {
-                CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, W>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
+                CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, VC>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
                 CD_LAUNCH(ctx, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
             }
         });
     }
 #undef CD_TIER_LAUNCH
+}
+
+template <int MODE>
+static void launch_tiers_vc(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool capture, int &branch) {
+    if (!g->weighted)
+        launch_tiers<MODE, VC_COUNT>(ctx, g, P, capture, branch);
+    else if (g->int_weights)
+        launch_tiers<MODE, VC_INT>(ctx, g, P, capture, branch);
+    else
+        launch_tiers<MODE, VC_REAL>(ctx, g, P, capture, branch);
 }
 
 void Sweeper::enqueue(bool capture) {
@@ -766,17 +879,10 @@ void Sweeper::enqueue(bool capture) {
         int branch = 0;
         if (capture)
             CD_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
-        if (plp) {
-            if (g->weighted)
-                launch_tiers<MODE_PLP, true>(ctx, g, P, capture, branch);
-            else
-                launch_tiers<MODE_PLP, false>(ctx, g, P, capture, branch);
-        } else {
-            if (g->weighted)
-                launch_tiers<MODE_PLM, true>(ctx, g, P, capture, branch);
-            else
-                launch_tiers<MODE_PLM, false>(ctx, g, P, capture, branch);
-        }
+        if (plp)
+            launch_tiers_vc<MODE_PLP>(ctx, g, P, capture, branch);
+        else
+            launch_tiers_vc<MODE_PLM>(ctx, g, P, capture, branch);
         for (int i = 0; i < branch; ++i)
             CD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[i], 0));
         if (c_.dense_best)
