@@ -406,7 +406,114 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const in
     (void)lane;
 }
 
+// Chunked flush of the global tables: the tables of all big rows are one
+// contiguous slot range; every block scans 8192 slots, finds each slot's row
+// by binary search and appends its entries with a warp-aggregated atomic on
+// the row's distinct counter (order is irrelevant: the sort phase follows).
+constexpr int64_t ENG_FLUSH_CHUNK = 8192;
+
+static __global__ void k_eng_global_zero(int64_t nb, const int32_t *rows, int64_t *deg2) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nb;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        deg2[rows[i]] = 0;
+}
+
+static __global__ void __launch_bounds__(256) k_eng_flush_chunked(const int64_t *fpre, const int32_t *rows, int64_t nb,
+                                                                  const int64_t *tab_off, int64_t total,
+                                                                  const int32_t *gkeys, const double *gvals,
+                                                                  const uint32_t *gcnts, int mode, EngineOut out) {
+    const int lane = lane_id();
+    const int64_t begin = static_cast<int64_t>(blockIdx.x) * ENG_FLUSH_CHUNK;
+    const int64_t end = min(total, begin + ENG_FLUSH_CHUNK);
+    for (int64_t s0 = begin + (threadIdx.x & ~31); s0 < end; s0 += blockDim.x) {
+        const int64_t s = s0 + lane;
+        const bool has = s < end && gkeys[s] != EMPTY_KEY;
+        int64_t i = -1;
+        if (has) {
+            int64_t lo = 0, hi = nb - 1;
+            while (lo < hi) {
+                const int64_t mid = (lo + hi + 1) >> 1;
+                if (tab_off[mid] <= s)
+                    lo = mid;
+                else
+                    hi = mid - 1;
+            }
+            i = lo;
+        }
+        const uint32_t hm = __ballot_sync(0xffffffffu, has);
+        const uint32_t peers = __match_any_sync(0xffffffffu, i) & hm;
+        int64_t base = 0;
+        const int leader = __ffs(peers) - 1;
+        const int64_t r = has ? rows[i] : 0;
+        if (has && lane == leader)
+            base = static_cast<int64_t>(atomicAdd(reinterpret_cast<unsigned long long *>(&out.deg2[r]),
+                                                  static_cast<unsigned long long>(__popc(peers))));
+        base = __shfl_sync(0xffffffffu, base, has ? leader : lane);
+        if (has) {
+            const int64_t pos = fpre[r] + base + __popc(peers & lanemask_lt());
+            out.tkey[pos] = gkeys[s];
+            out.tval[pos] = mode == DUP_ONE ? 1.0 : gvals[s];
+            if (gcnts[s] > 1 && out.flag && !*out.flag)
+                *out.flag = 1;
+        }
+    }
+}
+
 // ---- sort kernels -----------------------------------------------------------
+
+// rows of 33..512 distinct keys: one warp per row, bitonic sort in a
+// per-warp smem slice (__syncwarp only)
+constexpr int ENG_SORT_WARP_CAP = 512;
+
+static __global__ void __launch_bounds__(256) k_eng_sort_warpsmem(const int64_t *fpre, const int32_t *rows,
+                                                                  int64_t nrows, const int32_t *tkey,
+                                                                  const double *tval, const int64_t *off2,
+                                                                  int32_t *col, float *wout) {
+    __shared__ int32_t sk_all[8][ENG_SORT_WARP_CAP];
+    __shared__ float sv_all[8][ENG_SORT_WARP_CAP];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    int32_t *sk = sk_all[wid];
+    float *sv = sv_all[wid];
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t i = gw; i < nrows; i += nw) {
+        const int64_t r = rows[i];
+        const int64_t s = fpre[r], L = off2[r + 1] - off2[r];
+        int cap = 64;
+        while (cap < L)
+            cap <<= 1;
+        for (int t = lane; t < cap; t += 32) {
+            sk[t] = t < L ? tkey[s + t] : INT32_MAX;
+            sv[t] = t < L ? static_cast<float>(tval[s + t]) : 0.0f;
+        }
+        __syncwarp();
+        for (int kk = 2; kk <= cap; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+                for (int t = lane; t < cap; t += 32) {
+                    const int p = t ^ j;
+                    if (p > t) {
+                        const bool up = (t & kk) == 0;
+                        const int32_t a = sk[t], b = sk[p];
+                        if ((a > b) == up) {
+                            sk[t] = b;
+                            sk[p] = a;
+                            const float tv = sv[t];
+                            sv[t] = sv[p];
+                            sv[p] = tv;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        for (int t = lane; t < L; t += 32) {
+            col[off2[r] + t] = sk[t];
+            if (wout)
+                wout[off2[r] + t] = sv[t];
+        }
+        __syncwarp();
+    }
+}
 
 static __global__ void __launch_bounds__(256) k_eng_sort_warp(const int64_t *fpre, const int32_t *rows, int64_t nrows,
                                                        const int32_t *tkey, const double *tval,
@@ -706,8 +813,10 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         CD_LAUNCH(ctx, family, (k_eng_reduce_global_insert<Src>), static_cast<int>(ht[1]), 256, 0, src, fpre, L[3],
                   nb, static_cast<const int64_t *>(chunk_pre.p), static_cast<const int64_t *>(tab_off.p),
                   static_cast<const int64_t *>(tab_cap.p), gk.p, gv.p, gc.p);
-        CD_LAUNCH(ctx, family, k_eng_reduce_global_flush, grid_for(nb, 1, sms * 4), 512, 0, fpre, L[3], nb,
-                  static_cast<const int64_t *>(tab_off.p), static_cast<const int64_t *>(tab_cap.p),
+        CD_LAUNCH(ctx, family, k_eng_global_zero, grid_for(nb, 256, sms * 4), 256, 0, nb,
+                  static_cast<const int32_t *>(L[3]), deg2.p);
+        CD_LAUNCH(ctx, family, k_eng_flush_chunked, static_cast<int>((ht[0] + ENG_FLUSH_CHUNK - 1) / ENG_FLUSH_CHUNK),
+                  256, 0, fpre, static_cast<const int32_t *>(L[3]), nb, static_cast<const int64_t *>(tab_off.p), ht[0],
                   static_cast<const int32_t *>(gk.p), static_cast<const double *>(gv.p),
                   static_cast<const uint32_t *>(gc.p), int(mode), eo);
     }
@@ -732,8 +841,8 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
     // sort phase: classify by distinct length
     counts.zero();
     CD_LAUNCH(ctx, family, k_eng_classify, cls_blocks, 256, 0, nrows, static_cast<const int64_t *>(nullptr),
-              static_cast<const int64_t *>(deg2.p), int64_t(32), int64_t(ENG_SORT_BLOCK), int64_t(INT64_MAX), L[0],
-              L[1], L[2], L[3], counts.p);
+              static_cast<const int64_t *>(deg2.p), int64_t(32), int64_t(ENG_SORT_WARP_CAP), int64_t(ENG_SORT_BLOCK),
+              L[0], L[1], L[2], L[3], counts.p);
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
     float *wp = want_w ? wout.p : nullptr;
@@ -741,22 +850,26 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         CD_LAUNCH(ctx, family, k_eng_sort_warp, grid_for(hc[0], 8, sms * 8), 256, 0, fpre, L[0], int64_t(hc[0]),
                   static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
                   static_cast<const int64_t *>(off2.p), col.p, wp);
-    if (hc[1]) {
+    if (hc[1])
+        CD_LAUNCH(ctx, family, k_eng_sort_warpsmem, grid_for(hc[1], 8, sms * 8), 256, 0, fpre, L[1], int64_t(hc[1]),
+                  static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
+                  static_cast<const int64_t *>(off2.p), col.p, wp);
+    if (hc[2]) {
         const size_t smem = size_t(ENG_SORT_BLOCK) * (sizeof(double) + sizeof(int32_t));
         CD_CUDA(cudaFuncSetAttribute(k_eng_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        CD_LAUNCH(ctx, family, k_eng_sort_block, grid_for(hc[1], 1, sms * 2), 512, smem, fpre, L[1], int64_t(hc[1]),
+        CD_LAUNCH(ctx, family, k_eng_sort_block, grid_for(hc[2], 1, sms * 2), 512, smem, fpre, L[2], int64_t(hc[2]),
                   static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
                   static_cast<const int64_t *>(off2.p), col.p, wp);
     }
-    if (hc[2]) {
+    if (hc[3]) {
         DBuf<int32_t> k1(ctx, std::max<int64_t>(F_total, 1));
         DBuf<double> v1(ctx, std::max<int64_t>(F_total, 1));
         int bits = 1;
         while ((int64_t(1) << bits) < key_bound && bits < 31)
             ++bits;
         bits = (bits + 7) / 8 * 8;
-        CD_LAUNCH(ctx, family, k_eng_sort_radix, grid_for(hc[2], 1, sms), 1024, 0, fpre, L[2], int64_t(hc[2]), tkey.p,
+        CD_LAUNCH(ctx, family, k_eng_sort_radix, grid_for(hc[3], 1, sms), 1024, 0, fpre, L[3], int64_t(hc[3]), tkey.p,
                   tval.p, k1.p, v1.p, bits, static_cast<const int64_t *>(off2.p), col.p, wp);
     }
     return D2;
