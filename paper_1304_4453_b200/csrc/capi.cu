@@ -169,6 +169,26 @@ cd_status cd_ctx_create(int device, cd_ctx **out) {
         CD_CUDA(cudaDeviceGetDefaultMemPool(&ctx->pool, device));
         uint64_t thr = UINT64_MAX;
         CD_CUDA(cudaMemPoolSetAttribute(ctx->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        // Reserve device memory in the stream-ordered pool once: growing the
+        // pool inside a run maps pages (tens to hundreds of ms for large
+        // temporaries).  CD_POOL_RESERVE_FRAC (default 0.5) of free memory.
+        {
+            double frac = 0.5;
+            if (const char *e = std::getenv("CD_POOL_RESERVE_FRAC"))
+                frac = std::atof(e);
+            size_t free_b = 0, total_b = 0;
+            CD_CUDA(cudaMemGetInfo(&free_b, &total_b));
+            const size_t want = static_cast<size_t>(frac * static_cast<double>(free_b)) & ~size_t(0xFFFFF);
+            if (want > 0) {
+                void *p = nullptr;
+                if (cudaMallocAsync(&p, want, ctx->stream) == cudaSuccess) {
+                    cudaFreeAsync(p, ctx->stream);
+                    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
         cudaDeviceProp prop;
         CD_CUDA(cudaGetDeviceProperties(&prop, device));
         ctx->num_sms = prop.multiProcessorCount;

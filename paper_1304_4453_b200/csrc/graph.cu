@@ -248,17 +248,6 @@ __global__ void k_tier_scatter(int64_t n, const uint8_t *tier, int t, const int3
             out[rank[u]] = static_cast<int32_t>(u);
 }
 
-struct HubCapGen {
-    const int32_t *hubs;
-    const int64_t *off;
-    __device__ int64_t operator()(int64_t h) const {
-        const int64_t d = off[hubs[h] + 1] - off[hubs[h]];
-        int64_t c = 64;
-        while (c < 2 * d)
-            c <<= 1;
-        return c;
-    }
-};
 struct HubChunkGen {
     const int32_t *hubs;
     const int64_t *off;
@@ -268,22 +257,36 @@ struct HubChunkGen {
     }
 };
 
-__global__ void k_hub_chunks(int64_t nh, const int32_t *hubs, const int64_t *off, const int64_t *tab,
-                             const int64_t *chunk_pre, int32_t *mask, int32_t *chunk_hub, int32_t *chunk_part) {
+__host__ __device__ inline int hub_pbits_of(int64_t d) {
+    int b = 0;
+    while ((int64_t(HUB_PART) << b) < d && b < HUB_MAX_PBITS)
+        ++b;
+    return b;
+}
+
+struct HubPartGen {
+    const int32_t *hubs;
+    const int64_t *off;
+    __device__ int64_t operator()(int64_t h) const {
+        return int64_t(1) << hub_pbits_of(off[hubs[h] + 1] - off[hubs[h]]);
+    }
+};
+
+__global__ void k_hub_chunks(int64_t nh, const int32_t *hubs, const int64_t *off, const int64_t *chunk_pre,
+                             const int64_t *pbase, int32_t *pbits, int32_t *chunk_hub, int32_t *chunk_part,
+                             int32_t *part_hub) {
     for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
         const int64_t d = off[hubs[h] + 1] - off[hubs[h]];
-        int64_t c = 64;
-        while (c < 2 * d)
-            c <<= 1;
         if (threadIdx.x == 0)
-            mask[h] = static_cast<int32_t>(c - 1);
+            pbits[h] = hub_pbits_of(d);
         const int64_t nch = (d + HUB_CHUNK - 1) / HUB_CHUNK;
         for (int64_t k = threadIdx.x; k < nch; k += blockDim.x) {
             chunk_hub[chunk_pre[h] + k] = static_cast<int32_t>(h);
             chunk_part[chunk_pre[h] + k] = static_cast<int32_t>(k);
         }
+        for (int64_t q = pbase[h] + threadIdx.x; q < pbase[h + 1]; q += blockDim.x)
+            part_hub[q] = static_cast<int32_t>(h);
     }
-    (void)tab;
 }
 
 void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
@@ -322,32 +325,41 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
     // hubs
     g->n_hubs = g->tier_nodes[TIER_HUB];
     g->n_hub_chunks = 0;
-    g->hub_slots = 0;
+    g->n_hub_parts = 0;
+    g->hub_entries = 0;
     g->hubs = g->tlist.p + g->tier_start[TIER_HUB];
     if (g->n_hubs > 0) {
         const int64_t nh = g->n_hubs;
-        g->hub_tab.alloc(ctx, nh + 1);
         DBuf<int64_t> chunk_pre(ctx, nh + 1);
-        exclusive_scan<int64_t>(ctx, nh, HubCapGen{g->hubs, g->off.p}, g->hub_tab.p, g->hub_tab.p + nh);
+        g->hub_pbase.alloc(ctx, nh + 1);
         exclusive_scan<int64_t>(ctx, nh, HubChunkGen{g->hubs, g->off.p}, chunk_pre.p, chunk_pre.p + nh);
+        exclusive_scan<int64_t>(ctx, nh, HubPartGen{g->hubs, g->off.p}, g->hub_pbase.p, g->hub_pbase.p + nh);
         int64_t tot[2];
-        CD_CUDA(cudaMemcpyAsync(&tot[0], g->hub_tab.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
-        CD_CUDA(cudaMemcpyAsync(&tot[1], chunk_pre.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaMemcpyAsync(&tot[0], chunk_pre.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaMemcpyAsync(&tot[1], g->hub_pbase.p + nh, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
         CD_CUDA(cudaStreamSynchronize(ctx->stream));
-        g->hub_slots = tot[0];
-        g->n_hub_chunks = tot[1];
-        g->hub_mask.alloc(ctx, nh);
+        g->n_hub_chunks = tot[0];
+        g->n_hub_parts = tot[1];
+        g->hub_pbits.alloc(ctx, nh);
         g->chunk_hub.alloc(ctx, g->n_hub_chunks);
         g->chunk_part.alloc(ctx, g->n_hub_chunks);
+        g->part_hub.alloc(ctx, g->n_hub_parts);
         CD_LAUNCH(ctx, "bins", k_hub_chunks, grid_for(nh, 1, ctx->num_sms * 4), 128, 0, nh,
                   static_cast<const int32_t *>(g->hubs), static_cast<const int64_t *>(g->off.p),
-                  static_cast<const int64_t *>(g->hub_tab.p), static_cast<const int64_t *>(chunk_pre.p),
-                  g->hub_mask.p, g->chunk_hub.p, g->chunk_part.p);
-        g->hub_keys.alloc(ctx, g->hub_slots);
-        g->hub_vals.alloc(ctx, g->hub_slots);
+                  static_cast<const int64_t *>(chunk_pre.p), static_cast<const int64_t *>(g->hub_pbase.p),
+                  g->hub_pbits.p, g->chunk_hub.p, g->chunk_part.p, g->part_hub.p);
+        g->hub_entries = g->n_hub_chunks * HUB_CHUNK;  // >= sum of hub degrees
+        g->hp_cnt.alloc(ctx, g->n_hub_parts);
+        g->hp_cur.alloc(ctx, g->n_hub_parts);
+        g->hp_start.alloc(ctx, g->n_hub_parts + 1);
+        g->hp_key.alloc(ctx, g->hub_entries);
+        g->hp_val.alloc(ctx, g->hub_entries);
+        g->hp_best_val.alloc(ctx, g->n_hub_parts);
+        g->hp_best_key.alloc(ctx, g->n_hub_parts);
+        g->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));
+        g->hp_flag.alloc(ctx, 1);
+        g->hp_flag.zero();
         g->hub_aux.alloc(ctx, nh);
-        g->hub_keys.fill_bytes(0xff);
-        g->hub_vals.zero();
         g->hub_aux.zero();
     }
     g->binned = true;

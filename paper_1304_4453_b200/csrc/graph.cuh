@@ -32,6 +32,9 @@ constexpr int WARP_TABLE_CAP = 512;     // per-warp smem hash slots (>= 2*256)
 constexpr int BLOCK_TABLE_CAP = 2048;   // >= 2*1024
 constexpr int BLOCK2_TABLE_CAP = 8192;  // >= 2*4096
 constexpr int HUB_CHUNK = 4096;         // entries per hub chunk block
+constexpr int HUB_PART = 512;           // target pairs per hub partition
+constexpr int HUB_PART_CAP = 2048;      // smem slots of a partition block (4x HUB_PART)
+constexpr int HUB_MAX_PBITS = 13;       // partitions per hub <= 8192 (smem histogram)
 
 __host__ __device__ inline int tier_of_degree(int64_t d) {
     if (d <= 0)
@@ -78,15 +81,25 @@ struct cd_graph {
     int64_t tier_nodes[cdk::NUM_TIERS] = {};
     int64_t tier_start[cdk::NUM_TIERS + 1] = {};
     cdk::DBuf<int32_t> tlist;  // [tier_start[NUM_TIERS]]
-    // hub tier: static chunk grid and hash regions; hubs = tlist + tier_start[TIER_HUB]
-    int64_t n_hubs = 0, n_hub_chunks = 0, hub_slots = 0;
+    // hub tier: a static chunk grid (HUB_CHUNK entries per block) and a
+    // hash-partitioned pair scratch.  Hub h owns 2^hub_pbits[h] partitions
+    // [hub_pbase[h], hub_pbase[h+1]) of about HUB_PART pairs each.
+    int64_t n_hubs = 0, n_hub_chunks = 0, n_hub_parts = 0, hub_entries = 0;
     const int32_t *hubs = nullptr;  // [n_hubs] node ids (view into tlist)
-    cdk::DBuf<int64_t> hub_tab;     // [n_hubs] table offset
-    cdk::DBuf<int32_t> hub_mask;    // [n_hubs] capacity - 1
     cdk::DBuf<int32_t> chunk_hub;   // [n_hub_chunks]
     cdk::DBuf<int32_t> chunk_part;  // [n_hub_chunks] chunk index within hub
-    cdk::DBuf<int32_t> hub_keys;    // [hub_slots] EMPTY when free
-    cdk::DBuf<double> hub_vals;     // [hub_slots]
+    cdk::DBuf<int32_t> hub_pbits;   // [n_hubs]
+    cdk::DBuf<int64_t> hub_pbase;   // [n_hubs + 1]
+    cdk::DBuf<int32_t> part_hub;    // [n_hub_parts]
+    cdk::DBuf<int32_t> hp_cnt;      // [n_hub_parts] pairs per partition (per sub-sweep)
+    cdk::DBuf<int32_t> hp_cur;      // [n_hub_parts] scatter cursors
+    cdk::DBuf<int64_t> hp_start;    // [n_hub_parts + 1]
+    cdk::DBuf<int32_t> hp_key;      // [hub_entries] partitioned (label, weight) pairs
+    cdk::DBuf<double> hp_val;       // [hub_entries]
+    cdk::DBuf<double> hp_best_val;  // [n_hub_parts] per-partition best candidate
+    cdk::DBuf<int32_t> hp_best_key; // [n_hub_parts]
+    cdk::DBuf<int64_t> hp_scan;     // scan scratch (2 x tiles)
+    cdk::DBuf<int32_t> hp_flag;     // partition table overflow (sticky)
     cdk::DBuf<double> hub_aux;      // [n_hubs] per-hub w(u, C) accumulator (PLM)
 };
 

@@ -91,6 +91,27 @@ struct ArrayGen {
     __device__ T operator()(int64_t i) const { return a[i]; }
 };
 
+// Two-level exclusive scan on an explicit stream with caller-provided
+// scratch (no allocation: safe inside CUDA-graph capture).  n <= SCAN_TILE^2.
+// partial / pscan: >= ceil(n / SCAN_TILE) elements each.
+template <class T, class F>
+void exclusive_scan_on(cd_ctx *ctx, cudaStream_t s, int64_t n, F f, T *out, T *total, T *partial, T *pscan,
+                       const char *family) {
+    const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (tiles > SCAN_TILE)
+        fail(CD_EINTERNAL, "exclusive_scan_on: input too large");
+    if (tiles <= 1) {
+        CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, F>), 1, SCAN_THREADS, 0, n, f, static_cast<const T *>(nullptr),
+                    out, total);
+        return;
+    }
+    CD_LAUNCH_S(ctx, s, family, (k_scan_reduce<T, F>), static_cast<int>(tiles), SCAN_THREADS, 0, n, f, partial);
+    CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, ArrayGen<T>>), 1, SCAN_THREADS, 0, tiles,
+                ArrayGen<T>{partial}, static_cast<const T *>(nullptr), pscan, static_cast<T *>(nullptr));
+    CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, F>), static_cast<int>(tiles), SCAN_THREADS, 0, n, f,
+                static_cast<const T *>(pscan), out, total);
+}
+
 // out[i] = sum_{j<i} f(j) for i in [0, n); *total (device) = sum of all.
 // out may alias nothing read by f.
 template <class T, class F>

@@ -19,6 +19,9 @@
 #include "sweep.cuh"
 
 #include <cmath>
+#include <map>
+
+#include "scan.cuh"
 
 namespace cdk {
 
@@ -42,16 +45,22 @@ struct SweepParams {
     int32_t *dense_best;
     double *dense_gain;
     unsigned long long *stats;
-    // hub tier
+    // hub tier (hash-partitioned tally, graph.cuh)
     const int32_t *hubs;
-    const int64_t *hub_tab;
-    const int32_t *hub_mask;
     const int32_t *chunk_hub;
     const int32_t *chunk_part;
-    int32_t *hub_keys;
-    double *hub_vals;
+    const int32_t *hub_pbits;
+    const int64_t *hub_pbase;
+    const int32_t *part_hub;
+    int32_t *hp_cnt, *hp_cur;
+    const int64_t *hp_start;
+    int32_t *hp_key;
+    double *hp_val;
+    double *hp_best_val;
+    int32_t *hp_best_key;
+    int32_t *hp_flag;
     double *hub_aux;
-    int64_t n_hubs;
+    int64_t n_hubs, n_parts;
 };
 
 template <int VC>
@@ -499,24 +508,55 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
 }
 
 // ---------------------------------------------------------------------------
-// tier HUB: chunk blocks insert into a per-hub global hash, then finalize
+// tier HUB (deg > 4096): hash-partitioned tally.
+//   count   chunk blocks (HUB_CHUNK entries) pre-aggregate with match_any and
+//           count pairs per partition p = top pbits of (label * phi)
+//   scan    partition offsets
+//   scatter the same pairs, written contiguously per partition
+//   part    one block per partition aggregates its pairs in a smem hash and
+//           keeps the partition's best candidate
+//   decide  one block per hub reduces its partitions' candidates
+// A pass streams the hub's entries twice; there are no global hash tables.
 // ---------------------------------------------------------------------------
-template <int MODE, int VC>
-__global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
+struct CountGen {
+    const int32_t *c;
+    __device__ int64_t operator()(int64_t i) const { return c[i]; }
+};
+
+__device__ __forceinline__ int32_t hub_part(int32_t key, int pbits) {
+    return pbits ? static_cast<int32_t>((static_cast<uint32_t>(key) * 0x9E3779B1u) >> (32 - pbits)) : 0;
+}
+
+constexpr int HUB_PAIRS_SMEM = HUB_CHUNK * (sizeof(int32_t) + sizeof(double));
+
+template <int MODE, int VC, bool SCATTER>
+__global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
+    extern __shared__ unsigned char hub_smem[];
+    // count: hist[np]; scatter: pair list (HUB_CHUNK) + hist[np] + base[np]
+    double *pv = reinterpret_cast<double *>(hub_smem);
+    int32_t *pk = reinterpret_cast<int32_t *>(pv + (SCATTER ? HUB_CHUNK : 0));
+    int32_t *hist = pk + (SCATTER ? HUB_CHUNK : 0);
     __shared__ double scratch[8][32];
     __shared__ double red_wc[8];
+    __shared__ int32_t npairs;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int32_t h = P.chunk_hub[blockIdx.x];
     const int32_t u = P.hubs[h];
     if (!selected(P, load_key(P), u))
         return;
+    const int pbits = P.hub_pbits[h];
+    const int np = 1 << pbits;
+    int32_t *hbase = hist + np;
+    const int64_t pbase = P.hub_pbase[h];
     const int64_t s0 = P.off[u], e0 = P.off[u + 1];
     const int64_t s = s0 + static_cast<int64_t>(P.chunk_part[blockIdx.x]) * HUB_CHUNK;
     const int64_t e = min(e0, s + HUB_CHUNK);
-    int32_t *keys = P.hub_keys + P.hub_tab[h];
-    double *vals = P.hub_vals + P.hub_tab[h];
-    const uint32_t mask = static_cast<uint32_t>(P.hub_mask[h]);
     const int32_t cur = P.z[u];
+    for (int q = threadIdx.x; q < np; q += blockDim.x)
+        hist[q] = 0;
+    if (threadIdx.x == 0)
+        npairs = 0;
+    __syncthreads();
     double wc = 0.0;
     for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += 256 * SW_ILP) {
         int32_t vv[SW_ILP], kk[SW_ILP];
@@ -536,63 +576,122 @@ __global__ void __launch_bounds__(256) k_sweep_hub_insert(SweepParams P) {
             if (MODE == MODE_PLM)
                 valid = valid && vv[c] != u;
             const double wt = static_cast<double>(ww[c]);
-            if (MODE == MODE_PLM && valid && kk[c] == cur)
+            if (!SCATTER && MODE == MODE_PLM && valid && kk[c] == cur)
                 wc += wt;
             double agg;
-            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
-                tinsert<double>(keys, vals, mask, kk[c], agg);
+            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
+                const int32_t p = hub_part(kk[c], pbits);
+                atomicAdd(&hist[p], 1);
+                if (SCATTER) {
+                    const int32_t i = atomicAdd(&npairs, 1);
+                    pk[i] = kk[c];
+                    pv[i] = agg;
+                }
+            }
         }
     }
-    if (MODE == MODE_PLM) {
-        wc = warp_sum(wc);
-        if (lane == 0)
-            red_wc[wid] = wc;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            double t = 0.0;
-            for (int q = 0; q < 8; ++q)
-                t += red_wc[q];
-            if (t != 0.0)
-                atomicAdd(&P.hub_aux[h], t);
+    __syncthreads();
+    if (!SCATTER) {
+        for (int q = threadIdx.x; q < np; q += blockDim.x)
+            if (hist[q])
+                atomicAdd(&P.hp_cnt[pbase + q], hist[q]);
+        if (MODE == MODE_PLM) {
+            wc = warp_sum(wc);
+            if (lane == 0)
+                red_wc[wid] = wc;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double t = 0.0;
+                for (int q = 0; q < 8; ++q)
+                    t += red_wc[q];
+                if (t != 0.0)
+                    atomicAdd(&P.hub_aux[h], t);
+            }
         }
+        if (threadIdx.x == 0)
+            atomicAdd(&P.stats[P.w ? 2 : 1], static_cast<unsigned long long>(e - s));
+        return;
     }
-    if (threadIdx.x == 0)
-        atomicAdd(&P.stats[P.w ? 2 : 1], static_cast<unsigned long long>(e - s));
+    // scatter: one global reservation per (block, partition), then local slots
+    for (int q = threadIdx.x; q < np; q += blockDim.x) {
+        hbase[q] = hist[q] ? atomicAdd(&P.hp_cur[pbase + q], hist[q]) : 0;
+        hist[q] = 0;
+    }
+    __syncthreads();
+    const int32_t n = npairs;
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const int32_t key = pk[i];
+        const int32_t p = hub_part(key, pbits);
+        const int64_t pos = P.hp_start[pbase + p] + hbase[p] + atomicAdd(&hist[p], 1);
+        P.hp_key[pos] = key;
+        P.hp_val[pos] = pv[i];
+    }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
-    __shared__ double red_v[16];
-    __shared__ int32_t red_k[16];
-    const int lane = lane_id(), wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-    const unsigned long long bkey = load_key(P);
-    for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
-        const int32_t u = P.hubs[h];
-        if (!selected(P, bkey, u))
+template <int MODE, int VC>
+__global__ void __launch_bounds__(256) k_hub_part(SweepParams P) {
+    using V = TallyT<VC>;
+    extern __shared__ unsigned char hub_smem[];
+    V *vals = reinterpret_cast<V *>(hub_smem);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + HUB_PART_CAP);
+    __shared__ double red_v[8];
+    __shared__ int32_t red_k[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    for (int64_t q = blockIdx.x; q < P.n_parts; q += gridDim.x) {
+        const int32_t nq = P.hp_cnt[q];
+        if (nq == 0) {
+            if (threadIdx.x == 0) {
+                P.hp_best_val[q] = -INFINITY;
+                P.hp_best_key[q] = INT32_MAX;
+            }
             continue;
-        int32_t *keys = P.hub_keys + P.hub_tab[h];
-        double *vals = P.hub_vals + P.hub_tab[h];
-        const int64_t cap = static_cast<int64_t>(P.hub_mask[h]) + 1;
+        }
+        const int32_t h = P.part_hub[q];
+        const int32_t u = P.hubs[h];
         const int32_t cur = P.z[u];
+        uint32_t cap = 64;
+        while (cap < 2u * static_cast<uint32_t>(nq) && cap < HUB_PART_CAP)
+            cap <<= 1;
+        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+            keys[t] = EMPTY_KEY;
+            vals[t] = V(0);
+        }
+        __syncthreads();
+        const int64_t st = P.hp_start[q];
+        for (int32_t i = threadIdx.x; i < nq; i += blockDim.x) {
+            const int32_t key = P.hp_key[st + i];
+            const V w = static_cast<V>(P.hp_val[st + i]);
+            uint32_t sl = hash_slot(key, cap - 1);
+            bool done = false;
+            for (uint32_t probe = 0; probe < cap; ++probe) {
+                const int32_t old = atomicCAS(&keys[sl], EMPTY_KEY, key);
+                if (old == EMPTY_KEY || old == key) {
+                    atomicAdd(&vals[sl], w);
+                    done = true;
+                    break;
+                }
+                sl = (sl + 1) & (cap - 1);
+            }
+            if (!done)
+                *P.hp_flag = 1;  // more distinct labels than slots: reported by the host
+        }
+        __syncthreads();
         const double wc = (MODE == MODE_PLM) ? P.hub_aux[h] : 0.0;
         const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
         const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        double cv = -INFINITY;
         int32_t ck = INT32_MAX;
-        for (int64_t t = threadIdx.x; t < cap; t += blockDim.x) {
+        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
             const int32_t key = keys[t];
             if (key == EMPTY_KEY)
                 continue;
-            const double a = vals[t];
-            keys[t] = EMPTY_KEY;
-            vals[t] = 0.0;
             double val;
             if (MODE == MODE_PLP) {
-                val = a;
+                val = static_cast<double>(vals[t]);
             } else {
                 if (key == cur)
                     continue;
-                val = plm_delta(a, wc, vol_c, P.vols[key], vol_u, P);
+                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
             }
             if (better(val, key, cv, ck)) {
                 cv = val;
@@ -605,10 +704,52 @@ __global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
             red_k[wid] = ck;
         }
         __syncthreads();
+        if (threadIdx.x == 0) {
+            cv = red_v[0];
+            ck = red_k[0];
+            for (int w2 = 1; w2 < 8; ++w2)
+                if (better(red_v[w2], red_k[w2], cv, ck)) {
+                    cv = red_v[w2];
+                    ck = red_k[w2];
+                }
+            P.hp_best_val[q] = cv;
+            P.hp_best_key[q] = ck;
+        }
+        __syncthreads();
+    }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
+    __shared__ double red_v[8];
+    __shared__ int32_t red_k[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const unsigned long long bkey = load_key(P);
+    for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
+        const int32_t u = P.hubs[h];
+        if (!selected(P, bkey, u))
+            continue;
+        double cv = -INFINITY;
+        int32_t ck = INT32_MAX;
+        for (int64_t q = P.hub_pbase[h] + threadIdx.x; q < P.hub_pbase[h + 1]; q += blockDim.x) {
+            const double v = P.hp_best_val[q];
+            const int32_t k = P.hp_best_key[q];
+            if (better(v, k, cv, ck)) {
+                cv = v;
+                ck = k;
+            }
+        }
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
         if (wid == 0) {
-            cv = lane < nwarps ? red_v[lane] : -INFINITY;
-            ck = lane < nwarps ? red_k[lane] : INT32_MAX;
+            cv = lane < 8 ? red_v[lane] : -INFINITY;
+            ck = lane < 8 ? red_k[lane] : INT32_MAX;
             argmax_xor<32>(cv, ck);
+            const int32_t cur = P.z[u];
             decide<MODE>(P, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
                 if (MODE == MODE_PLM)
@@ -623,20 +764,35 @@ __global__ void __launch_bounds__(512) k_sweep_hub_final(SweepParams P) {
 // ---------------------------------------------------------------------------
 // apply: the bucket's moves become visible to the next sub-sweep
 // ---------------------------------------------------------------------------
+// A changed node activates its neighbours (H/plp.hpp:127-130).  When a
+// bucket moved more than n/16 nodes, every node is activated instead (n bytes
+// instead of sum-of-degrees scattered bytes): a node whose neighbourhood did
+// not change re-derives the label it already has, so the result is identical.
 __global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const int32_t *mv_label,
                                                    const int32_t *mv_count, int32_t *z, uint8_t *active,
-                                                   const int64_t *off, const int32_t *col, long long *total) {
+                                                   const int64_t *off, const int32_t *col, long long *total,
+                                                   int64_t n) {
     const int64_t count = *mv_count;
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
+    const bool dense = active && count > n / 16;
+    if (dense)
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 15) / 16;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            if (16 * i + 16 <= n)
+                reinterpret_cast<uint4 *>(active)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+            else
+                for (int64_t j = 16 * i; j < n; ++j)
+                    active[j] = 1;
+        }
     for (int64_t i = gw; i < count; i += nw) {
         const int32_t u = mv_node[i];
         if (lane == 0)
             z[u] = mv_label[i];
-        if (active)  // H/plp.hpp:127-130: a changed node activates its neighbours
+        if (active && !dense)
             for (int64_t e = off[u] + lane; e < off[u + 1]; e += 32)
                 active[col[e]] = 1;
     }
@@ -810,15 +966,39 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if (g->n_hubs) {
         fam = names[MODE][TIER_HUB];
-        const int nf = static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 4));
+        const int max_np = 1 << HUB_MAX_PBITS;
+        const size_t smem_count = size_t(max_np) * sizeof(int32_t);
+        const size_t smem_scatter = size_t(HUB_PAIRS_SMEM) + 2 * size_t(max_np) * sizeof(int32_t);
+        const size_t smem_part = size_t(HUB_PART_CAP) * (sizeof(V) + sizeof(int32_t));
+        static bool attr = false;
+        if (!attr) {
+            set_smem(k_hub_pairs<MODE, VC, false>, smem_count);
+            set_smem(k_hub_pairs<MODE, VC, true>, smem_scatter);
+            set_smem(k_hub_part<MODE, VC>, smem_part);
+            attr = true;
+        }
+        const int nchunks = static_cast<int>(g->n_hub_chunks);
+        const int npart = static_cast<int>(std::min<int64_t>(
+            g->n_hub_parts, int64_t(sms) * resident_blocks(k_hub_part<MODE, VC>, 256, smem_part)));
+        const int ndec = static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 8));
         go([&](cudaStream_t s) {
-            if (s) {
-                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_insert<MODE, VC>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
-                CD_LAUNCH_S(ctx, s, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
-            } else {
-                CD_LAUNCH(ctx, fam, (k_sweep_hub_insert<MODE, VC>), static_cast<int>(g->n_hub_chunks), 256, 0, P);
-                CD_LAUNCH(ctx, fam, (k_sweep_hub_final<MODE>), nf, 512, 0, P);
-            }
+            cudaStream_t st = s ? s : ctx->stream;
+            CD_CUDA(cudaMemsetAsync(g->hp_cnt.p, 0, g->n_hub_parts * sizeof(int32_t), st));
+            CD_CUDA(cudaMemsetAsync(g->hp_cur.p, 0, g->n_hub_parts * sizeof(int32_t), st));
+            const int64_t tiles = (g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1;
+            auto run = [&](auto launch_one) {
+                launch_one((k_hub_pairs<MODE, VC, false>), nchunks, smem_count);
+                exclusive_scan_on<int64_t>(ctx, st, g->n_hub_parts, CountGen{g->hp_cnt.p}, g->hp_start.p,
+                                           g->hp_start.p + g->n_hub_parts, g->hp_scan.p, g->hp_scan.p + tiles,
+                                           fam);
+                launch_one((k_hub_pairs<MODE, VC, true>), nchunks, smem_scatter);
+                launch_one((k_hub_part<MODE, VC>), npart, smem_part);
+                launch_one((k_hub_decide<MODE>), ndec, size_t(0));
+            };
+            if (s)
+                run([&](auto kernel, int grid, size_t smem) { CD_LAUNCH_S(ctx, s, fam, kernel, grid, 256, smem, P); });
+            else
+                run([&](auto kernel, int grid, size_t smem) { CD_LAUNCH(ctx, fam, kernel, grid, 256, smem, P); });
         });
     }
 #undef CD_TIER_LAUNCH
@@ -861,14 +1041,22 @@ void Sweeper::enqueue(bool capture) {
     P.dense_gain = c_.dense_gain;
     P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : 3);
     P.hubs = g->hubs;
-    P.hub_tab = g->hub_tab.p;
-    P.hub_mask = g->hub_mask.p;
     P.chunk_hub = g->chunk_hub.p;
     P.chunk_part = g->chunk_part.p;
-    P.hub_keys = g->hub_keys.p;
-    P.hub_vals = g->hub_vals.p;
+    P.hub_pbits = g->hub_pbits.p;
+    P.hub_pbase = g->hub_pbase.p;
+    P.part_hub = g->part_hub.p;
+    P.hp_cnt = g->hp_cnt.p;
+    P.hp_cur = g->hp_cur.p;
+    P.hp_start = g->hp_start.p;
+    P.hp_key = g->hp_key.p;
+    P.hp_val = g->hp_val.p;
+    P.hp_best_val = g->hp_best_val.p;
+    P.hp_best_key = g->hp_best_key.p;
+    P.hp_flag = g->hp_flag.p;
     P.hub_aux = g->hub_aux.p;
     P.n_hubs = g->n_hubs;
+    P.n_parts = g->n_hub_parts;
     const int sms = ctx->num_sms;
     const bool plp = c_.mode == MODE_PLP;
     if (!c_.dense_best)
@@ -892,7 +1080,8 @@ void Sweeper::enqueue(bool capture) {
             CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0,
                       static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
                       static_cast<const int32_t *>(cnt_.p + b), c_.z, c_.active,
-                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), total_.p);
+                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), total_.p,
+                      g->n);
         else
             CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0,
                       static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
@@ -932,9 +1121,14 @@ void Sweeper::pass(uint64_t key) {
 
 int64_t Sweeper::take_moves() {
     long long h = 0;
+    int32_t overflow = 0;
     CD_CUDA(cudaMemcpyAsync(&h, total_.p, sizeof(h), cudaMemcpyDeviceToHost, ctx_->stream));
     CD_CUDA(cudaMemsetAsync(total_.p, 0, sizeof(long long), ctx_->stream));
+    if (g_->n_hubs)
+        CD_CUDA(cudaMemcpyAsync(&overflow, g_->hp_flag.p, sizeof(overflow), cudaMemcpyDeviceToHost, ctx_->stream));
     CD_CUDA(cudaStreamSynchronize(ctx_->stream));
+    if (overflow)
+        fail(CD_EINTERNAL, "hub partition table overflow (more distinct labels per partition than slots)");
     return h;
 }
 
