@@ -77,6 +77,8 @@ typedef struct cd_louvain_config {
     int64_t move_theta;      /* device: stop a move phase once a pass moves <= this;
                                 <0: floor(n/100000) of the level's graph     */
     double move_tol;         /* device: ... or <= move_tol * n (0 disables)  */
+    double move_stall;       /* device: ... or (from pass 8 on) when a pass moves more than
+                                move_stall x the moves two passes earlier (0 disables) */
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */

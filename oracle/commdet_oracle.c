@@ -1257,6 +1257,7 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
     int32_t *mv_u = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     int32_t *mv_l = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     int changed = 0;
+    int64_t hist0 = -1, hist1 = -1; /* moves two passes / one pass earlier */
     for (int64_t pass = 0; pass < cfg->max_move_iterations; ++pass) {
         int64_t moved = 0;
         const uint64_t key = cdo_bucket_key(cfg->seed, salt + (uint64_t)pass);
@@ -1292,6 +1293,10 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
         changed = 1;
         if (moved <= theta)
             break;
+        if (cfg->move_stall > 0.0 && pass >= 8 && (double)moved > cfg->move_stall * (double)hist0)
+            break;
+        hist0 = hist1;
+        hist1 = moved;
     }
     *changed_out = changed;
     free(vols);

@@ -135,6 +135,7 @@ typedef struct {
     int32_t singleton_guard;
     int64_t move_theta; /* <0: floor(n/100000) per level */
     double move_tol;    /* stop also once a pass moves <= move_tol * n */
+    double move_stall;  /* ... or (pass >= 8) moves > move_stall * moves two passes earlier */
 } cdo_louvain_config;
 
 /* bucket key / id: the order every device driver uses. */

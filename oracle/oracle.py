@@ -51,7 +51,7 @@ class _LouvainCfg(C.Structure):
     _fields_ = [
         ("gamma", C.c_double), ("max_move_iterations", C.c_int64), ("max_levels", C.c_int64),
         ("seed", C.c_uint64), ("buckets", C.c_int32), ("refine", C.c_int32), ("singleton_guard", C.c_int32),
-        ("move_theta", C.c_int64), ("move_tol", C.c_double),
+        ("move_theta", C.c_int64), ("move_tol", C.c_double), ("move_stall", C.c_double),
     ]
 
 
@@ -437,9 +437,9 @@ def plp_bucketed(g: CSR, theta=-1, max_iterations=100, seed=1, buckets=4, initia
 
 
 def louvain_cfg(gamma=1.0, max_move_iterations=32, max_levels=64, seed=1, buckets=4, refine=False,
-                singleton_guard=True, move_theta=-1, move_tol=1e-3):
+                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95):
     return _LouvainCfg(gamma, max_move_iterations, max_levels, seed, buckets, int(refine), int(singleton_guard),
-                       move_theta, move_tol)
+                       move_theta, move_tol, move_stall)
 
 
 def move_phase_bucketed(g: CSR, z, salt=0, **kw):

@@ -156,6 +156,7 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
+    int64_t hist[2] = {-1, -1};  // moves of the two previous passes
     for (int64_t pass = 0; pass < cfg.max_move_iterations; ++pass) {
         sw.pass(bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass)));
         const int64_t moved = sw.take_moves();
@@ -171,6 +172,12 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
         changed = true;
         if (moved <= theta)
             break;
+        // stalled: a non-converging tail of oscillating movers
+        if (cfg.move_stall > 0.0 && pass >= 8 &&
+            static_cast<double>(moved) > cfg.move_stall * static_cast<double>(hist[0]))
+            break;
+        hist[0] = hist[1];
+        hist[1] = moved;
     }
     return changed;
 }

@@ -35,10 +35,10 @@ def main():
     if "r20w" in names:
         graphs["r20w"] = P.generate_rmat(20, 16, weighted=True, seed=1, ctx=ctx)
     variants = []
-    for K in (2, 4, 8):
-        for tol in (0.0, 1e-4, 1e-3):
-            variants.append(dict(buckets=K, move_tol=tol, singleton_guard=True))
-    variants.append(dict(buckets=4, move_tol=0.0, singleton_guard=False))
+    for stall in (0.0, 0.95, 0.9):
+        for tol in (0.0, 1e-3):
+            variants.append(dict(buckets=4, move_tol=tol, move_stall=stall, singleton_guard=True))
+    variants.append(dict(buckets=8, move_tol=1e-3, move_stall=0.95, singleton_guard=True))
     for name, g in graphs.items():
         for v in variants:
             for refine in (False,):
