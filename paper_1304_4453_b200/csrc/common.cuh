@@ -309,6 +309,26 @@ __device__ __forceinline__ int32_t warp_append(int32_t *counter, bool pred) {
     return base + __popc(mask & lanemask_lt());
 }
 
+// Sum v over the lanes (with pred) sharing `key`; returns true on the group
+// leader (lowest lane), which receives the sum in `out`.  scratch is 32
+// doubles private to the calling warp.  Must be called by the full warp.
+__device__ __forceinline__ bool warp_aggregate_sum(int32_t key, double v, bool pred, double *scratch, double &out) {
+    const int lane = lane_id();
+    const uint32_t vm = __ballot_sync(0xffffffffu, pred);
+    const uint32_t peers = __match_any_sync(0xffffffffu, key) & vm;
+    scratch[lane] = v;
+    __syncwarp();
+    const bool leader = pred && (__ffs(peers) - 1) == lane;
+    if (leader) {
+        double s = 0.0;
+        for (uint32_t p = peers; p; p &= p - 1)
+            s += scratch[__ffs(p) - 1];
+        out = s;
+    }
+    __syncwarp();
+    return leader;
+}
+
 inline uint64_t next_pow2(uint64_t x) {
     uint64_t p = 1;
     while (p < x)

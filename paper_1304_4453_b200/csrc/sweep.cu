@@ -66,6 +66,8 @@ struct SweepParams {
 template <int VC>
 using TallyT = typename std::conditional<VC == VC_REAL, double, unsigned int>::type;
 
+constexpr int SW_ILP = 4;  // independent loads per lane per round
+
 __device__ __forceinline__ double plm_delta(double aff_d, double w_c, double vol_c, double vols_d, double vol_u,
                                             const SweepParams &P) {
     // (aff[d] - w_c) * inv_total + gamma * (vol_c - vols[d]) * vol_u * inv_sq2
@@ -153,11 +155,53 @@ __device__ __forceinline__ unsigned long long load_key(const SweepParams &P) {
     return P.buckets > 1 ? *P.keyp : 0ULL;
 }
 
-// Applies one decision.  Must be reached by all lanes of the warp (the move
-// append is warp-aggregated); only lanes with `act` carry a decision.
+// Per-warp register queue of moves: lane i holds entry i; one global atomic
+// per 32 moves instead of one per warp-round (the bucket's move counter is a
+// single hot address).
+struct MoveQueue {
+    int32_t u = 0, l = 0;
+    int n = 0;  // warp-uniform fill
+
+    __device__ __forceinline__ void flush(const SweepParams &P) {
+        if (n == 0)
+            return;
+        int32_t base = 0;
+        if (lane_id() == 0)
+            base = atomicAdd(P.mv_count, n);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (lane_id() < n) {
+            P.mv_node[base + lane_id()] = u;
+            P.mv_label[base + lane_id()] = l;
+        }
+        n = 0;
+    }
+    // all lanes: lanes with `moved` enqueue (node, label)
+    __device__ __forceinline__ void push(const SweepParams &P, bool moved, int32_t node, int32_t label) {
+        const uint32_t mask = __ballot_sync(0xffffffffu, moved);
+        const int cnt = __popc(mask);
+        if (cnt == 0)
+            return;
+        if (n + cnt > 32)
+            flush(P);
+        const int lane = lane_id();
+        const int k = lane - n;  // this lane receives the k-th mover
+        const bool recv = k >= 0 && k < cnt;
+        const int src = recv ? static_cast<int>(__fns(mask, 0, k + 1)) : lane;
+        const int32_t nu = __shfl_sync(0xffffffffu, node, src);
+        const int32_t nl = __shfl_sync(0xffffffffu, label, src);
+        if (recv) {
+            u = nu;
+            l = nl;
+        }
+        n += cnt;
+    }
+};
+
+// Applies one decision.  Must be reached by all lanes of the warp (moves are
+// queued warp-collectively); only lanes with `act` carry a decision.
 template <int MODE>
-__device__ __forceinline__ void decide(const SweepParams &P, bool act, int32_t u, int32_t cur, int32_t best,
-                                       double val) {
+__device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool act, int32_t u, int32_t cur,
+                                       int32_t best, double val) {
     bool moved = false;
     if (act) {
         if (MODE == MODE_PLP) {
@@ -176,11 +220,7 @@ __device__ __forceinline__ void decide(const SweepParams &P, bool act, int32_t u
         }
         return;
     }
-    const int32_t pos = warp_append(P.mv_count, moved);
-    if (moved) {
-        P.mv_node[pos] = u;
-        P.mv_label[pos] = best;
-    }
+    q.push(P, moved, u, best);
     if (MODE == MODE_PLP && act && !moved && P.active)
         P.active[u] = 0;
 }
@@ -212,6 +252,7 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
     // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
     // many of them, so the tail of a sub-sweep stays occupied
     for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
@@ -258,13 +299,14 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
             }
             argmax_xor<G>(cv, ck);
             const bool act = has && k == 0;
-            decide<MODE>(P, act, u, cur, ck, cv);
+            decide<MODE>(P, q, act, u, cur, ck, cv);
             if (act) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(d);
             }
         }
     }
+    q.flush(P);
     flush_stats(P, st_n, st_e);
 }
 
@@ -291,6 +333,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
     // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
     // many of them, so the tail of a sub-sweep stays occupied
     for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
@@ -343,25 +386,35 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
             int32_t ck = INT32_MAX;
             const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
             const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-            for (uint32_t t = lane; t < cap; t += 32) {
-                const int32_t key = keys[t];
-                if (key == EMPTY_KEY)
-                    continue;
-                double val;
-                if (MODE == MODE_PLP) {
-                    val = static_cast<double>(vals[t]);
-                } else {
-                    if (key == cur)
-                        continue;
-                    val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+            // slots in rounds of SW_ILP per lane: the vols[key] gathers of a
+            // round are independent and in flight together
+            for (uint32_t t0 = lane; t0 < cap; t0 += 32 * SW_ILP) {
+                int32_t key[SW_ILP];
+                double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    const uint32_t t = t0 + 32 * c;
+                    key[c] = t < cap ? keys[t] : EMPTY_KEY;
+                    aff[c] = t < cap ? static_cast<double>(vals[t]) : 0.0;
                 }
-                if (better(val, key, cv, ck)) {
-                    cv = val;
-                    ck = key;
+                if (MODE == MODE_PLM) {
+#pragma unroll
+                    for (int c = 0; c < SW_ILP; ++c)
+                        vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
+                        continue;
+                    const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
+                    if (better(val, key[c], cv, ck)) {
+                        cv = val;
+                        ck = key[c];
+                    }
                 }
             }
             argmax_xor<32>(cv, ck);
-            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(e - s);
@@ -369,6 +422,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
             __syncwarp();
         }
     }
+    q.flush(P);
     flush_stats(P, st_n, st_e);
 }
 
@@ -378,7 +432,6 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
 // independent global loads in flight.
 // ---------------------------------------------------------------------------
 constexpr int SW_BLOCK_THREADS = 256;
-constexpr int SW_ILP = 4;
 
 template <int MODE, int VC, int CAP, int TIER>
 __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
@@ -395,6 +448,7 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     const int64_t count = P.tstart[TIER + 1] - P.tstart[TIER];
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
     // one candidate per block iteration; unselected candidates cost one load
     for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
         const int32_t u = list[i];
@@ -495,7 +549,7 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
             cv = lane < 8 ? red_v[lane] : -INFINITY;
             ck = lane < 8 ? red_k[lane] : INT32_MAX;
             argmax_xor<32>(cv, ck);
-            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(e - s);
@@ -504,7 +558,8 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
         __syncthreads();
     }
     if (wid == 0)
-        flush_stats(P, st_n, st_e);
+        q.flush(P);
+    flush_stats(P, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
@@ -681,21 +736,29 @@ __global__ void __launch_bounds__(256) k_hub_part(SweepParams P) {
         const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
         double cv = -INFINITY;
         int32_t ck = INT32_MAX;
-        for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
-            const int32_t key = keys[t];
-            if (key == EMPTY_KEY)
-                continue;
-            double val;
-            if (MODE == MODE_PLP) {
-                val = static_cast<double>(vals[t]);
-            } else {
-                if (key == cur)
-                    continue;
-                val = plm_delta(static_cast<double>(vals[t]), wc, vol_c, P.vols[key], vol_u, P);
+        for (uint32_t t0 = threadIdx.x; t0 < cap; t0 += blockDim.x * SW_ILP) {
+            int32_t key[SW_ILP];
+            double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                const uint32_t t = t0 + blockDim.x * c;
+                key[c] = t < cap ? keys[t] : EMPTY_KEY;
+                aff[c] = t < cap ? static_cast<double>(vals[t]) : 0.0;
             }
-            if (better(val, key, cv, ck)) {
-                cv = val;
-                ck = key;
+            if (MODE == MODE_PLM) {
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c)
+                    vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
+                    continue;
+                const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
+                if (better(val, key[c], cv, ck)) {
+                    cv = val;
+                    ck = key[c];
+                }
             }
         }
         argmax_xor<32>(cv, ck);
@@ -725,6 +788,7 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
     __shared__ int32_t red_k[8];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const unsigned long long bkey = load_key(P);
+    MoveQueue mq;
     for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
         const int32_t u = P.hubs[h];
         if (!selected(P, bkey, u))
@@ -750,7 +814,7 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
             ck = lane < 8 ? red_k[lane] : INT32_MAX;
             argmax_xor<32>(cv, ck);
             const int32_t cur = P.z[u];
-            decide<MODE>(P, lane == 0, u, cur, ck, cv);
+            decide<MODE>(P, mq, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
                 if (MODE == MODE_PLM)
                     P.hub_aux[h] = 0.0;
@@ -759,6 +823,8 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
         }
         __syncthreads();
     }
+    if (wid == 0)
+        mq.flush(P);
 }
 
 // ---------------------------------------------------------------------------
@@ -801,20 +867,35 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const
 __global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const int32_t *mv_label,
                                                    const int32_t *mv_count, int32_t *z, double *vols, int32_t *csize,
                                                    const double *vol, long long *total) {
+    __shared__ double scratch[8][32];
     const int64_t count = *mv_count;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
-    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int32_t u = mv_node[i], d = mv_label[i];
-        const int32_t c = z[u];
-        z[u] = d;
-        const double vu = vol[u];  // H/louvain.hpp:121-125
-        atomicAdd(&vols[c], -vu);
-        atomicAdd(&vols[d], vu);
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < count;
+         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < count;
+        const int32_t u = valid ? mv_node[i] : 0;
+        const int32_t d = valid ? mv_label[i] : -1;
+        const int32_t c = valid ? z[u] : -1;
+        if (valid)
+            z[u] = d;
+        const double vu = valid ? vol[u] : 0.0;  // H/louvain.hpp:121-125
+        // moves into / out of the same community combine per warp first
+        double s;
+        if (warp_aggregate_sum(d, vu, valid, scratch[wid], s))
+            atomicAdd(&vols[d], s);
+        if (warp_aggregate_sum(c, vu, valid, scratch[wid], s))
+            atomicAdd(&vols[c], -s);
         if (csize) {
-            atomicSub(&csize[c], 1);
-            atomicAdd(&csize[d], 1);
+            const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+            const uint32_t pd = __match_any_sync(0xffffffffu, d) & vm;
+            if (valid && (__ffs(pd) - 1) == lane)
+                atomicAdd(&csize[d], __popc(pd));
+            const uint32_t pc = __match_any_sync(0xffffffffu, c) & vm;
+            if (valid && (__ffs(pc) - 1) == lane)
+                atomicSub(&csize[c], __popc(pc));
         }
     }
 }
