@@ -131,6 +131,11 @@ typedef struct cd_graph_info {
     int32_t reserved;
     int64_t max_degree;
     int64_t isolated;
+    /* row shard (cd_graph_shard): rows [own_lo, own_hi) of shard_rank / shard_size;
+     * a whole graph reports 0 / 1 and [0, n).  D counts the local entries. */
+    int32_t shard_rank, shard_size;
+    int64_t own_lo, own_hi;
+    int64_t D_global;
 } cd_graph_info;
 
 /* LFR-shaped benchmark spec (new generator; the reference has none). */
@@ -240,6 +245,32 @@ CD_API cd_status cd_louvain_run(cd_ctx *ctx, const cd_graph *g, const cd_louvain
 /* run_epp; z compacted. */
 CD_API cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *cfg, int32_t *z,
                             cd_report *report);
+
+/* ---- sharded execution --------------------------------------
+ * One rank per GPU.  Attach a communicator to each rank's context; every
+ * detector then evaluates only the rank's nodes (1D degree-balanced ranges,
+ * cd_shard_bounds) and exchanges the per-sub-sweep move lists, so labels stay
+ * replicated and equal to the one-device result.  The graph may be whole on
+ * every rank (replicated) or a row shard (cd_graph_shard: owned rows only);
+ * coarse levels are replicated.  Outputs are the full labels on every rank.
+ * The reference's equivalent is its OpenMP `workers` (H/graph.hpp:34-36). */
+typedef struct cd_loopback cd_loopback;
+/* ncclGetUniqueId (libnccl.so.2 is loaded on first use). */
+CD_API cd_status cd_nccl_unique_id(uint8_t id[128]);
+/* ncclCommInitRank on the context's device; collective across the ranks. */
+CD_API cd_status cd_ctx_attach_nccl(cd_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t id[128]);
+/* In-process emulation: nranks host threads, each with its own context on
+ * one device, exchange through host barriers and device copies. */
+CD_API cd_status cd_loopback_create(int32_t nranks, cd_loopback **out);
+CD_API cd_status cd_loopback_destroy(cd_loopback *lb);
+CD_API cd_status cd_ctx_attach_loopback(cd_ctx *ctx, cd_loopback *lb, int32_t rank);
+CD_API cd_status cd_ctx_detach(cd_ctx *ctx);
+CD_API cd_status cd_ctx_world(const cd_ctx *ctx, int32_t *rank, int32_t *size);
+/* Ownership ranges: bounds[r] = first node whose offset reaches D*r/nranks
+ * (host offsets, n+1 entries; bounds has nranks+1 entries).  No GPU needed. */
+CD_API cd_status cd_shard_bounds(int64_t n, const int64_t *off, int32_t nranks, int64_t *bounds);
+/* This rank's row shard of a whole graph (ranges of cd_shard_bounds). */
+CD_API cd_status cd_graph_shard(cd_ctx *ctx, const cd_graph *full, cd_graph **out);
 
 #ifdef __cplusplus
 }

@@ -1229,7 +1229,70 @@ int cdo_plp_bucketed(const cdo_graph *g, const cdo_plp_config *cfg, const int32_
     return 0;
 }
 
-/* Bucketed move phase: see paper_1304_4453_b200/csrc/louvain.cu. */
+/* One PLP sub-sweep restricted to the nodes [lo, hi) one rank owns (the
+ * sharded protocol of the device drivers): evaluates the
+ * bucket's active nodes against the frozen labels, deactivates non-movers
+ * and returns the moves without applying them.  The caller concatenates the
+ * ranks' moves in rank order and applies them as cdo_plp_bucketed does. */
+int64_t cdo_plp_subsweep(const cdo_graph *g, const int32_t *labels, uint8_t *active, uint64_t key, int32_t bucket,
+                         int32_t buckets, int64_t lo, int64_t hi, int32_t *mv_u, int32_t *mv_l) {
+    scratch_t s;
+    if (scratch_init(&s, max_label_plus_one(g->n, labels), max_degree(g))) {
+        scratch_free(&s);
+        return CDO_ENOMEM;
+    }
+    int64_t nm = 0;
+    for (int64_t u = lo; u < hi; ++u) {
+        if (!active[u] || g->off[u + 1] == g->off[u])
+            continue;
+        if (buckets > 1 && cdo_bucket_of(key, (int32_t)u, buckets) != bucket)
+            continue;
+        const int32_t best = plp_best(g, labels, (int32_t)u, &s);
+        if (best != labels[u]) {
+            mv_u[nm] = (int32_t)u;
+            mv_l[nm++] = best;
+        } else {
+            active[u] = 0;
+        }
+    }
+    scratch_free(&s);
+    return nm;
+}
+
+/* One move-phase sub-sweep over [lo, hi) against frozen (z, vols, csize);
+ * the decision rule of cdo_move_phase_bucketed; moves are returned. */
+int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
+                          const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo, int64_t hi,
+                          int32_t *mv_u, int32_t *mv_l) {
+    const int32_t K = cfg->buckets > 0 ? cfg->buckets : 1;
+    const double inv_total = 1.0 / g->total;
+    const double inv_sq2 = 1.0 / (2.0 * g->total * g->total);
+    scratch_t s;
+    if (scratch_init(&s, g->n, max_degree(g))) {
+        scratch_free(&s);
+        return CDO_ENOMEM;
+    }
+    int64_t nm = 0;
+    for (int64_t u = lo; u < hi; ++u) {
+        if (g->off[u + 1] == g->off[u])
+            continue;
+        if (K > 1 && cdo_bucket_of(key, (int32_t)u, K) != bucket)
+            continue;
+        double gain;
+        const int32_t c = z[u];
+        const int32_t best = move_best(g, z, vols, cfg->gamma, inv_total, inv_sq2, (int32_t)u, &s, &gain);
+        if (best == c || !(gain > 0.0))
+            continue;
+        if (cfg->singleton_guard && csize[c] == 1 && csize[best] == 1 && best > c)
+            continue;
+        mv_u[nm] = (int32_t)u;
+        mv_l[nm++] = best;
+    }
+    scratch_free(&s);
+    return nm;
+}
+
+/* Bucketed move phase: the order of paper_1304_4453_b200/csrc/detect.cu move_phase_dev. */
 int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_config *cfg, uint64_t salt,
                             int32_t *changed_out) {
     const int64_t n = g->n;

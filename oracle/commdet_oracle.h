@@ -148,6 +148,13 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
                             int32_t *changed);
 int cdo_louvain_bucketed(const cdo_graph *g, const cdo_louvain_config *cfg, int32_t *z, int64_t *k,
                          int64_t *levels);
+/* Sharded protocol: one sub-sweep over the owned nodes
+ * [lo, hi); returns the number of moves written (not applied). */
+int64_t cdo_plp_subsweep(const cdo_graph *g, const int32_t *labels, uint8_t *active, uint64_t key, int32_t bucket,
+                         int32_t buckets, int64_t lo, int64_t hi, int32_t *mv_u, int32_t *mv_l);
+int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
+                          const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo, int64_t hi,
+                          int32_t *mv_u, int32_t *mv_l);
 int cdo_epp_bucketed(const cdo_graph *g, int64_t ensemble_size, uint64_t seed, const cdo_plp_config *base,
                      const cdo_louvain_config *final_cfg, int32_t *z, int64_t *k);
 

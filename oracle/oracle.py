@@ -141,6 +141,12 @@ def lib():
                                            C.POINTER(C.c_int64)]
         L.cdo_epp_bucketed.argtypes = [gp, C.c_int64, C.c_uint64, C.POINTER(_PlpCfg), C.POINTER(_LouvainCfg), i32p,
                                        C.POINTER(C.c_int64)]
+        L.cdo_plp_subsweep.argtypes = [gp, i32p, C.c_void_p, C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
+                                       C.c_int64, i32p, i32p]
+        L.cdo_plp_subsweep.restype = C.c_int64
+        L.cdo_move_subsweep.argtypes = [gp, i32p, f64p, i32p, C.POINTER(_LouvainCfg), C.c_uint64, C.c_int32,
+                                        C.c_int64, C.c_int64, i32p, i32p]
+        L.cdo_move_subsweep.restype = C.c_int64
         _LIB = L
     return _LIB
 
@@ -465,6 +471,30 @@ def epp_bucketed(g: CSR, ensemble_size=4, seed=1, theta=-1, max_iterations=100, 
     k = C.c_int64()
     _check(lib().cdo_epp_bucketed(_Borrow(g).ref, ensemble_size, seed, C.byref(base), C.byref(fc), z, C.byref(k)))
     return z, k.value
+
+
+def plp_subsweep(g: CSR, labels, active, key, bucket, buckets, lo, hi):
+    """One sharded-protocol PLP sub-sweep over [lo, hi): returns the moves
+    (node, label) and deactivates non-movers in `active` (uint8, in place)."""
+    mu = np.zeros(max(hi - lo, 1), np.int32)
+    ml = np.zeros(max(hi - lo, 1), np.int32)
+    assert active.dtype == np.uint8 and active.flags.c_contiguous
+    nm = lib().cdo_plp_subsweep(_Borrow(g).ref, _i32(labels), active.ctypes.data, key, bucket, buckets, lo, hi,
+                                mu, ml)
+    if nm < 0:
+        _check(int(nm))
+    return mu[:nm].copy(), ml[:nm].copy()
+
+
+def move_subsweep(g: CSR, z, vols, csize, key, bucket, lo, hi, **kw):
+    cfg = louvain_cfg(**kw)
+    mu = np.zeros(max(hi - lo, 1), np.int32)
+    ml = np.zeros(max(hi - lo, 1), np.int32)
+    nm = lib().cdo_move_subsweep(_Borrow(g).ref, _i32(z), np.ascontiguousarray(vols, np.float64), _i32(csize),
+                                 C.byref(cfg), key, bucket, lo, hi, mu, ml)
+    if nm < 0:
+        _check(int(nm))
+    return mu[:nm].copy(), ml[:nm].copy()
 
 
 # --------------------------------------------------------------------------- #

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -38,6 +39,7 @@ __all__ = [
     "run_louvain", "modularity", "coverage", "community_volumes", "coarsen", "prolong", "compacted",
     "community_count", "combine_hashed", "plp_sweep_sync", "move_eval", "move_phase", "dominant_label",
     "is_stable", "library_path", "load_library", "default_context", "ALGO_PLP", "ALGO_PLM", "ALGO_PLMR",
+    "LoopbackGroup", "nccl_unique_id", "shard_bounds",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -111,7 +113,8 @@ class _Report(C.Structure):
 class _GraphInfo(C.Structure):
     _fields_ = [("n", C.c_int64), ("D", C.c_int64), ("m", C.c_int64), ("total_weight", C.c_double),
                 ("weighted", C.c_int32), ("reserved", C.c_int32), ("max_degree", C.c_int64),
-                ("isolated", C.c_int64)]
+                ("isolated", C.c_int64), ("shard_rank", C.c_int32), ("shard_size", C.c_int32),
+                ("own_lo", C.c_int64), ("own_hi", C.c_int64), ("D_global", C.c_int64)]
 
 
 class _LfrSpec(C.Structure):
@@ -136,6 +139,8 @@ EXPORTS = [
     "cd_graph_generate_lfr", "cd_graph_get_info", "cd_graph_download", "cd_graph_destroy", "cd_modularity",
     "cd_community_volumes", "cd_compact", "cd_community_count", "cd_coarsen", "cd_prolong", "cd_combine_hashed",
     "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_plp_run", "cd_louvain_run", "cd_epp_run",
+    "cd_nccl_unique_id", "cd_ctx_attach_nccl", "cd_loopback_create", "cd_loopback_destroy",
+    "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard",
 ]
 
 
@@ -179,6 +184,10 @@ def load_library():
         "cd_plp_run": [vp, vp, C.POINTER(_PlpConfig), vp, vp, C.POINTER(_Report)],
         "cd_louvain_run": [vp, vp, C.POINTER(_LouvainConfig), vp, C.POINTER(_Report)],
         "cd_epp_run": [vp, vp, C.POINTER(_EnsembleConfig), vp, C.POINTER(_Report)],
+        "cd_nccl_unique_id": [vp], "cd_ctx_attach_nccl": [vp, i32, i32, vp],
+        "cd_loopback_create": [i32, vpp], "cd_loopback_destroy": [vp], "cd_ctx_attach_loopback": [vp, vp, i32],
+        "cd_ctx_detach": [vp], "cd_ctx_world": [vp, C.POINTER(i32), C.POINTER(i32)],
+        "cd_shard_bounds": [i64, vp, i32, vp], "cd_graph_shard": [vp, vp, vpp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -216,9 +225,12 @@ class Context:
         _check(L.cd_ctx_create(device, C.byref(h)))
         self.h = h
         self.device = device
+        self._graphs = weakref.WeakValueDictionary()  # id -> Graph living on this context's pool
 
     def close(self):
         if getattr(self, "h", None):
+            for g in list(self._graphs.values()):  # a graph must not outlive its context
+                g._release()
             load_library().cd_ctx_destroy(self.h)
             self.h = None
 
@@ -256,6 +268,60 @@ class Context:
         c = C.c_int64()
         _check(load_library().cd_ctx_launch_count(self.h, C.byref(c)))
         return c.value
+
+    # ---- sharded execution ----------------------------------
+    def attach_nccl(self, nranks: int, rank: int, unique_id: bytes):
+        """Join an NCCL communicator (one rank per GPU); collective over the ranks."""
+        uid = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        _check(load_library().cd_ctx_attach_nccl(self.h, nranks, rank, uid))
+
+    def attach_loopback(self, group: "LoopbackGroup", rank: int):
+        """Join an in-process loopback group (ranks = host threads on one device)."""
+        _check(load_library().cd_ctx_attach_loopback(self.h, group.h, rank))
+        self._group = group
+
+    def detach(self):
+        _check(load_library().cd_ctx_detach(self.h))
+        self._group = None
+
+    @property
+    def world(self):
+        r, n = C.c_int32(), C.c_int32()
+        _check(load_library().cd_ctx_world(self.h, C.byref(r), C.byref(n)))
+        return r.value, n.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(load_library().cd_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class LoopbackGroup:
+    """In-process emulation of `nranks` ranks on one device (cd_loopback)."""
+
+    def __init__(self, nranks: int):
+        h = C.c_void_p()
+        _check(load_library().cd_loopback_create(nranks, C.byref(h)))
+        self.h = h
+        self.nranks = nranks
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None):
+                load_library().cd_loopback_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+
+def shard_bounds(off, nranks: int):
+    """Ownership ranges of `nranks` ranks over CSR offsets `off` (host)."""
+    off = np.ascontiguousarray(np.asarray(off), dtype=np.int64)
+    n = off.shape[0] - 1
+    out = np.zeros(nranks + 1, dtype=np.int64)
+    _check(load_library().cd_shard_bounds(n, off.ctypes.data, nranks, out.ctypes.data))
+    return out
 
 
 _default_ctx = None
@@ -302,12 +368,16 @@ class Graph:
         _check(load_library().cd_graph_get_info(self.h, C.byref(info)))
         self._info = info
         self._host = None
+        ctx._graphs[id(self)] = self
+
+    def _release(self):
+        if getattr(self, "h", None):
+            load_library().cd_graph_destroy(self.h)
+            self.h = None
 
     def __del__(self):
         try:
-            if getattr(self, "h", None):
-                load_library().cd_graph_destroy(self.h)
-                self.h = None
+            self._release()
         except Exception:
             pass
 
@@ -373,6 +443,22 @@ class Graph:
     @property
     def isolated(self) -> int:
         return self._info.isolated
+
+    # --- sharding --------------------------------------------
+    def shard(self, ctx: Context = None) -> "Graph":
+        """This rank's row shard (owned rows only) under ctx's communicator."""
+        ctx = ctx or self.ctx
+        h = C.c_void_p()
+        _check(load_library().cd_graph_shard(ctx.h, self.h, C.byref(h)))
+        return Graph(h, ctx)
+
+    @property
+    def owned_range(self):
+        return self._info.own_lo, self._info.own_hi
+
+    @property
+    def is_shard(self) -> bool:
+        return self._info.shard_size > 1 or self._info.own_hi - self._info.own_lo < self._info.n
 
     def csr(self):
         """Host copy: dict(off, col, w (None if unweighted), vol, loop)."""

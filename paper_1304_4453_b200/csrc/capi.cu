@@ -6,6 +6,7 @@
 #include <cstring>
 #include <new>
 
+#include "comm.cuh"
 #include "detect.cuh"
 
 namespace cdk {
@@ -227,6 +228,7 @@ cd_status cd_ctx_destroy(cd_ctx *ctx) {
         cudaEventDestroy(e);
     if (ctx->dstats)
         cudaFree(ctx->dstats);
+    delete ctx->comm;
     cudaStreamDestroy(ctx->stream);
     delete ctx;
     return CD_OK;
@@ -416,6 +418,11 @@ cd_status cd_graph_get_info(const cd_graph *g, cd_graph_info *out) {
         out->reserved = 0;
         out->max_degree = g->max_degree;
         out->isolated = g->isolated;
+        out->shard_rank = g->rows_local ? g->shard_rank : 0;
+        out->shard_size = g->rows_local ? g->shard_size : 1;
+        out->own_lo = g->rows_local ? g->own_lo : 0;
+        out->own_hi = g->rows_local ? g->own_hi : g->n;
+        out->D_global = g->rows_local ? g->D_global : g->D;
     })
 }
 
@@ -505,7 +512,7 @@ cd_status cd_coarsen(cd_ctx *ctx, const cd_graph *g, const int32_t *z, cd_graph 
         CD_REQUIRE(nc >= 0, CD_EINVAL, "coarsen requires a compacted partition");
         CD_REQUIRE(g->n == 0 || is_compact_dev(ctx, g->n, dz.d, nc), CD_EINVAL,
                    "coarsen requires a compacted partition");  // H/louvain.hpp:156-157
-        *coarse = coarsen_dev(ctx, g, dz.d, nc);
+        *coarse = coarsen_sharded_dev(ctx, g, dz.d, nc);  // a row shard's coarse graph is the ranks' sum
         if (pi_out && g->n)
             CD_CUDA(cudaMemcpyAsync(pi_out, dz.d, g->n * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
         ctx_sync(ctx);
@@ -559,6 +566,7 @@ cd_status cd_combine_hashed(cd_ctx *ctx, int64_t b, int64_t n, const int32_t *co
 cd_status cd_plp_sweep_sync(cd_ctx *ctx, const cd_graph *g, const int32_t *z_in, int32_t *z_out, int64_t *updated) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && g && (g->n == 0 || (z_in && z_out)), CD_EINVAL, "invalid argument");
+        CD_REQUIRE(!g->rows_local || g->shard_size == 1, CD_EINVAL, "sub-kernel needs a whole graph, not a row shard");
         InArr<int32_t> dzi(ctx, z_in, g->n);
         OutArr<int32_t> dzo(ctx, z_out, g->n);
         const int64_t upd = plp_sweep_sync_dev(ctx, const_cast<cd_graph *>(g), dzi.d, dzo.d);
@@ -573,6 +581,7 @@ cd_status cd_move_eval(cd_ctx *ctx, const cd_graph *g, const int32_t *z, const d
                        int32_t *best, double *gain) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && g && (g->n == 0 || (z && vols && best)) && ub >= 1, CD_EINVAL, "invalid argument");
+        CD_REQUIRE(!g->rows_local || g->shard_size == 1, CD_EINVAL, "sub-kernel needs a whole graph, not a row shard");
         InArr<int32_t> dz(ctx, z, g->n);
         InArr<double> dv(ctx, vols, ub);
         const int64_t mx = max_label_dev(ctx, g->n, dz.d);
@@ -677,6 +686,78 @@ cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *c
         }
         dz.finish();
         ctx_sync(ctx);
+    })
+}
+
+// ---- sharded execution ----------------------------------------------------------
+
+cd_status cd_nccl_unique_id(uint8_t id[128]) {
+    CD_GUARD(static_cast<cd_ctx *>(nullptr), CD_REQUIRE(id, CD_EINVAL, "null argument"); nccl_unique_id(id))
+}
+
+cd_status cd_ctx_attach_nccl(cd_ctx *ctx, int32_t nranks, int32_t rank, const uint8_t id[128]) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && id && nranks >= 1 && rank >= 0 && rank < nranks, CD_EINVAL, "invalid argument");
+        Comm *c = comm_nccl_create(nranks, rank, id);
+        delete ctx->comm;
+        ctx->comm = c;
+    })
+}
+
+cd_status cd_loopback_create(int32_t nranks, cd_loopback **out) {
+    CD_GUARD(static_cast<cd_ctx *>(nullptr), {
+        CD_REQUIRE(out && nranks >= 1, CD_EINVAL, "invalid argument");
+        auto *lb = new cd_loopback();
+        lb->nranks = nranks;
+        lb->slot.assign(nranks, nullptr);
+        lb->host.resize(nranks);
+        *out = lb;
+    })
+}
+
+cd_status cd_loopback_destroy(cd_loopback *lb) {
+    delete lb;
+    return CD_OK;
+}
+
+cd_status cd_ctx_attach_loopback(cd_ctx *ctx, cd_loopback *lb, int32_t rank) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && lb && rank >= 0 && rank < lb->nranks, CD_EINVAL, "invalid argument");
+        Comm *c = comm_loopback_create(lb, rank);
+        delete ctx->comm;
+        ctx->comm = c;
+    })
+}
+
+cd_status cd_ctx_detach(cd_ctx *ctx) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx, CD_EINVAL, "null context");
+        delete ctx->comm;
+        ctx->comm = nullptr;
+    })
+}
+
+cd_status cd_ctx_world(const cd_ctx *ctx, int32_t *rank, int32_t *size) {
+    CD_GUARD(static_cast<cd_ctx *>(nullptr), {
+        CD_REQUIRE(ctx, CD_EINVAL, "null context");
+        if (rank)
+            *rank = world_rank(ctx);
+        if (size)
+            *size = world_size(ctx);
+    })
+}
+
+cd_status cd_shard_bounds(int64_t n, const int64_t *off, int32_t nranks, int64_t *bounds) {
+    CD_GUARD(static_cast<cd_ctx *>(nullptr), {
+        CD_REQUIRE(n >= 0 && off && bounds && nranks >= 1, CD_EINVAL, "invalid argument");
+        shard_bounds_host(n, off, nranks, bounds);
+    })
+}
+
+cd_status cd_graph_shard(cd_ctx *ctx, const cd_graph *full, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && full && out, CD_EINVAL, "invalid argument");
+        *out = graph_shard_dev(ctx, full);
     })
 }
 

@@ -49,6 +49,8 @@ struct PendingEvent {
     cudaEvent_t a, b;
 };
 
+class Comm;
+
 }  // namespace cdk
 
 struct cd_ctx {
@@ -75,6 +77,8 @@ struct cd_ctx {
     cudaEvent_t fork_ev = nullptr;
     cudaEvent_t join_ev[NSIDE] = {};
     bool use_graphs = true;
+    // sharded execution (comm.cuh); nullptr = one device, no exchange
+    cdk::Comm *comm = nullptr;
 };
 
 namespace cdk {

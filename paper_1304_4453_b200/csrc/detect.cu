@@ -15,7 +15,29 @@
 
 #include "detect.cuh"
 
+#include "comm.cuh"
+
 namespace cdk {
+
+// Runs its scope on this device alone (no exchange, whole node range).
+struct LocalScope {
+    cd_ctx *ctx;
+    Comm *saved;
+    explicit LocalScope(cd_ctx *c) : ctx(c), saved(c->comm) { c->comm = nullptr; }
+    ~LocalScope() { ctx->comm = saved; }
+};
+
+// Below this many entries a replicated graph is not worth the per-sub-sweep
+// exchange: every rank runs the phase alone and rank 0's labels are broadcast
+// (fp64 atomics may order volume updates differently on different ranks).
+static int64_t shard_min_entries() {
+    const char *e = std::getenv("CD_SHARD_MIN_ENTRIES");
+    return e ? std::atoll(e) : (int64_t(1) << 22);
+}
+
+static bool run_replicated(cd_ctx *ctx, const cd_graph *g) {
+    return world_size(ctx) > 1 && !g->rows_local && g->D < shard_min_entries();
+}
 
 DevTimer::DevTimer(cd_ctx *c) : ctx(c) {
     CD_CUDA(cudaEventCreate(&a));
@@ -50,6 +72,14 @@ __global__ void k_count_diff(int64_t n, const int32_t *a, const int32_t *b, unsi
 void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32_t *initial, int32_t *labels,
                  Report rep) {
     const int64_t n = g->n;
+    if (run_replicated(ctx, g)) {
+        {
+            LocalScope local(ctx);
+            plp_run_dev(ctx, g, cfg, initial, labels, rep);
+        }
+        ctx->comm->broadcast(ctx, labels, n * sizeof(int32_t), 0);
+        return;
+    }
     const int64_t theta = cfg.theta >= 0 ? cfg.theta : std::max<int64_t>(1, n / 100000);  // H/plp.hpp:24-28
     const int K = cfg.buckets > 0 ? cfg.buckets : 4;
     if (initial)
@@ -63,6 +93,12 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
     c.z = labels;
     c.active = active.p;
     c.buckets = K;
+    owned_range(ctx, g, c.own_lo, c.own_hi);
+    if (g->rows_local && world_size(ctx) > 1) {
+        graph_ensure_transpose(ctx, g);
+        c.toff = g->toff.p;
+        c.tcol = g->tcol.p;
+    }
     Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
     int64_t updated = n, iter = 0;
@@ -139,6 +175,21 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     const int64_t n = g->n;
     if (n == 0 || g->total == 0.0)  // H/louvain.hpp:67-68
         return false;
+    if (run_replicated(ctx, g)) {
+        bool ch;
+        {
+            LocalScope local(ctx);
+            ch = move_phase_dev(ctx, g, z, cfg, salt, passes, moves);
+        }
+        ctx->comm->broadcast(ctx, z, n * sizeof(int32_t), 0);
+        int32_t chv = ch ? 1 : 0;
+        DBuf<int32_t> d(ctx, 1);
+        CD_CUDA(cudaMemcpyAsync(d.p, &chv, sizeof(chv), cudaMemcpyHostToDevice, ctx->stream));
+        ctx->comm->broadcast(ctx, d.p, sizeof(int32_t), 0);
+        CD_CUDA(cudaMemcpyAsync(&chv, d.p, sizeof(chv), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        return chv != 0;
+    }
     const int K = cfg.buckets > 0 ? cfg.buckets : 4;
     const int64_t theta = std::max<int64_t>(cfg.move_theta >= 0 ? cfg.move_theta : n / 100000,
                                             static_cast<int64_t>(cfg.move_tol * static_cast<double>(n)));
@@ -153,6 +204,7 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     c.gamma = cfg.gamma;
     c.guard = cfg.singleton_guard;
     c.buckets = K;
+    owned_range(ctx, g, c.own_lo, c.own_hi);
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
@@ -204,7 +256,7 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
         const int64_t k = compact_dev(ctx, n, z, n, zc.p);  // :248
         if (k < n) {                                        // :249
             t.start();
-            cd_graph *coarse = coarsen_dev(ctx, g, zc.p, k);  // :251
+            cd_graph *coarse = coarsen_sharded_dev(ctx, g, zc.p, k);  // :251
             const double cm = t.stop_ms();
             if (auto *L = rep.level(level))
                 L->coarsen_ms += cm;
@@ -252,9 +304,14 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     DevTimer t(ctx);
     // bases (:152-161): seed + i
     t.start();
-    DBuf<int32_t> bases(ctx, std::max<int64_t>(n * b, 1));
-    for (int64_t i = 0; i < b; ++i) {
-        int32_t *zi = bases.p + i * n;
+    const int G = world_size(ctx), rank = world_rank(ctx);
+    // ensemble parallelism: with a replicated graph, rank r computes bases
+    // r, r+G, ... alone and the bases are allgathered; a row shard computes
+    // every base cooperatively
+    const bool base_parallel = G > 1 && !g->rows_local;
+    const int64_t slots = base_parallel ? (b + G - 1) / G * G : b;
+    DBuf<int32_t> bases(ctx, std::max<int64_t>(n * slots, 1));
+    auto run_base = [&](int64_t i, int32_t *zi) {
         if (cfg.base == CD_ALGO_PLP) {
             cd_plp_config pc = cfg.base_plp;
             pc.seed = cfg.seed + static_cast<uint64_t>(i);
@@ -265,6 +322,22 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
             lc.refine = cfg.base == CD_ALGO_PLMR;
             louvain_run_dev(ctx, g, lc, zi, Report{nullptr});
         }
+    };
+    if (base_parallel) {
+        for (int64_t j = 0; j < slots; j += G) {
+            const int64_t i = j + rank;
+            int32_t *zi = bases.p + i * n;
+            if (i < b) {
+                LocalScope local(ctx);
+                run_base(i, zi);
+            } else if (n) {
+                CD_CUDA(cudaMemsetAsync(zi, 0, n * sizeof(int32_t), ctx->stream));
+            }
+            ctx->comm->allgather(ctx, zi, bases.p + j * n, n * sizeof(int32_t));  // in place
+        }
+    } else {
+        for (int64_t i = 0; i < b; ++i)
+            run_base(i, bases.p + i * n);
     }
     const double base_ms = t.stop_ms();
     // combine (:163-165)
@@ -279,7 +352,7 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     const double combine_ms = t.stop_ms();
     // coarsen (:167-169)
     t.start();
-    cd_graph *coarse = coarsen_dev(ctx, g, core.p, k);
+    cd_graph *coarse = coarsen_sharded_dev(ctx, g, core.p, k);
     const double coarsen_ms = t.stop_ms();
     double final_ms = 0.0;
     try {

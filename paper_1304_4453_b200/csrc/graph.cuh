@@ -101,6 +101,18 @@ struct cd_graph {
     cdk::DBuf<int64_t> hp_scan;     // scan scratch (2 x tiles)
     cdk::DBuf<int32_t> hp_flag;     // partition table overflow (sticky)
     cdk::DBuf<double> hub_aux;      // [n_hubs] per-hub w(u, C) accumulator (PLM)
+
+    // row shard (comm.cuh): only rows [own_lo, own_hi) carry
+    // entries (global column ids); every other row is empty.  vol, loop, m,
+    // total, max_degree, isolated, int_weights and max_vol are the GLOBAL
+    // graph's; D counts the local entries.  toff/tcol (built on first PLP use)
+    // is the transposed block: for every node, its owned neighbours.
+    bool rows_local = false;
+    int shard_rank = 0, shard_size = 1;
+    int64_t own_lo = 0, own_hi = 0;
+    int64_t D_global = 0;
+    cdk::DBuf<int64_t> toff;
+    cdk::DBuf<int32_t> tcol;
 };
 
 namespace cdk {
@@ -114,6 +126,14 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g);
 cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, const int32_t *v, const float *w,
                            DupMode mode);  // device arrays; symmetrises
 void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D);
+
+// shard.cu
+cd_graph *graph_shard_dev(cd_ctx *ctx, const cd_graph *full);  // rows of this rank (ctx->comm)
+void graph_ensure_transpose(cd_ctx *ctx, cd_graph *g);         // toff / tcol of a row shard
+// ownership range of this rank on a replicated graph (whole graph on one device)
+void owned_range(cd_ctx *ctx, const cd_graph *g, int64_t &lo, int64_t &hi);
+// sum of the row-shard partial coarse graphs of all ranks (replicated result)
+cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc);
 
 // quality.cu
 void community_volumes_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, double *vols, int64_t ub);

@@ -1,6 +1,7 @@
 // quality.cu -- modularity / coverage (H/quality.hpp:21-51) and community
 // volumes (H/louvain.hpp:27-31).  Every accumulator is fp64: Q is a
 // difference of O(1) terms that cancel to ~1e-5 on R-MAT (SURVEY.md finding 11).
+#include "comm.cuh"
 #include "graph.cuh"
 
 namespace cdk {
@@ -157,6 +158,9 @@ void modularity_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub
         CD_LAUNCH(ctx, "modularity", k_mod_intra, grid_for(g->D, 256 * MOD_ITEMS, ctx->num_sms * 8), 256, 0, g->n,
                   g->D, static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
                   static_cast<const float *>(g->weighted ? g->w.p : nullptr), z, acc.p);
+    // a row shard holds only its rows' intra-community entries
+    if (g->rows_local && world_size(ctx) > 1)
+        ctx->comm->allreduce_sum_f64(ctx, acc.p, 1);
     CD_LAUNCH(ctx, "modularity", k_sum_sq, grid_for(ub, 256, ctx->num_sms * 8), 256, 0, ub,
               static_cast<const double *>(vols.p), acc.p + 1);
     double h[2];

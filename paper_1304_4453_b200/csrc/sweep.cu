@@ -20,7 +20,9 @@
 
 #include <cmath>
 #include <map>
+#include <mutex>
 
+#include "comm.cuh"
 #include "scan.cuh"
 
 namespace cdk {
@@ -39,9 +41,12 @@ struct SweepParams {
     const unsigned long long *keyp;  // bucket key of the current pass (device)
     int bucket, buckets;
     const int32_t *tlist;
-    int64_t tstart[NUM_TIERS + 1];
+    // this rank's slice [tbeg[t], tend[t]) of each tier list (whole lists on
+    // one device); nodes outside [own_lo, own_hi) are never evaluated
+    int64_t tbeg[NUM_TIERS], tend[NUM_TIERS];
+    int32_t own_lo, own_hi;
     int32_t *mv_count;  // moves of this bucket
-    int32_t *mv_node, *mv_label;
+    int2 *mv;           // (node, label) of this bucket's moves
     int32_t *dense_best;
     double *dense_gain;
     unsigned long long *stats;
@@ -146,6 +151,8 @@ __device__ __forceinline__ double load_w(const SweepParams &P, int64_t f, bool v
 }
 
 __device__ __forceinline__ bool selected(const SweepParams &P, unsigned long long key, int32_t u) {
+    if (u < P.own_lo || u >= P.own_hi)
+        return false;
     if (P.buckets > 1 && bucket_of(key, u, P.buckets) != P.bucket)
         return false;
     return !P.active || P.active[u];
@@ -169,10 +176,8 @@ struct MoveQueue {
         if (lane_id() == 0)
             base = atomicAdd(P.mv_count, n);
         base = __shfl_sync(0xffffffffu, base, 0);
-        if (lane_id() < n) {
-            P.mv_node[base + lane_id()] = u;
-            P.mv_label[base + lane_id()] = l;
-        }
+        if (lane_id() < n)
+            P.mv[base + lane_id()] = make_int2(u, l);
         n = 0;
     }
     // all lanes: lanes with `moved` enqueue (node, label)
@@ -246,8 +251,8 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int sub = lane / G, k = lane % G;
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
-    const int32_t *list = P.tlist + P.tstart[tier];
-    const int64_t count = P.tstart[tier + 1] - P.tstart[tier];
+    const int32_t *list = P.tlist + P.tbeg[tier];
+    const int64_t count = P.tend[tier] - P.tbeg[tier];
     const unsigned long long bkey = load_key(P);
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -327,8 +332,8 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     int32_t *keys = skeys[wid];
     V *vals = svals[wid];
-    const int32_t *list = P.tlist + P.tstart[TIER_WARP];
-    const int64_t count = P.tstart[TIER_WARP + 1] - P.tstart[TIER_WARP];
+    const int32_t *list = P.tlist + P.tbeg[TIER_WARP];
+    const int64_t count = P.tend[TIER_WARP] - P.tbeg[TIER_WARP];
     const unsigned long long bkey = load_key(P);
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -444,8 +449,8 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     __shared__ int32_t red_k[8];
     __shared__ double red_wc[8];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int32_t *list = P.tlist + P.tstart[TIER];
-    const int64_t count = P.tstart[TIER + 1] - P.tstart[TIER];
+    const int32_t *list = P.tlist + P.tbeg[TIER];
+    const int64_t count = P.tend[TIER] - P.tbeg[TIER];
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
@@ -834,11 +839,22 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
 // bucket moved more than n/16 nodes, every node is activated instead (n bytes
 // instead of sum-of-degrees scattered bytes): a node whose neighbourhood did
 // not change re-derives the label it already has, so the result is identical.
-__global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const int32_t *mv_label,
-                                                   const int32_t *mv_count, int32_t *z, uint8_t *active,
-                                                   const int64_t *off, const int32_t *col, long long *total,
-                                                   int64_t n) {
-    const int64_t count = *mv_count;
+//
+// The move list is `nseg` segments of `stride` entries, segment s holding
+// counts[s] moves (one segment on one device; one per rank, rank order, after
+// the sharded exchange).  Activation walks (toff, tcol): the graph itself, or
+// on a row shard its transposed block -- the owned neighbours of every node.
+__device__ __forceinline__ int64_t seg_total(const int32_t *counts, int nseg) {
+    int64_t t = 0;
+    for (int s = 0; s < nseg; ++s)
+        t += counts[s];
+    return t;
+}
+
+__global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
+                                                   int32_t *z, uint8_t *active, const int64_t *toff,
+                                                   const int32_t *tcol, long long *total, int64_t n) {
+    const int64_t count = seg_total(counts, nseg);
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -854,48 +870,56 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int32_t *mv_node, const
                 for (int64_t j = 16 * i; j < n; ++j)
                     active[j] = 1;
         }
-    for (int64_t i = gw; i < count; i += nw) {
-        const int32_t u = mv_node[i];
-        if (lane == 0)
-            z[u] = mv_label[i];
-        if (active && !dense)
-            for (int64_t e = off[u] + lane; e < off[u + 1]; e += 32)
-                active[col[e]] = 1;
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int2 *m = mv + sg * stride;
+        const int64_t cnt = counts[sg];
+        for (int64_t i = gw; i < cnt; i += nw) {
+            const int2 e2 = m[i];
+            if (lane == 0)
+                z[e2.x] = e2.y;
+            if (active && !dense)
+                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
+                    active[tcol[e]] = 1;
+        }
     }
 }
 
-__global__ void __launch_bounds__(256) k_apply_plm(const int32_t *mv_node, const int32_t *mv_label,
-                                                   const int32_t *mv_count, int32_t *z, double *vols, int32_t *csize,
-                                                   const double *vol, long long *total) {
+__global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
+                                                   int32_t *z, double *vols, int32_t *csize, const double *vol,
+                                                   long long *total) {
     __shared__ double scratch[8][32];
-    const int64_t count = *mv_count;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < count;
-         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const bool valid = i < count;
-        const int32_t u = valid ? mv_node[i] : 0;
-        const int32_t d = valid ? mv_label[i] : -1;
-        const int32_t c = valid ? z[u] : -1;
-        if (valid)
-            z[u] = d;
-        const double vu = valid ? vol[u] : 0.0;  // H/louvain.hpp:121-125
-        // moves into / out of the same community combine per warp first
-        double s;
-        if (warp_aggregate_sum(d, vu, valid, scratch[wid], s))
-            atomicAdd(&vols[d], s);
-        if (warp_aggregate_sum(c, vu, valid, scratch[wid], s))
-            atomicAdd(&vols[c], -s);
-        if (csize) {
-            const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-            const uint32_t pd = __match_any_sync(0xffffffffu, d) & vm;
-            if (valid && (__ffs(pd) - 1) == lane)
-                atomicAdd(&csize[d], __popc(pd));
-            const uint32_t pc = __match_any_sync(0xffffffffu, c) & vm;
-            if (valid && (__ffs(pc) - 1) == lane)
-                atomicSub(&csize[c], __popc(pc));
+        atomicAdd(reinterpret_cast<unsigned long long *>(total),
+                  static_cast<unsigned long long>(seg_total(counts, nseg)));
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int2 *m = mv + sg * stride;
+        const int64_t count = counts[sg];
+        for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < count;
+             base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            const int64_t i = base + threadIdx.x;
+            const bool valid = i < count;
+            const int2 e2 = valid ? m[i] : make_int2(0, -1);
+            const int32_t u = e2.x, d = e2.y;
+            const int32_t c = valid ? z[u] : -1;
+            if (valid)
+                z[u] = d;
+            const double vu = valid ? vol[u] : 0.0;  // H/louvain.hpp:121-125
+            // moves into / out of the same community combine per warp first
+            double s;
+            if (warp_aggregate_sum(d, vu, valid, scratch[wid], s))
+                atomicAdd(&vols[d], s);
+            if (warp_aggregate_sum(c, vu, valid, scratch[wid], s))
+                atomicAdd(&vols[c], -s);
+            if (csize) {
+                const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+                const uint32_t pd = __match_any_sync(0xffffffffu, d) & vm;
+                if (valid && (__ffs(pd) - 1) == lane)
+                    atomicAdd(&csize[d], __popc(pd));
+                const uint32_t pc = __match_any_sync(0xffffffffu, c) & vm;
+                if (valid && (__ffs(pc) - 1) == lane)
+                    atomicSub(&csize[c], __popc(pc));
+            }
         }
     }
 }
@@ -913,11 +937,28 @@ static void ensure_side_streams(cd_ctx *ctx) {
     CD_CUDA(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
 }
 
+// first index of each tier list segment holding ids >= lo / >= hi (tier
+// lists are ascending within a tier)
+__global__ void k_tier_narrow(const int32_t *tlist, const int64_t *tstart, int64_t lo, int64_t hi, int64_t *out) {
+    const int t = threadIdx.x >> 1;
+    if (t >= NUM_TIERS)
+        return;
+    const int64_t bound = (threadIdx.x & 1) ? hi : lo;
+    int64_t a = tstart[t], b = tstart[t + 1];
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (tlist[mid] < bound)
+            a = mid + 1;
+        else
+            b = mid;
+    }
+    out[threadIdx.x] = a;
+}
+
 Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g), c_(c) {
     graph_ensure_bins(ctx, g);
     cnt_.alloc(ctx, 8);
-    mv_node_.alloc(ctx, std::max<int64_t>(g->n, 1));
-    mv_label_.alloc(ctx, std::max<int64_t>(g->n, 1));
+    mv_.alloc(ctx, std::max<int64_t>(g->n, 1));
     total_.alloc(ctx, 1);
     total_.zero();
     key_.alloc(ctx, 1);
@@ -926,6 +967,33 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
         c_.buckets = 1;
     if (c_.buckets > 8)
         fail(CD_EINVAL, "at most 8 buckets per pass");
+    if (c_.own_hi < 0) {
+        c_.own_lo = 0;
+        c_.own_hi = g->n;
+    }
+    // any attached communicator takes the exchange path (also at size 1)
+    exchange_ = !c_.dense_best && ctx->comm != nullptr;
+    world_ = exchange_ ? ctx->comm->size : 1;
+    for (int t = 0; t < NUM_TIERS; ++t) {
+        tbeg_[t] = g->tier_start[t];
+        tend_[t] = g->tier_start[t + 1];
+    }
+    if (c_.own_lo > 0 || c_.own_hi < g->n) {
+        DBuf<int64_t> ts(ctx, NUM_TIERS + 1), nb(ctx, 2 * NUM_TIERS);
+        CD_CUDA(cudaMemcpyAsync(ts.p, g->tier_start, (NUM_TIERS + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
+                                ctx->stream));
+        CD_LAUNCH(ctx, "shard", k_tier_narrow, 1, 32, 0, static_cast<const int32_t *>(g->tlist.p),
+                  static_cast<const int64_t *>(ts.p), c_.own_lo, c_.own_hi, nb.p);
+        int64_t h[2 * NUM_TIERS];
+        CD_CUDA(cudaMemcpyAsync(h, nb.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        for (int t = 0; t < NUM_TIERS; ++t) {
+            tbeg_[t] = h[2 * t];
+            tend_[t] = h[2 * t + 1];
+        }
+    }
+    if (exchange_)
+        rcnt_.alloc(ctx, world_);
 }
 
 Sweeper::~Sweeper() {
@@ -944,6 +1012,8 @@ static void set_smem(K kernel, size_t bytes) {
 template <class K>
 static int resident_blocks(K kernel, int threads, size_t smem) {
     static std::map<const void *, int> cache;
+    static std::mutex mu;  // loopback ranks are host threads
+    std::lock_guard<std::mutex> lk(mu);
     const void *key = reinterpret_cast<const void *>(kernel);
     auto it = cache.find(key);
     if (it != cache.end())
@@ -995,35 +1065,35 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         else                                                                                         \
             CD_LAUNCH(ctx, fam, KERNEL, GRID, BLOCK, SMEM, __VA_ARGS__);                             \
     })
-    if (g->tier_nodes[TIER_G8]) {
+    if ((P.tend[TIER_G8] - P.tbeg[TIER_G8])) {
         fam = names[MODE][TIER_G8];
         const int ch = chunk_for(4);
         auto kfn = k_sweep_direct<8, MODE, VC>;
-        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G8], 256, ch);
+        const int grid = warps_grid_k(kfn, (P.tend[TIER_G8] - P.tbeg[TIER_G8]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G8), ch);
     }
-    if (g->tier_nodes[TIER_G16]) {
+    if ((P.tend[TIER_G16] - P.tbeg[TIER_G16])) {
         fam = names[MODE][TIER_G16];
         const int ch = chunk_for(2);
         auto kfn = k_sweep_direct<16, MODE, VC>;
-        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G16], 256, ch);
+        const int grid = warps_grid_k(kfn, (P.tend[TIER_G16] - P.tbeg[TIER_G16]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16), ch);
     }
-    if (g->tier_nodes[TIER_G32]) {
+    if ((P.tend[TIER_G32] - P.tbeg[TIER_G32])) {
         fam = names[MODE][TIER_G32];
         const int ch = chunk_for(1);
         auto kfn = k_sweep_direct<32, MODE, VC>;
-        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_G32], 256, ch);
+        const int grid = warps_grid_k(kfn, (P.tend[TIER_G32] - P.tbeg[TIER_G32]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G32), ch);
     }
-    if (g->tier_nodes[TIER_WARP]) {
+    if ((P.tend[TIER_WARP] - P.tbeg[TIER_WARP])) {
         fam = names[MODE][TIER_WARP];
         const int ch = chunk_for(1);
         auto kfn = k_sweep_warp<MODE, VC>;
-        const int grid = warps_grid_k(kfn, g->tier_nodes[TIER_WARP], 128, ch);
+        const int grid = warps_grid_k(kfn, (P.tend[TIER_WARP] - P.tbeg[TIER_WARP]), 128, ch);
         CD_TIER_LAUNCH(kfn, grid, 128, 0, P, ch);
     }
-    if (g->tier_nodes[TIER_BLOCK]) {
+    if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
         fam = names[MODE][TIER_BLOCK];
         const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
         static bool attr = false;
@@ -1031,10 +1101,10 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             set_smem(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>, smem);
             attr = true;
         }
-        const int nb = grid_for(g->tier_nodes[TIER_BLOCK], 1, sms * 8);
+        const int nb = grid_for((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1, sms * 8);
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), nb, SW_BLOCK_THREADS, smem, P);
     }
-    if (g->tier_nodes[TIER_BLOCK2]) {
+    if ((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2])) {
         fam = names[MODE][TIER_BLOCK2];
         const size_t smem = size_t(BLOCK2_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
         static bool attr2 = false;
@@ -1042,10 +1112,10 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             set_smem(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>, smem);
             attr2 = true;
         }
-        const int nb = grid_for(g->tier_nodes[TIER_BLOCK2], 1, sms * (VC == VC_REAL ? 2 : 3));
+        const int nb = grid_for((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1, sms * (VC == VC_REAL ? 2 : 3));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
     }
-    if (g->n_hubs) {
+    if (P.tend[TIER_HUB] > P.tbeg[TIER_HUB]) {
         fam = names[MODE][TIER_HUB];
         const int max_np = 1 << HUB_MAX_PBITS;
         const size_t smem_count = size_t(max_np) * sizeof(int32_t);
@@ -1114,10 +1184,13 @@ void Sweeper::enqueue(bool capture) {
     P.keyp = key_.p;
     P.buckets = c_.buckets;
     P.tlist = g->tlist.p;
-    for (int t = 0; t <= NUM_TIERS; ++t)
-        P.tstart[t] = g->tier_start[t];
-    P.mv_node = mv_node_.p;
-    P.mv_label = mv_label_.p;
+    for (int t = 0; t < NUM_TIERS; ++t) {
+        P.tbeg[t] = tbeg_[t];
+        P.tend[t] = tend_[t];
+    }
+    P.own_lo = static_cast<int32_t>(c_.own_lo);
+    P.own_hi = static_cast<int32_t>(c_.own_hi);
+    P.mv = mv_.p;
     P.dense_best = c_.dense_best;
     P.dense_gain = c_.dense_gain;
     P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : 3);
@@ -1138,7 +1211,6 @@ void Sweeper::enqueue(bool capture) {
     P.hub_aux = g->hub_aux.p;
     P.n_hubs = g->n_hubs;
     P.n_parts = g->n_hub_parts;
-    const int sms = ctx->num_sms;
     const bool plp = c_.mode == MODE_PLP;
     if (!c_.dense_best)
         CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
@@ -1156,25 +1228,51 @@ void Sweeper::enqueue(bool capture) {
             CD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[i], 0));
         if (c_.dense_best)
             continue;
-        const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, sms * 4));
-        if (plp)
-            CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0,
-                      static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
-                      static_cast<const int32_t *>(cnt_.p + b), c_.z, c_.active,
-                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), total_.p,
-                      g->n);
+        if (exchange_)
+            exchange_and_apply(b);
         else
-            CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0,
-                      static_cast<const int32_t *>(mv_node_.p), static_cast<const int32_t *>(mv_label_.p),
-                      static_cast<const int32_t *>(cnt_.p + b), c_.z, c_.vols, c_.csize,
-                      static_cast<const double *>(g->vol.p), total_.p);
+            apply(mv_.p, cnt_.p + b, 1, 0);
     }
+}
+
+void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride) {
+    cd_ctx *ctx = ctx_;
+    cd_graph *g = g_;
+    const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, ctx->num_sms * 4));
+    if (c_.mode == MODE_PLP)
+        CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
+                  c_.active, c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
+                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), total_.p, g->n);
+    else
+        CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
+                  c_.vols, c_.csize, static_cast<const double *>(g->vol.p), total_.p);
+}
+
+// Sharded sub-sweep exchange: allgather the per-rank move counts, then the
+// move lists padded to the largest count; every rank applies all segments in
+// rank order.  One host synchronisation per sub-sweep (the padded size).
+void Sweeper::exchange_and_apply(int b) {
+    cd_ctx *ctx = ctx_;
+    Comm *comm = ctx->comm;
+    comm->allgather(ctx, cnt_.p + b, rcnt_.p, sizeof(int32_t));
+    std::vector<int32_t> hc(world_);
+    CD_CUDA(cudaMemcpyAsync(hc.data(), rcnt_.p, world_ * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t maxc = 0;
+    for (int r = 0; r < world_; ++r)
+        maxc = std::max<int64_t>(maxc, hc[r]);
+    if (maxc == 0)
+        return;
+    if (rmv_.n < static_cast<size_t>(world_ * maxc))
+        rmv_.alloc(ctx, static_cast<size_t>(world_) * std::max<int64_t>(maxc, g_->n / world_ + 1));
+    comm->allgather(ctx, mv_.p, rmv_.p, maxc * sizeof(int2));
+    apply(rmv_.p, rcnt_.p, world_, maxc);
 }
 
 void Sweeper::pass(uint64_t key) {
     unsigned long long k = key;
     CD_CUDA(cudaMemcpyAsync(key_.p, &k, sizeof(k), cudaMemcpyHostToDevice, ctx_->stream));
-    if (ctx_->profiling || !ctx_->use_graphs) {
+    if (ctx_->profiling || !ctx_->use_graphs || exchange_) {
         enqueue(false);
         return;
     }

@@ -20,6 +20,11 @@ struct SweepCall {
     int buckets = 1;
     int32_t *dense_best = nullptr;  // evaluation only: write decisions densely, apply nothing
     double *dense_gain = nullptr;
+    // sharded execution: this rank evaluates [own_lo, own_hi) (-1: all nodes);
+    // PLP activation walks (toff, tcol) when set (a row shard's transpose)
+    int64_t own_lo = 0, own_hi = -1;
+    const int64_t *toff = nullptr;
+    const int32_t *tcol = nullptr;
 };
 
 // One iteration / pass = `buckets` sub-sweeps.  Each sub-sweep evaluates the
@@ -27,6 +32,11 @@ struct SweepCall {
 // kernels run as parallel branches) and then applies its moves.  After the
 // first pass the launch sequence is replayed from a CUDA graph; the bucket key
 // lives in device memory so the graph is reusable.
+//
+// With a communicator of size G > 1 (comm.cuh) every rank evaluates only the
+// nodes it owns; after each sub-sweep the ranks allgather their move lists
+// and every rank applies all of them in rank order, so labels, volumes and
+// the move count stay replicated and identical to the one-device run.
 class Sweeper {
   public:
     Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c);
@@ -39,11 +49,18 @@ class Sweeper {
 
   private:
     void enqueue(bool capture);
+    void apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride);
+    void exchange_and_apply(int b);
     cd_ctx *ctx_;
     cd_graph *g_;
     SweepCall c_;
+    int world_ = 1;
+    bool exchange_ = false;
+    int64_t tbeg_[NUM_TIERS] = {}, tend_[NUM_TIERS] = {};
     DBuf<int32_t> cnt_;     // [8]: [b] moves of bucket b
-    DBuf<int32_t> mv_node_, mv_label_;
+    DBuf<int2> mv_;         // this rank's moves of the current bucket
+    DBuf<int32_t> rcnt_;    // [G] gathered counts
+    DBuf<int2> rmv_;        // [G][stride] gathered moves
     DBuf<long long> total_;
     DBuf<unsigned long long> key_;
     cudaGraph_t graph_ = nullptr;

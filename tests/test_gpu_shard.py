@@ -1,0 +1,191 @@
+"""Sharded execution on one GPU through the C ABI.
+
+G ranks are emulated by the loopback transport: G host threads, each with its
+own cd_ctx on cuda:0, exchanging through host barriers and stream-ordered
+device copies (no kernel waits on another rank; B200_PROFILING.md).  The
+sharded drivers evaluate only each rank's nodes and apply every rank's move
+list after each sub-sweep, so for unweighted / integer-weight graphs the
+labels must be bit-identical to the one-device run -- PLP, PLM, PLMR, EPP,
+with replicated graphs and with row shards, coarse levels included
+(CD_SHARD_MIN_ENTRIES=0 keeps even tiny coarse graphs on the exchange path).
+The NCCL transport itself is exercised at world size 1 (every sub-sweep still
+goes through ncclAllGather).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+JOIN_S = 300
+
+
+@pytest.fixture(autouse=True)
+def _exchange_everywhere(monkeypatch):
+    monkeypatch.setenv("CD_SHARD_MIN_ENTRIES", "0")
+    monkeypatch.setenv("CD_POOL_RESERVE_FRAC", "0")  # many short-lived contexts
+
+
+def run_ranks(dev, G, fn):
+    """fn(ctx, rank) on G loopback ranks; returns the per-rank results."""
+    group = dev.LoopbackGroup(G)
+    out, errs = [None] * G, [None] * G
+
+    def work(r):
+        ctx = None
+        try:
+            ctx = dev.Context(0)
+            ctx.attach_loopback(group, r)
+            out[r] = fn(ctx, r)
+        except BaseException as e:  # noqa: BLE001 -- re-raised below
+            errs[r] = e
+        finally:
+            if ctx is not None:
+                ctx.close()
+
+    ts = [threading.Thread(target=work, args=(r,), daemon=True) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(JOIN_S)
+        assert not t.is_alive(), "loopback rank hung"
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
+
+
+def build(dev, kind, ctx):
+    if kind == "rmat":
+        return dev.generate_rmat(12, 8, seed=3, ctx=ctx)
+    if kind == "rmat_int":
+        # integer weights through a CSR round trip of the R-MAT structure
+        g = dev.generate_rmat(11, 8, seed=5, ctx=ctx)
+        c = g.csr()
+        # symmetric integer weights: w(u,v) = f(min, max)
+        rows = np.repeat(np.arange(len(c["off"]) - 1), np.diff(c["off"]))
+        lo, hi = np.minimum(rows, c["col"]), np.maximum(rows, c["col"])
+        w = ((lo * 31 + hi * 17) % 5 + 1).astype(np.float32)
+        return dev.Graph.from_csr(len(c["off"]) - 1, c["off"], c["col"], w, ctx=ctx)
+    if kind == "lfr":
+        g, _ = dev.generate_lfr(seed=2, ctx=ctx, n=20000, max_degree=120, min_community=20, max_community=400)
+        return g
+    if kind == "planted":
+        g, _ = dev.generate_planted(4000, 40, 0.1, 0.002, seed=1, ctx=ctx)
+        return g
+    raise ValueError(kind)
+
+
+def detect(dev, algo, g):
+    if algo == "plp":
+        cfg = dev.PlpConfig(randomize_order=True, seed=7)
+        z, rep = dev.run_plp(g, cfg)
+    elif algo == "plm":
+        z, rep = dev.run_plm(g, dev.LouvainConfig(seed=7))
+    elif algo == "plmr":
+        z, rep = dev.run_plmr(g, dev.LouvainConfig(seed=7))
+    elif algo == "epp":
+        z, rep = dev.run_epp(g, dev.EnsembleConfig(ensemble_size=3, seed=7))
+    else:
+        raise ValueError(algo)
+    return np.array(z), rep.modularity
+
+
+def single(dev, kind, algo):
+    ctx = dev.Context(0)
+    try:
+        return detect(dev, algo, build(dev, kind, ctx))
+    finally:
+        ctx.close()
+
+
+CASES = [("rmat", "plp"), ("lfr", "plp"), ("rmat", "plm"), ("lfr", "plm"), ("planted", "plmr"),
+         ("rmat_int", "plmr"), ("rmat", "epp"), ("lfr", "epp")]
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("layout", ["replicated", "rows"])
+@pytest.mark.parametrize("kind,algo", CASES)
+def test_sharded_equals_single(dev, G, layout, kind, algo):
+    z1, q1 = single(dev, kind, algo)
+
+    def fn(ctx, r):
+        g = build(dev, kind, ctx)
+        if layout == "rows":
+            g = g.shard(ctx)
+            lo, hi = g.owned_range
+            assert 0 <= lo <= hi <= g.node_count()
+        return detect(dev, algo, g)
+
+    res = run_ranks(dev, G, fn)
+    for r, (z, q) in enumerate(res):
+        assert np.array_equal(z, z1), f"rank {r}: labels differ from the one-device run"
+        assert q == pytest.approx(q1, rel=1e-9, abs=1e-12)
+
+
+def test_sharded_real_weights_quality(dev):
+    """fp32 weights: volumes are fp64 atomics (order-dependent even on one
+    device), so only the labels' consistency across ranks and the quality
+    are pinned."""
+    def mk(ctx):
+        return dev.generate_rmat(12, 8, weighted=True, seed=9, ctx=ctx)
+
+    ctx = dev.Context(0)
+    _, rep1 = dev.run_plmr(mk(ctx), dev.LouvainConfig(seed=3))
+    ctx.close()
+    res = run_ranks(dev, 2, lambda c, r: dev.run_plmr(mk(c).shard(c), dev.LouvainConfig(seed=3)))
+    z0 = np.array(res[0][0])
+    assert np.array_equal(z0, np.array(res[1][0]))
+    assert abs(res[0][1].modularity - rep1.modularity) < 0.005
+
+
+def test_shard_layout_and_quality(dev):
+    """A row shard keeps only its rows; modularity and coarsening over the
+    shards equal the whole graph's."""
+    ctx0 = dev.Context(0)
+    g1 = build(dev, "lfr", ctx0)
+    z1, _ = dev.run_plm(g1, dev.LouvainConfig(seed=1))
+    q1 = dev.modularity(g1, z1)
+    full = g1.csr()
+    coarse1 = dev.coarsen(g1, z1)[0].csr()
+
+    def fn(ctx, r):
+        g = build(dev, "lfr", ctx).shard(ctx)
+        lo, hi = g.owned_range
+        c = g.csr()
+        deg = np.diff(c["off"])
+        assert np.all(deg[:lo] == 0) and np.all(deg[hi:] == 0)
+        assert np.array_equal(c["col"], full["col"][full["off"][lo]:full["off"][hi]])
+        np.testing.assert_array_equal(c["vol"], full["vol"])
+        q = dev.modularity(g, z1)
+        cg = dev.coarsen(g, z1)[0].csr()
+        return lo, hi, q, cg
+
+    res = run_ranks(dev, 3, fn)
+    bounds = [res[0][0]] + [r[1] for r in res]
+    assert bounds[0] == 0 and bounds[-1] == g1.node_count()
+    assert all(res[i][1] == res[i + 1][0] for i in range(2))
+    assert list(bounds) == list(dev.shard_bounds(full["off"], 3))
+    for _, _, q, cg in res:
+        assert q == pytest.approx(q1, rel=1e-12)
+        for key in ("off", "col", "w", "vol", "loop"):
+            np.testing.assert_array_equal(cg[key], coarse1[key])
+    ctx0.close()
+
+
+def test_nccl_world_one(dev):
+    """The NCCL transport (libnccl.so.2, loaded on first use) at world size 1:
+    every sub-sweep still goes through ncclAllGather."""
+    z1, q1 = single(dev, "lfr", "plm")
+    ctx = dev.Context(0)
+    try:
+        ctx.attach_nccl(1, 0, dev.nccl_unique_id())
+        assert ctx.world == (0, 1)
+        z, q = detect(dev, "plm", build(dev, "lfr", ctx))
+        assert np.array_equal(z, z1) and q == q1
+        z, _ = detect(dev, "plp", build(dev, "lfr", ctx).shard(ctx))
+        z2, _ = single(dev, "lfr", "plp")
+        assert np.array_equal(z, z2)
+    finally:
+        ctx.close()
