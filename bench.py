@@ -20,8 +20,15 @@ roofline   dominant kernel family (per-launch CUDA events on a profiled pass of
 cpu_baseline  the unmodified reference (oracle/_ref) on identical bytes (the C
            port of the generator), all host threads, rank 0 at N=1.
 --impl reference  the reference arm: the same metric from oracle/_ref only.
-Multi-GPU (torchrun): one replica per rank ("replicas", weak scaling); value =
-all ranks' edges / max-over-ranks time.
+Multi-GPU (torchrun), --parallel:
+  replicas   one independent graph per rank, no collective (weak scaling);
+             value = all ranks' edges / max-over-ranks time.  Default for the
+             graphs that fit one GPU's work (C1, C2, C4).
+  rows       one graph sharded by rows across the ranks:
+             every rank evaluates its own nodes, move lists are allgathered
+             over NCCL after each sub-sweep, coarse levels replicated (strong
+             scaling); value = m / max-over-ranks time.  Default for C3 / C5.
+  replicated the same with the whole graph on every rank.
 """
 import argparse
 import json
@@ -56,6 +63,8 @@ WORKLOADS = {
     "c4_rmat22w_epp": dict(gen="rmat", scale=22, weighted=True, algo="epp", seed=1,
                            desc="EPP(4,PLP,PLMR) on weighted R-MAT scale 22 ef 16"),
 }
+# graphs whose multi-GPU mode is one sharded graph rather than replicas
+SHARDED_BY_DEFAULT = {"c3_rmat24_plp", "c3_rmat24_plm"}
 
 
 def parse():
@@ -65,6 +74,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--parallel", default=None, choices=["replicas", "rows", "replicated"],
+                    help="multi-GPU mode (default: rows for C3, replicas otherwise)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0, help="bound on the cpu_baseline sample")
     return ap.parse_args()
@@ -192,7 +203,7 @@ def bench_reference(args, wl):
         return 0
     from oracle import oracle as O
     if not O.ref_available():
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libcommdet_ref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libcommdet_ref.so not built"})
         return 0
     og = make_oracle_graph(O, wl)
     rg = O.RefGraph.from_csr(og)
@@ -217,7 +228,7 @@ def bench_reference(args, wl):
                                    f"OMP workers={threads}) on the identical graph"},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -237,8 +248,23 @@ def bench_b200(args, wl):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     ctx = P.Context(local)
+    mode = "1gpu"
+    if world > 1:
+        mode = args.parallel or ("rows" if args.workload in SHARDED_BY_DEFAULT else "replicas")
+    elif args.parallel in ("rows", "replicated"):
+        mode = args.parallel  # world size 1 through the same NCCL exchange path
+    sharded = mode in ("rows", "replicated")
+    if sharded:
+        # the library's own NCCL communicator (torch only carries the unique id)
+        uid = [P.nccl_unique_id() if rank == 0 else None]
+        if dist:
+            dist.broadcast_object_list(uid, src=0)
+        ctx.attach_nccl(world, rank, uid[0])
     g = make_device_graph(P, ctx, wl)
+    if mode == "rows":
+        g = g.shard(ctx)
     n, m = g.node_count(), g.edge_count()
+    units = 1 if sharded else world  # graphs processed per step, all ranks
     out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
     stream = torch.cuda.ExternalStream(ctx.stream, device=f"cuda:{local}")
@@ -277,7 +303,7 @@ def bench_b200(args, wl):
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
-    value = world * m * args.steps / (total_ms / 1e3)
+    value = units * m * args.steps / (total_ms / 1e3)
 
     # ---- quality of the run (modularity vs the CPU reference below) --------------
     z, rep = run_device(P, g, wl["algo"], None, report=True)
@@ -319,7 +345,8 @@ def bench_b200(args, wl):
             roofline["traffic"] = ps["dram_bytes_per_launch"]
 
     # ---- end to end through the C ABI with host buffers ----------------------------
-    c = g.csr()
+    # (a row shard uploads the whole CSR and cuts its rows on the device)
+    c = make_device_graph(P, ctx, wl).csr() if mode == "rows" else g.csr()
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     h_off, h_col = pin(c["off"]), pin(c["col"])
     h_w = pin(c["w"]) if c["w"] is not None else None
@@ -332,6 +359,8 @@ def bench_b200(args, wl):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         gh = P.Graph.from_csr(n, h_off, h_col, h_w, ctx=ctx)
+        if mode == "rows":
+            gh = gh.shard(ctx)
         run_device(P, gh, wl["algo"], h_out, report=False)
         e1.record(stream)
         e1.synchronize()
@@ -340,7 +369,11 @@ def bench_b200(args, wl):
         del gh
     e2e_ms /= e2e_steps
     h2d = h_off.nbytes + h_col.nbytes + (h_w.nbytes if h_w is not None else 0)
-    e2e = {"value": world * m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
+    if dist:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": units * m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(4 * n), "ms_per_step": e2e_ms}
 
     # ---- CPU baseline: the reference on identical bytes (rank 0, N = 1) -----------
@@ -372,20 +405,35 @@ def bench_b200(args, wl):
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32+f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "int32+f64",
+            "data": "synthetic",
             "config": {"workload": args.workload, "desc": wl["desc"], "n": n, "m": m, "entries": g.entries,
-                       "algo": wl["algo"], "seed": wl["seed"], "parallelism": "replicas" if world > 1 else "1gpu",
+                       "algo": wl["algo"], "seed": wl["seed"],
+                       "parallelism": f"{mode} x{world}" if mode != "1gpu" else "1gpu",
                        "l2": "flushed (256 MiB write) before every timed step",
                        "quality": quality},
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
         }
-        print(json.dumps(line))
+        emit(line)
     if dist:
         dist.destroy_process_group()
     return 0
 
 
+_OUT = None  # the JSON line's stream (the original stdout)
+
+
+def emit(line):
+    print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
+
+
 def main():
+    global _OUT
+    # Libraries (NCCL's version banner, ...) may write to fd 1; keep stdout
+    # for the one JSON line and send everything else to stderr.
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     args = parse()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
