@@ -79,6 +79,10 @@ typedef struct cd_louvain_config {
     double move_tol;         /* device: ... or <= move_tol * n (0 disables)  */
     double move_stall;       /* device: ... or (from pass 8 on) when a pass moves more than
                                 move_stall x the moves two passes earlier (0 disables) */
+    int32_t prune;           /* device: re-evaluate a node only after a neighbour (or the node
+                                itself) moved since its last evaluation; 1 (default) in the
+                                input graph's move phases, 2 on every level, 0 never */
+    int32_t reserved;
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */

@@ -1259,11 +1259,24 @@ int64_t cdo_plp_subsweep(const cdo_graph *g, const int32_t *labels, uint8_t *act
     return nm;
 }
 
+void cdo_activate(const cdo_graph *g, int64_t nm, const int32_t *mv_u, uint8_t *active) {
+    if (nm > g->n / 16) { /* dense activation (device k_apply_*) */
+        memset(active, 1, (size_t)g->n);
+        return;
+    }
+    for (int64_t j = 0; j < nm; ++j) {
+        const int32_t u = mv_u[j];
+        for (int64_t i = g->off[u]; i < g->off[u + 1]; ++i)
+            active[g->col[i]] = 1;
+    }
+}
+
 /* One move-phase sub-sweep over [lo, hi) against frozen (z, vols, csize);
- * the decision rule of cdo_move_phase_bucketed; moves are returned. */
+ * the decision rule of cdo_move_phase_bucketed; moves are returned.  With
+ * cfg->prune, only active nodes are evaluated and non-movers deactivated. */
 int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
-                          const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo, int64_t hi,
-                          int32_t *mv_u, int32_t *mv_l) {
+                          uint8_t *active, const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo,
+                          int64_t hi, int32_t *mv_u, int32_t *mv_l) {
     const int32_t K = cfg->buckets > 0 ? cfg->buckets : 1;
     const double inv_total = 1.0 / g->total;
     const double inv_sq2 = 1.0 / (2.0 * g->total * g->total);
@@ -1272,19 +1285,26 @@ int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vo
         scratch_free(&s);
         return CDO_ENOMEM;
     }
+    const int prune = cfg->prune && active;
     int64_t nm = 0;
     for (int64_t u = lo; u < hi; ++u) {
         if (g->off[u + 1] == g->off[u])
             continue;
         if (K > 1 && cdo_bucket_of(key, (int32_t)u, K) != bucket)
             continue;
+        if (prune && !active[u])
+            continue;
         double gain;
         const int32_t c = z[u];
         const int32_t best = move_best(g, z, vols, cfg->gamma, inv_total, inv_sq2, (int32_t)u, &s, &gain);
-        if (best == c || !(gain > 0.0))
+        int moved = best != c && gain > 0.0;
+        if (moved && cfg->singleton_guard && csize[c] == 1 && csize[best] == 1 && best > c)
+            moved = 0;
+        if (!moved) {
+            if (prune)
+                active[u] = 0;
             continue;
-        if (cfg->singleton_guard && csize[c] == 1 && csize[best] == 1 && best > c)
-            continue;
+        }
         mv_u[nm] = (int32_t)u;
         mv_l[nm++] = best;
     }
@@ -1319,6 +1339,11 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
     scratch_init(&s, ub, max_degree(g));
     int32_t *mv_u = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
     int32_t *mv_l = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
+    uint8_t *active = NULL;
+    if (cfg->prune) {
+        active = (uint8_t *)malloc((size_t)n);
+        memset(active, 1, (size_t)n);
+    }
     int changed = 0;
     int64_t hist0 = -1, hist1 = -1; /* moves two passes / one pass earlier */
     for (int64_t pass = 0; pass < cfg->max_move_iterations; ++pass) {
@@ -1331,13 +1356,19 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
                     continue;
                 if (K > 1 && cdo_bucket_of(key, (int32_t)u, K) != b)
                     continue;
+                if (active && !active[u])
+                    continue;
                 double gain;
                 const int32_t c = z[u];
                 const int32_t best = move_best(g, z, vols, cfg->gamma, inv_total, inv_sq2, (int32_t)u, &s, &gain);
-                if (best == c || !(gain > 0.0))
+                int mv = best != c && gain > 0.0;
+                if (mv && cfg->singleton_guard && csize[c] == 1 && csize[best] == 1 && best > c)
+                    mv = 0;
+                if (!mv) {
+                    if (active)
+                        active[u] = 0; /* pruned until a neighbour moves */
                     continue;
-                if (cfg->singleton_guard && csize[c] == 1 && csize[best] == 1 && best > c)
-                    continue;
+                }
                 mv_u[nm] = (int32_t)u;
                 mv_l[nm++] = best;
             }
@@ -1349,6 +1380,8 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
                 csize[d]++;
                 z[u] = d;
             }
+            if (active)
+                cdo_activate(g, nm, mv_u, active);
             moved += nm;
         }
         if (moved == 0)
@@ -1362,6 +1395,7 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
         hist1 = moved;
     }
     *changed_out = changed;
+    free(active);
     free(vols);
     free(csize);
     scratch_free(&s);
@@ -1390,6 +1424,11 @@ static int louvain_recurse(const cdo_graph *g, const cdo_louvain_config *cfg, in
     for (int64_t u = 0; u < n; ++u)
         z[u] = (int32_t)u;
     int32_t changed = 0;
+    /* pruning: 1 = the input graph's move phases only, 2 = every level */
+    cdo_louvain_config lc = *cfg;
+    if (level > 0 && lc.prune < 2)
+        lc.prune = 0;
+    cfg = &lc;
     int rc = cdo_move_phase_bucketed(g, z, cfg, louvain_salt(level, 0), &changed);
     if (rc)
         return rc;

@@ -136,6 +136,8 @@ typedef struct {
     int64_t move_theta; /* <0: floor(n/100000) per level */
     double move_tol;    /* stop also once a pass moves <= move_tol * n */
     double move_stall;  /* ... or (pass >= 8) moves > move_stall * moves two passes earlier */
+    int32_t prune;      /* evaluate only nodes whose neighbourhood changed (device prune):
+                           1 = level-0 move phases, 2 = every level */
 } cdo_louvain_config;
 
 /* bucket key / id: the order every device driver uses. */
@@ -153,8 +155,11 @@ int cdo_louvain_bucketed(const cdo_graph *g, const cdo_louvain_config *cfg, int3
 int64_t cdo_plp_subsweep(const cdo_graph *g, const int32_t *labels, uint8_t *active, uint64_t key, int32_t bucket,
                          int32_t buckets, int64_t lo, int64_t hi, int32_t *mv_u, int32_t *mv_l);
 int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
-                          const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo, int64_t hi,
-                          int32_t *mv_u, int32_t *mv_l);
+                          uint8_t *active, const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo,
+                          int64_t hi, int32_t *mv_u, int32_t *mv_l);
+/* Activation after a sub-sweep's moves (PLP and pruned PLM): all nodes when
+ * more than n/16 moved, else the neighbours of the moved nodes. */
+void cdo_activate(const cdo_graph *g, int64_t nm, const int32_t *mv_u, uint8_t *active);
 int cdo_epp_bucketed(const cdo_graph *g, int64_t ensemble_size, uint64_t seed, const cdo_plp_config *base,
                      const cdo_louvain_config *final_cfg, int32_t *z, int64_t *k);
 

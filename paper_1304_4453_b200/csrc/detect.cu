@@ -205,6 +205,17 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     c.guard = cfg.singleton_guard;
     c.buckets = K;
     owned_range(ctx, g, c.own_lo, c.own_hi);
+    DBuf<uint8_t> active;
+    if (cfg.prune) {
+        active.alloc(ctx, n);
+        active.fill_bytes(1);
+        c.active = active.p;
+        if (g->rows_local && world_size(ctx) > 1) {
+            graph_ensure_transpose(ctx, g);
+            c.toff = g->toff.p;
+            c.tcol = g->tcol.p;
+        }
+    }
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
@@ -235,9 +246,14 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
 }
 
 // H/louvain.hpp:237-267
-static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg, int64_t level, int32_t *z,
+static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg_in, int64_t level, int32_t *z,
                             Report rep) {
     const int64_t n = g->n;
+    // pruning: 1 = the input graph's move phases (where most nodes settle
+    // early), 2 = every level
+    cd_louvain_config cfg = cfg_in;
+    if (level > 0 && cfg.prune < 2)
+        cfg.prune = 0;
     iota_dev(ctx, z, n);  // singleton_partition (:242)
     DevTimer t(ctx);
     t.start();
@@ -262,7 +278,7 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
                 L->coarsen_ms += cm;
             try {
                 DBuf<int32_t> zcoarse(ctx, std::max<int64_t>(k, 1));
-                louvain_recurse(ctx, coarse, cfg, level + 1, zcoarse.p, rep);  // :255
+                louvain_recurse(ctx, coarse, cfg_in, level + 1, zcoarse.p, rep);  // :255
                 prolong_dev(ctx, k, zcoarse.p, n, zc.p, z);                     // :256
             } catch (...) {
                 delete coarse;

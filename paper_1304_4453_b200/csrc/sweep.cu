@@ -226,7 +226,9 @@ __device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool 
         return;
     }
     q.push(P, moved, u, best);
-    if (MODE == MODE_PLP && act && !moved && P.active)
+    // PLP active set (H/plp.hpp:127-133); PLM pruning: a non-mover sleeps
+    // until a neighbour moves
+    if (act && !moved && P.active)
         P.active[u] = 0;
 }
 
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
             const bool has = pos < 32;
             const int32_t u = __shfl_sync(0xffffffffu, cand, has ? pos : 0);
 #pragma unroll
-            for (int q = 0; q < NPW; ++q)
+            for (int j = 0; j < NPW; ++j)
                 selmask &= selmask - 1;
             int64_t s = 0, d = 0;
             if (has) {
@@ -318,7 +320,10 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
 // ---------------------------------------------------------------------------
 // tier WARP: one warp per node (deg <= 256), per-warp smem hash (cap <= 512).
 // All of a row's neighbour ids, then all labels, are loaded up front (8 per
-// lane) so a node costs two rounds of memory latency, not deg/32.
+// lane) so a node costs two rounds of memory latency, not deg/32.  (Parking
+// vols[label] in the table at insert time was measured slower: the extra
+// 4 KB of shared memory per warp costs more occupancy than the scan's
+// gather rounds.)
 // ---------------------------------------------------------------------------
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
@@ -365,6 +370,9 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                 vv[c] = f < e ? P.col[f] : -1;
                 ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
             }
+            // the mover's own volume terms, off the critical path
+            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+            const double vols_cur = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
 #pragma unroll
             for (int c = 0; c < SW_WARP_ITEMS; ++c)
                 kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
@@ -389,8 +397,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                 wc = warp_sum(wc);
             double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
             int32_t ck = INT32_MAX;
-            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(vols_cur, vol_u) : 0.0;
             // slots in rounds of SW_ILP per lane: the vols[key] gathers of a
             // round are independent and in flight together
             for (uint32_t t0 = lane; t0 < cap; t0 += 32 * SW_ILP) {
@@ -884,14 +891,46 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
     }
 }
 
+__device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
+                                               int64_t count, uint8_t *active, const int64_t *toff,
+                                               const int32_t *tcol, int64_t n) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    if (count > n / 16) {
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 15) / 16;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            if (16 * i + 16 <= n)
+                reinterpret_cast<uint4 *>(active)[i] = make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+            else
+                for (int64_t j = 16 * i; j < n; ++j)
+                    active[j] = 1;
+        }
+        return;
+    }
+    for (int sg = 0; sg < nseg; ++sg) {
+        const int2 *m = mv + sg * stride;
+        const int64_t cnt = counts[sg];
+        for (int64_t i = gw; i < cnt; i += nw) {
+            const int32_t u = m[i].x;
+            for (int64_t e = toff[u] + lane; e < toff[u + 1]; e += 32)
+                active[tcol[e]] = 1;
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, double *vols, int32_t *csize, const double *vol,
-                                                   long long *total) {
+                                                   uint8_t *active, const int64_t *toff, const int32_t *tcol,
+                                                   int64_t n, long long *total) {
     __shared__ double scratch[8][32];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int64_t count_all = seg_total(counts, nseg);
     if (blockIdx.x == 0 && threadIdx.x == 0)
-        atomicAdd(reinterpret_cast<unsigned long long *>(total),
-                  static_cast<unsigned long long>(seg_total(counts, nseg)));
+        atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count_all));
+    // pruning: the movers' neighbours wake up (same rule as PLP's active set)
+    if (active)
+        activate_moved(mv, counts, nseg, stride, count_all, active, toff, tcol, n);
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t count = counts[sg];
@@ -1050,7 +1089,14 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     };
     // candidates per warp: about two rounds of work per warp (a round serves
     // 32/G nodes; a bucket selects 1/buckets of the candidates)
-    auto chunk_for = [&](int npw) { return static_cast<int>(std::min<int64_t>(32, 2LL * npw * P.buckets)); };
+    // (short tier lists: about one selected node per warp, so the few nodes
+    // of a coarse level run on many warps instead of a few serial ones)
+    auto chunk_for = [&](int npw, int64_t nodes, int64_t wave_warps) {
+        const int64_t hi = std::min<int64_t>(32, 2LL * npw * P.buckets);
+        const int64_t lo = std::min<int64_t>(hi, static_cast<int64_t>(npw) * P.buckets);
+        const int64_t fit = (nodes + wave_warps - 1) / std::max<int64_t>(wave_warps, 1);
+        return static_cast<int>(std::max(lo, std::min(hi, fit)));
+    };
     // grid: one resident wave (grid-stride over the chunks), fewer blocks if
     // the tier list is short
     auto wave = [&](auto kernel, int threads, size_t smem) { return sms * resident_blocks(kernel, threads, smem); };
@@ -1067,29 +1113,29 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     })
     if ((P.tend[TIER_G8] - P.tbeg[TIER_G8])) {
         fam = names[MODE][TIER_G8];
-        const int ch = chunk_for(4);
         auto kfn = k_sweep_direct<8, MODE, VC>;
+        const int ch = chunk_for(4, P.tend[TIER_G8] - P.tbeg[TIER_G8], int64_t(wave(kfn, 256, 0)) * (256 / 32));
         const int grid = warps_grid_k(kfn, (P.tend[TIER_G8] - P.tbeg[TIER_G8]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G8), ch);
     }
     if ((P.tend[TIER_G16] - P.tbeg[TIER_G16])) {
         fam = names[MODE][TIER_G16];
-        const int ch = chunk_for(2);
         auto kfn = k_sweep_direct<16, MODE, VC>;
+        const int ch = chunk_for(2, P.tend[TIER_G16] - P.tbeg[TIER_G16], int64_t(wave(kfn, 256, 0)) * (256 / 32));
         const int grid = warps_grid_k(kfn, (P.tend[TIER_G16] - P.tbeg[TIER_G16]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16), ch);
     }
     if ((P.tend[TIER_G32] - P.tbeg[TIER_G32])) {
         fam = names[MODE][TIER_G32];
-        const int ch = chunk_for(1);
         auto kfn = k_sweep_direct<32, MODE, VC>;
+        const int ch = chunk_for(1, P.tend[TIER_G32] - P.tbeg[TIER_G32], int64_t(wave(kfn, 256, 0)) * (256 / 32));
         const int grid = warps_grid_k(kfn, (P.tend[TIER_G32] - P.tbeg[TIER_G32]), 256, ch);
         CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G32), ch);
     }
     if ((P.tend[TIER_WARP] - P.tbeg[TIER_WARP])) {
         fam = names[MODE][TIER_WARP];
-        const int ch = chunk_for(1);
         auto kfn = k_sweep_warp<MODE, VC>;
+        const int ch = chunk_for(1, P.tend[TIER_WARP] - P.tbeg[TIER_WARP], int64_t(wave(kfn, 128, 0)) * (128 / 32));
         const int grid = warps_grid_k(kfn, (P.tend[TIER_WARP] - P.tbeg[TIER_WARP]), 128, ch);
         CD_TIER_LAUNCH(kfn, grid, 128, 0, P, ch);
     }
@@ -1245,7 +1291,9 @@ void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t str
                   c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), total_.p, g->n);
     else
         CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
-                  c_.vols, c_.csize, static_cast<const double *>(g->vol.p), total_.p);
+                  c_.vols, c_.csize, static_cast<const double *>(g->vol.p), c_.active,
+                  c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
+                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), g->n, total_.p);
 }
 
 // Sharded sub-sweep exchange: allgather the per-rank move counts, then the

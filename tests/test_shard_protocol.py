@@ -76,14 +76,16 @@ def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterat
     z = np.arange(n, dtype=np.int32)
     vols = O.community_volumes(g, z, n)
     csize = np.ones(n, np.int32)
+    active = np.ones(n, np.uint8)  # pruning (default on)
     theta = max(n // 100000, int(move_tol * n))
     hist = [-1, -1]
     for p in range(max_move_iterations):
         key = O.bucket_key(seed, p)  # salt 0 = level 0, first phase
         moved = 0
         for bk in range(buckets):
-            mu, ml = O.move_subsweep(g, z, vols, csize, key, bk, lo, hi, seed=seed, buckets=buckets)
-            for ru, rl in allgather((mu, ml)):
+            mu, ml = O.move_subsweep(g, z, vols, csize, active, key, bk, lo, hi, seed=seed, buckets=buckets)
+            gathered = allgather((mu, ml))
+            for ru, rl in gathered:
                 for u, d in zip(ru.tolist(), rl.tolist()):
                     c = z[u]
                     vols[c] -= g.vol[u]
@@ -92,6 +94,7 @@ def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterat
                     csize[d] += 1
                     z[u] = d
                 moved += len(ru)
+            O.activate(g, np.concatenate([ru for ru, _ in gathered]), active)
         if moved == 0 or moved <= theta:
             break
         if move_stall > 0 and p >= 8 and moved > move_stall * hist[0]:

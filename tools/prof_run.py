@@ -21,12 +21,20 @@ def main():
     ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--runs", type=int, default=2)
     ap.add_argument("--no-graphs", action="store_true")
+    ap.add_argument("--set", action="append", default=[], help="LouvainConfig field=value (PLM/PLMR)")
     a = ap.parse_args()
+    over = {}
+    for kv in a.set:
+        k, v = kv.split("=")
+        over[k] = type(getattr(P.LouvainConfig(), k))(eval(v))
     wl = bench.WORKLOADS[a.workload]
     ctx = P.Context(0)
     g = bench.make_device_graph(P, ctx, wl)
     for i in range(a.runs):
-        z, rep = bench.run_device(P, g, wl["algo"], None, report=True)
+        if over and wl["algo"] in ("plm", "plmr"):
+            z, rep = P.run_louvain(g, P.LouvainConfig(refine=wl["algo"] == "plmr", **over))
+        else:
+            z, rep = bench.run_device(P, g, wl["algo"], None, report=True)
         print(a.workload, "run", i, "m", g.edge_count(), "Q", round(rep.modularity, 6), "k", rep.community_count,
               "ms", round(rep.total_ms, 3),
               "levels", [(l["nodes"], l["passes"], round(l["move_ms"], 2), round(l["coarsen_ms"], 2))
