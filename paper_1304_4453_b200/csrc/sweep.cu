@@ -145,6 +145,22 @@ __device__ __forceinline__ void tinsert(int32_t *keys, V *vals, uint32_t mask, i
     }
 }
 
+// insert; true if this call claimed a new slot for `key` (*slot = its index)
+template <class V>
+__device__ __forceinline__ bool tinsert_claim(int32_t *keys, V *vals, uint32_t mask, int32_t key, V w,
+                                              uint32_t *slot) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
+        if (old == EMPTY_KEY || old == key) {
+            atomicAdd(&vals[s], w);
+            *slot = s;
+            return old == EMPTY_KEY;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
 template <int VC>
 __device__ __forceinline__ double load_w(const SweepParams &P, int64_t f, bool valid) {
     return (VC != VC_COUNT && valid) ? static_cast<double>(P.w[f]) : 1.0;
@@ -325,6 +341,24 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
 // 4 KB of shared memory per warp costs more occupancy than the scan's
 // gather rounds.)
 // ---------------------------------------------------------------------------
+#ifdef CD_PHASE_TIMING
+// debug build only: clock64 phase sums of the warp tier (lane 0 of each warp)
+__device__ unsigned long long g_phase[16];
+#define CD_PT_START(t) long long t = clock64()
+#define CD_PT(t, i)                                                                                  \
+    do {                                                                                             \
+        __syncwarp();                                                                                \
+        if (lane == 0) {                                                                             \
+            const long long now_ = clock64();                                                        \
+            atomicAdd(&g_phase[i], static_cast<unsigned long long>(now_ - t));                       \
+            t = now_;                                                                                \
+        }                                                                                            \
+    } while (0)
+#else
+#define CD_PT_START(t)
+#define CD_PT(t, i)
+#endif
+
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
@@ -334,9 +368,11 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][SW_WARP_CAP];
     __shared__ V svals[4][SW_WARP_CAP];
+    __shared__ uint16_t sdist[4][SW_WARP_CAP / 2];  // claimed slots = the distinct labels
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     int32_t *keys = skeys[wid];
     V *vals = svals[wid];
+    uint16_t *dist = sdist[wid];
     const int32_t *list = P.tlist + P.tbeg[TIER_WARP];
     const int64_t count = P.tend[TIER_WARP] - P.tbeg[TIER_WARP];
     const unsigned long long bkey = load_key(P);
@@ -353,10 +389,12 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
         while (selmask) {
             const int32_t u = __shfl_sync(0xffffffffu, cand, __ffs(selmask) - 1);
             selmask &= selmask - 1;
+            CD_PT_START(pt);
             const int64_t s = P.off[u], e = P.off[u + 1];
             uint32_t cap = 64;
             while (cap < 2 * (e - s))
                 cap <<= 1;
+            CD_PT(pt, 0);
             for (uint32_t t = lane; t < cap; t += 32) {
                 keys[t] = EMPTY_KEY;
                 vals[t] = V(0);
@@ -373,11 +411,14 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
             // the mover's own volume terms, off the critical path
             const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
             const double vols_cur = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
+            CD_PT(pt, 1);
 #pragma unroll
             for (int c = 0; c < SW_WARP_ITEMS; ++c)
                 kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
             __syncwarp();
+            CD_PT(pt, 2);
             double wc = 0.0;
+            int nd = 0;  // distinct labels so far (warp-uniform)
 #pragma unroll
             for (int c = 0; c < SW_WARP_ITEMS; ++c) {
                 if (s + c * 32 >= e)
@@ -388,26 +429,226 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                 const double wt = static_cast<double>(ww[c]);
                 if (MODE == MODE_PLM && valid && kk[c] == cur)
                     wc += wt;
-                double agg;
-                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
-                    tinsert<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg));
+                bool claimed = false;
+                uint32_t slot = 0;
+                if (VC == VC_REAL) {
+                    // fp64 tallies: combine equal labels in lane order first,
+                    // so every slot sees one add per round (deterministic)
+                    double agg;
+                    if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                        claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+                } else if (valid) {
+                    // integer tallies are order-free: insert directly
+                    claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(ww[c]), &slot);
+                }
+                const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
+                if (claimed)
+                    dist[nd + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
+                nd += __popc(cm);
             }
             __syncwarp();
+            CD_PT(pt, 3);
             if (MODE == MODE_PLM)
                 wc = warp_sum(wc);
             double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
             int32_t ck = INT32_MAX;
             const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(vols_cur, vol_u) : 0.0;
-            // slots in rounds of SW_ILP per lane: the vols[key] gathers of a
-            // round are independent and in flight together
-            for (uint32_t t0 = lane; t0 < cap; t0 += 32 * SW_ILP) {
+            // the distinct labels in rounds of SW_ILP per lane: the vols[key]
+            // gathers of a round are independent and in flight together
+            for (int j0 = lane; j0 < nd; j0 += 32 * SW_ILP) {
                 int32_t key[SW_ILP];
                 double aff[SW_ILP], vd[SW_ILP];
 #pragma unroll
                 for (int c = 0; c < SW_ILP; ++c) {
-                    const uint32_t t = t0 + 32 * c;
-                    key[c] = t < cap ? keys[t] : EMPTY_KEY;
-                    aff[c] = t < cap ? static_cast<double>(vals[t]) : 0.0;
+                    const int j = j0 + 32 * c;
+                    const uint32_t t = j < nd ? dist[j] : 0;
+                    key[c] = j < nd ? keys[t] : EMPTY_KEY;
+                    aff[c] = j < nd ? static_cast<double>(vals[t]) : 0.0;
+                }
+                if (MODE == MODE_PLM) {
+#pragma unroll
+                    for (int c = 0; c < SW_ILP; ++c)
+                        vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
+                        continue;
+                    const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
+                    if (better(val, key[c], cv, ck)) {
+                        cv = val;
+                        ck = key[c];
+                    }
+                }
+            }
+            CD_PT(pt, 4);
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(e - s);
+            }
+            __syncwarp();
+            CD_PT(pt, 5);
+#ifdef CD_PHASE_TIMING
+            if (lane == 0) {
+                atomicAdd(&g_phase[8], 1ULL);
+                atomicAdd(&g_phase[9], static_cast<unsigned long long>(e - s));
+            }
+#endif
+        }
+    }
+    q.flush(P);
+    flush_stats(P, st_n, st_e);
+}
+
+#ifdef CD_PHASE_TIMING
+extern "C" __attribute__((visibility("default"))) int cd_debug_phase(unsigned long long *out) {
+    cudaMemcpyFromSymbol(out, g_phase, sizeof(g_phase));
+    unsigned long long z[16] = {};
+    cudaMemcpyToSymbol(g_phase, z, sizeof(z));
+    return 0;
+}
+#endif
+
+// ---------------------------------------------------------------------------
+// tiers BLOCK / BLOCK2: one block per node, block smem hash of CAP slots.
+// Entry and slot loops are unrolled 4-wide so each thread keeps 4
+// independent global loads in flight.
+// ---------------------------------------------------------------------------
+constexpr int SW_BLOCK_THREADS = 256;
+
+// next power of two >= 2*deg, at least 64 (the table size of a node)
+__device__ __forceinline__ uint32_t table_cap(int64_t deg) {
+    const uint32_t want = static_cast<uint32_t>(2 * deg);
+    return want <= 64 ? 64u : (1u << (32 - __clz(want - 1)));
+}
+
+// Block-cooperative selection: the block's next SW_BLOCK_THREADS candidates
+// (indices blockIdx.x + k * gridDim.x) are tested in parallel and the
+// selected ones compacted into sel[] (ascending k).  Returns their number.
+__device__ __forceinline__ int block_select(const SweepParams &P, unsigned long long bkey, const int32_t *list,
+                                            int64_t count, int64_t k0, int32_t *sel, int *wcount) {
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int64_t i = static_cast<int64_t>(blockIdx.x) + (k0 + threadIdx.x) * gridDim.x;
+    const int32_t u = i < count ? list[i] : 0;
+    const bool take = i < count && selected(P, bkey, u);
+    const uint32_t m = __ballot_sync(0xffffffffu, take);
+    if (lane == 0)
+        wcount[wid] = __popc(m);
+    __syncthreads();
+    int base = 0, total = 0;
+#pragma unroll
+    for (int w = 0; w < SW_BLOCK_THREADS / 32; ++w) {
+        base += w < wid ? wcount[w] : 0;
+        total += wcount[w];
+    }
+    if (take)
+        sel[base + __popc(m & lanemask_lt())] = u;
+    __syncthreads();
+    return total;
+}
+
+template <int MODE, int VC, int CAP, int TIER>
+__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
+    using V = TallyT<VC>;
+    extern __shared__ unsigned char smem_raw[];
+    V *vals = reinterpret_cast<V *>(smem_raw);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
+    uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CAP);  // claimed slots (distinct <= deg <= CAP/2)
+    static_assert(CAP <= 65536, "slot ids are 16-bit");
+    __shared__ double scratch[8][32];
+    __shared__ double red_v[8];
+    __shared__ int32_t red_k[8];
+    __shared__ double red_wc[8];
+    __shared__ int32_t sel[SW_BLOCK_THREADS];
+    __shared__ int wcount[SW_BLOCK_THREADS / 32];
+    __shared__ int ndist;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int32_t *list = P.tlist + P.tbeg[TIER];
+    const int64_t count = P.tend[TIER] - P.tbeg[TIER];
+    const unsigned long long bkey = load_key(P);
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
+    for (int64_t k0 = 0; k0 < per_block; k0 += SW_BLOCK_THREADS) {
+        const int nsel = block_select(P, bkey, list, count, k0, sel, wcount);
+        for (int j = 0; j < nsel; ++j) {
+            const int32_t u = sel[j];
+            const int64_t s = P.off[u], e = P.off[u + 1];
+            const int32_t cur = P.z[u];
+            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+            const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
+            const uint32_t cap = table_cap(e - s);
+            for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
+                keys[t] = EMPTY_KEY;
+                vals[t] = V(0);
+            }
+            if (threadIdx.x == 0)
+                ndist = 0;
+            __syncthreads();
+            double wc = 0.0;
+            for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
+                int32_t vv[SW_ILP], kk[SW_ILP];
+                float ww[SW_ILP];
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    const int64_t f = f0 + c * 32 + lane;
+                    vv[c] = f < e ? P.col[f] : -1;
+                    ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
+                }
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c)
+                    kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    bool valid = vv[c] >= 0;
+                    if (MODE == MODE_PLM)
+                        valid = valid && vv[c] != u;
+                    const double wt = static_cast<double>(ww[c]);
+                    if (MODE == MODE_PLM && valid && kk[c] == cur)
+                        wc += wt;
+                    double agg;
+                    bool claimed = false;
+                    uint32_t slot = 0;
+                    if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                        claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+                    // the claimers of new slots list them (one counter add per warp)
+                    const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
+                    int base = 0;
+                    if (lane == 0 && cm)
+                        base = atomicAdd(&ndist, __popc(cm));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (claimed)
+                        dlist[base + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
+                }
+            }
+            if (MODE == MODE_PLM) {
+                wc = warp_sum(wc);
+                if (lane == 0)
+                    red_wc[wid] = wc;
+            }
+            __syncthreads();
+            if (MODE == MODE_PLM) {
+                wc = 0.0;
+#pragma unroll
+                for (int w = 0; w < 8; ++w)
+                    wc += red_wc[w];
+            }
+            const int nd = ndist;
+            double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+            int32_t ck = INT32_MAX;
+            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
+            // candidates = the distinct labels only (not the whole table)
+            for (int j0 = threadIdx.x; j0 < nd; j0 += SW_BLOCK_THREADS * SW_ILP) {
+                int32_t key[SW_ILP];
+                double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    const int jj = j0 + c * SW_BLOCK_THREADS;
+                    const uint32_t t = jj < nd ? dlist[jj] : 0;
+                    key[c] = jj < nd ? keys[t] : EMPTY_KEY;
+                    aff[c] = jj < nd ? static_cast<double>(vals[t]) : 0.0;
                 }
                 if (MODE == MODE_PLM) {
 #pragma unroll
@@ -426,148 +667,23 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                 }
             }
             argmax_xor<32>(cv, ck);
-            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
             if (lane == 0) {
-                ++st_n;
-                st_e += static_cast<unsigned long long>(e - s);
+                red_v[wid] = cv;
+                red_k[wid] = ck;
             }
-            __syncwarp();
-        }
-    }
-    q.flush(P);
-    flush_stats(P, st_n, st_e);
-}
-
-// ---------------------------------------------------------------------------
-// tiers BLOCK / BLOCK2: one block per node, block smem hash of CAP slots.
-// Entry and slot loops are unrolled 4-wide so each thread keeps 4
-// independent global loads in flight.
-// ---------------------------------------------------------------------------
-constexpr int SW_BLOCK_THREADS = 256;
-
-template <int MODE, int VC, int CAP, int TIER>
-__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
-    using V = TallyT<VC>;
-    extern __shared__ unsigned char smem_raw[];
-    V *vals = reinterpret_cast<V *>(smem_raw);
-    int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
-    __shared__ double scratch[8][32];
-    __shared__ double red_v[8];
-    __shared__ int32_t red_k[8];
-    __shared__ double red_wc[8];
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int32_t *list = P.tlist + P.tbeg[TIER];
-    const int64_t count = P.tend[TIER] - P.tbeg[TIER];
-    const unsigned long long bkey = load_key(P);
-    unsigned long long st_n = 0, st_e = 0;
-    MoveQueue q;
-    // one candidate per block iteration; unselected candidates cost one load
-    for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
-        const int32_t u = list[i];
-        if (!selected(P, bkey, u))
-            continue;
-        const int64_t s = P.off[u], e = P.off[u + 1];
-        const int32_t cur = P.z[u];
-        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-        uint32_t cap = 64;
-        while (cap < 2 * (e - s))
-            cap <<= 1;
-        for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
-            keys[t] = EMPTY_KEY;
-            vals[t] = V(0);
-        }
-        __syncthreads();
-        double wc = 0.0;
-        for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
-            int32_t vv[SW_ILP], kk[SW_ILP];
-            float ww[SW_ILP];
-#pragma unroll
-            for (int c = 0; c < SW_ILP; ++c) {
-                const int64_t f = f0 + c * 32 + lane;
-                vv[c] = f < e ? P.col[f] : -1;
-                ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
-            }
-#pragma unroll
-            for (int c = 0; c < SW_ILP; ++c)
-                kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
-#pragma unroll
-            for (int c = 0; c < SW_ILP; ++c) {
-                bool valid = vv[c] >= 0;
-                if (MODE == MODE_PLM)
-                    valid = valid && vv[c] != u;
-                const double wt = static_cast<double>(ww[c]);
-                if (MODE == MODE_PLM && valid && kk[c] == cur)
-                    wc += wt;
-                double agg;
-                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
-                    tinsert<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg));
-            }
-        }
-        const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
-        if (MODE == MODE_PLM) {
-            wc = warp_sum(wc);
-            if (lane == 0)
-                red_wc[wid] = wc;
-        }
-        __syncthreads();
-        if (MODE == MODE_PLM) {
-            wc = 0.0;
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                wc += red_wc[q];
-        }
-        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
-        int32_t ck = INT32_MAX;
-        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
-        for (uint32_t t0 = threadIdx.x; t0 < cap; t0 += SW_BLOCK_THREADS * SW_ILP) {
-            int32_t key[SW_ILP];
-            double aff[SW_ILP], vd[SW_ILP];
-#pragma unroll
-            for (int c = 0; c < SW_ILP; ++c) {
-                const uint32_t t = t0 + c * SW_BLOCK_THREADS;
-                key[c] = t < cap ? keys[t] : EMPTY_KEY;
-                aff[c] = t < cap ? static_cast<double>(vals[t]) : 0.0;
-            }
-            if (MODE == MODE_PLM) {
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c)
-                    vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
-            }
-#pragma unroll
-            for (int c = 0; c < SW_ILP; ++c) {
-                if (key[c] == EMPTY_KEY)
-                    continue;
-                double val;
-                if (MODE == MODE_PLP) {
-                    val = aff[c];
-                } else {
-                    if (key[c] == cur)
-                        continue;
-                    val = plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
-                }
-                if (better(val, key[c], cv, ck)) {
-                    cv = val;
-                    ck = key[c];
+            __syncthreads();
+            if (wid == 0) {
+                cv = lane < 8 ? red_v[lane] : -INFINITY;
+                ck = lane < 8 ? red_k[lane] : INT32_MAX;
+                argmax_xor<32>(cv, ck);
+                decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+                if (lane == 0) {
+                    ++st_n;
+                    st_e += static_cast<unsigned long long>(e - s);
                 }
             }
+            __syncthreads();
         }
-        argmax_xor<32>(cv, ck);
-        if (lane == 0) {
-            red_v[wid] = cv;
-            red_k[wid] = ck;
-        }
-        __syncthreads();
-        if (wid == 0) {
-            cv = lane < 8 ? red_v[lane] : -INFINITY;
-            ck = lane < 8 ? red_k[lane] : INT32_MAX;
-            argmax_xor<32>(cv, ck);
-            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
-            if (lane == 0) {
-                ++st_n;
-                st_e += static_cast<unsigned long long>(e - s);
-            }
-        }
-        __syncthreads();
     }
     if (wid == 0)
         q.flush(P);
@@ -1141,24 +1257,26 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
         fam = names[MODE][TIER_BLOCK];
-        const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
+        const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(BLOCK_TABLE_CAP / 2) * sizeof(uint16_t);
         static bool attr = false;
         if (!attr) {
             set_smem(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>, smem);
             attr = true;
         }
-        const int nb = grid_for((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1, sms * 8);
+        const int nb = grid_for((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1,
+                                wave((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), SW_BLOCK_THREADS, smem));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), nb, SW_BLOCK_THREADS, smem, P);
     }
     if ((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2])) {
         fam = names[MODE][TIER_BLOCK2];
-        const size_t smem = size_t(BLOCK2_TABLE_CAP) * (sizeof(V) + sizeof(int32_t));
+        const size_t smem = size_t(BLOCK2_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(BLOCK2_TABLE_CAP / 2) * sizeof(uint16_t);
         static bool attr2 = false;
         if (!attr2) {
             set_smem(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>, smem);
             attr2 = true;
         }
-        const int nb = grid_for((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1, sms * (VC == VC_REAL ? 2 : 3));
+        const int nb = grid_for((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1,
+                                wave((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), SW_BLOCK_THREADS, smem));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
     }
     if (P.tend[TIER_HUB] > P.tbeg[TIER_HUB]) {

@@ -39,11 +39,12 @@ def main():
     ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--levels", type=int, default=3)
     ap.add_argument("--start", type=int, default=0, help="levels below this only run once (ncu --launch-skip)")
+    ap.add_argument("--buckets", type=int, default=4)
     a = ap.parse_args()
     wl = bench.WORKLOADS[a.workload]
     ctx = P.Context(0)
     g = bench.make_device_graph(P, ctx, wl)
-    cfg = P.LouvainConfig()
+    cfg = P.LouvainConfig(buckets=a.buckets)
     for level in range(a.levels):
         n = g.node_count()
         z0 = np.arange(n, dtype=np.int32)

@@ -22,6 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--ref", action="store_true")
     ap.add_argument("--graphs", default="c1,c2,r20,r20w")
+    ap.add_argument("--variants", default=None,
+                    help="';'-separated LouvainConfig overrides, e.g. 'move_tol=1e-3;move_tol=1e-2,prune=2'")
     a = ap.parse_args()
     ctx = P.Context(0)
     graphs = {}
@@ -39,6 +41,14 @@ def main():
         for tol in (0.0, 1e-3):
             variants.append(dict(buckets=4, move_tol=tol, move_stall=stall, singleton_guard=True))
     variants.append(dict(buckets=8, move_tol=1e-3, move_stall=0.95, singleton_guard=True))
+    if a.variants:
+        variants = []
+        for spec in a.variants.split(";"):
+            d = {}
+            for kv in filter(None, spec.split(",")):
+                k, v = kv.split("=")
+                d[k] = type(getattr(P.LouvainConfig(), k))(eval(v))
+            variants.append(d)
     for name, g in graphs.items():
         for v in variants:
             for refine in (False,):
