@@ -45,6 +45,13 @@ struct SweepParams {
     // one device); nodes outside [own_lo, own_hi) are never evaluated
     int64_t tbeg[NUM_TIERS], tend[NUM_TIERS];
     int32_t own_lo, own_hi;
+    // pre-bucketed tiers (bit t of pre_mask): once per pass k_prebucket
+    // partitions the tier's segment by bucket into blist (same offsets as
+    // tlist), bucket b at [boff[9t + b], boff[9t + b + 1]) of the segment
+    uint32_t pre_mask;
+    int32_t pre_tiers[NUM_TIERS], n_pre;
+    int32_t *blist;
+    int32_t *boff;
     int32_t *mv_count;  // moves of this bucket
     int2 *mv;           // (node, label) of this bucket's moves
     int32_t *dense_best;
@@ -176,6 +183,83 @@ __device__ __forceinline__ bool selected(const SweepParams &P, unsigned long lon
 
 __device__ __forceinline__ unsigned long long load_key(const SweepParams &P) {
     return P.buckets > 1 ? *P.keyp : 0ULL;
+}
+
+// candidates of tier t in this sub-sweep: a pre-bucketed tier lists exactly
+// the bucket's nodes (only the active flag is left to test)
+__device__ __forceinline__ bool tier_range(const SweepParams &P, int t, const int32_t *&list, int64_t &count) {
+    if ((P.pre_mask >> t) & 1u) {
+        const int32_t *bo = P.boff + 9 * t;
+        list = P.blist + P.tbeg[t] + bo[P.bucket];
+        count = bo[P.bucket + 1] - bo[P.bucket];
+        return true;
+    }
+    list = P.tlist + P.tbeg[t];
+    count = P.tend[t] - P.tbeg[t];
+    return false;
+}
+
+__device__ __forceinline__ bool selected_in(const SweepParams &P, unsigned long long key, int32_t u, bool pre) {
+    return pre ? (!P.active || P.active[u]) : selected(P, key, u);
+}
+
+// Once per pass: stable partition of each pre-bucketed tier segment by bucket
+// (one block per tier; ballots per bucket give the in-warp ranks).
+__global__ void __launch_bounds__(1024) k_prebucket(SweepParams P) {
+    const int t = P.pre_tiers[blockIdx.x];
+    const int32_t *list = P.tlist + P.tbeg[t];
+    int32_t *out = P.blist + P.tbeg[t];
+    const int64_t count = P.tend[t] - P.tbeg[t];
+    const int K = P.buckets;
+    const unsigned long long key = *P.keyp;
+    __shared__ int wcnt[32][8];
+    __shared__ int run[8], tot[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    if (threadIdx.x < 8)
+        tot[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = threadIdx.x; i < count; i += blockDim.x)
+        atomicAdd(&tot[bucket_of(key, list[i], K)], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int s = 0;
+        for (int b = 0; b < K; ++b) {
+            run[b] = s;
+            P.boff[9 * t + b] = s;
+            s += tot[b];
+        }
+        P.boff[9 * t + K] = s;
+    }
+    __syncthreads();
+    for (int64_t base = 0; base < count; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const bool valid = i < count;
+        const int32_t u = valid ? list[i] : 0;
+        const int b = valid ? bucket_of(key, u, K) : -1;
+        int rank = 0;
+        for (int bb = 0; bb < K; ++bb) {
+            const uint32_t m = __ballot_sync(0xffffffffu, b == bb);
+            if (lane == 0)
+                wcnt[wid][bb] = __popc(m);
+            if (b == bb)
+                rank = __popc(m & lanemask_lt());
+        }
+        __syncthreads();
+        if (valid) {
+            int pre = run[b];
+            for (int w = 0; w < wid; ++w)
+                pre += wcnt[w][b];
+            out[pre + rank] = u;
+        }
+        __syncthreads();
+        if (threadIdx.x < K) {
+            int s = 0;
+            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
+                s += wcnt[w][threadIdx.x];
+            run[threadIdx.x] += s;
+        }
+        __syncthreads();
+    }
 }
 
 // Per-warp register queue of moves: lane i holds entry i; one global atomic
@@ -373,8 +457,9 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     int32_t *keys = skeys[wid];
     V *vals = svals[wid];
     uint16_t *dist = sdist[wid];
-    const int32_t *list = P.tlist + P.tbeg[TIER_WARP];
-    const int64_t count = P.tend[TIER_WARP] - P.tbeg[TIER_WARP];
+    const int32_t *list;
+    int64_t count;
+    const bool pre = tier_range(P, TIER_WARP, list, count);
     const unsigned long long bkey = load_key(P);
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -385,7 +470,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
         const bool in = lane < chunk && base + lane < count;
         const int32_t cand = in ? list[base + lane] : 0;
-        uint32_t selmask = __ballot_sync(0xffffffffu, in && selected(P, bkey, cand));
+        uint32_t selmask = __ballot_sync(0xffffffffu, in && selected_in(P, bkey, cand, pre));
         while (selmask) {
             const int32_t u = __shfl_sync(0xffffffffu, cand, __ffs(selmask) - 1);
             selmask &= selmask - 1;
@@ -517,6 +602,7 @@ extern "C" __attribute__((visibility("default"))) int cd_debug_phase(unsigned lo
 // independent global loads in flight.
 // ---------------------------------------------------------------------------
 constexpr int SW_BLOCK_THREADS = 256;
+constexpr int64_t SW_PREBUCKET_MAX = 1 << 16;  // tiers up to this size are pre-bucketed
 
 // next power of two >= 2*deg, at least 64 (the table size of a node)
 __device__ __forceinline__ uint32_t table_cap(int64_t deg) {
@@ -528,11 +614,11 @@ __device__ __forceinline__ uint32_t table_cap(int64_t deg) {
 // (indices blockIdx.x + k * gridDim.x) are tested in parallel and the
 // selected ones compacted into sel[] (ascending k).  Returns their number.
 __device__ __forceinline__ int block_select(const SweepParams &P, unsigned long long bkey, const int32_t *list,
-                                            int64_t count, int64_t k0, int32_t *sel, int *wcount) {
+                                            int64_t count, int64_t k0, int32_t *sel, int *wcount, bool pre) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int64_t i = static_cast<int64_t>(blockIdx.x) + (k0 + threadIdx.x) * gridDim.x;
     const int32_t u = i < count ? list[i] : 0;
-    const bool take = i < count && selected(P, bkey, u);
+    const bool take = i < count && selected_in(P, bkey, u, pre);
     const uint32_t m = __ballot_sync(0xffffffffu, take);
     if (lane == 0)
         wcount[wid] = __popc(m);
@@ -565,14 +651,15 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     __shared__ int wcount[SW_BLOCK_THREADS / 32];
     __shared__ int ndist;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int32_t *list = P.tlist + P.tbeg[TIER];
-    const int64_t count = P.tend[TIER] - P.tbeg[TIER];
+    const int32_t *list;
+    int64_t count;
+    const bool pre = tier_range(P, TIER, list, count);
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
     const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
     for (int64_t k0 = 0; k0 < per_block; k0 += SW_BLOCK_THREADS) {
-        const int nsel = block_select(P, bkey, list, count, k0, sel, wcount);
+        const int nsel = block_select(P, bkey, list, count, k0, sel, wcount, pre);
         for (int j = 0; j < nsel; ++j) {
             const int32_t u = sel[j];
             const int64_t s = P.off[u], e = P.off[u + 1];
@@ -1149,6 +1236,19 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
     }
     if (exchange_)
         rcnt_.alloc(ctx, world_);
+    if (c_.buckets > 1 && !c_.dense_best) {
+        for (int t : {int(TIER_WARP), int(TIER_BLOCK), int(TIER_BLOCK2)}) {
+            const int64_t cnt = tend_[t] - tbeg_[t];
+            if (cnt > 0 && cnt <= SW_PREBUCKET_MAX) {
+                pre_mask_ |= 1u << t;
+                pre_tiers_[n_pre_++] = t;
+            }
+        }
+        if (n_pre_) {
+            blist_.alloc(ctx, std::max<int64_t>(g->tier_start[NUM_TIERS], 1));
+            boff_.alloc(ctx, NUM_TIERS * 9);
+        }
+    }
 }
 
 Sweeper::~Sweeper() {
@@ -1178,6 +1278,15 @@ static int resident_blocks(K kernel, int threads, size_t smem) {
     b = b > 0 ? b : 1;
     cache[key] = b;
     return b;
+}
+
+// nodes a tier kernel gets per sub-sweep (a pre-bucketed tier: about 1/K of
+// its list, with 1/8 headroom for uneven buckets; the kernels grid-stride)
+static int64_t pre_count(const SweepParams &P, int t, int64_t cnt) {
+    if (!((P.pre_mask >> t) & 1u))
+        return cnt;
+    const int64_t per = (cnt + P.buckets - 1) / P.buckets;
+    return std::min(cnt, per + per / 8 + 1);
 }
 
 template <int MODE, int VC>
@@ -1251,8 +1360,14 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     if ((P.tend[TIER_WARP] - P.tbeg[TIER_WARP])) {
         fam = names[MODE][TIER_WARP];
         auto kfn = k_sweep_warp<MODE, VC>;
-        const int ch = chunk_for(1, P.tend[TIER_WARP] - P.tbeg[TIER_WARP], int64_t(wave(kfn, 128, 0)) * (128 / 32));
-        const int grid = warps_grid_k(kfn, (P.tend[TIER_WARP] - P.tbeg[TIER_WARP]), 128, ch);
+        const int64_t wave_warps = int64_t(wave(kfn, 128, 0)) * (128 / 32);
+        const int64_t cnt = P.tend[TIER_WARP] - P.tbeg[TIER_WARP];
+        // pre-bucketed: every listed node is a candidate of this sub-sweep
+        const int64_t per = pre_count(P, TIER_WARP, cnt);
+        const int ch = (P.pre_mask >> TIER_WARP) & 1u
+                           ? static_cast<int>(std::min<int64_t>(32, std::max<int64_t>(1, (per + wave_warps - 1) / wave_warps)))
+                           : chunk_for(1, cnt, wave_warps);
+        const int grid = warps_grid_k(kfn, per, 128, ch);
         CD_TIER_LAUNCH(kfn, grid, 128, 0, P, ch);
     }
     if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
@@ -1263,7 +1378,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             set_smem(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>, smem);
             attr = true;
         }
-        const int nb = grid_for((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1,
+        const int nb = grid_for(pre_count(P, TIER_BLOCK, P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1,
                                 wave((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), SW_BLOCK_THREADS, smem));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), nb, SW_BLOCK_THREADS, smem, P);
     }
@@ -1275,7 +1390,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             set_smem(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>, smem);
             attr2 = true;
         }
-        const int nb = grid_for((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1,
+        const int nb = grid_for(pre_count(P, TIER_BLOCK2, P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1,
                                 wave((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), SW_BLOCK_THREADS, smem));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
     }
@@ -1354,6 +1469,12 @@ void Sweeper::enqueue(bool capture) {
     }
     P.own_lo = static_cast<int32_t>(c_.own_lo);
     P.own_hi = static_cast<int32_t>(c_.own_hi);
+    P.pre_mask = pre_mask_;
+    P.n_pre = n_pre_;
+    for (int i = 0; i < NUM_TIERS; ++i)
+        P.pre_tiers[i] = pre_tiers_[i];
+    P.blist = blist_.p;
+    P.boff = boff_.p;
     P.mv = mv_.p;
     P.dense_best = c_.dense_best;
     P.dense_gain = c_.dense_gain;
@@ -1378,6 +1499,8 @@ void Sweeper::enqueue(bool capture) {
     const bool plp = c_.mode == MODE_PLP;
     if (!c_.dense_best)
         CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
+    if (n_pre_)
+        CD_LAUNCH(ctx, "prebucket", k_prebucket, n_pre_, 1024, 0, P);
     for (int b = 0; b < c_.buckets; ++b) {
         P.bucket = b;
         P.mv_count = cnt_.p + b;

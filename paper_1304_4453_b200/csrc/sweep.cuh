@@ -57,6 +57,11 @@ class Sweeper {
     int world_ = 1;
     bool exchange_ = false;
     int64_t tbeg_[NUM_TIERS] = {}, tend_[NUM_TIERS] = {};
+    // short tier lists are partitioned by bucket once per pass (balanced
+    // sub-sweeps on coarse levels); see k_prebucket
+    uint32_t pre_mask_ = 0;
+    int pre_tiers_[NUM_TIERS] = {}, n_pre_ = 0;
+    DBuf<int32_t> blist_, boff_;
     DBuf<int32_t> cnt_;     // [8]: [b] moves of bucket b
     DBuf<int2> mv_;         // this rank's moves of the current bucket
     DBuf<int32_t> rcnt_;    // [G] gathered counts
