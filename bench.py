@@ -328,8 +328,9 @@ def bench_b200(args, wl):
     s = stats[fam]
     peak, peak_kind = measured_peak()
     achieved = s["bytes"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 and s["bytes"] > 0 else None
-    # "plp_sweep" / "plm_move" aggregate their per-tier ".g8/.warp/..." entries
-    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in ("plp_sweep", "plm_move"))
+    # bases ("plm_move", "coarsen") aggregate their ".warp/.sort/..." entries
+    bases = {k.split(".")[0] for k in stats if "." in k}
+    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in bases)
     roofline = {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "peak_kind": peak_kind, "bytes_per_launch": s["bytes"] / max(s["launches"], 1),

@@ -261,19 +261,20 @@ cd_status cd_ctx_kernel_stats(cd_ctx *ctx, cd_kernel_stat *out, int32_t capacity
         unsigned long long ds[DSTATS];
         CD_CUDA(cudaMemcpyAsync(ds, ctx->dstats, sizeof(ds), cudaMemcpyDeviceToHost, ctx->stream));
         ctx_sync(ctx);
-        // aggregate the per-tier families ("plm_move.warp", ...) into "plm_move"
-        for (const char *agg : {"plp_sweep", "plm_move"}) {
-            KStat tot;
-            bool any = false;
-            const std::string pre = std::string(agg) + ".";
-            for (auto &kv : ctx->stats)
-                if (kv.first.compare(0, pre.size(), pre) == 0) {
-                    tot.launches += kv.second.launches;
-                    tot.total_ms += kv.second.total_ms;
-                    any = true;
-                }
-            if (any)
-                ctx->stats[agg] = tot;
+        // aggregate sub-families ("plm_move.warp", "coarsen.sort", ...) into
+        // their base ("plm_move", "coarsen"); a base never has its own launches
+        {
+            std::map<std::string, KStat> agg;
+            for (auto &kv : ctx->stats) {
+                const size_t dot = kv.first.find('.');
+                if (dot == std::string::npos)
+                    continue;
+                auto &t = agg[kv.first.substr(0, dot)];
+                t.launches += kv.second.launches;
+                t.total_ms += kv.second.total_ms;
+            }
+            for (auto &kv : agg)
+                ctx->stats[kv.first] = kv.second;
         }
         if (ctx->stats.count("plp_sweep")) {
             auto &s = ctx->stats["plp_sweep"];

@@ -750,6 +750,10 @@ template <class Src>
 int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t *fpre, int64_t F_total,
                        int64_t key_bound, DupMode mode, bool &want_w, DBuf<int64_t> &off2, DBuf<int32_t> &col,
                        DBuf<float> &wout, bool *dup, const char *family) {
+    // per-phase profiler families "<family>.<phase>" (cd_ctx_kernel_stats sums them)
+    const std::string fam(family);
+    const std::string f_cls = fam + ".classify", f_red = fam + ".reduce", f_glob = fam + ".reduce_global",
+                      f_sort = fam + ".sort", f_radix = fam + ".radix";
     off2.alloc(ctx, nrows + 1);
     if (nrows == 0) {
         off2.zero();
@@ -769,8 +773,8 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
     counts.zero();
     const int cls_blocks = grid_for(nrows, 256, INT32_MAX);
     int32_t *L[4] = {lists.p, lists.p + nrows, lists.p + 2 * nrows, lists.p + 3 * nrows};
-    CD_LAUNCH(ctx, family, k_eng_zero_rows, cls_blocks, 256, 0, nrows, fpre, deg2.p);
-    CD_LAUNCH(ctx, family, k_eng_classify, cls_blocks, 256, 0, nrows, fpre, static_cast<const int64_t *>(nullptr),
+    CD_LAUNCH(ctx, f_cls.c_str(), k_eng_zero_rows, cls_blocks, 256, 0, nrows, fpre, deg2.p);
+    CD_LAUNCH(ctx, f_cls.c_str(), k_eng_classify, cls_blocks, 256, 0, nrows, fpre, static_cast<const int64_t *>(nullptr),
               int64_t(32), int64_t(ENG_WARP_F), int64_t(ENG_BLOCK_F), L[0], L[1], L[2], L[3], counts.p);
     int32_t hc[8];
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
@@ -781,16 +785,16 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
     EngineOut eo{tkey.p, tval.p, deg2.p, track ? flag.p : nullptr};
     const int sms = ctx->num_sms;
     if (hc[0])
-        CD_LAUNCH(ctx, family, (k_eng_reduce_direct<Src>), grid_for(hc[0], 8, sms * 8), 256, 0, src, fpre, L[0],
+        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_direct<Src>), grid_for(hc[0], 8, sms * 8), 256, 0, src, fpre, L[0],
                   int64_t(hc[0]), int(mode), eo);
     if (hc[1])
-        CD_LAUNCH(ctx, family, (k_eng_reduce_warp<Src>), grid_for(hc[1], 4, sms * 8), 128, 0, src, fpre, L[1],
+        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_warp<Src>), grid_for(hc[1], 4, sms * 8), 128, 0, src, fpre, L[1],
                   int64_t(hc[1]), key_bound, int(mode), eo);
     if (hc[2]) {
         const size_t smem = size_t(2 * ENG_BLOCK_F) * (sizeof(double) + sizeof(int32_t) + sizeof(uint32_t));
         CD_CUDA(cudaFuncSetAttribute(k_eng_reduce_block<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        CD_LAUNCH(ctx, family, (k_eng_reduce_block<Src>), grid_for(hc[2], 1, sms * 2), 512, smem, src, fpre, L[2],
+        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_block<Src>), grid_for(hc[2], 1, sms * 2), 512, smem, src, fpre, L[2],
                   int64_t(hc[2]), key_bound, int(mode), eo);
     }
     if (hc[3]) {
@@ -799,7 +803,7 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         DBuf<int64_t> totals(ctx, 2);
         exclusive_scan<int64_t>(ctx, nb, CapGen{L[3], fpre, key_bound}, tab_off.p, totals.p);
         exclusive_scan<int64_t>(ctx, nb, ChunkGen{L[3], fpre}, chunk_pre.p, totals.p + 1);
-        CD_LAUNCH(ctx, family, k_cap_from_prefix, grid_for(nb, 256, INT32_MAX), 256, 0, nb,
+        CD_LAUNCH(ctx, f_glob.c_str(), k_cap_from_prefix, grid_for(nb, 256, INT32_MAX), 256, 0, nb,
                   static_cast<const int64_t *>(tab_off.p), static_cast<const int64_t *>(totals.p), tab_cap.p);
         int64_t ht[2];
         CD_CUDA(cudaMemcpyAsync(ht, totals.p, sizeof(ht), cudaMemcpyDeviceToHost, ctx->stream));
@@ -810,12 +814,12 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         gk.fill_bytes(0xff);
         gv.zero();
         gc.zero();
-        CD_LAUNCH(ctx, family, (k_eng_reduce_global_insert<Src>), static_cast<int>(ht[1]), 256, 0, src, fpre, L[3],
+        CD_LAUNCH(ctx, f_glob.c_str(), (k_eng_reduce_global_insert<Src>), static_cast<int>(ht[1]), 256, 0, src, fpre, L[3],
                   nb, static_cast<const int64_t *>(chunk_pre.p), static_cast<const int64_t *>(tab_off.p),
                   static_cast<const int64_t *>(tab_cap.p), gk.p, gv.p, gc.p);
-        CD_LAUNCH(ctx, family, k_eng_global_zero, grid_for(nb, 256, sms * 4), 256, 0, nb,
+        CD_LAUNCH(ctx, f_glob.c_str(), k_eng_global_zero, grid_for(nb, 256, sms * 4), 256, 0, nb,
                   static_cast<const int32_t *>(L[3]), deg2.p);
-        CD_LAUNCH(ctx, family, k_eng_flush_chunked, static_cast<int>((ht[0] + ENG_FLUSH_CHUNK - 1) / ENG_FLUSH_CHUNK),
+        CD_LAUNCH(ctx, f_glob.c_str(), k_eng_flush_chunked, static_cast<int>((ht[0] + ENG_FLUSH_CHUNK - 1) / ENG_FLUSH_CHUNK),
                   256, 0, fpre, static_cast<const int32_t *>(L[3]), nb, static_cast<const int64_t *>(tab_off.p), ht[0],
                   static_cast<const int32_t *>(gk.p), static_cast<const double *>(gv.p),
                   static_cast<const uint32_t *>(gc.p), int(mode), eo);
@@ -840,25 +844,25 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         wout.alloc(ctx, 0);
     // sort phase: classify by distinct length
     counts.zero();
-    CD_LAUNCH(ctx, family, k_eng_classify, cls_blocks, 256, 0, nrows, static_cast<const int64_t *>(nullptr),
+    CD_LAUNCH(ctx, f_cls.c_str(), k_eng_classify, cls_blocks, 256, 0, nrows, static_cast<const int64_t *>(nullptr),
               static_cast<const int64_t *>(deg2.p), int64_t(32), int64_t(ENG_SORT_WARP_CAP), int64_t(ENG_SORT_BLOCK),
               L[0], L[1], L[2], L[3], counts.p);
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
     float *wp = want_w ? wout.p : nullptr;
     if (hc[0])
-        CD_LAUNCH(ctx, family, k_eng_sort_warp, grid_for(hc[0], 8, sms * 8), 256, 0, fpre, L[0], int64_t(hc[0]),
+        CD_LAUNCH(ctx, f_sort.c_str(), k_eng_sort_warp, grid_for(hc[0], 8, sms * 8), 256, 0, fpre, L[0], int64_t(hc[0]),
                   static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
                   static_cast<const int64_t *>(off2.p), col.p, wp);
     if (hc[1])
-        CD_LAUNCH(ctx, family, k_eng_sort_warpsmem, grid_for(hc[1], 8, sms * 8), 256, 0, fpre, L[1], int64_t(hc[1]),
+        CD_LAUNCH(ctx, f_sort.c_str(), k_eng_sort_warpsmem, grid_for(hc[1], 8, sms * 8), 256, 0, fpre, L[1], int64_t(hc[1]),
                   static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
                   static_cast<const int64_t *>(off2.p), col.p, wp);
     if (hc[2]) {
         const size_t smem = size_t(ENG_SORT_BLOCK) * (sizeof(double) + sizeof(int32_t));
         CD_CUDA(cudaFuncSetAttribute(k_eng_sort_block, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
-        CD_LAUNCH(ctx, family, k_eng_sort_block, grid_for(hc[2], 1, sms * 2), 512, smem, fpre, L[2], int64_t(hc[2]),
+        CD_LAUNCH(ctx, f_sort.c_str(), k_eng_sort_block, grid_for(hc[2], 1, sms * 2), 512, smem, fpre, L[2], int64_t(hc[2]),
                   static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p),
                   static_cast<const int64_t *>(off2.p), col.p, wp);
     }
@@ -869,7 +873,7 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         while ((int64_t(1) << bits) < key_bound && bits < 31)
             ++bits;
         bits = (bits + 7) / 8 * 8;
-        CD_LAUNCH(ctx, family, k_eng_sort_radix, grid_for(hc[3], 1, sms), 1024, 0, fpre, L[3], int64_t(hc[3]), tkey.p,
+        CD_LAUNCH(ctx, f_radix.c_str(), k_eng_sort_radix, grid_for(hc[3], 1, sms), 1024, 0, fpre, L[3], int64_t(hc[3]), tkey.p,
                   tval.p, k1.p, v1.p, bits, static_cast<const int64_t *>(off2.p), col.p, wp);
     }
     return D2;

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--runs", type=int, default=2)
     ap.add_argument("--no-graphs", action="store_true")
     ap.add_argument("--set", action="append", default=[], help="LouvainConfig field=value (PLM/PLMR)")
+    ap.add_argument("--families", action="store_true", help="per-family kernel times of one profiled run")
     a = ap.parse_args()
     over = {}
     for kv in a.set:
@@ -39,6 +40,14 @@ def main():
               "ms", round(rep.total_ms, 3),
               "levels", [(l["nodes"], l["passes"], round(l["move_ms"], 2), round(l["coarsen_ms"], 2))
                          for l in rep.levels], "iters", len(rep.iterations), flush=True)
+    if a.families:
+        ctx.reset_stats()
+        ctx.set_profiling(True)
+        bench.run_device(P, g, wl["algo"], None, report=False)
+        ctx.set_profiling(False)
+        st = ctx.kernel_stats()
+        for k, v in sorted(st.items(), key=lambda kv: -kv[1]["total_ms"])[:30]:
+            print(f"  {k:28s} {v['total_ms']:9.3f} ms {v['launches']:6d} launches")
 
 
 if __name__ == "__main__":
