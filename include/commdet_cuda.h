@@ -250,6 +250,21 @@ CD_API cd_status cd_louvain_run(cd_ctx *ctx, const cd_graph *g, const cd_louvain
 CD_API cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *cfg, int32_t *z,
                             cd_report *report);
 
+/* ---- text ingest (H/io.hpp) ------------------------------------------------
+ * The file's bytes (host or device memory) are parsed on the device with the
+ * reference reader's rules and errors (CD_EINPUT + message). */
+/* io::read_metis (H/io.hpp:83-165): header "n m [fmt]", '%' comments. */
+CD_API cd_status cd_graph_read_metis(cd_ctx *ctx, const char *text, int64_t len, cd_graph **out);
+/* io::read_edge_list (H/io.hpp:190-237): "u v [w]" lines, '#' comments, ids
+ * densified in ascending order (cd_graph_original_ids). */
+CD_API cd_status cd_graph_read_edge_list(cd_ctx *ctx, const char *text, int64_t len, int32_t merge_duplicates,
+                                         cd_graph **out);
+/* Same, reading the file at `path` first ("cannot open <path>" -> CD_EINPUT). */
+CD_API cd_status cd_graph_load_metis(cd_ctx *ctx, const char *path, cd_graph **out);
+CD_API cd_status cd_graph_load_edge_list(cd_ctx *ctx, const char *path, int32_t merge_duplicates, cd_graph **out);
+/* The original id of every dense node of an edge-list graph (n entries). */
+CD_API cd_status cd_graph_original_ids(const cd_graph *g, uint64_t *out);
+
 /* ---- sharded execution --------------------------------------
  * One rank per GPU.  Attach a communicator to each rank's context; every
  * detector then evaluates only the rank's nodes (1D degree-balanced ranges,

@@ -192,6 +192,8 @@ def ref():
         R.ref_combine_exact.argtypes = [C.c_int64, C.c_int64, C.POINTER(C.c_void_p), i32p]
         R.ref_djb2.argtypes = [C.c_char_p, C.c_uint64]
         R.ref_djb2.restype = C.c_uint64
+        R.ref_read_metis.argtypes = [C.c_char_p, vpp]
+        R.ref_read_edge_list.argtypes = [C.c_char_p, C.c_int, vpp, C.c_void_p, C.c_int64]
         R.ref_run_epp.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int, i32p, C.POINTER(_RefReport)]
         R.ref_max_threads.restype = C.c_int
         _REF = R
@@ -541,6 +543,23 @@ class RefGraph:
         truth = np.zeros(max(n, 1), np.int32)
         _rcheck(ref().ref_generate_planted(n, k, p_in, p_out, seed, workers, C.byref(h), truth.ctypes.data))
         return cls(h.value), truth[:n]
+
+    @classmethod
+    def read_metis(cls, path):
+        """io::read_metis (H/io.hpp:83) on a file."""
+        h = C.c_void_p()
+        _rcheck(ref().ref_read_metis(str(path).encode(), C.byref(h)))
+        return cls(h.value)
+
+    @classmethod
+    def read_edge_list(cls, path, merge_duplicates=False, max_ids=1 << 20):
+        """io::read_edge_list (H/io.hpp:190) on a file: (RefGraph, original ids)."""
+        h = C.c_void_p()
+        ids = np.zeros(max_ids, np.uint64)
+        _rcheck(ref().ref_read_edge_list(str(path).encode(), int(merge_duplicates), C.byref(h), ids.ctypes.data,
+                                         max_ids))
+        g = cls(h.value)
+        return g, ids[: g.info()[0]].copy()
 
     def __del__(self):
         if self.h and _REF is not None:

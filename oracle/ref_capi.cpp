@@ -14,6 +14,7 @@
 //   run_plm / run_plmr / move_phase / coarsen / delta_mod   H/louvain.hpp
 //   run_epp / combine_hashed     H/ensemble.hpp:111, :86
 //   modularity / coverage        H/quality.hpp:35, :21
+//   io::read_metis / read_edge_list   H/io.hpp:83, :190
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -22,6 +23,7 @@
 
 #include <commdet/ensemble.hpp>
 #include <commdet/generator.hpp>
+#include <commdet/io.hpp>
 #include <commdet/louvain.hpp>
 #include <commdet/plp.hpp>
 #include <commdet/quality.hpp>
@@ -307,5 +309,21 @@ int ref_run_epp(const void *gp, int64_t ensemble_size, uint64_t seed, int worker
 }
 
 int ref_max_threads(void) { return omp_get_max_threads(); }
+
+// io::read_metis (H/io.hpp:83-165)
+int ref_read_metis(const char *path, void **out) {
+    return guarded([&] { *out = new cd::Graph(cd::io::read_metis(path)); });
+}
+
+// io::read_edge_list (H/io.hpp:190-237); ids (nullable) receives n original ids
+int ref_read_edge_list(const char *path, int merge, void **out, uint64_t *ids, int64_t ids_cap) {
+    return guarded([&] {
+        std::vector<std::uint64_t> orig;
+        *out = new cd::Graph(cd::io::read_edge_list(path, merge != 0, &orig));
+        if (ids)
+            for (size_t i = 0; i < orig.size() && static_cast<int64_t>(i) < ids_cap; ++i)
+                ids[i] = orig[i];
+    });
+}
 
 } // extern "C"

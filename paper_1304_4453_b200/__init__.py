@@ -39,7 +39,7 @@ __all__ = [
     "run_louvain", "modularity", "coverage", "community_volumes", "coarsen", "prolong", "compacted",
     "community_count", "combine_hashed", "plp_sweep_sync", "move_eval", "move_phase", "dominant_label",
     "is_stable", "library_path", "load_library", "default_context", "ALGO_PLP", "ALGO_PLM", "ALGO_PLMR",
-    "LoopbackGroup", "nccl_unique_id", "shard_bounds",
+    "LoopbackGroup", "nccl_unique_id", "shard_bounds", "read_metis", "read_edge_list",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -141,6 +141,8 @@ EXPORTS = [
     "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_plp_run", "cd_louvain_run", "cd_epp_run",
     "cd_nccl_unique_id", "cd_ctx_attach_nccl", "cd_loopback_create", "cd_loopback_destroy",
     "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard",
+    "cd_graph_read_metis", "cd_graph_read_edge_list", "cd_graph_load_metis", "cd_graph_load_edge_list",
+    "cd_graph_original_ids",
 ]
 
 
@@ -188,6 +190,9 @@ def load_library():
         "cd_loopback_create": [i32, vpp], "cd_loopback_destroy": [vp], "cd_ctx_attach_loopback": [vp, vp, i32],
         "cd_ctx_detach": [vp], "cd_ctx_world": [vp, C.POINTER(i32), C.POINTER(i32)],
         "cd_shard_bounds": [i64, vp, i32, vp], "cd_graph_shard": [vp, vp, vpp],
+        "cd_graph_read_metis": [vp, vp, i64, vpp], "cd_graph_read_edge_list": [vp, vp, i64, i32, vpp],
+        "cd_graph_load_metis": [vp, C.c_char_p, vpp], "cd_graph_load_edge_list": [vp, C.c_char_p, i32, vpp],
+        "cd_graph_original_ids": [vp, vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -452,6 +457,12 @@ class Graph:
         _check(load_library().cd_graph_shard(ctx.h, self.h, C.byref(h)))
         return Graph(h, ctx)
 
+    def original_ids(self):
+        """Dense id -> original id of a graph read by read_edge_list."""
+        out = np.zeros(max(self.node_count(), 1), np.uint64)
+        _check(load_library().cd_graph_original_ids(self.h, out.ctypes.data))
+        return out[: self.node_count()]
+
     @property
     def owned_range(self):
         return self._info.own_lo, self._info.own_hi
@@ -539,6 +550,49 @@ def generate_lfr(seed=1, ctx=None, **spec):
     h = C.c_void_p()
     _check(load_library().cd_graph_generate_lfr(ctx.h, C.byref(cs), seed, C.byref(h), truth.ctypes.data))
     return Graph(h, ctx), truth
+
+
+# ---------------------------------------------------------------------------
+# text ingest (H/io.hpp) -- parsed on the device
+# ---------------------------------------------------------------------------
+def _text_arg(source):
+    if isinstance(source, (bytes, bytearray, memoryview)):
+        return bytes(source), None
+    if _is_dev(source):
+        return source, None
+    return None, os.fspath(source)
+
+
+def read_metis(source, ctx=None) -> Graph:
+    """io::read_metis (H/io.hpp:83-165).  `source`: a path, or the file's bytes
+    (host bytes or a uint8 CUDA tensor)."""
+    ctx = _ctx(ctx)
+    data, path = _text_arg(source)
+    h = C.c_void_p()
+    L = load_library()
+    if path is not None:
+        _check(L.cd_graph_load_metis(ctx.h, path.encode(), C.byref(h)))
+    else:
+        ptr = data.data_ptr() if _is_dev(data) else C.cast(C.c_char_p(data), C.c_void_p).value
+        n = data.numel() if _is_dev(data) else len(data)
+        _check(L.cd_graph_read_metis(ctx.h, ptr, n, C.byref(h)))
+    return Graph(h, ctx)
+
+
+def read_edge_list(source, merge_duplicates=False, ctx=None) -> Graph:
+    """io::read_edge_list (H/io.hpp:190-237); `Graph.original_ids()` gives the
+    dense -> original id map."""
+    ctx = _ctx(ctx)
+    data, path = _text_arg(source)
+    h = C.c_void_p()
+    L = load_library()
+    if path is not None:
+        _check(L.cd_graph_load_edge_list(ctx.h, path.encode(), int(merge_duplicates), C.byref(h)))
+    else:
+        ptr = data.data_ptr() if _is_dev(data) else C.cast(C.c_char_p(data), C.c_void_p).value
+        n = data.numel() if _is_dev(data) else len(data)
+        _check(L.cd_graph_read_edge_list(ctx.h, ptr, n, int(merge_duplicates), C.byref(h)))
+    return Graph(h, ctx)
 
 
 # ---------------------------------------------------------------------------

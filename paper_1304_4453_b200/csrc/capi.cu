@@ -691,6 +691,67 @@ cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *c
     })
 }
 
+// ---- text ingest -------------------------------------------------------------------
+
+namespace {
+std::vector<char> read_file(const char *path) {
+    FILE *f = std::fopen(path, "rb");
+    if (!f)
+        fail(CD_EINPUT, std::string("cannot open ") + path);  // H/io.hpp:23-28
+    std::vector<char> buf;
+    char tmp[1 << 16];
+    size_t r;
+    while ((r = std::fread(tmp, 1, sizeof(tmp), f)) > 0)
+        buf.insert(buf.end(), tmp, tmp + r);
+    const bool bad = std::ferror(f) != 0;
+    std::fclose(f);
+    if (bad)
+        fail(CD_EINPUT, std::string("cannot read ") + path);
+    return buf;
+}
+}  // namespace
+
+cd_status cd_graph_read_metis(cd_ctx *ctx, const char *text, int64_t len, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out && len >= 0 && (len == 0 || text), CD_EINVAL, "invalid argument");
+        *out = read_metis_dev(ctx, text, len, "<metis>");
+    })
+}
+
+cd_status cd_graph_read_edge_list(cd_ctx *ctx, const char *text, int64_t len, int32_t merge, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out && len >= 0 && (len == 0 || text), CD_EINVAL, "invalid argument");
+        *out = read_edge_list_dev(ctx, text, len, merge != 0, "<edge list>");
+    })
+}
+
+cd_status cd_graph_load_metis(cd_ctx *ctx, const char *path, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out && path, CD_EINVAL, "invalid argument");
+        const std::vector<char> buf = read_file(path);
+        *out = read_metis_dev(ctx, buf.data(), static_cast<int64_t>(buf.size()), path);
+    })
+}
+
+cd_status cd_graph_load_edge_list(cd_ctx *ctx, const char *path, int32_t merge, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out && path, CD_EINVAL, "invalid argument");
+        const std::vector<char> buf = read_file(path);
+        *out = read_edge_list_dev(ctx, buf.data(), static_cast<int64_t>(buf.size()), merge != 0, path);
+    })
+}
+
+cd_status cd_graph_original_ids(const cd_graph *g, uint64_t *out) {
+    cd_ctx *ctx = g ? g->ctx : nullptr;
+    CD_GUARD(ctx, {
+        CD_REQUIRE(g && out, CD_EINVAL, "invalid argument");
+        CD_REQUIRE(g->orig_ids.p != nullptr || g->n == 0, CD_EINVAL, "graph was not read from an edge list");
+        if (g->n)
+            CD_CUDA(cudaMemcpyAsync(out, g->orig_ids.p, g->n * sizeof(uint64_t), cudaMemcpyDefault, ctx->stream));
+        ctx_sync(ctx);
+    })
+}
+
 // ---- sharded execution ----------------------------------------------------------
 
 cd_status cd_nccl_unique_id(uint8_t id[128]) {

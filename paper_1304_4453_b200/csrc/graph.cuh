@@ -113,6 +113,9 @@ struct cd_graph {
     int64_t D_global = 0;
     cdk::DBuf<int64_t> toff;
     cdk::DBuf<int32_t> tcol;
+
+    // edge-list ingest: dense id -> original id (ascending; H/io.hpp:220-235)
+    cdk::DBuf<uint64_t> orig_ids;
 };
 
 namespace cdk {
@@ -126,6 +129,10 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g);
 cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, const int32_t *v, const float *w,
                            DupMode mode);  // device arrays; symmetrises
 void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D);
+
+// text.cu (H/io.hpp:83-165, :190-237); `name` prefixes error messages
+cd_graph *read_metis_dev(cd_ctx *ctx, const char *text, int64_t len, const std::string &name);
+cd_graph *read_edge_list_dev(cd_ctx *ctx, const char *text, int64_t len, bool merge, const std::string &name);
 
 // shard.cu
 cd_graph *graph_shard_dev(cd_ctx *ctx, const cd_graph *full);  // rows of this rank (ctx->comm)
