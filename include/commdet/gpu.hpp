@@ -660,6 +660,31 @@ inline std::pair<Graph, Partition> generate_planted(const PlantedPartitionSpec &
     return {adopt_graph(h), t};
 }
 
+// ---- text readers (H/io.hpp) -- parsed on the device ------------------------------------
+namespace io {
+
+/// io::read_metis (H/io.hpp:83-165).
+inline Graph read_metis(const std::string &path) {
+    cd_graph *h = nullptr;
+    detail::check(cd_graph_load_metis(Context::instance().get(), path.c_str(), &h));
+    return adopt_graph(h);
+}
+
+/// io::read_edge_list (H/io.hpp:190-237).
+inline Graph read_edge_list(const std::string &path, bool merge_duplicates = false,
+                            std::vector<std::uint64_t> *original_ids = nullptr) {
+    cd_graph *h = nullptr;
+    detail::check(cd_graph_load_edge_list(Context::instance().get(), path.c_str(), merge_duplicates ? 1 : 0, &h));
+    Graph g = adopt_graph(h);
+    if (original_ids) {
+        original_ids->resize(g.node_count());
+        detail::check(cd_graph_original_ids(h, original_ids->empty() ? nullptr : original_ids->data()));
+    }
+    return g;
+}
+
+}  // namespace io
+
 }  // namespace gpu
 
 #ifdef COMMDET_GPU_DROP_IN

@@ -128,6 +128,34 @@ int main() {
     CHECK(pg == two_triangles());
     CHECK_THROWS_AS(generate_planted({10, 0, 0.5, 0.1, 1}), std::invalid_argument);
 
+    // io (T/test_io.cpp): METIS / edge-list readers, parsed on the device
+    {
+        const char *mp = "/tmp/shim_kat_tri.metis";
+        if (FILE *f = std::fopen(mp, "w")) {
+            std::fputs("% two triangles\n6 6\n2 3\n1 3\n1 2\n5 6\n4 6\n4 5\n", f);
+            std::fclose(f);
+        }
+        CHECK(io::read_metis(mp) == two_triangles());
+        const char *bad = "/tmp/shim_kat_bad.metis";
+        if (FILE *f = std::fopen(bad, "w")) {
+            std::fputs("2 1\n2\n\n", f);
+            std::fclose(f);
+        }
+        CHECK_THROWS_AS(io::read_metis(bad), input_error);  // asymmetric adjacency
+        CHECK_THROWS_AS(io::read_metis("/tmp/shim_kat_missing.metis"), input_error);
+        const char *ep = "/tmp/shim_kat.edges";
+        if (FILE *f = std::fopen(ep, "w")) {
+            std::fputs("# c\n10 20\n20 30 2.5\n", f);
+            std::fclose(f);
+        }
+        std::vector<std::uint64_t> ids;
+        Graph eg = io::read_edge_list(ep, false, &ids);
+        CHECK((eg.node_count() == 3 && eg.edge_count() == 2 && ids == std::vector<std::uint64_t>{10, 20, 30}));
+        std::remove(mp);
+        std::remove(bad);
+        std::remove(ep);
+    }
+
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
     return failures ? 1 : 0;
 }
