@@ -216,6 +216,9 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
             c.tcol = g->tcol.p;
         }
     }
+    if (small_move_eligible(ctx, g, c))
+        return small_move_phase(ctx, g, c, cfg.seed, salt, cfg.max_move_iterations, theta, cfg.move_stall, passes,
+                                moves);
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;

@@ -18,7 +18,10 @@
 // ones and processes them -- no worklist kernel, no global atomics.
 #include "sweep.cuh"
 
+#include <cooperative_groups.h>
+
 #include <cmath>
+#include <cstdio>
 #include <map>
 #include <mutex>
 
@@ -635,6 +638,135 @@ __device__ __forceinline__ int block_select(const SweepParams &P, unsigned long 
     return total;
 }
 
+// Shared state of the block evaluator (one node per block at a time).
+struct BlockShared {
+    double scratch[8][32];
+    double red_v[8];
+    int32_t red_k[8];
+    double red_wc[8];
+    int ndist;
+};
+
+// Evaluates node u with the whole block (256 threads): smem hash tally of
+// its neighbours' labels (table of table_cap(deg) slots, claimed slots listed
+// in dlist), Δ / affinity of every distinct label, block argmax, decision.
+// Called by all threads of the block; ends with a block barrier.
+template <int MODE, int VC>
+__device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u, TallyT<VC> *vals, int32_t *keys,
+                                                uint16_t *dlist, BlockShared &sh, MoveQueue &q,
+                                                unsigned long long &st_n, unsigned long long &st_e) {
+    using V = TallyT<VC>;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int64_t s = P.off[u], e = P.off[u + 1];
+    const int32_t cur = P.z[u];
+    const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+    const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
+    const uint32_t cap = table_cap(e - s);
+    for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
+        keys[t] = EMPTY_KEY;
+        vals[t] = V(0);
+    }
+    if (threadIdx.x == 0)
+        sh.ndist = 0;
+    __syncthreads();
+    double wc = 0.0;
+    for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
+        int32_t vv[SW_ILP], kk[SW_ILP];
+        float ww[SW_ILP];
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            const int64_t f = f0 + c * 32 + lane;
+            vv[c] = f < e ? P.col[f] : -1;
+            ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
+        }
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c)
+            kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            bool valid = vv[c] >= 0;
+            if (MODE == MODE_PLM)
+                valid = valid && vv[c] != u;
+            const double wt = static_cast<double>(ww[c]);
+            if (MODE == MODE_PLM && valid && kk[c] == cur)
+                wc += wt;
+            double agg;
+            bool claimed = false;
+            uint32_t slot = 0;
+            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, sh.scratch[wid], agg))
+                claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+            // the claimers of new slots list them (one counter add per warp)
+            const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
+            int base = 0;
+            if (lane == 0 && cm)
+                base = atomicAdd(&sh.ndist, __popc(cm));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (claimed)
+                dlist[base + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
+        }
+    }
+    if (MODE == MODE_PLM) {
+        wc = warp_sum(wc);
+        if (lane == 0)
+            sh.red_wc[wid] = wc;
+    }
+    __syncthreads();
+    if (MODE == MODE_PLM) {
+        wc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w)
+            wc += sh.red_wc[w];
+    }
+    const int nd = sh.ndist;
+    double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+    int32_t ck = INT32_MAX;
+    const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
+    // candidates = the distinct labels only (not the whole table)
+    for (int j0 = threadIdx.x; j0 < nd; j0 += SW_BLOCK_THREADS * SW_ILP) {
+        int32_t key[SW_ILP];
+        double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            const int jj = j0 + c * SW_BLOCK_THREADS;
+            const uint32_t t = jj < nd ? dlist[jj] : 0;
+            key[c] = jj < nd ? keys[t] : EMPTY_KEY;
+            aff[c] = jj < nd ? static_cast<double>(vals[t]) : 0.0;
+        }
+        if (MODE == MODE_PLM) {
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c)
+                vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
+                continue;
+            const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
+            if (better(val, key[c], cv, ck)) {
+                cv = val;
+                ck = key[c];
+            }
+        }
+    }
+    argmax_xor<32>(cv, ck);
+    if (lane == 0) {
+        sh.red_v[wid] = cv;
+        sh.red_k[wid] = ck;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        cv = lane < 8 ? sh.red_v[lane] : -INFINITY;
+        ck = lane < 8 ? sh.red_k[lane] : INT32_MAX;
+        argmax_xor<32>(cv, ck);
+        decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+        if (lane == 0) {
+            ++st_n;
+            st_e += static_cast<unsigned long long>(e - s);
+        }
+    }
+    __syncthreads();
+}
+
 template <int MODE, int VC, int CAP, int TIER>
 __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
     using V = TallyT<VC>;
@@ -643,14 +775,10 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
     uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CAP);  // claimed slots (distinct <= deg <= CAP/2)
     static_assert(CAP <= 65536, "slot ids are 16-bit");
-    __shared__ double scratch[8][32];
-    __shared__ double red_v[8];
-    __shared__ int32_t red_k[8];
-    __shared__ double red_wc[8];
+    __shared__ BlockShared sh;
     __shared__ int32_t sel[SW_BLOCK_THREADS];
     __shared__ int wcount[SW_BLOCK_THREADS / 32];
-    __shared__ int ndist;
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int wid = threadIdx.x >> 5;
     const int32_t *list;
     int64_t count;
     const bool pre = tier_range(P, TIER, list, count);
@@ -660,121 +788,138 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
     for (int64_t k0 = 0; k0 < per_block; k0 += SW_BLOCK_THREADS) {
         const int nsel = block_select(P, bkey, list, count, k0, sel, wcount, pre);
-        for (int j = 0; j < nsel; ++j) {
-            const int32_t u = sel[j];
-            const int64_t s = P.off[u], e = P.off[u + 1];
-            const int32_t cur = P.z[u];
-            const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
-            const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
-            const uint32_t cap = table_cap(e - s);
-            for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
-                keys[t] = EMPTY_KEY;
-                vals[t] = V(0);
-            }
-            if (threadIdx.x == 0)
-                ndist = 0;
-            __syncthreads();
-            double wc = 0.0;
-            for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
-                int32_t vv[SW_ILP], kk[SW_ILP];
-                float ww[SW_ILP];
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c) {
-                    const int64_t f = f0 + c * 32 + lane;
-                    vv[c] = f < e ? P.col[f] : -1;
-                    ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
-                }
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c)
-                    kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c) {
-                    bool valid = vv[c] >= 0;
-                    if (MODE == MODE_PLM)
-                        valid = valid && vv[c] != u;
-                    const double wt = static_cast<double>(ww[c]);
-                    if (MODE == MODE_PLM && valid && kk[c] == cur)
-                        wc += wt;
-                    double agg;
-                    bool claimed = false;
-                    uint32_t slot = 0;
-                    if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
-                        claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
-                    // the claimers of new slots list them (one counter add per warp)
-                    const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
-                    int base = 0;
-                    if (lane == 0 && cm)
-                        base = atomicAdd(&ndist, __popc(cm));
-                    base = __shfl_sync(0xffffffffu, base, 0);
-                    if (claimed)
-                        dlist[base + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
-                }
-            }
-            if (MODE == MODE_PLM) {
-                wc = warp_sum(wc);
-                if (lane == 0)
-                    red_wc[wid] = wc;
-            }
-            __syncthreads();
-            if (MODE == MODE_PLM) {
-                wc = 0.0;
-#pragma unroll
-                for (int w = 0; w < 8; ++w)
-                    wc += red_wc[w];
-            }
-            const int nd = ndist;
-            double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
-            int32_t ck = INT32_MAX;
-            const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
-            // candidates = the distinct labels only (not the whole table)
-            for (int j0 = threadIdx.x; j0 < nd; j0 += SW_BLOCK_THREADS * SW_ILP) {
-                int32_t key[SW_ILP];
-                double aff[SW_ILP], vd[SW_ILP];
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c) {
-                    const int jj = j0 + c * SW_BLOCK_THREADS;
-                    const uint32_t t = jj < nd ? dlist[jj] : 0;
-                    key[c] = jj < nd ? keys[t] : EMPTY_KEY;
-                    aff[c] = jj < nd ? static_cast<double>(vals[t]) : 0.0;
-                }
-                if (MODE == MODE_PLM) {
-#pragma unroll
-                    for (int c = 0; c < SW_ILP; ++c)
-                        vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
-                }
-#pragma unroll
-                for (int c = 0; c < SW_ILP; ++c) {
-                    if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
-                        continue;
-                    const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
-                    if (better(val, key[c], cv, ck)) {
-                        cv = val;
-                        ck = key[c];
-                    }
-                }
-            }
-            argmax_xor<32>(cv, ck);
-            if (lane == 0) {
-                red_v[wid] = cv;
-                red_k[wid] = ck;
-            }
-            __syncthreads();
-            if (wid == 0) {
-                cv = lane < 8 ? red_v[lane] : -INFINITY;
-                ck = lane < 8 ? red_k[lane] : INT32_MAX;
-                argmax_xor<32>(cv, ck);
-                decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
-                if (lane == 0) {
-                    ++st_n;
-                    st_e += static_cast<unsigned long long>(e - s);
-                }
-            }
-            __syncthreads();
-        }
+        for (int j = 0; j < nsel; ++j)
+            block_eval_node<MODE, VC>(P, sel[j], vals, keys, dlist, sh, q, st_n, st_e);
     }
     if (wid == 0)
         q.flush(P);
     flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
+// Small graphs (coarse levels): the whole move phase in one cooperative
+// launch.  Every pass partitions the nodes by bucket (grid-wide atomics into
+// per-bucket lists, heaviest nodes first), every sub-sweep hands nodes to
+// blocks through a work counter (block_eval_node, the BLOCK-tier evaluator),
+// grid barriers separate evaluation, apply and the next sub-sweep, and the
+// stop rules of move_phase_dev run on the device.  No launches, graph
+// replays or host round trips between sub-sweeps: on a level of a few
+// thousand nodes those, not the work, set the time.
+// ---------------------------------------------------------------------------
+struct SmallPhase {
+    const int32_t *order;  // nodes with deg > 0, heavy tiers first
+    int32_t nn;
+    int32_t *bsel;         // [nn] bucket of order[i] (scratch)
+    int32_t *blist;        // [nn] bucket-partitioned nodes
+    int32_t *ctr;          // [0,8) counts [8,16) cursors [16,24) work [24,32) moves
+    unsigned long long seed, salt;
+    int K;
+    int max_passes;
+    long long theta;
+    double stall;
+    uint32_t cap_max;
+    long long *result;     // passes, moves, changed
+    int trace;
+};
+
+template <int VC>
+__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_small_move(SweepParams P, SmallPhase S) {
+    namespace cg = cooperative_groups;
+    using V = TallyT<VC>;
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ unsigned char smem_raw[];
+    V *vals = reinterpret_cast<V *>(smem_raw);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + S.cap_max);
+    uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + S.cap_max);
+    __shared__ BlockShared sh;
+    __shared__ int s_idx;
+    const int wid = threadIdx.x >> 5;
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gsize = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int32_t *ctr = S.ctr;
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    long long hist0 = -1, hist1 = -1, moves_total = 0;
+    int passes = 0;
+    bool changed = false;
+    for (int pass = 0; pass < S.max_passes; ++pass) {
+        const unsigned long long key = bucket_key(S.seed, S.salt + static_cast<unsigned long long>(pass));
+        for (int64_t i = gtid; i < S.nn; i += gsize) {
+            const int b = S.K > 1 ? bucket_of(key, S.order[i], S.K) : 0;
+            S.bsel[i] = b;
+            atomicAdd(&ctr[b], 1);
+        }
+        grid.sync();
+        for (int64_t i = gtid; i < S.nn; i += gsize) {
+            const int b = S.bsel[i];
+            int off = 0;
+            for (int c = 0; c < b; ++c)
+                off += ctr[c];
+            S.blist[off + atomicAdd(&ctr[8 + b], 1)] = S.order[i];
+        }
+        grid.sync();
+        long long pass_moves = 0;
+        int base = 0;
+        for (int b = 0; b < S.K; ++b) {
+            const int cnt = ctr[b];
+            P.bucket = b;
+            P.mv_count = ctr + 24 + b;
+            while (true) {
+                if (threadIdx.x == 0)
+                    s_idx = atomicAdd(&ctr[16 + b], 1);
+                __syncthreads();
+                const int idx = s_idx;
+                __syncthreads();
+                if (idx >= cnt)
+                    break;
+                block_eval_node<MODE_PLM, VC>(P, S.blist[base + idx], vals, keys, dlist, sh, q, st_n, st_e);
+            }
+            if (wid == 0)
+                q.flush(P);
+            grid.sync();
+            const int mc = ctr[24 + b];
+            for (int64_t i = gtid; i < mc; i += gsize) {  // H/louvain.hpp:121-125
+                const int2 m = P.mv[i];
+                const int32_t c = P.z[m.x];
+                const_cast<int32_t *>(P.z)[m.x] = m.y;
+                const double vu = P.vol[m.x];
+                atomicAdd(const_cast<double *>(&P.vols[m.y]), vu);
+                atomicAdd(const_cast<double *>(&P.vols[c]), -vu);
+                atomicAdd(const_cast<int32_t *>(&P.csize[m.y]), 1);
+                atomicSub(const_cast<int32_t *>(&P.csize[c]), 1);
+            }
+            pass_moves += mc;
+            base += cnt;
+            grid.sync();
+        }
+        ++passes;
+        moves_total += pass_moves;
+        if (S.trace && gtid == 0)
+            printf("[cd] move(small) nodes=%d pass=%d moved=%lld\n", S.nn, pass, pass_moves);
+        bool stop = false;  // the rules of move_phase_dev, identical on every thread
+        if (pass_moves == 0) {
+            stop = true;
+        } else {
+            changed = true;
+            if (pass_moves <= S.theta)
+                stop = true;
+            else if (S.stall > 0.0 && pass >= 8 && static_cast<double>(pass_moves) > S.stall * static_cast<double>(hist0))
+                stop = true;
+            hist0 = hist1;
+            hist1 = pass_moves;
+        }
+        if (blockIdx.x == 0 && threadIdx.x < 32)
+            ctr[threadIdx.x] = 0;
+        grid.sync();
+        if (stop)
+            break;
+    }
+    flush_stats(P, st_n, st_e);
+    if (gtid == 0) {
+        S.result[0] = passes;
+        S.result[1] = moves_total;
+        S.result[2] = changed ? 1 : 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1585,6 +1730,105 @@ void Sweeper::pass(uint64_t key) {
     }
     CD_CUDA(cudaGraphLaunch(exec_, ctx_->stream));
     ctx_->launches += kernels_per_pass_;
+}
+
+// Eligible: one device (no exchange), no pruning, no hubs (the block
+// evaluator's table holds up to 8192 slots), and a graph small enough that
+// launch and synchronisation overheads dominate (CD_SMALL_N, default 2^15).
+bool small_move_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c) {
+    static const int64_t limit = [] {
+        const char *e = std::getenv("CD_SMALL_N");
+        return e ? std::atoll(e) : (int64_t(1) << 15);
+    }();
+    return ctx->comm == nullptr && !c.active && !c.dense_best && c.mode == MODE_PLM && g->n > 0 && g->n <= limit &&
+           g->max_degree <= 4096 && c.buckets >= 1 && c.buckets <= 8;
+}
+
+template <int VC>
+static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S, size_t smem) {
+    auto kfn = k_small_move<VC>;
+    CD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int per_sm = 0;
+    CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, SW_BLOCK_THREADS, smem));
+    if (per_sm < 1)
+        fail(CD_EINTERNAL, "small move phase: kernel does not fit an SM");
+    const int grid = std::max(1, std::min<int>(per_sm * ctx->num_sms, static_cast<int>((S.nn + 1) / 2)));
+    SweepParams p = P;
+    SmallPhase s = S;
+    void *args[] = {&p, &s};
+    LaunchScope ls(ctx, "plm_move.small");
+    CD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kfn), dim3(grid), dim3(SW_BLOCK_THREADS), args,
+                                        smem, ctx->stream));
+}
+
+bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
+                      int64_t theta, double stall, int64_t *passes, int64_t *moves) {
+    graph_ensure_bins(ctx, g);
+    const int64_t nn = g->tier_start[NUM_TIERS];
+    DBuf<int32_t> order(ctx, std::max<int64_t>(nn, 1)), bsel(ctx, std::max<int64_t>(nn, 1)),
+        blist(ctx, std::max<int64_t>(nn, 1)), ctr(ctx, 32);
+    DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
+    DBuf<long long> result(ctx, 4);
+    ctr.zero();
+    // heaviest tiers first (longest-processing-time first over the work counter)
+    int64_t pos = 0;
+    for (int t = NUM_TIERS - 1; t >= 0; --t) {
+        const int64_t cnt = g->tier_start[t + 1] - g->tier_start[t];
+        if (cnt)
+            CD_CUDA(cudaMemcpyAsync(order.p + pos, g->tlist.p + g->tier_start[t], cnt * sizeof(int32_t),
+                                    cudaMemcpyDeviceToDevice, ctx->stream));
+        pos += cnt;
+    }
+    SweepParams P{};
+    P.off = g->off.p;
+    P.col = g->col.p;
+    P.w = g->weighted ? g->w.p : nullptr;
+    P.vol = g->vol.p;
+    P.z = c.z;
+    P.active = nullptr;
+    P.vols = c.vols;
+    P.csize = c.csize;
+    P.gamma = c.gamma;
+    P.inv_total = g->total > 0 ? 1.0 / g->total : 0.0;
+    P.inv_sq2 = g->total > 0 ? 1.0 / (2.0 * g->total * g->total) : 0.0;
+    P.guard = c.guard;
+    P.buckets = c.buckets;
+    P.own_lo = 0;
+    P.own_hi = static_cast<int32_t>(g->n);
+    P.mv = mv.p;
+    P.stats = ctx->dstats + 3;
+    SmallPhase S{};
+    S.order = order.p;
+    S.nn = static_cast<int32_t>(nn);
+    S.bsel = bsel.p;
+    S.blist = blist.p;
+    S.ctr = ctr.p;
+    S.seed = seed;
+    S.salt = salt;
+    S.K = c.buckets;
+    S.max_passes = static_cast<int>(max_passes);
+    S.theta = theta;
+    S.stall = stall;
+    S.cap_max = std::max<uint32_t>(64, static_cast<uint32_t>(next_pow2(static_cast<uint64_t>(2 * std::max<int64_t>(g->max_degree, 1)))));
+    S.result = result.p;
+    S.trace = std::getenv("CD_TRACE") != nullptr;
+    const int vc = !g->weighted ? VC_COUNT : (g->int_weights ? VC_INT : VC_REAL);
+    const size_t vbytes = vc == VC_REAL ? sizeof(double) : sizeof(unsigned int);
+    const size_t smem = size_t(S.cap_max) * (vbytes + sizeof(int32_t)) + size_t(S.cap_max / 2) * sizeof(uint16_t);
+    if (vc == VC_COUNT)
+        launch_small<VC_COUNT>(ctx, P, S, smem);
+    else if (vc == VC_INT)
+        launch_small<VC_INT>(ctx, P, S, smem);
+    else
+        launch_small<VC_REAL>(ctx, P, S, smem);
+    long long h[3];
+    CD_CUDA(cudaMemcpyAsync(h, result.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (passes)
+        *passes += h[0];
+    if (moves)
+        *moves += h[1];
+    return h[2] != 0;
 }
 
 int64_t Sweeper::take_moves() {

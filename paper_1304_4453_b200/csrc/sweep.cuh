@@ -73,4 +73,10 @@ class Sweeper {
     int64_t kernels_per_pass_ = 0;
 };
 
+// Whole PLM move phase of a small graph in one cooperative kernel (same
+// decisions, order and stop rules as the Sweeper path); returns `changed`.
+bool small_move_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c);
+bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
+                      int64_t theta, double stall, int64_t *passes, int64_t *moves);
+
 }  // namespace cdk
