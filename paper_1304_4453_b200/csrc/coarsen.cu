@@ -61,6 +61,112 @@ __global__ void k_check_used(int64_t nc, const int32_t *csz, int *flag) {
             *flag = 1;
 }
 
+// ---------------------------------------------------------------------------
+// Dense contraction (nc <= COARSEN_DENSE_MAX): a coarse row's tally is a dense
+// fp64 array of nc slots in shared memory, indexed by the coarse id -- no
+// hashing and no sort: the nonzero slots, read in index order, ARE the sorted
+// coarse row.  Members of the row are walked warp by warp.
+// ---------------------------------------------------------------------------
+constexpr int64_t COARSEN_DENSE_MAX = 8192;  // 64 KB of fp64 slots
+constexpr int DENSE_THREADS = 512;
+
+__global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
+                                                              const int64_t *off, const int32_t *col, const float *w,
+                                                              const int32_t *z, const int64_t *fpre, int32_t *tkey,
+                                                              double *tval, int64_t *deg2) {
+    extern __shared__ double acc[];
+    __shared__ int wsum[DENSE_THREADS / 32 + 1];
+    __shared__ double scr[DENSE_THREADS / 32][32];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    constexpr int NW = DENSE_THREADS / 32;
+    const int per = static_cast<int>((nc + DENSE_THREADS - 1) / DENSE_THREADS);  // slots per thread
+    for (int64_t c = blockIdx.x; c < nc; c += gridDim.x) {
+        for (int64_t k = threadIdx.x; k < nc; k += DENSE_THREADS)
+            acc[k] = 0.0;
+        __syncthreads();
+        // tally: entry (u -> v) of a member u adds w to slot z[v]; intra-community
+        // entries once (v >= u), H/louvain.hpp:180-186.  The row's own slot
+        // (most entries: the community's internal weight) is summed in
+        // registers; other labels combine per warp (match_any) before the
+        // shared-memory atomic.
+        double self = 0.0;
+        for (int64_t p = moff[c] + wid; p < moff[c + 1]; p += NW) {
+            const int32_t u = mem[p];
+            const int64_t e0 = off[u], e1 = off[u + 1];
+            for (int64_t base = e0; base < e1; base += 32) {
+                const int64_t e = base + lane;
+                bool valid = e < e1;
+                const int32_t v = valid ? col[e] : 0;
+                const int32_t k = valid ? z[v] : -1;
+                const double wt = valid ? (w ? static_cast<double>(w[e]) : 1.0) : 0.0;
+                if (k == static_cast<int32_t>(c)) {
+                    if (v >= u)
+                        self += wt;
+                    valid = false;
+                }
+                double sum;
+                if (warp_aggregate_sum(k, wt, valid, scr[wid], sum))
+                    atomicAdd(&acc[k], sum);
+            }
+        }
+        self = warp_sum(self);
+        if (lane == 0 && self != 0.0)
+            atomicAdd(&acc[c], self);
+        __syncthreads();
+        // emit the nonzero slots in index order at the row's scratch offset
+        const int64_t k0 = static_cast<int64_t>(threadIdx.x) * per;
+        int mine = 0;
+        for (int i = 0; i < per; ++i)
+            mine += (k0 + i < nc && acc[k0 + i] != 0.0) ? 1 : 0;
+        int incl = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o)
+                incl += t;
+        }
+        if (lane == 31)
+            wsum[wid] = incl;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int s = 0;
+            for (int i = 0; i < NW; ++i) {
+                const int t = wsum[i];
+                wsum[i] = s;
+                s += t;
+            }
+            wsum[NW] = s;
+        }
+        __syncthreads();
+        int64_t pos = fpre[c] + wsum[wid] + incl - mine;
+        for (int i = 0; i < per; ++i) {
+            const int64_t k = k0 + i;
+            if (k < nc && acc[k] != 0.0) {
+                tkey[pos] = static_cast<int32_t>(k);
+                tval[pos] = acc[k];
+                ++pos;
+            }
+        }
+        if (threadIdx.x == 0)
+            deg2[c] = wsum[NW];
+        __syncthreads();
+    }
+}
+
+__global__ void k_dense_copy(int64_t nc, const int64_t *fpre, const int64_t *off2, const int32_t *tkey,
+                             const double *tval, int32_t *col, float *w) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t c = gw; c < nc; c += nw) {
+        const int64_t s = fpre[c], d = off2[c], len = off2[c + 1] - off2[c];
+        for (int64_t i = lane; i < len; i += 32) {
+            col[d + i] = tkey[s + i];
+            w[d + i] = static_cast<float>(tval[s + i]);
+        }
+    }
+}
+
 cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc) {
     const int64_t n = g->n;
     const int grid = grid_for(n, 256, ctx->num_sms * 8);
@@ -86,6 +192,39 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
     cg->ctx = ctx;
     cg->n = nc;
     cg->weighted = true;
+    if (nc > 0 && nc <= COARSEN_DENSE_MAX) {
+        try {
+            DBuf<int32_t> tkey(ctx, std::max<int64_t>(g->D, 1));
+            DBuf<double> tval(ctx, std::max<int64_t>(g->D, 1));
+            DBuf<int64_t> deg2(ctx, nc);
+            const size_t smem = size_t(nc) * sizeof(double);
+            CD_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(std::max<size_t>(smem, 1))));
+            int per_sm = 0;
+            CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_rows, DENSE_THREADS, smem));
+            CD_LAUNCH(ctx, "coarsen.dense", k_dense_rows,
+                      grid_for(nc, 1, std::max(1, per_sm) * ctx->num_sms), DENSE_THREADS, smem, nc,
+                      static_cast<const int64_t *>(moff.p), static_cast<const int32_t *>(mem.p),
+                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                      static_cast<const float *>(g->weighted ? g->w.p : nullptr), z,
+                      static_cast<const int64_t *>(fpre.p), tkey.p, tval.p, deg2.p);
+            cg->off.alloc(ctx, nc + 1);
+            exclusive_scan<int64_t>(ctx, nc, ArrayGen<int64_t>{deg2.p}, cg->off.p, cg->off.p + nc);
+            CD_CUDA(cudaMemcpyAsync(&cg->D, cg->off.p + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+            CD_CUDA(cudaStreamSynchronize(ctx->stream));
+            cg->col.alloc(ctx, std::max<int64_t>(cg->D, 1));
+            cg->w.alloc(ctx, std::max<int64_t>(cg->D, 1));
+            CD_LAUNCH(ctx, "coarsen.dense", k_dense_copy, grid_for(nc, 8, ctx->num_sms * 8), 256, 0, nc,
+                      static_cast<const int64_t *>(fpre.p), static_cast<const int64_t *>(cg->off.p),
+                      static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p), cg->col.p,
+                      cg->w.p);
+            graph_finalize(ctx, cg);
+        } catch (...) {
+            delete cg;
+            throw;
+        }
+        return cg;
+    }
     try {
         SrcCoarsen src{moff.p, mem.p, mpre.p, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, z};
         bool want_w = true;
