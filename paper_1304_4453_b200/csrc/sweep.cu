@@ -639,11 +639,12 @@ __device__ __forceinline__ int block_select(const SweepParams &P, unsigned long 
 }
 
 // Shared state of the block evaluator (one node per block at a time).
+template <int NW = SW_BLOCK_THREADS / 32>
 struct BlockShared {
-    double scratch[8][32];
-    double red_v[8];
-    int32_t red_k[8];
-    double red_wc[8];
+    double scratch[NW][32];
+    double red_v[NW];
+    int32_t red_k[NW];
+    double red_wc[NW];
     int ndist;
 };
 
@@ -651,9 +652,9 @@ struct BlockShared {
 // its neighbours' labels (table of table_cap(deg) slots, claimed slots listed
 // in dlist), Δ / affinity of every distinct label, block argmax, decision.
 // Called by all threads of the block; ends with a block barrier.
-template <int MODE, int VC>
+template <int MODE, int VC, int NT = SW_BLOCK_THREADS>
 __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u, TallyT<VC> *vals, int32_t *keys,
-                                                uint16_t *dlist, BlockShared &sh, MoveQueue &q,
+                                                uint16_t *dlist, BlockShared<NT / 32> &sh, MoveQueue &q,
                                                 unsigned long long &st_n, unsigned long long &st_e) {
     using V = TallyT<VC>;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
@@ -662,7 +663,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
     const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
     const uint32_t cap = table_cap(e - s);
-    for (uint32_t t = threadIdx.x; t < cap; t += SW_BLOCK_THREADS) {
+    for (uint32_t t = threadIdx.x; t < cap; t += NT) {
         keys[t] = EMPTY_KEY;
         vals[t] = V(0);
     }
@@ -670,7 +671,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
         sh.ndist = 0;
     __syncthreads();
     double wc = 0.0;
-    for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += SW_BLOCK_THREADS * SW_ILP) {
+    for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += NT * SW_ILP) {
         int32_t vv[SW_ILP], kk[SW_ILP];
         float ww[SW_ILP];
 #pragma unroll
@@ -714,7 +715,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     if (MODE == MODE_PLM) {
         wc = 0.0;
 #pragma unroll
-        for (int w = 0; w < 8; ++w)
+        for (int w = 0; w < NT / 32; ++w)
             wc += sh.red_wc[w];
     }
     const int nd = sh.ndist;
@@ -722,12 +723,12 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     int32_t ck = INT32_MAX;
     const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
     // candidates = the distinct labels only (not the whole table)
-    for (int j0 = threadIdx.x; j0 < nd; j0 += SW_BLOCK_THREADS * SW_ILP) {
+    for (int j0 = threadIdx.x; j0 < nd; j0 += NT * SW_ILP) {
         int32_t key[SW_ILP];
         double aff[SW_ILP], vd[SW_ILP];
 #pragma unroll
         for (int c = 0; c < SW_ILP; ++c) {
-            const int jj = j0 + c * SW_BLOCK_THREADS;
+            const int jj = j0 + c * NT;
             const uint32_t t = jj < nd ? dlist[jj] : 0;
             key[c] = jj < nd ? keys[t] : EMPTY_KEY;
             aff[c] = jj < nd ? static_cast<double>(vals[t]) : 0.0;
@@ -755,8 +756,8 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     }
     __syncthreads();
     if (wid == 0) {
-        cv = lane < 8 ? sh.red_v[lane] : -INFINITY;
-        ck = lane < 8 ? sh.red_k[lane] : INT32_MAX;
+        cv = lane < NT / 32 ? sh.red_v[lane] : -INFINITY;
+        ck = lane < NT / 32 ? sh.red_k[lane] : INT32_MAX;
         argmax_xor<32>(cv, ck);
         decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
         if (lane == 0) {
@@ -775,7 +776,7 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
     uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CAP);  // claimed slots (distinct <= deg <= CAP/2)
     static_assert(CAP <= 65536, "slot ids are 16-bit");
-    __shared__ BlockShared sh;
+    __shared__ BlockShared<> sh;
     __shared__ int32_t sel[SW_BLOCK_THREADS];
     __shared__ int wcount[SW_BLOCK_THREADS / 32];
     const int wid = threadIdx.x >> 5;
@@ -822,8 +823,10 @@ struct SmallPhase {
     int trace;
 };
 
+constexpr int SMALL_THREADS = 256;  // one node per block (512 measured slower: C2 level 1 2.06 -> 2.50 ms)
+
 template <int VC>
-__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_small_move(SweepParams P, SmallPhase S) {
+__global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, SmallPhase S) {
     namespace cg = cooperative_groups;
     using V = TallyT<VC>;
     cg::grid_group grid = cg::this_grid();
@@ -831,7 +834,7 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_small_move(SweepParams P, 
     V *vals = reinterpret_cast<V *>(smem_raw);
     int32_t *keys = reinterpret_cast<int32_t *>(vals + S.cap_max);
     uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + S.cap_max);
-    __shared__ BlockShared sh;
+    __shared__ BlockShared<SMALL_THREADS / 32> sh;
     __shared__ int s_idx;
     const int wid = threadIdx.x >> 5;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -872,7 +875,8 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_small_move(SweepParams P, 
                 __syncthreads();
                 if (idx >= cnt)
                     break;
-                block_eval_node<MODE_PLM, VC>(P, S.blist[base + idx], vals, keys, dlist, sh, q, st_n, st_e);
+                block_eval_node<MODE_PLM, VC, SMALL_THREADS>(P, S.blist[base + idx], vals, keys, dlist, sh, q, st_n,
+                                                             st_e);
             }
             if (wid == 0)
                 q.flush(P);
@@ -1749,7 +1753,7 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
     auto kfn = k_small_move<VC>;
     CD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int per_sm = 0;
-    CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, SW_BLOCK_THREADS, smem));
+    CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, SMALL_THREADS, smem));
     if (per_sm < 1)
         fail(CD_EINTERNAL, "small move phase: kernel does not fit an SM");
     const int grid = std::max(1, std::min<int>(per_sm * ctx->num_sms, static_cast<int>((S.nn + 1) / 2)));
@@ -1757,7 +1761,7 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
     SmallPhase s = S;
     void *args[] = {&p, &s};
     LaunchScope ls(ctx, "plm_move.small");
-    CD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kfn), dim3(grid), dim3(SW_BLOCK_THREADS), args,
+    CD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kfn), dim3(grid), dim3(SMALL_THREADS), args,
                                         smem, ctx->stream));
 }
 
