@@ -224,11 +224,13 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
     int64_t hist[2] = {-1, -1};  // moves of the two previous passes
     for (int64_t pass = 0; pass < cfg.max_move_iterations; ++pass) {
+        const auto t0 = std::chrono::steady_clock::now();
         sw.pass(bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass)));
         const int64_t moved = sw.take_moves();
         if (trace)
-            std::fprintf(stderr, "[cd] move n=%lld D=%lld pass=%lld moved=%lld\n", static_cast<long long>(n),
-                         static_cast<long long>(g->D), static_cast<long long>(pass), static_cast<long long>(moved));
+            std::fprintf(stderr, "[cd] move n=%lld D=%lld pass=%lld moved=%lld %.3f ms\n", static_cast<long long>(n),
+                         static_cast<long long>(g->D), static_cast<long long>(pass), static_cast<long long>(moved),
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         if (passes)
             ++*passes;
         if (moves)

@@ -447,10 +447,13 @@ __device__ unsigned long long g_phase[16];
 #endif
 
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
+#ifndef SW_WARP_MINB
+#define SW_WARP_MINB 1
+#endif
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
 template <int MODE, int VC>
-__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
+__global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P, int chunk) {
     using V = TallyT<VC>;
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][SW_WARP_CAP];
@@ -1715,6 +1718,9 @@ void Sweeper::pass(uint64_t key) {
         return;
     }
     if (!exec_) {
+        // the first pass runs eagerly; the host records and instantiates the
+        // graph for the remaining passes while the device executes it
+        enqueue(false);
         ensure_side_streams(ctx_);
         const int64_t l0 = ctx_->launches;
         CD_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
@@ -1731,6 +1737,7 @@ void Sweeper::pass(uint64_t key) {
         CD_CUDA(cudaGraphInstantiate(&exec_, graph_, 0));
         kernels_per_pass_ = ctx_->launches - l0;
         ctx_->launches = l0;
+        return;
     }
     CD_CUDA(cudaGraphLaunch(exec_, ctx_->stream));
     ctx_->launches += kernels_per_pass_;
