@@ -1568,19 +1568,30 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             CD_CUDA(cudaMemsetAsync(g->hp_cnt.p, 0, g->n_hub_parts * sizeof(int32_t), st));
             CD_CUDA(cudaMemsetAsync(g->hp_cur.p, 0, g->n_hub_parts * sizeof(int32_t), st));
             const int64_t tiles = (g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1;
+            // per-step profiler families: <mode>.hub_count / _scatter / _part / _decide
+            static const std::string sub[2][5] = {
+                {"plp_sweep.hub_count", "plp_sweep.hub_scan", "plp_sweep.hub_scatter", "plp_sweep.hub_part",
+                 "plp_sweep.hub_decide"},
+                {"plm_move.hub_count", "plm_move.hub_scan", "plm_move.hub_scatter", "plm_move.hub_part",
+                 "plm_move.hub_decide"}};
+            const std::string *nm = sub[MODE];
             auto run = [&](auto launch_one) {
-                launch_one((k_hub_pairs<MODE, VC, false>), nchunks, smem_count);
+                launch_one((k_hub_pairs<MODE, VC, false>), nchunks, smem_count, nm[0].c_str());
                 exclusive_scan_on<int64_t>(ctx, st, g->n_hub_parts, CountGen{g->hp_cnt.p}, g->hp_start.p,
                                            g->hp_start.p + g->n_hub_parts, g->hp_scan.p, g->hp_scan.p + tiles,
-                                           fam);
-                launch_one((k_hub_pairs<MODE, VC, true>), nchunks, smem_scatter);
-                launch_one((k_hub_part<MODE, VC>), npart, smem_part);
-                launch_one((k_hub_decide<MODE>), ndec, size_t(0));
+                                           nm[1].c_str());
+                launch_one((k_hub_pairs<MODE, VC, true>), nchunks, smem_scatter, nm[2].c_str());
+                launch_one((k_hub_part<MODE, VC>), npart, smem_part, nm[3].c_str());
+                launch_one((k_hub_decide<MODE>), ndec, size_t(0), nm[4].c_str());
             };
             if (s)
-                run([&](auto kernel, int grid, size_t smem) { CD_LAUNCH_S(ctx, s, fam, kernel, grid, 256, smem, P); });
+                run([&](auto kernel, int grid, size_t smem, const char *f) {
+                    CD_LAUNCH_S(ctx, s, f, kernel, grid, 256, smem, P);
+                });
             else
-                run([&](auto kernel, int grid, size_t smem) { CD_LAUNCH(ctx, fam, kernel, grid, 256, smem, P); });
+                run([&](auto kernel, int grid, size_t smem, const char *f) {
+                    CD_LAUNCH(ctx, f, kernel, grid, 256, smem, P);
+                });
         });
     }
 #undef CD_TIER_LAUNCH
