@@ -12,7 +12,7 @@ OBJS = $(patsubst $(SRC_DIR)/%.cu,$(OBJ_DIR)/%.o,$(SRCS))
 HDRS = $(wildcard $(SRC_DIR)/*.cuh) include/commdet_cuda.h
 LIB = paper_1304_4453_b200/libcommdet_cuda.so
 
-all: lib shim oracle
+all: lib shim cli oracle
 
 lib: $(LIB)
 
@@ -22,6 +22,14 @@ shim: $(SHIM)
 $(SHIM): tests/cpp/shim_kat.cpp include/commdet/gpu.hpp include/commdet_cuda.h $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Iinclude tests/cpp/shim_kat.cpp -o $@ -Lpaper_1304_4453_b200 -lcommdet_cuda \
+	    -Wl,-rpath,'$$ORIGIN/../paper_1304_4453_b200'
+
+# the reference CLI's drop-in (tools/commdet_gpu.cpp over the shim)
+CLI = build/commdet_gpu
+cli: $(CLI)
+$(CLI): tools/commdet_gpu.cpp include/commdet/gpu.hpp include/commdet_cuda.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude tools/commdet_gpu.cpp -o $@ -Lpaper_1304_4453_b200 -lcommdet_cuda \
 	    -Wl,-rpath,'$$ORIGIN/../paper_1304_4453_b200'
 
 $(OBJ_DIR)/%.o: $(SRC_DIR)/%.cu $(HDRS)

@@ -22,7 +22,12 @@
 #pragma once
 
 #include <algorithm>
+#include <charconv>
+#include <cmath>
 #include <cstdint>
+#include <cctype>
+#include <cstdio>
+#include <fstream>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -379,6 +384,130 @@ struct IterationRecord {
     double ms = 0.0;
 };
 
+/// Minimal JSON value (objects keep sorted keys, like nlohmann::json's
+/// default std::map), enough for RunReport::to_json and the CLI reports.
+class Json {
+  public:
+    enum class Kind { null, number, integer, string, array, object };
+    Json() = default;
+    Json(double v) : kind_(Kind::number), num_(v) {}  // NOLINT
+    Json(long long v) : kind_(Kind::integer), int_(v) {}  // NOLINT
+    Json(int v) : kind_(Kind::integer), int_(v) {}  // NOLINT
+    Json(unsigned long long v) : kind_(Kind::integer), int_(static_cast<long long>(v)) {}  // NOLINT
+    Json(unsigned long v) : kind_(Kind::integer), int_(static_cast<long long>(v)) {}  // NOLINT
+    Json(const std::string &v) : kind_(Kind::string), str_(v) {}  // NOLINT
+    Json(const char *v) : kind_(Kind::string), str_(v) {}  // NOLINT
+    static Json array() {
+        Json j;
+        j.kind_ = Kind::array;
+        return j;
+    }
+    static Json object() {
+        Json j;
+        j.kind_ = Kind::object;
+        return j;
+    }
+    Json &operator[](const std::string &k) {
+        if (kind_ == Kind::null)
+            kind_ = Kind::object;
+        return obj_[k];
+    }
+    void push_back(Json v) {
+        if (kind_ == Kind::null)
+            kind_ = Kind::array;
+        arr_.push_back(std::move(v));
+    }
+    std::string dump(int indent = -1) const {
+        std::string out;
+        write(out, indent, 0);
+        return out;
+    }
+
+  private:
+    static void esc(std::string &o, const std::string &s) {
+        o += '"';
+        for (char c : s) {
+            if (c == '"' || c == '\\') {
+                o += '\\';
+                o += c;
+            } else if (static_cast<unsigned char>(c) < 0x20) {
+                char b[8];
+                std::snprintf(b, sizeof(b), "\\u%04x", c);
+                o += b;
+            } else {
+                o += c;
+            }
+        }
+        o += '"';
+    }
+    void write(std::string &o, int indent, int depth) const {
+        const std::string nl = indent >= 0 ? "\n" : "";
+        const std::string pad = indent >= 0 ? std::string(size_t(indent) * (depth + 1), ' ') : "";
+        const std::string pad0 = indent >= 0 ? std::string(size_t(indent) * depth, ' ') : "";
+        switch (kind_) {
+        case Kind::null:
+            o += "null";
+            break;
+        case Kind::integer:
+            o += std::to_string(int_);
+            break;
+        case Kind::number: {
+            if (!std::isfinite(num_)) {
+                o += "null";
+                break;
+            }
+            char b[64];
+            auto r = std::to_chars(b, b + sizeof(b), num_);  // shortest round trip
+            std::string t(b, r.ptr);
+            if (t.find_first_of(".eE") == std::string::npos)
+                t += ".0";
+            o += t;
+            break;
+        }
+        case Kind::string:
+            esc(o, str_);
+            break;
+        case Kind::array: {
+            if (arr_.empty()) {
+                o += "[]";
+                break;
+            }
+            o += "[" + nl;
+            for (size_t i = 0; i < arr_.size(); ++i) {
+                o += pad;
+                arr_[i].write(o, indent, depth + 1);
+                o += (i + 1 < arr_.size() ? "," : "") + nl;
+            }
+            o += pad0 + "]";
+            break;
+        }
+        case Kind::object: {
+            if (obj_.empty()) {
+                o += "{}";
+                break;
+            }
+            o += "{" + nl;
+            size_t i = 0;
+            for (const auto &kv : obj_) {
+                o += pad;
+                esc(o, kv.first);
+                o += indent >= 0 ? ": " : ":";
+                kv.second.write(o, indent, depth + 1);
+                o += (++i < obj_.size() ? "," : "") + nl;
+            }
+            o += pad0 + "}";
+            break;
+        }
+        }
+    }
+    Kind kind_ = Kind::null;
+    double num_ = 0.0;
+    long long int_ = 0;
+    std::string str_;
+    std::vector<Json> arr_;
+    std::map<std::string, Json> obj_;
+};
+
 struct RunReport {
     std::string algorithm;
     std::string input;
@@ -394,6 +523,49 @@ struct RunReport {
     double combine_ms = 0.0;
     double coarsen_ms = 0.0;
     double final_ms = 0.0;
+
+    /// RunReport::to_json (H/report.hpp:42-70): same fields and nesting.
+    Json to_json() const {
+        Json j = Json::object();
+        j["algorithm"] = algorithm;
+        j["input"] = input;
+        j["workers"] = workers;
+        j["seed"] = static_cast<unsigned long long>(seed);
+        j["total_ms"] = total_ms;
+        j["modularity"] = modularity;
+        j["coverage"] = coverage;
+        j["communities"] = static_cast<unsigned long long>(community_count);
+        if (!levels.empty()) {
+            Json arr = Json::array();
+            for (const auto &l : levels) {
+                Json e = Json::object();
+                e["move_ms"] = l.move_ms;
+                e["coarsen_ms"] = l.coarsen_ms;
+                e["refine_ms"] = l.refine_ms;
+                arr.push_back(e);
+            }
+            j["levels"] = arr;
+        }
+        if (!iterations.empty()) {
+            Json arr = Json::array();
+            for (const auto &it : iterations) {
+                Json e = Json::object();
+                e["updated"] = static_cast<unsigned long long>(it.updated);
+                e["ms"] = it.ms;
+                arr.push_back(e);
+            }
+            j["iterations"] = arr;
+        }
+        if (algorithm == "epp") {
+            Json ph = Json::object();
+            ph["base_ms"] = base_ms;
+            ph["combine_ms"] = combine_ms;
+            ph["coarsen_ms"] = coarsen_ms;
+            ph["final_ms"] = final_ms;
+            j["phases"] = ph;
+        }
+        return j;
+    }
 };
 
 namespace detail {
@@ -457,6 +629,30 @@ inline double coverage(const Graph &g, const Partition &z) {
     return c;
 }
 
+/// Dense int32 relabelling that preserves label equality (ids may exceed int32).
+inline std::vector<int32_t> dense_labels(const Partition &z) {
+    std::unordered_map<index, int32_t> m;
+    std::vector<int32_t> out(z.size());
+    for (std::size_t u = 0; u < z.size(); ++u) {
+        auto it = m.find(z[u]);
+        if (it == m.end())
+            it = m.emplace(z[u], static_cast<int32_t>(m.size())).first;
+        out[u] = it->second;
+    }
+    return out;
+}
+
+/// graph_rand_index (H/quality.hpp:56-69), on the device.
+inline double graph_rand_index(const Graph &g, const Partition &a, const Partition &b) {
+    detail::check_cover(g, a);
+    detail::check_cover(g, b);
+    const auto la = dense_labels(a), lb = dense_labels(b);
+    double r = 0.0;
+    detail::check(cd_rand_index(Context::instance().get(), g.handle(), la.empty() ? nullptr : la.data(),
+                                lb.empty() ? nullptr : lb.data(), &r));
+    return r;
+}
+
 inline double modularity(const Graph &g, const Partition &z, double gamma = 1.0) {
     detail::check_cover(g, z);
     auto l = z.to_device_labels();
@@ -464,6 +660,40 @@ inline double modularity(const Graph &g, const Partition &z, double gamma = 1.0)
     detail::check(cd_modularity(Context::instance().get(), g.handle(), l.data(),
                                 static_cast<int64_t>(std::max<index>(z.upper_bound(), 1)), gamma, &q, &c));
     return q;
+}
+
+struct QualityReport {
+    double modularity = 0.0;
+    double coverage = 0.0;
+    count community_count = 0;
+    std::map<count, count> size_histogram;  // community size -> number of communities
+
+    /// QualityReport::to_text (H/quality.hpp:78-88).
+    std::string to_text() const {
+        char b[64];
+        std::string os;
+        std::snprintf(b, sizeof(b), "%.15g", modularity);
+        os += std::string("modularity ") + b + "\n";
+        std::snprintf(b, sizeof(b), "%.15g", coverage);
+        os += std::string("coverage ") + b + "\n";
+        os += "communities " + std::to_string(community_count) + "\n";
+        for (auto [size, n] : size_histogram)
+            os += "size_" + std::to_string(size) + " " + std::to_string(n) + "\n";
+        return os;
+    }
+};
+
+/// evaluate (H/quality.hpp:91-102).
+inline QualityReport evaluate(const Graph &g, const Partition &z, double gamma = 1.0) {
+    QualityReport r;
+    r.coverage = coverage(g, z);
+    r.modularity = g.total_edge_weight() > 0 ? modularity(g, z, gamma) : 0.0;
+    const Partition zc = z.compacted();
+    const auto sizes = zc.community_sizes();
+    r.community_count = sizes.size();
+    for (count sz : sizes)
+        ++r.size_histogram[sz];
+    return r;
 }
 
 // ---- PLP (H/plp.hpp) ------------------------------------------------------------------
@@ -681,6 +911,115 @@ inline Graph read_edge_list(const std::string &path, bool merge_duplicates = fal
         detail::check(cd_graph_original_ids(h, original_ids->empty() ? nullptr : original_ids->data()));
     }
     return g;
+}
+
+namespace detail {
+inline std::string format_weight(double w) {  // io::detail::format_weight (H/io.hpp:70-77)
+    char buf[32];
+    if (w == std::floor(w) && std::abs(w) < 1e15)
+        std::snprintf(buf, sizeof(buf), "%.0f", w);
+    else
+        std::snprintf(buf, sizeof(buf), "%.17g", w);
+    return buf;
+}
+inline std::ofstream open_output(const std::string &path) {
+    std::ofstream out(path);
+    if (!out)
+        throw input_error("cannot open " + path + " for writing");
+    return out;
+}
+}  // namespace detail
+
+/// io::write_metis (H/io.hpp:168-183): fmt 1, 1-based neighbours with weights.
+inline void write_metis(const Graph &g, const std::string &path) {
+    auto out = detail::open_output(path);
+    out << g.node_count() << " " << g.edge_count() << " 1\n";
+    for (node u = 0; u < g.node_count(); ++u) {
+        bool first = true;
+        g.for_neighbors(u, [&](node v, edgeweight w) {
+            if (!first)
+                out << " ";
+            out << (v + 1) << " " << detail::format_weight(w);
+            first = false;
+        });
+        out << "\n";
+    }
+    if (!out)
+        throw input_error("write failed: " + path);
+}
+
+/// io::write_edge_list (H/io.hpp:239-245): "u v w", one line per undirected edge.
+inline void write_edge_list(const Graph &g, const std::string &path) {
+    auto out = detail::open_output(path);
+    for (node u = 0; u < g.node_count(); ++u)
+        g.for_neighbors(u, [&](node v, edgeweight w) {
+            if (v >= u)
+                out << u << " " << v << " " << detail::format_weight(w) << "\n";
+        });
+    if (!out)
+        throw input_error("write failed: " + path);
+}
+
+/// io::write_partition (H/io.hpp:248-255).
+inline void write_partition(const Partition &z, const std::string &path) {
+    auto out = detail::open_output(path);
+    for (node u = 0; u < z.size(); ++u)
+        out << z[u] << "\n";
+    if (!out)
+        throw input_error("write failed: " + path);
+}
+
+/// io::read_partition (H/io.hpp:257-275).
+inline Partition read_partition(const std::string &path) {
+    std::ifstream in(path);
+    if (!in)
+        throw input_error("cannot open " + path);
+    Partition z;
+    std::string line;
+    std::size_t lineno = 0;
+    index ub = 0;
+    while (std::getline(in, line)) {
+        ++lineno;
+        std::vector<std::string> toks;
+        std::size_t i = 0;
+        while (i < line.size()) {
+            while (i < line.size() && std::isspace(static_cast<unsigned char>(line[i])))
+                ++i;
+            std::size_t j = i;
+            while (j < line.size() && !std::isspace(static_cast<unsigned char>(line[j])))
+                ++j;
+            if (j > i)
+                toks.push_back(line.substr(i, j - i));
+            i = j;
+        }
+        if (toks.empty())
+            continue;
+        const std::string ctx = path + ":" + std::to_string(lineno);
+        if (toks.size() != 1)
+            throw input_error(ctx + ": expected one community id per line");
+        std::uint64_t c = 0;
+        auto [p, ec] = std::from_chars(toks[0].data(), toks[0].data() + toks[0].size(), c);
+        if (ec != std::errc{} || p != toks[0].data() + toks[0].size())
+            throw input_error("malformed integer '" + toks[0] + "' in " + ctx);
+        z.data().push_back(c);
+        ub = std::max<index>(ub, c + 1);
+    }
+    z.set_upper_bound(ub > 0 ? ub : 1);
+    return z;
+}
+
+/// io::write_community_graph (H/io.hpp:279-289): the contraction (on the
+/// device) in METIS format, plus "<path>.sizes" with "community_id size" lines.
+inline void write_community_graph(const Graph &g, const Partition &z, const std::string &path) {
+    const Partition zc = z.is_compact() ? z : z.compacted();
+    CoarseningResult cr = coarsen(g, zc);
+    write_metis(cr.coarse, path);
+    auto sizes = zc.community_sizes();
+    auto out = detail::open_output(path + ".sizes");
+    for (index c = 0; c < sizes.size(); ++c)
+        out << c << " " << sizes[c] << "\n";
+    if (!out)
+        throw input_error("write failed: " + path + ".sizes");
 }
 
 }  // namespace io

@@ -207,6 +207,9 @@ CD_API cd_status cd_graph_destroy(cd_graph *g);
  * lie in [0, ub) (CD_ERANGE otherwise); w(E) == 0 -> CD_EDOMAIN, coverage 0. */
 CD_API cd_status cd_modularity(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub, double gamma,
                                double *modularity, double *coverage);
+/* graph_rand_index (H/quality.hpp:56-69): fraction of edges on which the two
+ * partitions agree; w(E)-independent; CD_EDOMAIN for an edgeless graph. */
+CD_API cd_status cd_rand_index(cd_ctx *ctx, const cd_graph *g, const int32_t *a, const int32_t *b, double *out);
 /* community_volumes (H/louvain.hpp:27-31) */
 CD_API cd_status cd_community_volumes(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub, double *vols);
 

@@ -193,6 +193,10 @@ def ref():
         R.ref_djb2.argtypes = [C.c_char_p, C.c_uint64]
         R.ref_djb2.restype = C.c_uint64
         R.ref_read_metis.argtypes = [C.c_char_p, vpp]
+        R.ref_write_metis.argtypes = [C.c_void_p, C.c_char_p]
+        R.ref_write_partition.argtypes = [C.c_int64, i32p, C.c_char_p]
+        R.ref_write_community_graph.argtypes = [C.c_void_p, i32p, C.c_char_p]
+        R.ref_graph_rand_index.argtypes = [C.c_void_p, i32p, i32p, C.POINTER(C.c_double)]
         R.ref_read_edge_list.argtypes = [C.c_char_p, C.c_int, vpp, C.c_void_p, C.c_int64]
         R.ref_run_epp.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int, i32p, C.POINTER(_RefReport)]
         R.ref_max_threads.restype = C.c_int
@@ -560,6 +564,17 @@ class RefGraph:
                                          max_ids))
         g = cls(h.value)
         return g, ids[: g.info()[0]].copy()
+
+    def write_metis(self, path):
+        _rcheck(ref().ref_write_metis(self.h, str(path).encode()))
+
+    def write_community_graph(self, z, path):
+        _rcheck(ref().ref_write_community_graph(self.h, _i32(z), str(path).encode()))
+
+    def rand_index(self, a, b):
+        out = C.c_double()
+        _rcheck(ref().ref_graph_rand_index(self.h, _i32(a), _i32(b), C.byref(out)))
+        return out.value
 
     def __del__(self):
         if self.h and _REF is not None:

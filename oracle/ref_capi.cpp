@@ -310,6 +310,31 @@ int ref_run_epp(const void *gp, int64_t ensemble_size, uint64_t seed, int worker
 
 int ref_max_threads(void) { return omp_get_max_threads(); }
 
+// io::write_metis / write_partition / write_community_graph (H/io.hpp:168, :248, :279)
+int ref_write_metis(const void *gp, const char *path) {
+    return guarded([&] { cd::io::write_metis(*static_cast<const cd::Graph *>(gp), path); });
+}
+
+int ref_write_partition(int64_t n, const int32_t *z, const char *path) {
+    return guarded([&] { cd::io::write_partition(to_partition(n, z, 0), path); });
+}
+
+int ref_write_community_graph(const void *gp, const int32_t *z, const char *path) {
+    return guarded([&] {
+        const auto &g = *static_cast<const cd::Graph *>(gp);
+        cd::io::write_community_graph(g, to_partition(static_cast<int64_t>(g.node_count()), z, 0), path);
+    });
+}
+
+// graph_rand_index (H/quality.hpp:56-69)
+int ref_graph_rand_index(const void *gp, const int32_t *a, const int32_t *b, double *out) {
+    return guarded([&] {
+        const auto &g = *static_cast<const cd::Graph *>(gp);
+        const int64_t n = static_cast<int64_t>(g.node_count());
+        *out = cd::graph_rand_index(g, to_partition(n, a, 0), to_partition(n, b, 0));
+    });
+}
+
 // io::read_metis (H/io.hpp:83-165)
 int ref_read_metis(const char *path, void **out) {
     return guarded([&] { *out = new cd::Graph(cd::io::read_metis(path)); });

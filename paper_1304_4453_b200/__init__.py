@@ -39,7 +39,7 @@ __all__ = [
     "run_louvain", "modularity", "coverage", "community_volumes", "coarsen", "prolong", "compacted",
     "community_count", "combine_hashed", "plp_sweep_sync", "move_eval", "move_phase", "dominant_label",
     "is_stable", "library_path", "load_library", "default_context", "ALGO_PLP", "ALGO_PLM", "ALGO_PLMR",
-    "LoopbackGroup", "nccl_unique_id", "shard_bounds", "read_metis", "read_edge_list",
+    "LoopbackGroup", "nccl_unique_id", "shard_bounds", "read_metis", "read_edge_list", "graph_rand_index",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -142,7 +142,7 @@ EXPORTS = [
     "cd_nccl_unique_id", "cd_ctx_attach_nccl", "cd_loopback_create", "cd_loopback_destroy",
     "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard",
     "cd_graph_read_metis", "cd_graph_read_edge_list", "cd_graph_load_metis", "cd_graph_load_edge_list",
-    "cd_graph_original_ids",
+    "cd_graph_original_ids", "cd_rand_index",
 ]
 
 
@@ -192,7 +192,7 @@ def load_library():
         "cd_shard_bounds": [i64, vp, i32, vp], "cd_graph_shard": [vp, vp, vpp],
         "cd_graph_read_metis": [vp, vp, i64, vpp], "cd_graph_read_edge_list": [vp, vp, i64, i32, vpp],
         "cd_graph_load_metis": [vp, C.c_char_p, vpp], "cd_graph_load_edge_list": [vp, C.c_char_p, i32, vpp],
-        "cd_graph_original_ids": [vp, vp],
+        "cd_graph_original_ids": [vp, vp], "cd_rand_index": [vp, vp, vp, vp, C.POINTER(f64)],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -778,6 +778,18 @@ def modularity(g: Graph, z, gamma=1.0, ub=None) -> float:
     q, cov = C.c_double(), C.c_double()
     _check(load_library().cd_modularity(g.ctx.h, g.h, pz, _ub(z, ub), gamma, C.byref(q), C.byref(cov)))
     return q.value
+
+
+def graph_rand_index(g: Graph, a, b) -> float:
+    """graph_rand_index (H/quality.hpp:56-69): fraction of edges on which the
+    partitions agree; DomainError for an edgeless graph."""
+    _check_cover(g, a)
+    _check_cover(g, b)
+    pa, ka = _ptr(a, np.int32)
+    pb, kb = _ptr(b, np.int32)
+    out = C.c_double()
+    _check(load_library().cd_rand_index(g.ctx.h, g.h, pa, pb, C.byref(out)))
+    return out.value
 
 
 def coverage(g: Graph, z) -> float:

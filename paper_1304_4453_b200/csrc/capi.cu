@@ -467,6 +467,14 @@ cd_status cd_modularity(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_
     })
 }
 
+cd_status cd_rand_index(cd_ctx *ctx, const cd_graph *g, const int32_t *a, const int32_t *b, double *out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && g && out && (g->n == 0 || (a && b)), CD_EINVAL, "invalid argument");
+        InArr<int32_t> da(ctx, a, g->n), db(ctx, b, g->n);
+        *out = rand_index_dev(ctx, g, da.d, db.d);
+    })
+}
+
 cd_status cd_community_volumes(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub, double *vols) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && g && z && vols && ub >= 1, CD_EINVAL, "invalid argument");

@@ -149,6 +149,7 @@ void community_volumes_sizes_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *
                                  int64_t ub);
 void modularity_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub, double gamma, double *q,
                     double *cov);
+double rand_index_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *a, const int32_t *b);
 
 // partition.cu
 int64_t max_label_dev(cd_ctx *ctx, int64_t n, const int32_t *z);  // max+1 (>= 1); -1 if a label < 0

@@ -182,4 +182,41 @@ void modularity_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t ub
         *q = h[0] / total - gamma * h[1] / (4.0 * total * total);
 }
 
+// graph_rand_index (H/quality.hpp:56-69): edges {u <= v} on which the two
+// partitions agree (both join or both separate the endpoints; loops agree)
+__global__ void k_rand_agree(int64_t n, const int64_t *off, const int32_t *col, const int32_t *a, const int32_t *b,
+                             unsigned long long *agree) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long c = 0;
+    for (int64_t u = gw; u < n; u += nw) {
+        const int32_t au = a[u], bu = b[u];
+        for (int64_t e = off[u] + lane; e < off[u + 1]; e += 32) {
+            const int32_t v = col[e];
+            if (v >= u)
+                c += ((au == a[v]) == (bu == b[v])) ? 1 : 0;
+        }
+    }
+    c = warp_sum(c);
+    if (lane == 0 && c)
+        atomicAdd(agree, c);
+}
+
+double rand_index_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *a, const int32_t *b) {
+    if (g->m == 0)
+        fail(CD_EDOMAIN, "graph-structural Rand index undefined for edgeless graph");
+    DBuf<unsigned long long> agree(ctx, 1);
+    agree.zero();
+    if (g->n)
+        CD_LAUNCH(ctx, "quality", k_rand_agree, grid_for(g->n, 8, ctx->num_sms * 16), 256, 0, g->n,
+                  static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), a, b, agree.p);
+    if (g->rows_local && world_size(ctx) > 1)
+        ctx->comm->allreduce_sum_i64(ctx, reinterpret_cast<int64_t *>(agree.p), 1);
+    unsigned long long h = 0;
+    CD_CUDA(cudaMemcpyAsync(&h, agree.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    return static_cast<double>(h) / static_cast<double>(g->m);
+}
+
 }  // namespace cdk
