@@ -83,6 +83,8 @@ typedef struct cd_louvain_config {
                                 itself) moved since its last evaluation; 1 (default) in the
                                 input graph's move phases, 2 on every level, 0 never */
     int32_t reserved;
+    double move_qtol;        /* device: ... or once a pass's summed gain is <= move_qtol x the
+                                phase's summed gain so far (0 disables; default 1e-3) */
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */

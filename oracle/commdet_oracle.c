@@ -7,6 +7,9 @@
  */
 #include "commdet_oracle.h"
 
+/* per-move gains summed in fixed point (units of 2^-44): order-free, like the device */
+#define CDO_GAIN_FX_SCALE 17592186044416.0
+
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1276,7 +1279,9 @@ void cdo_activate(const cdo_graph *g, int64_t nm, const int32_t *mv_u, uint8_t *
  * cfg->prune, only active nodes are evaluated and non-movers deactivated. */
 int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
                           uint8_t *active, const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo,
-                          int64_t hi, int32_t *mv_u, int32_t *mv_l) {
+                          int64_t hi, int32_t *mv_u, int32_t *mv_l, long long *gain_fx) {
+    if (gain_fx)
+        *gain_fx = 0;
     const int32_t K = cfg->buckets > 0 ? cfg->buckets : 1;
     const double inv_total = 1.0 / g->total;
     const double inv_sq2 = 1.0 / (2.0 * g->total * g->total);
@@ -1307,6 +1312,8 @@ int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vo
         }
         mv_u[nm] = (int32_t)u;
         mv_l[nm++] = best;
+        if (gain_fx)
+            *gain_fx += llrint(gain * CDO_GAIN_FX_SCALE);
     }
     scratch_free(&s);
     return nm;
@@ -1346,8 +1353,10 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
     }
     int changed = 0;
     int64_t hist0 = -1, hist1 = -1; /* moves two passes / one pass earlier */
+    long long cum_fx = 0;           /* the phase's summed gain, fixed point 2^-44 */
     for (int64_t pass = 0; pass < cfg->max_move_iterations; ++pass) {
         int64_t moved = 0;
+        long long pass_fx = 0;
         const uint64_t key = cdo_bucket_key(cfg->seed, salt + (uint64_t)pass);
         for (int32_t b = 0; b < K; ++b) {
             int64_t nm = 0;
@@ -1371,6 +1380,7 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
                 }
                 mv_u[nm] = (int32_t)u;
                 mv_l[nm++] = best;
+                pass_fx += llrint(gain * CDO_GAIN_FX_SCALE);
             }
             for (int64_t j = 0; j < nm; ++j) {
                 const int32_t u = mv_u[j], d = mv_l[j], c = z[u];
@@ -1390,6 +1400,9 @@ int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_co
         if (moved <= theta)
             break;
         if (cfg->move_stall > 0.0 && pass >= 8 && (double)moved > cfg->move_stall * (double)hist0)
+            break;
+        cum_fx += pass_fx;
+        if (cfg->move_qtol > 0.0 && (double)pass_fx <= cfg->move_qtol * (double)cum_fx)
             break;
         hist0 = hist1;
         hist1 = moved;

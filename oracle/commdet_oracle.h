@@ -138,6 +138,7 @@ typedef struct {
     double move_stall;  /* ... or (pass >= 8) moves > move_stall * moves two passes earlier */
     int32_t prune;      /* evaluate only nodes whose neighbourhood changed (device prune):
                            1 = level-0 move phases, 2 = every level */
+    double move_qtol;   /* ... or a pass's summed gain <= move_qtol x the phase's (fixed point 2^-44) */
 } cdo_louvain_config;
 
 /* bucket key / id: the order every device driver uses. */
@@ -156,7 +157,7 @@ int64_t cdo_plp_subsweep(const cdo_graph *g, const int32_t *labels, uint8_t *act
                          int32_t buckets, int64_t lo, int64_t hi, int32_t *mv_u, int32_t *mv_l);
 int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vols, const int32_t *csize,
                           uint8_t *active, const cdo_louvain_config *cfg, uint64_t key, int32_t bucket, int64_t lo,
-                          int64_t hi, int32_t *mv_u, int32_t *mv_l);
+                          int64_t hi, int32_t *mv_u, int32_t *mv_l, long long *gain_fx);
 /* Activation after a sub-sweep's moves (PLP and pruned PLM): all nodes when
  * more than n/16 moved, else the neighbours of the moved nodes. */
 void cdo_activate(const cdo_graph *g, int64_t nm, const int32_t *mv_u, uint8_t *active);

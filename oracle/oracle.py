@@ -52,6 +52,7 @@ class _LouvainCfg(C.Structure):
         ("gamma", C.c_double), ("max_move_iterations", C.c_int64), ("max_levels", C.c_int64),
         ("seed", C.c_uint64), ("buckets", C.c_int32), ("refine", C.c_int32), ("singleton_guard", C.c_int32),
         ("move_theta", C.c_int64), ("move_tol", C.c_double), ("move_stall", C.c_double), ("prune", C.c_int32),
+        ("move_qtol", C.c_double),
     ]
 
 
@@ -145,7 +146,7 @@ def lib():
                                        C.c_int64, i32p, i32p]
         L.cdo_plp_subsweep.restype = C.c_int64
         L.cdo_move_subsweep.argtypes = [gp, i32p, f64p, i32p, C.c_void_p, C.POINTER(_LouvainCfg), C.c_uint64,
-                                        C.c_int32, C.c_int64, C.c_int64, i32p, i32p]
+                                        C.c_int32, C.c_int64, C.c_int64, i32p, i32p, C.POINTER(C.c_longlong)]
         L.cdo_activate.argtypes = [gp, C.c_int64, i32p, C.c_void_p]
         L.cdo_activate.restype = None
         L.cdo_move_subsweep.restype = C.c_int64
@@ -451,9 +452,9 @@ def plp_bucketed(g: CSR, theta=-1, max_iterations=100, seed=1, buckets=4, initia
 
 
 def louvain_cfg(gamma=1.0, max_move_iterations=32, max_levels=64, seed=1, buckets=4, refine=False,
-                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True):
+                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True, move_qtol=1e-3):
     return _LouvainCfg(gamma, max_move_iterations, max_levels, seed, buckets, int(refine), int(singleton_guard),
-                       move_theta, move_tol, move_stall, int(prune))
+                       move_theta, move_tol, move_stall, int(prune), move_qtol)
 
 
 def move_phase_bucketed(g: CSR, z, salt=0, **kw):
@@ -506,11 +507,12 @@ def move_subsweep(g: CSR, z, vols, csize, active, key, bucket, lo, hi, **kw):
     mu = np.zeros(max(hi - lo, 1), np.int32)
     ml = np.zeros(max(hi - lo, 1), np.int32)
     assert active.dtype == np.uint8 and active.flags.c_contiguous
+    gfx = C.c_longlong()
     nm = lib().cdo_move_subsweep(_Borrow(g).ref, _i32(z), np.ascontiguousarray(vols, np.float64), _i32(csize),
-                                 active.ctypes.data, C.byref(cfg), key, bucket, lo, hi, mu, ml)
+                                 active.ctypes.data, C.byref(cfg), key, bucket, lo, hi, mu, ml, C.byref(gfx))
     if nm < 0:
         _check(int(nm))
-    return mu[:nm].copy(), ml[:nm].copy()
+    return mu[:nm].copy(), ml[:nm].copy(), gfx.value
 
 
 # --------------------------------------------------------------------------- #

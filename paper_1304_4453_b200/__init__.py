@@ -83,7 +83,8 @@ class _LouvainConfig(C.Structure):
     _fields_ = [("gamma", C.c_double), ("max_move_iterations", C.c_int64), ("max_levels", C.c_int64),
                 ("seed", C.c_uint64), ("workers", C.c_int32), ("refine", C.c_int32), ("buckets", C.c_int32),
                 ("singleton_guard", C.c_int32), ("move_theta", C.c_int64), ("move_tol", C.c_double),
-                ("move_stall", C.c_double), ("prune", C.c_int32), ("reserved", C.c_int32)]
+                ("move_stall", C.c_double), ("prune", C.c_int32), ("reserved", C.c_int32),
+                ("move_qtol", C.c_double)]
 
 
 class _EnsembleConfig(C.Structure):
@@ -625,12 +626,13 @@ class LouvainConfig:
     move_theta: int = -1
     move_tol: float = 1e-3
     move_stall: float = 0.95
-    prune: bool = True
+    prune: int = 1
+    move_qtol: float = 1e-3
 
     def _c(self):
         return _LouvainConfig(self.gamma, self.max_move_iterations, self.max_levels, self.seed, self.workers,
                               int(self.refine), self.buckets, int(self.singleton_guard), self.move_theta,
-                              self.move_tol, self.move_stall, int(self.prune), 0)
+                              self.move_tol, self.move_stall, int(self.prune), 0, self.move_qtol)
 
 
 @dataclass

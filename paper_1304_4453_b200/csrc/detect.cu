@@ -217,19 +217,21 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
         }
     }
     if (small_move_eligible(ctx, g, c))
-        return small_move_phase(ctx, g, c, cfg.seed, salt, cfg.max_move_iterations, theta, cfg.move_stall, passes,
-                                moves);
+        return small_move_phase(ctx, g, c, cfg.seed, salt, cfg.max_move_iterations, theta, cfg.move_stall,
+                                cfg.move_qtol, passes, moves);
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
     int64_t hist[2] = {-1, -1};  // moves of the two previous passes
+    long long cum_fx = 0;        // the phase's summed gain (fixed point 2^-44)
     for (int64_t pass = 0; pass < cfg.max_move_iterations; ++pass) {
         const auto t0 = std::chrono::steady_clock::now();
         sw.pass(bucket_key(cfg.seed, salt + static_cast<uint64_t>(pass)));
         const int64_t moved = sw.take_moves();
         if (trace)
-            std::fprintf(stderr, "[cd] move n=%lld D=%lld pass=%lld moved=%lld %.3f ms\n", static_cast<long long>(n),
-                         static_cast<long long>(g->D), static_cast<long long>(pass), static_cast<long long>(moved),
+            std::fprintf(stderr, "[cd] move n=%lld D=%lld pass=%lld moved=%lld gain=%.4e %.3f ms\n",
+                         static_cast<long long>(n), static_cast<long long>(g->D), static_cast<long long>(pass),
+                         static_cast<long long>(moved), sw.last_gain(),
                          std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
         if (passes)
             ++*passes;
@@ -243,6 +245,11 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
         // stalled: a non-converging tail of oscillating movers
         if (cfg.move_stall > 0.0 && pass >= 8 &&
             static_cast<double>(moved) > cfg.move_stall * static_cast<double>(hist[0]))
+            break;
+        // converged in value: the pass added a negligible share of the phase's gain
+        cum_fx += sw.last_gain_fx();
+        if (cfg.move_qtol > 0.0 &&
+            static_cast<double>(sw.last_gain_fx()) <= cfg.move_qtol * static_cast<double>(cum_fx))
             break;
         hist[0] = hist[1];
         hist[1] = moved;

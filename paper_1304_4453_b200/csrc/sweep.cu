@@ -60,6 +60,7 @@ struct SweepParams {
     int32_t *dense_best;
     double *dense_gain;
     unsigned long long *stats;
+    long long *gain_fx;  // PLM: sum of the movers' Δ in units of 2^-44 (fixed point: order-free)
     // hub tier (hash-partitioned tally, graph.cuh)
     const int32_t *hubs;
     const int32_t *chunk_hub;
@@ -268,9 +269,20 @@ __global__ void __launch_bounds__(1024) k_prebucket(SweepParams P) {
 // Per-warp register queue of moves: lane i holds entry i; one global atomic
 // per 32 moves instead of one per warp-round (the bucket's move counter is a
 // single hot address).
+constexpr double GAIN_FX_SCALE = 17592186044416.0;  // 2^44
+
 struct MoveQueue {
     int32_t u = 0, l = 0;
-    int n = 0;  // warp-uniform fill
+    int n = 0;           // warp-uniform fill
+    long long gain = 0;  // this lane's movers' Δ (fixed point)
+
+    // at kernel end, by all lanes of the warp
+    __device__ __forceinline__ void flush_gain(const SweepParams &P) {
+        const long long g = warp_sum(gain);
+        if (lane_id() == 0 && g && P.gain_fx)
+            atomicAdd(reinterpret_cast<unsigned long long *>(P.gain_fx), static_cast<unsigned long long>(g));
+        gain = 0;
+    }
 
     __device__ __forceinline__ void flush(const SweepParams &P) {
         if (n == 0)
@@ -329,6 +341,8 @@ __device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool 
         return;
     }
     q.push(P, moved, u, best);
+    if (MODE == MODE_PLM && moved)
+        q.gain += llrint(val * GAIN_FX_SCALE);
     // PLP active set (H/plp.hpp:127-133); PLM pruning: a non-mover sleeps
     // until a neighbour moves
     if (act && !moved && P.active)
@@ -417,6 +431,7 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
         }
     }
     q.flush(P);
+    q.flush_gain(P);
     flush_stats(P, st_n, st_e);
 }
 
@@ -590,6 +605,7 @@ __global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P,
         }
     }
     q.flush(P);
+    q.flush_gain(P);
     flush_stats(P, st_n, st_e);
 }
 
@@ -795,8 +811,10 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
         for (int j = 0; j < nsel; ++j)
             block_eval_node<MODE, VC>(P, sel[j], vals, keys, dlist, sh, q, st_n, st_e);
     }
-    if (wid == 0)
+    if (wid == 0) {
         q.flush(P);
+        q.flush_gain(P);
+    }
     flush_stats(P, st_n, st_e);
 }
 
@@ -820,7 +838,8 @@ struct SmallPhase {
     int K;
     int max_passes;
     long long theta;
-    double stall;
+    double stall, qtol;
+    long long *gain;       // [1] this pass's movers' gain (fixed point)
     uint32_t cap_max;
     long long *result;     // passes, moves, changed
     int trace;
@@ -845,7 +864,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
     int32_t *ctr = S.ctr;
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
-    long long hist0 = -1, hist1 = -1, moves_total = 0;
+    long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
     int passes = 0;
     bool changed = false;
     for (int pass = 0; pass < S.max_passes; ++pass) {
@@ -881,8 +900,10 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
                 block_eval_node<MODE_PLM, VC, SMALL_THREADS>(P, S.blist[base + idx], vals, keys, dlist, sh, q, st_n,
                                                              st_e);
             }
-            if (wid == 0)
+            if (wid == 0) {
                 q.flush(P);
+                q.flush_gain(P);
+            }
             grid.sync();
             const int mc = ctr[24 + b];
             for (int64_t i = gtid; i < mc; i += gsize) {  // H/louvain.hpp:121-125
@@ -912,11 +933,20 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
                 stop = true;
             else if (S.stall > 0.0 && pass >= 8 && static_cast<double>(pass_moves) > S.stall * static_cast<double>(hist0))
                 stop = true;
+            if (!stop) {
+                const long long pass_fx = *S.gain;
+                cum_fx += pass_fx;
+                if (S.qtol > 0.0 && static_cast<double>(pass_fx) <= S.qtol * static_cast<double>(cum_fx))
+                    stop = true;
+            }
             hist0 = hist1;
             hist1 = pass_moves;
         }
+        grid.sync();  // every thread has read this pass's counters and gain
         if (blockIdx.x == 0 && threadIdx.x < 32)
             ctr[threadIdx.x] = 0;
+        if (gtid == 0)
+            *S.gain = 0;
         grid.sync();
         if (stop)
             break;
@@ -1190,8 +1220,10 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
         }
         __syncthreads();
     }
-    if (wid == 0)
+    if (wid == 0) {
         mq.flush(P);
+        mq.flush_gain(P);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1355,6 +1387,8 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
     mv_.alloc(ctx, std::max<int64_t>(g->n, 1));
     total_.alloc(ctx, 1);
     total_.zero();
+    gain_.alloc(ctx, 1);
+    gain_.zero();
     key_.alloc(ctx, 1);
     key_.zero();
     if (c_.buckets < 1)
@@ -1639,6 +1673,7 @@ void Sweeper::enqueue(bool capture) {
     P.blist = blist_.p;
     P.boff = boff_.p;
     P.mv = mv_.p;
+    P.gain_fx = c_.mode == MODE_PLM ? gain_.p : nullptr;
     P.dense_best = c_.dense_best;
     P.dense_gain = c_.dense_gain;
     P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : 3);
@@ -1784,14 +1819,15 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
 }
 
 bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
-                      int64_t theta, double stall, int64_t *passes, int64_t *moves) {
+                      int64_t theta, double stall, double qtol, int64_t *passes, int64_t *moves) {
     graph_ensure_bins(ctx, g);
     const int64_t nn = g->tier_start[NUM_TIERS];
     DBuf<int32_t> order(ctx, std::max<int64_t>(nn, 1)), bsel(ctx, std::max<int64_t>(nn, 1)),
         blist(ctx, std::max<int64_t>(nn, 1)), ctr(ctx, 32);
     DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
-    DBuf<long long> result(ctx, 4);
+    DBuf<long long> result(ctx, 4), gain(ctx, 1);
     ctr.zero();
+    gain.zero();
     // heaviest tiers first (longest-processing-time first over the work counter)
     int64_t pos = 0;
     for (int t = NUM_TIERS - 1; t >= 0; --t) {
@@ -1819,6 +1855,7 @@ bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t see
     P.own_hi = static_cast<int32_t>(g->n);
     P.mv = mv.p;
     P.stats = ctx->dstats + 3;
+    P.gain_fx = gain.p;
     SmallPhase S{};
     S.order = order.p;
     S.nn = static_cast<int32_t>(nn);
@@ -1831,6 +1868,8 @@ bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t see
     S.max_passes = static_cast<int>(max_passes);
     S.theta = theta;
     S.stall = stall;
+    S.qtol = qtol;
+    S.gain = gain.p;
     S.cap_max = std::max<uint32_t>(64, static_cast<uint32_t>(next_pow2(static_cast<uint64_t>(2 * std::max<int64_t>(g->max_degree, 1)))));
     S.result = result.p;
     S.trace = std::getenv("CD_TRACE") != nullptr;
@@ -1854,15 +1893,21 @@ bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t see
 }
 
 int64_t Sweeper::take_moves() {
-    long long h = 0;
+    long long h = 0, gfx = 0;
     int32_t overflow = 0;
     CD_CUDA(cudaMemcpyAsync(&h, total_.p, sizeof(h), cudaMemcpyDeviceToHost, ctx_->stream));
     CD_CUDA(cudaMemsetAsync(total_.p, 0, sizeof(long long), ctx_->stream));
+    if (exchange_)  // each rank summed its own movers' gains
+        ctx_->comm->allreduce_sum_i64(ctx_, reinterpret_cast<int64_t *>(gain_.p), 1);
+    CD_CUDA(cudaMemcpyAsync(&gfx, gain_.p, sizeof(gfx), cudaMemcpyDeviceToHost, ctx_->stream));
+    CD_CUDA(cudaMemsetAsync(gain_.p, 0, sizeof(long long), ctx_->stream));
     if (g_->n_hubs)
         CD_CUDA(cudaMemcpyAsync(&overflow, g_->hp_flag.p, sizeof(overflow), cudaMemcpyDeviceToHost, ctx_->stream));
     CD_CUDA(cudaStreamSynchronize(ctx_->stream));
     if (overflow)
         fail(CD_EINTERNAL, "hub partition table overflow (more distinct labels per partition than slots)");
+    last_gain_fx_ = gfx;
+    last_gain_ = static_cast<double>(gfx) / GAIN_FX_SCALE;
     return h;
 }
 

@@ -46,6 +46,8 @@ class Sweeper {
 
     void pass(uint64_t key);   // enqueue one full pass with this bucket key
     int64_t take_moves();      // moves since the last call (syncs)
+    double last_gain() const { return last_gain_; }        // their summed Δ
+    long long last_gain_fx() const { return last_gain_fx_; }  // the same in units of 2^-44 (exact)
 
   private:
     void enqueue(bool capture);
@@ -67,6 +69,9 @@ class Sweeper {
     DBuf<int32_t> rcnt_;    // [G] gathered counts
     DBuf<int2> rmv_;        // [G][stride] gathered moves
     DBuf<long long> total_;
+    DBuf<long long> gain_;
+    double last_gain_ = 0.0;
+    long long last_gain_fx_ = 0;
     DBuf<unsigned long long> key_;
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
@@ -77,6 +82,6 @@ class Sweeper {
 // decisions, order and stop rules as the Sweeper path); returns `changed`.
 bool small_move_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c);
 bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
-                      int64_t theta, double stall, int64_t *passes, int64_t *moves);
+                      int64_t theta, double stall, double qtol, int64_t *passes, int64_t *moves);
 
 }  // namespace cdk

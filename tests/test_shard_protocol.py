@@ -68,7 +68,7 @@ def plp_sharded(g, rank, G, allgather, seed=3, buckets=4, max_iterations=100):
 
 
 def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterations=32, move_tol=1e-3,
-                       move_stall=0.95):
+                       move_stall=0.95, move_qtol=1e-3):
     from oracle import oracle as O
     b = _bounds(g.off, G)
     lo, hi = int(b[rank]), int(b[rank + 1])
@@ -79,13 +79,16 @@ def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterat
     active = np.ones(n, np.uint8)  # pruning (default on)
     theta = max(n // 100000, int(move_tol * n))
     hist = [-1, -1]
+    cum = 0
     for p in range(max_move_iterations):
         key = O.bucket_key(seed, p)  # salt 0 = level 0, first phase
         moved = 0
+        pass_fx = 0
         for bk in range(buckets):
-            mu, ml = O.move_subsweep(g, z, vols, csize, active, key, bk, lo, hi, seed=seed, buckets=buckets)
-            gathered = allgather((mu, ml))
-            for ru, rl in gathered:
+            mu, ml, gfx = O.move_subsweep(g, z, vols, csize, active, key, bk, lo, hi, seed=seed, buckets=buckets)
+            gathered = allgather((mu, ml, gfx))
+            pass_fx += sum(x[2] for x in gathered)
+            for ru, rl, _ in gathered:
                 for u, d in zip(ru.tolist(), rl.tolist()):
                     c = z[u]
                     vols[c] -= g.vol[u]
@@ -94,10 +97,13 @@ def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterat
                     csize[d] += 1
                     z[u] = d
                 moved += len(ru)
-            O.activate(g, np.concatenate([ru for ru, _ in gathered]), active)
+            O.activate(g, np.concatenate([ru for ru, _, _ in gathered]), active)
         if moved == 0 or moved <= theta:
             break
         if move_stall > 0 and p >= 8 and moved > move_stall * hist[0]:
+            break
+        cum += pass_fx
+        if move_qtol > 0 and float(pass_fx) <= move_qtol * float(cum):
             break
         hist = [hist[1], moved]
     return z
