@@ -24,13 +24,15 @@ enum Tier : int {
     TIER_WARP = 3,    // deg <= 256    : one warp per node, per-warp smem hash
     TIER_BLOCK = 4,   // deg <= 1024   : one block per node, 2048-slot smem hash
     TIER_BLOCK2 = 5,  // deg <= 4096   : one block per node, 8192-slot smem hash
-    TIER_HUB = 6,     // deg >  4096   : multi-block per node, global hash
-    NUM_TIERS = 7,
+    TIER_BLOCK3 = 6,  // deg <= 8192   : one 1024-thread block per node, 16384-slot smem hash
+    TIER_HUB = 7,     // deg >  8192   : hash-partitioned multi-block tally
+    NUM_TIERS = 8,
     TIER_NONE = 255
 };
 constexpr int WARP_TABLE_CAP = 512;     // per-warp smem hash slots (>= 2*256)
 constexpr int BLOCK_TABLE_CAP = 2048;   // >= 2*1024
 constexpr int BLOCK2_TABLE_CAP = 8192;  // >= 2*4096
+constexpr int BLOCK3_TABLE_CAP = 16384; // >= 2*8192
 constexpr int HUB_CHUNK = 4096;         // entries per hub chunk block
 constexpr int HUB_PART = 512;           // target pairs per hub partition
 constexpr int HUB_PART_CAP = 2048;      // smem slots of a partition block (4x HUB_PART)
@@ -51,6 +53,8 @@ __host__ __device__ inline int tier_of_degree(int64_t d) {
         return TIER_BLOCK;
     if (d <= 4096)
         return TIER_BLOCK2;
+    if (d <= 8192)
+        return TIER_BLOCK3;
     return TIER_HUB;
 }
 

@@ -635,6 +635,7 @@ __device__ __forceinline__ uint32_t table_cap(int64_t deg) {
 // Block-cooperative selection: the block's next SW_BLOCK_THREADS candidates
 // (indices blockIdx.x + k * gridDim.x) are tested in parallel and the
 // selected ones compacted into sel[] (ascending k).  Returns their number.
+template <int NT = SW_BLOCK_THREADS>
 __device__ __forceinline__ int block_select(const SweepParams &P, unsigned long long bkey, const int32_t *list,
                                             int64_t count, int64_t k0, int32_t *sel, int *wcount, bool pre) {
     const int lane = lane_id(), wid = threadIdx.x >> 5;
@@ -647,7 +648,7 @@ __device__ __forceinline__ int block_select(const SweepParams &P, unsigned long 
     __syncthreads();
     int base = 0, total = 0;
 #pragma unroll
-    for (int w = 0; w < SW_BLOCK_THREADS / 32; ++w) {
+    for (int w = 0; w < NT / 32; ++w) {
         base += w < wid ? wcount[w] : 0;
         total += wcount[w];
     }
@@ -787,17 +788,17 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     __syncthreads();
 }
 
-template <int MODE, int VC, int CAP, int TIER>
-__global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P) {
+template <int MODE, int VC, int CAP, int TIER, int NT = SW_BLOCK_THREADS>
+__global__ void __launch_bounds__(NT) k_sweep_block(SweepParams P) {
     using V = TallyT<VC>;
     extern __shared__ unsigned char smem_raw[];
     V *vals = reinterpret_cast<V *>(smem_raw);
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
     uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CAP);  // claimed slots (distinct <= deg <= CAP/2)
     static_assert(CAP <= 65536, "slot ids are 16-bit");
-    __shared__ BlockShared<> sh;
-    __shared__ int32_t sel[SW_BLOCK_THREADS];
-    __shared__ int wcount[SW_BLOCK_THREADS / 32];
+    __shared__ BlockShared<NT / 32> sh;
+    __shared__ int32_t sel[NT];
+    __shared__ int wcount[NT / 32];
     const int wid = threadIdx.x >> 5;
     const int32_t *list;
     int64_t count;
@@ -806,10 +807,10 @@ __global__ void __launch_bounds__(SW_BLOCK_THREADS) k_sweep_block(SweepParams P)
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
     const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
-    for (int64_t k0 = 0; k0 < per_block; k0 += SW_BLOCK_THREADS) {
-        const int nsel = block_select(P, bkey, list, count, k0, sel, wcount, pre);
+    for (int64_t k0 = 0; k0 < per_block; k0 += NT) {
+        const int nsel = block_select<NT>(P, bkey, list, count, k0, sel, wcount, pre);
         for (int j = 0; j < nsel; ++j)
-            block_eval_node<MODE, VC>(P, sel[j], vals, keys, dlist, sh, q, st_n, st_e);
+            block_eval_node<MODE, VC, NT>(P, sel[j], vals, keys, dlist, sh, q, st_n, st_e);
     }
     if (wid == 0) {
         q.flush(P);
@@ -1306,11 +1307,20 @@ __device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *co
     }
 }
 
+// Volume / size updates meet in a block-level table first (moves of a coarse
+// level pour into a few large communities: without it every warp's update
+// hits the same global address), one global atomic per touched community and
+// block at the end; full tables fall back to direct atomics.
+constexpr int AP_SLOTS = 1024;
+
 __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, double *vols, int32_t *csize, const double *vol,
                                                    uint8_t *active, const int64_t *toff, const int32_t *tcol,
                                                    int64_t n, long long *total) {
     __shared__ double scratch[8][32];
+    __shared__ int32_t tk[AP_SLOTS];
+    __shared__ double tv[AP_SLOTS];
+    __shared__ int32_t tc[AP_SLOTS];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int64_t count_all = seg_total(counts, nseg);
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -1318,6 +1328,27 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t
     // pruning: the movers' neighbours wake up (same rule as PLP's active set)
     if (active)
         activate_moved(mv, counts, nseg, stride, count_all, active, toff, tcol, n);
+    for (int t = threadIdx.x; t < AP_SLOTS; t += blockDim.x) {
+        tk[t] = EMPTY_KEY;
+        tv[t] = 0.0;
+        tc[t] = 0;
+    }
+    __syncthreads();
+    auto add = [&](int32_t key, double v, int32_t cnt) {
+        uint32_t sl = hash_slot(key, AP_SLOTS - 1);
+        for (int probe = 0; probe < 8; ++probe) {
+            const int32_t old = atomicCAS(&tk[sl], EMPTY_KEY, key);
+            if (old == EMPTY_KEY || old == key) {
+                atomicAdd(&tv[sl], v);
+                atomicAdd(&tc[sl], cnt);
+                return;
+            }
+            sl = (sl + 1) & (AP_SLOTS - 1);
+        }
+        atomicAdd(&vols[key], v);
+        if (csize)
+            atomicAdd(&csize[key], cnt);
+    };
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t count = counts[sg];
@@ -1332,21 +1363,27 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t
                 z[u] = d;
             const double vu = valid ? vol[u] : 0.0;  // H/louvain.hpp:121-125
             // moves into / out of the same community combine per warp first
-            double s;
-            if (warp_aggregate_sum(d, vu, valid, scratch[wid], s))
-                atomicAdd(&vols[d], s);
-            if (warp_aggregate_sum(c, vu, valid, scratch[wid], s))
-                atomicAdd(&vols[c], -s);
-            if (csize) {
-                const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-                const uint32_t pd = __match_any_sync(0xffffffffu, d) & vm;
-                if (valid && (__ffs(pd) - 1) == lane)
-                    atomicAdd(&csize[d], __popc(pd));
-                const uint32_t pc = __match_any_sync(0xffffffffu, c) & vm;
-                if (valid && (__ffs(pc) - 1) == lane)
-                    atomicSub(&csize[c], __popc(pc));
-            }
+            const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+            double sd, sc;
+            const bool ld = warp_aggregate_sum(d, vu, valid, scratch[wid], sd);
+            const int nd = __popc(__match_any_sync(0xffffffffu, d) & vm);
+            if (ld)
+                add(d, sd, nd);
+            const bool lc = warp_aggregate_sum(c, vu, valid, scratch[wid], sc);
+            const int ncm = __popc(__match_any_sync(0xffffffffu, c) & vm);
+            if (lc)
+                add(c, -sc, -ncm);
         }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < AP_SLOTS; t += blockDim.x) {
+        const int32_t key = tk[t];
+        if (key == EMPTY_KEY)
+            continue;
+        if (tv[t] != 0.0)
+            atomicAdd(&vols[key], tv[t]);
+        if (csize && tc[t] != 0)
+            atomicAdd(&csize[key], tc[t]);
     }
 }
 
@@ -1423,7 +1460,7 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
     if (exchange_)
         rcnt_.alloc(ctx, world_);
     if (c_.buckets > 1 && !c_.dense_best) {
-        for (int t : {int(TIER_WARP), int(TIER_BLOCK), int(TIER_BLOCK2)}) {
+        for (int t : {int(TIER_WARP), int(TIER_BLOCK), int(TIER_BLOCK2), int(TIER_BLOCK3)}) {
             const int64_t cnt = tend_[t] - tbeg_[t];
             if (cnt > 0 && cnt <= SW_PREBUCKET_MAX) {
                 pre_mask_ |= 1u << t;
@@ -1483,9 +1520,9 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     // and "plm_move.*" into the family the roofline reports
     static const char *names[2][NUM_TIERS] = {
         {"plp_sweep.g8", "plp_sweep.g16", "plp_sweep.g32", "plp_sweep.warp", "plp_sweep.block", "plp_sweep.block2",
-         "plp_sweep.hub"},
+         "plp_sweep.block3", "plp_sweep.hub"},
         {"plm_move.g8", "plm_move.g16", "plm_move.g32", "plm_move.warp", "plm_move.block", "plm_move.block2",
-         "plm_move.hub"}};
+         "plm_move.block3", "plm_move.hub"}};
     const char *fam = names[MODE][0];
     auto go = [&](auto launch) {
         if (capture) {
@@ -1579,6 +1616,21 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const int nb = grid_for(pre_count(P, TIER_BLOCK2, P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1,
                                 wave((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), SW_BLOCK_THREADS, smem));
         CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
+    }
+    if ((P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3])) {
+        fam = names[MODE][TIER_BLOCK3];
+        constexpr int NT3 = 1024;
+        auto kfn = k_sweep_block<MODE, VC, BLOCK3_TABLE_CAP, TIER_BLOCK3, NT3>;
+        const size_t smem = size_t(BLOCK3_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) +
+                            size_t(BLOCK3_TABLE_CAP / 2) * sizeof(uint16_t);
+        static bool attr3 = false;
+        if (!attr3) {
+            set_smem(kfn, smem);
+            attr3 = true;
+        }
+        const int nb = grid_for(pre_count(P, TIER_BLOCK3, P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3]), 1,
+                                wave(kfn, NT3, smem));
+        CD_TIER_LAUNCH(kfn, nb, NT3, smem, P);
     }
     if (P.tend[TIER_HUB] > P.tbeg[TIER_HUB]) {
         fam = names[MODE][TIER_HUB];

@@ -20,7 +20,8 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 import paper_1304_4453_b200 as P  # noqa: E402
 
-TIERS = [(8, "g8"), (16, "g16"), (32, "g32"), (256, "warp"), (1024, "block"), (4096, "block2"), (1 << 62, "hub")]
+TIERS = [(8, "g8"), (16, "g16"), (32, "g32"), (256, "warp"), (1024, "block"), (4096, "block2"), (8192, "block3"),
+         (1 << 62, "hub")]
 
 
 def tiers(g):
@@ -46,6 +47,8 @@ def main():
     g = bench.make_device_graph(P, ctx, wl)
     cfg = P.LouvainConfig(buckets=a.buckets)
     for level in range(a.levels):
+        # louvain_recurse prunes only the input graph's move phases
+        cfg = P.LouvainConfig(buckets=a.buckets, prune=1 if level == 0 else 0)
         n = g.node_count()
         z0 = np.arange(n, dtype=np.int32)
         if level < a.start:
