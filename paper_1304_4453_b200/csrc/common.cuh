@@ -72,7 +72,7 @@ struct cd_ctx {
     unsigned long long *dstats = nullptr;
     // side streams + events used to capture independent kernels as parallel
     // branches of a CUDA graph
-    static constexpr int NSIDE = 8;  // >= number of degree tiers
+    static constexpr int NSIDE = 10;  // >= number of degree tiers
     cudaStream_t side[NSIDE] = {};
     cudaEvent_t fork_ev = nullptr;
     cudaEvent_t join_ev[NSIDE] = {};

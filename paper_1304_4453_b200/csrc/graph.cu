@@ -218,14 +218,15 @@ void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_
 // ---------------------------------------------------------------------------
 // degree tiers and hub tables
 // ---------------------------------------------------------------------------
-__global__ void k_tiers(int64_t n, const int64_t *off, uint8_t *tier, unsigned long long *counts) {
+__global__ void k_tiers(int64_t n, const int64_t *off, int64_t cluster_max, uint8_t *tier,
+                        unsigned long long *counts) {
     __shared__ unsigned int sc[NUM_TIERS];
     if (threadIdx.x < NUM_TIERS)
         sc[threadIdx.x] = 0;
     __syncthreads();
     for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
          u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int t = tier_of_degree(off[u + 1] - off[u]);
+        const int t = tier_of_degree(off[u + 1] - off[u], cluster_max);
         tier[u] = static_cast<uint8_t>(t);
         if (t != TIER_NONE)
             atomicAdd(&sc[t], 1u);
@@ -298,7 +299,9 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
     counts.zero();
     if (n > 0)
         CD_LAUNCH(ctx, "bins", k_tiers, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
-                  static_cast<const int64_t *>(g->off.p), g->tier.p, counts.p);
+                  static_cast<const int64_t *>(g->off.p),
+                  // distributed-smem fp64 atomics are slow: real-weight graphs keep the HUB path
+                  (g->weighted && !g->int_weights) ? int64_t(0) : CLUSTER_MAX_DEG, g->tier.p, counts.p);
     unsigned long long hc[NUM_TIERS];
     CD_CUDA(cudaMemcpyAsync(hc, counts.p, sizeof(hc), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));

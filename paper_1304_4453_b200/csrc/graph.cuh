@@ -25,8 +25,10 @@ enum Tier : int {
     TIER_BLOCK = 4,   // deg <= 1024   : one block per node, 2048-slot smem hash
     TIER_BLOCK2 = 5,  // deg <= 4096   : one block per node, 8192-slot smem hash
     TIER_BLOCK3 = 6,  // deg <= 8192   : one 1024-thread block per node, 16384-slot smem hash
-    TIER_HUB = 7,     // deg >  8192   : hash-partitioned multi-block tally
-    NUM_TIERS = 8,
+    TIER_CLUSTER = 7, // deg <= 32768  : one 4-CTA cluster per node, hash table in distributed smem
+                      //                 (integer tallies only; fp64 graphs use HUB)
+    TIER_HUB = 8,     // larger        : hash-partitioned multi-block tally
+    NUM_TIERS = 9,
     TIER_NONE = 255
 };
 constexpr int WARP_TABLE_CAP = 512;     // per-warp smem hash slots (>= 2*256)
@@ -38,7 +40,10 @@ constexpr int HUB_PART = 512;           // target pairs per hub partition
 constexpr int HUB_PART_CAP = 2048;      // smem slots of a partition block (4x HUB_PART)
 constexpr int HUB_MAX_PBITS = 13;       // partitions per hub <= 8192 (smem histogram)
 
-__host__ __device__ inline int tier_of_degree(int64_t d) {
+constexpr int64_t CLUSTER_MAX_DEG = 32768;
+
+// cluster_max: CLUSTER_MAX_DEG, or 0 when the cluster tier is not used
+__host__ __device__ inline int tier_of_degree(int64_t d, int64_t cluster_max = CLUSTER_MAX_DEG) {
     if (d <= 0)
         return TIER_NONE;
     if (d <= 8)
@@ -55,6 +60,8 @@ __host__ __device__ inline int tier_of_degree(int64_t d) {
         return TIER_BLOCK2;
     if (d <= 8192)
         return TIER_BLOCK3;
+    if (d <= cluster_max)
+        return TIER_CLUSTER;
     return TIER_HUB;
 }
 

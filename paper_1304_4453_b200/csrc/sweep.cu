@@ -820,6 +820,205 @@ __global__ void __launch_bounds__(NT) k_sweep_block(SweepParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// tier CLUSTER (8192 < deg <= 32768, integer tallies): one 4-CTA cluster per node.
+// The node's label tally is one hash table spread over the CTAs' shared
+// memory (distributed shared memory): label k lives in CTA owner(k), every
+// CTA streams a slice of the row and inserts into the owners' tables with
+// remote shared-memory atomics; each CTA then scans its own distinct labels,
+// and CTA 0 reduces the CTAs' best candidates.  One pass over the row, no
+// global scratch -- the partitioned HUB path needs three.
+// ---------------------------------------------------------------------------
+constexpr int CL_THREADS = 1024;
+constexpr int CL_CAP = 16384;  // slots per CTA
+
+template <int CL>
+__device__ __forceinline__ int cluster_owner(int32_t key) {
+    return static_cast<int>((static_cast<uint32_t>(key) * 0x9E3779B1u) >> 27) % CL;
+}
+
+template <int MODE, int VC, int CL>
+__global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep_cluster(SweepParams P) {
+    namespace cg = cooperative_groups;
+    using V = TallyT<VC>;
+    cg::cluster_group cluster = cg::this_cluster();
+    extern __shared__ unsigned char smem_raw[];
+    V *vals = reinterpret_cast<V *>(smem_raw);
+    int32_t *keys = reinterpret_cast<int32_t *>(vals + CL_CAP);
+    uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CL_CAP);
+    __shared__ double scratch[CL_THREADS / 32][32];
+    __shared__ double red_v[CL_THREADS / 32];
+    __shared__ int32_t red_k[CL_THREADS / 32];
+    __shared__ double red_wc[CL_THREADS / 32];
+    __shared__ int ndist, overflow;
+    __shared__ double part_wc, best_v;
+    __shared__ int32_t best_k;
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    constexpr int NW = CL_THREADS / 32;
+    const int rank = static_cast<int>(cluster.block_rank());
+    const int64_t cid = blockIdx.x / CL, ncl = gridDim.x / CL;
+    const int32_t *list;
+    int64_t count;
+    const bool pre = tier_range(P, TIER_CLUSTER, list, count);
+    const unsigned long long bkey = load_key(P);
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    for (int t = threadIdx.x; t < CL_CAP; t += CL_THREADS) {
+        keys[t] = EMPTY_KEY;
+        vals[t] = V(0);
+    }
+    if (threadIdx.x == 0) {
+        ndist = 0;
+        overflow = 0;
+    }
+    cluster.sync();
+    for (int64_t i = cid; i < count; i += ncl) {
+        const int32_t u = list[i];
+        if (!selected_in(P, bkey, u, pre))  // uniform across the cluster
+            continue;
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        const int32_t cur = P.z[u];
+        double wc = 0.0;
+        for (int64_t f0 = s + (static_cast<int64_t>(rank) * NW + wid) * 32 * SW_ILP; f0 < e;
+             f0 += static_cast<int64_t>(CL) * CL_THREADS * SW_ILP) {
+            int32_t vv[SW_ILP], kk[SW_ILP];
+            float ww[SW_ILP];
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                const int64_t f = f0 + c * 32 + lane;
+                vv[c] = f < e ? P.col[f] : -1;
+                ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
+            }
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c)
+                kk[c] = vv[c] >= 0 ? P.z[vv[c]] : 0;
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                bool valid = vv[c] >= 0;
+                if (MODE == MODE_PLM)
+                    valid = valid && vv[c] != u;
+                const double wt = static_cast<double>(ww[c]);
+                if (MODE == MODE_PLM && valid && kk[c] == cur)
+                    wc += wt;
+                double agg;
+                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
+                    const int owner = cluster_owner<CL>(kk[c]);
+                    int32_t *rk = cluster.map_shared_rank(keys, owner);
+                    V *rv = cluster.map_shared_rank(vals, owner);
+                    uint32_t sl = hash_slot(kk[c], CL_CAP - 1);
+                    bool done = false;
+                    for (int probe = 0; probe < CL_CAP; ++probe) {
+                        const int32_t old = atomicCAS(&rk[sl], EMPTY_KEY, kk[c]);
+                        if (old == EMPTY_KEY || old == kk[c]) {
+                            atomicAdd(&rv[sl], static_cast<V>(agg));
+                            if (old == EMPTY_KEY) {
+                                const int pos = atomicAdd(cluster.map_shared_rank(&ndist, owner), 1);
+                                cluster.map_shared_rank(dlist, owner)[pos] = static_cast<uint16_t>(sl);
+                            }
+                            done = true;
+                            break;
+                        }
+                        sl = (sl + 1) & (CL_CAP - 1);
+                    }
+                    if (!done)
+                        atomicExch(cluster.map_shared_rank(&overflow, owner), 1);
+                }
+            }
+        }
+        if (MODE == MODE_PLM) {
+            wc = warp_sum(wc);
+            if (lane == 0)
+                red_wc[wid] = wc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < NW; ++w)
+                t += red_wc[w];
+            part_wc = t;
+        }
+        cluster.sync();  // tallies and partial w(u, C) complete everywhere
+        if (overflow && threadIdx.x == 0 && P.hp_flag)
+            *P.hp_flag = 1;
+        double wc_all = 0.0;
+        if (MODE == MODE_PLM)
+            for (int r = 0; r < CL; ++r)  // rank order: the same sum on every CTA
+                wc_all += *cluster.map_shared_rank(&part_wc, r);
+        const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
+        const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
+        const int nd = ndist;
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        int32_t ck = INT32_MAX;
+        for (int j0 = threadIdx.x; j0 < nd; j0 += CL_THREADS * SW_ILP) {
+            int32_t key[SW_ILP];
+            double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                const int jj = j0 + c * CL_THREADS;
+                const uint32_t t = jj < nd ? dlist[jj] : 0;
+                key[c] = jj < nd ? keys[t] : EMPTY_KEY;
+                aff[c] = jj < nd ? static_cast<double>(vals[t]) : 0.0;
+            }
+            if (MODE == MODE_PLM) {
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c)
+                    vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < SW_ILP; ++c) {
+                if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
+                    continue;
+                const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc_all, vol_c, vd[c], vol_u, P);
+                if (better(val, key[c], cv, ck)) {
+                    cv = val;
+                    ck = key[c];
+                }
+            }
+        }
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cv = lane < NW ? red_v[lane] : -INFINITY;
+            ck = lane < NW ? red_k[lane] : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            if (lane == 0) {
+                best_v = cv;
+                best_k = ck;
+            }
+        }
+        cluster.sync();  // every CTA's best is visible
+        if (rank == 0 && wid == 0) {
+            cv = lane < CL ? *cluster.map_shared_rank(&best_v, lane < CL ? lane : 0) : -INFINITY;
+            ck = lane < CL ? *cluster.map_shared_rank(&best_k, lane < CL ? lane : 0) : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+            if (lane == 0) {
+                ++st_n;
+                st_e += static_cast<unsigned long long>(e - s);
+            }
+        }
+        // clear this CTA's claimed slots for the next node
+        for (int j = threadIdx.x; j < nd; j += CL_THREADS) {
+            const uint32_t t = dlist[j];
+            keys[t] = EMPTY_KEY;
+            vals[t] = V(0);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            ndist = 0;
+        cluster.sync();  // nobody inserts before every table is clean
+    }
+    if (rank == 0 && wid == 0) {
+        q.flush(P);
+        q.flush_gain(P);
+    }
+    flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
 // Small graphs (coarse levels): the whole move phase in one cooperative
 // launch.  Every pass partitions the nodes by bucket (grid-wide atomics into
 // per-bucket lists, heaviest nodes first), every sub-sweep hands nodes to
@@ -1460,7 +1659,7 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
     if (exchange_)
         rcnt_.alloc(ctx, world_);
     if (c_.buckets > 1 && !c_.dense_best) {
-        for (int t : {int(TIER_WARP), int(TIER_BLOCK), int(TIER_BLOCK2), int(TIER_BLOCK3)}) {
+        for (int t : {int(TIER_WARP), int(TIER_BLOCK), int(TIER_BLOCK2), int(TIER_BLOCK3), int(TIER_CLUSTER)}) {
             const int64_t cnt = tend_[t] - tbeg_[t];
             if (cnt > 0 && cnt <= SW_PREBUCKET_MAX) {
                 pre_mask_ |= 1u << t;
@@ -1520,9 +1719,9 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     // and "plm_move.*" into the family the roofline reports
     static const char *names[2][NUM_TIERS] = {
         {"plp_sweep.g8", "plp_sweep.g16", "plp_sweep.g32", "plp_sweep.warp", "plp_sweep.block", "plp_sweep.block2",
-         "plp_sweep.block3", "plp_sweep.hub"},
+         "plp_sweep.block3", "plp_sweep.cluster", "plp_sweep.hub"},
         {"plm_move.g8", "plm_move.g16", "plm_move.g32", "plm_move.warp", "plm_move.block", "plm_move.block2",
-         "plm_move.block3", "plm_move.hub"}};
+         "plm_move.block3", "plm_move.cluster", "plm_move.hub"}};
     const char *fam = names[MODE][0];
     auto go = [&](auto launch) {
         if (capture) {
@@ -1631,6 +1830,32 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const int nb = grid_for(pre_count(P, TIER_BLOCK3, P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3]), 1,
                                 wave(kfn, NT3, smem));
         CD_TIER_LAUNCH(kfn, nb, NT3, smem, P);
+    }
+    if ((P.tend[TIER_CLUSTER] - P.tbeg[TIER_CLUSTER])) {
+        fam = names[MODE][TIER_CLUSTER];
+        constexpr int CLN = 4;  // 4 x 16384 slots: <= 50 % load at deg 32768
+        auto kfn = k_sweep_cluster<MODE, VC, CLN>;
+        const size_t smem = size_t(CL_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(CL_CAP / 2) * sizeof(uint16_t);
+        static int max_clusters = 0;
+        if (!max_clusters) {
+            set_smem(kfn, smem);
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3(CLN * ctx->num_sms);
+            lc.blockDim = dim3(CL_THREADS);
+            lc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute at;
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = CLN;
+            at.val.clusterDim.y = 1;
+            at.val.clusterDim.z = 1;
+            lc.attrs = &at;
+            lc.numAttrs = 1;
+            CD_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, reinterpret_cast<const void *>(kfn), &lc));
+            max_clusters = std::max(1, max_clusters);
+        }
+        const int64_t nodes = pre_count(P, TIER_CLUSTER, P.tend[TIER_CLUSTER] - P.tbeg[TIER_CLUSTER]);
+        const int ncl = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_clusters, nodes)));
+        CD_TIER_LAUNCH(kfn, ncl * CLN, CL_THREADS, smem, P);
     }
     if (P.tend[TIER_HUB] > P.tbeg[TIER_HUB]) {
         fam = names[MODE][TIER_HUB];

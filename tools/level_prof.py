@@ -21,6 +21,7 @@ import bench  # noqa: E402
 import paper_1304_4453_b200 as P  # noqa: E402
 
 TIERS = [(8, "g8"), (16, "g16"), (32, "g32"), (256, "warp"), (1024, "block"), (4096, "block2"), (8192, "block3"),
+         (65536, "cluster"),
          (1 << 62, "hub")]
 
 
