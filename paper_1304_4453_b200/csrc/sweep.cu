@@ -478,6 +478,11 @@ __global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P,
     int32_t *keys = skeys[wid];
     V *vals = svals[wid];
     uint16_t *dist = sdist[wid];
+    for (int t = lane; t < SW_WARP_CAP; t += 32) {  // empty once; each node cleans up after itself
+        keys[t] = EMPTY_KEY;
+        vals[t] = V(0);
+    }
+    __syncwarp();
     const int32_t *list;
     int64_t count;
     const bool pre = tier_range(P, TIER_WARP, list, count);
@@ -501,10 +506,6 @@ __global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P,
             while (cap < 2 * (e - s))
                 cap <<= 1;
             CD_PT(pt, 0);
-            for (uint32_t t = lane; t < cap; t += 32) {
-                keys[t] = EMPTY_KEY;
-                vals[t] = V(0);
-            }
             const int32_t cur = P.z[u];
             int32_t vv[SW_WARP_ITEMS], kk[SW_WARP_ITEMS];
             float ww[SW_WARP_ITEMS];
@@ -594,6 +595,12 @@ __global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P,
                 ++st_n;
                 st_e += static_cast<unsigned long long>(e - s);
             }
+            // leave the table empty for the next node: only the claimed slots
+            for (int j = lane; j < nd; j += 32) {
+                const uint32_t t = dist[j];
+                keys[t] = EMPTY_KEY;
+                vals[t] = V(0);
+            }
             __syncwarp();
             CD_PT(pt, 5);
 #ifdef CD_PHASE_TIMING
@@ -682,14 +689,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     const int32_t cur = P.z[u];
     const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
     const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
-    const uint32_t cap = table_cap(e - s);
-    for (uint32_t t = threadIdx.x; t < cap; t += NT) {
-        keys[t] = EMPTY_KEY;
-        vals[t] = V(0);
-    }
-    if (threadIdx.x == 0)
-        sh.ndist = 0;
-    __syncthreads();
+    const uint32_t cap = table_cap(e - s);  // the table is empty on entry (block_table_init)
     double wc = 0.0;
     for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += NT * SW_ILP) {
         int32_t vv[SW_ILP], kk[SW_ILP];
@@ -785,6 +785,28 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
             st_e += static_cast<unsigned long long>(e - s);
         }
     }
+    // leave the table empty for the next node: only the claimed slots
+    for (int j = threadIdx.x; j < nd; j += NT) {
+        const uint32_t t = dlist[j];
+        keys[t] = EMPTY_KEY;
+        vals[t] = V(0);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+        sh.ndist = 0;
+    __syncthreads();
+}
+
+// Empties a block evaluator's table once per kernel (nodes then clean up
+// after themselves); ends with a block barrier.
+template <class V, class SH>
+__device__ __forceinline__ void block_table_init(V *vals, int32_t *keys, uint32_t cap, SH &sh) {
+    for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
+        keys[t] = EMPTY_KEY;
+        vals[t] = V(0);
+    }
+    if (threadIdx.x == 0)
+        sh.ndist = 0;
     __syncthreads();
 }
 
@@ -806,6 +828,7 @@ __global__ void __launch_bounds__(NT) k_sweep_block(SweepParams P) {
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
+    block_table_init(vals, keys, CAP, sh);
     const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
     for (int64_t k0 = 0; k0 < per_block; k0 += NT) {
         const int nsel = block_select<NT>(P, bkey, list, count, k0, sel, wcount, pre);
@@ -1064,6 +1087,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
     int32_t *ctr = S.ctr;
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
+    block_table_init(vals, keys, S.cap_max, sh);
     long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
     int passes = 0;
     bool changed = false;
