@@ -2065,10 +2065,11 @@ void Sweeper::pass(uint64_t key) {
         return;
     }
     if (!exec_) {
-        // the first pass runs eagerly; the host records and instantiates the
-        // graph for the remaining passes while the device executes it
-        enqueue(false);
+        // the first pass runs eagerly (tier kernels on parallel side streams
+        // as in the graph); the host records and instantiates the graph for
+        // the remaining passes while the device executes it
         ensure_side_streams(ctx_);
+        enqueue(true);
         const int64_t l0 = ctx_->launches;
         CD_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
         try {
