@@ -1530,20 +1530,11 @@ __device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *co
     }
 }
 
-// Volume / size updates meet in a block-level table first (moves of a coarse
-// level pour into a few large communities: without it every warp's update
-// hits the same global address), one global atomic per touched community and
-// block at the end; full tables fall back to direct atomics.
-constexpr int AP_SLOTS = 1024;
-
 __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, double *vols, int32_t *csize, const double *vol,
                                                    uint8_t *active, const int64_t *toff, const int32_t *tcol,
                                                    int64_t n, long long *total) {
     __shared__ double scratch[8][32];
-    __shared__ int32_t tk[AP_SLOTS];
-    __shared__ double tv[AP_SLOTS];
-    __shared__ int32_t tc[AP_SLOTS];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int64_t count_all = seg_total(counts, nseg);
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -1551,27 +1542,6 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t
     // pruning: the movers' neighbours wake up (same rule as PLP's active set)
     if (active)
         activate_moved(mv, counts, nseg, stride, count_all, active, toff, tcol, n);
-    for (int t = threadIdx.x; t < AP_SLOTS; t += blockDim.x) {
-        tk[t] = EMPTY_KEY;
-        tv[t] = 0.0;
-        tc[t] = 0;
-    }
-    __syncthreads();
-    auto add = [&](int32_t key, double v, int32_t cnt) {
-        uint32_t sl = hash_slot(key, AP_SLOTS - 1);
-        for (int probe = 0; probe < 8; ++probe) {
-            const int32_t old = atomicCAS(&tk[sl], EMPTY_KEY, key);
-            if (old == EMPTY_KEY || old == key) {
-                atomicAdd(&tv[sl], v);
-                atomicAdd(&tc[sl], cnt);
-                return;
-            }
-            sl = (sl + 1) & (AP_SLOTS - 1);
-        }
-        atomicAdd(&vols[key], v);
-        if (csize)
-            atomicAdd(&csize[key], cnt);
-    };
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t count = counts[sg];
@@ -1586,27 +1556,21 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t
                 z[u] = d;
             const double vu = valid ? vol[u] : 0.0;  // H/louvain.hpp:121-125
             // moves into / out of the same community combine per warp first
-            const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-            double sd, sc;
-            const bool ld = warp_aggregate_sum(d, vu, valid, scratch[wid], sd);
-            const int nd = __popc(__match_any_sync(0xffffffffu, d) & vm);
-            if (ld)
-                add(d, sd, nd);
-            const bool lc = warp_aggregate_sum(c, vu, valid, scratch[wid], sc);
-            const int ncm = __popc(__match_any_sync(0xffffffffu, c) & vm);
-            if (lc)
-                add(c, -sc, -ncm);
+            double s;
+            if (warp_aggregate_sum(d, vu, valid, scratch[wid], s))
+                atomicAdd(&vols[d], s);
+            if (warp_aggregate_sum(c, vu, valid, scratch[wid], s))
+                atomicAdd(&vols[c], -s);
+            if (csize) {
+                const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+                const uint32_t pd = __match_any_sync(0xffffffffu, d) & vm;
+                if (valid && (__ffs(pd) - 1) == lane)
+                    atomicAdd(&csize[d], __popc(pd));
+                const uint32_t pc = __match_any_sync(0xffffffffu, c) & vm;
+                if (valid && (__ffs(pc) - 1) == lane)
+                    atomicSub(&csize[c], __popc(pc));
+            }
         }
-    }
-    __syncthreads();
-    for (int t = threadIdx.x; t < AP_SLOTS; t += blockDim.x) {
-        const int32_t key = tk[t];
-        if (key == EMPTY_KEY)
-            continue;
-        if (tv[t] != 0.0)
-            atomicAdd(&vols[key], tv[t]);
-        if (csize && tc[t] != 0)
-            atomicAdd(&csize[key], tc[t]);
     }
 }
 
