@@ -189,3 +189,26 @@ def test_nccl_world_one(dev):
         assert np.array_equal(z, z2)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("layout", ["replicated", "rows"])
+def test_sharded_tiny_graphs_more_ranks_than_nodes(dev, layout):
+    """Ranks owning no nodes (G > n), isolated nodes and a self-loop."""
+    cases = [(3, [(0, 1), (1, 2)]), (5, [(0, 1), (1, 2), (2, 0), (3, 3)]), (2, [(0, 1)])]
+    for n, edges in cases:
+        def mk(ctx):
+            return dev.Graph.from_edges(n, edges, ctx=ctx)
+
+        ctx0 = dev.Context(0)
+        z1 = {a: detect(dev, a, mk(ctx0))[0] for a in ("plp", "plm", "plmr")}
+        ctx0.close()
+
+        def fn(ctx, r):
+            g = mk(ctx)
+            if layout == "rows":
+                g = g.shard(ctx)
+            return {a: detect(dev, a, g)[0] for a in ("plp", "plm", "plmr")}
+
+        for res in run_ranks(dev, 4, fn):
+            for a in z1:
+                assert np.array_equal(res[a], z1[a]), (n, a)
