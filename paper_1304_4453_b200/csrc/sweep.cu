@@ -7,15 +7,20 @@
 //        best = argmax delta with ties -> smallest d, move iff delta > 0.
 //
 // Tiers (graph.cuh): G8/G16/G32 one pass with __match_any_sync, lanes grouped
-// 8/16/32 per node; WARP per-warp smem hash; BLOCK / BLOCK2 block smem hash
-// (2048 / 8192 slots); HUB multi-block insert into a global hash + per-hub
-// finalize.  Every tally is exact (integer counts / integral weights in
-// uint32, general weights in fp64), so the decision does not depend on the
-// summation order and equals the sequential reference's.
+// 8/16/32 per node; WARP per-warp smem hash; BLOCK / BLOCK2 / BLOCK3 block
+// smem hash (2048 / 8192 / 16384 slots); CLUSTER one 4-CTA cluster per node
+// with the hash in distributed shared memory; HUB a hash-partitioned
+// multi-block tally.  Every table lists its claimed slots, so the candidate
+// scan visits only distinct labels and the table cleans up after each node.
+// Integer tallies are exact in uint32, general weights in fp64, so the
+// decision does not depend on the summation order and equals the
+// sequential reference's (tests/test_gpu_tiers.py).
 //
-// Selection (bucket of this sub-sweep, PLP active flag) is done inline: each
-// warp loads 32 candidates of its tier's static list, ballots the selected
-// ones and processes them -- no worklist kernel, no global atomics.
+// Selection (bucket of this sub-sweep, active flag) is inline: each warp
+// loads up to 32 candidates of its tier's static list and ballots the
+// selected ones; block tiers select 256 candidates cooperatively; short tier
+// lists are pre-bucketed once per pass (k_prebucket).  Small coarse levels run
+// the whole move phase in one cooperative kernel (k_small_move).
 #include "sweep.cuh"
 
 #include <cooperative_groups.h>
@@ -141,19 +146,6 @@ __device__ __forceinline__ bool aggregate(int32_t key, double w, bool valid, uin
         val = static_cast<double>(__popc(peers));
     }
     return leader;
-}
-
-template <class V>
-__device__ __forceinline__ void tinsert(int32_t *keys, V *vals, uint32_t mask, int32_t key, V w) {
-    uint32_t s = hash_slot(key, mask);
-    while (true) {
-        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
-        if (old == EMPTY_KEY || old == key) {
-            atomicAdd(&vals[s], w);
-            return;
-        }
-        s = (s + 1) & mask;
-    }
 }
 
 // insert; true if this call claimed a new slot for `key` (*slot = its index)
@@ -462,13 +454,10 @@ __device__ unsigned long long g_phase[16];
 #endif
 
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
-#ifndef SW_WARP_MINB
-#define SW_WARP_MINB 1
-#endif
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
 template <int MODE, int VC>
-__global__ void __launch_bounds__(128, SW_WARP_MINB) k_sweep_warp(SweepParams P, int chunk) {
+__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
     using V = TallyT<VC>;
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][SW_WARP_CAP];
