@@ -99,6 +99,15 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
         c.toff = g->toff.p;
         c.tcol = g->tcol.p;
     }
+    if (fused_eligible(ctx, g, c)) {  // the whole run in one cooperative kernel
+        if (n > theta && cfg.max_iterations > 0) {
+            FusedResult fr;
+            fused_phase(ctx, g, c, cfg.seed, 0, cfg.max_iterations, theta, 0.0, 0.0, fr);
+            for (size_t i = 0; i < fr.trace.size(); ++i)
+                rep.iteration(fr.trace[i], fr.ms[i]);
+        }
+        return;
+    }
     Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
     int64_t updated = n, iter = 0;
@@ -219,6 +228,17 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     if (small_move_eligible(ctx, g, c))
         return small_move_phase(ctx, g, c, cfg.seed, salt, cfg.max_move_iterations, theta, cfg.move_stall,
                                 cfg.move_qtol, passes, moves);
+    if (fused_eligible(ctx, g, c)) {
+        if (cfg.max_move_iterations <= 0)
+            return false;
+        FusedResult fr;
+        fused_phase(ctx, g, c, cfg.seed, salt, cfg.max_move_iterations, theta, cfg.move_stall, cfg.move_qtol, fr);
+        if (passes)
+            *passes += fr.passes;
+        if (moves)
+            *moves += fr.moves;
+        return fr.changed;
+    }
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;

@@ -26,6 +26,7 @@
 #include <cooperative_groups.h>
 
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <map>
 #include <mutex>
@@ -355,20 +356,17 @@ __device__ __forceinline__ void flush_stats(const SweepParams &P, unsigned long 
 // ---------------------------------------------------------------------------
 // tiers G8 / G16 / G32: one entry per lane, G lanes per node
 // ---------------------------------------------------------------------------
+// One warp's share of a direct tier in one sub-sweep (warps gw of nw).
 template <int G, int MODE, int VC>
-__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, int chunk) {
-    __shared__ double scratch[8][32];
+__device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int chunk, unsigned long long bkey,
+                                            int64_t gw, int64_t nw, double *scratch_w, MoveQueue &q,
+                                            unsigned long long &st_n, unsigned long long &st_e) {
     constexpr int NPW = 32 / G;
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const int lane = lane_id();
     const int sub = lane / G, k = lane % G;
     const uint32_t gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (sub * G));
     const int32_t *list = P.tlist + P.tbeg[tier];
     const int64_t count = P.tend[tier] - P.tbeg[tier];
-    const unsigned long long bkey = load_key(P);
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    unsigned long long st_n = 0, st_e = 0;
-    MoveQueue q;
     // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
     // many of them, so the tail of a sub-sweep stays occupied
     for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
@@ -394,7 +392,7 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
                 valid = valid && v != u;
             const int32_t key = valid ? P.z[v] : 0;
             double agg;
-            const bool leader = aggregate<VC>(key, wt, valid, gmask, scratch[wid], agg);
+            const bool leader = aggregate<VC>(key, wt, valid, gmask, scratch_w, agg);
             const int32_t cur = has ? P.z[u] : 0;
             double cv;
             int32_t ck;
@@ -422,6 +420,17 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
             }
         }
     }
+}
+
+template <int G, int MODE, int VC>
+__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, int chunk) {
+    __shared__ double scratch[8][32];
+    const int wid = threadIdx.x >> 5;
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    direct_tier<G, MODE, VC>(P, tier, chunk, load_key(P), gw, nw, scratch[wid], q, st_n, st_e);
     q.flush(P);
     q.flush_gain(P);
     flush_stats(P, st_n, st_e);
@@ -456,30 +465,18 @@ __device__ unsigned long long g_phase[16];
 constexpr int SW_WARP_CAP = WARP_TABLE_CAP;
 constexpr int SW_WARP_ITEMS = 8;  // 256 / 32
 
+// One warp's share of the WARP tier in one sub-sweep; the warp's table
+// (keys / vals / dist) is empty on entry and left empty.
 template <int MODE, int VC>
-__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
+__device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsigned long long bkey, int64_t gw,
+                                          int64_t nw, int32_t *keys, TallyT<VC> *vals, uint16_t *dist,
+                                          double *scratch_w, MoveQueue &q, unsigned long long &st_n,
+                                          unsigned long long &st_e) {
     using V = TallyT<VC>;
-    __shared__ double scratch[4][32];
-    __shared__ int32_t skeys[4][SW_WARP_CAP];
-    __shared__ V svals[4][SW_WARP_CAP];
-    __shared__ uint16_t sdist[4][SW_WARP_CAP / 2];  // claimed slots = the distinct labels
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
-    int32_t *keys = skeys[wid];
-    V *vals = svals[wid];
-    uint16_t *dist = sdist[wid];
-    for (int t = lane; t < SW_WARP_CAP; t += 32) {  // empty once; each node cleans up after itself
-        keys[t] = EMPTY_KEY;
-        vals[t] = V(0);
-    }
-    __syncwarp();
+    const int lane = lane_id();
     const int32_t *list;
     int64_t count;
     const bool pre = tier_range(P, TIER_WARP, list, count);
-    const unsigned long long bkey = load_key(P);
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    unsigned long long st_n = 0, st_e = 0;
-    MoveQueue q;
     // each warp owns `chunk` (<= 32) candidates per iteration: short warps,
     // many of them, so the tail of a sub-sweep stays occupied
     for (int64_t base = gw * chunk; base < count; base += nw * chunk) {
@@ -531,7 +528,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                     // fp64 tallies: combine equal labels in lane order first,
                     // so every slot sees one add per round (deterministic)
                     double agg;
-                    if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg))
+                    if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch_w, agg))
                         claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
                 } else if (valid) {
                     // integer tallies are order-free: insert directly
@@ -600,6 +597,27 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
 #endif
         }
     }
+}
+
+template <int MODE, int VC>
+__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
+    using V = TallyT<VC>;
+    __shared__ double scratch[4][32];
+    __shared__ int32_t skeys[4][SW_WARP_CAP];
+    __shared__ V svals[4][SW_WARP_CAP];
+    __shared__ uint16_t sdist[4][SW_WARP_CAP / 2];  // claimed slots = the distinct labels
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    for (int t = lane; t < SW_WARP_CAP; t += 32) {  // empty once; each node cleans up after itself
+        skeys[wid][t] = EMPTY_KEY;
+        svals[wid][t] = V(0);
+    }
+    __syncwarp();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    warp_tier<MODE, VC>(P, chunk, load_key(P), gw, nw, skeys[wid], svals[wid], sdist[wid], scratch[wid], q, st_n,
+                        st_e);
     q.flush(P);
     q.flush_gain(P);
     flush_stats(P, st_n, st_e);
@@ -1028,6 +1046,156 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         q.flush_gain(P);
     }
     flush_stats(P, st_n, st_e);
+}
+
+// ---------------------------------------------------------------------------
+// Fused phase: a whole PLP run or PLM move phase on a graph whose degrees
+// stay within the warp-granular tiers (G8 / G16 / G32 / WARP, deg <= 256) in
+// one cooperative kernel.  Every warp takes its share of every tier, grid
+// barriers replace the kernel boundaries between evaluation, apply and the
+// next sub-sweep, and the stop rules run on the device -- no launch gaps, no
+// graph replays, no host round trip per pass.  Same decisions, order and
+// stop rules as the Sweeper path (tests/test_gpu_parity.py, bit-exact).
+// ---------------------------------------------------------------------------
+struct FusedPhase {
+    int K;
+    unsigned long long seed, salt;
+    int max_passes;
+    long long theta;      // PLP: iterate while updated > theta; PLM: stop at <= theta
+    double stall, qtol;   // PLM rules
+    int chunk[4];         // G8, G16, G32, WARP
+    int32_t *ctr;         // [0,8) moves of bucket b
+    long long *gain;      // [1] this pass's gain (PLM, fixed point)
+    long long *result;    // passes, moves, changed
+    long long *trace;     // [trace_cap] moves per pass
+    unsigned long long *stamp;  // [trace_cap] globaltimer at each pass end
+    int trace_cap;
+    int print;
+};
+
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr int FUSED_THREADS = 128;
+
+template <int MODE, int VC>
+__global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, FusedPhase F) {
+    namespace cg = cooperative_groups;
+    using V = TallyT<VC>;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double scratch[4][32];
+    __shared__ int32_t skeys[4][SW_WARP_CAP];
+    __shared__ V svals[4][SW_WARP_CAP];
+    __shared__ uint16_t sdist[4][SW_WARP_CAP / 2];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    for (int t = lane; t < SW_WARP_CAP; t += 32) {
+        skeys[wid][t] = EMPTY_KEY;
+        svals[wid][t] = V(0);
+    }
+    __syncwarp();
+    const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t gsize = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t gw = gtid >> 5, nw = gsize >> 5;
+    const int64_t n = P.own_hi;  // whole graph (single device)
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
+    int passes = 0;
+    bool changed = false;
+    for (int pass = 0; pass < F.max_passes; ++pass) {
+        const unsigned long long key = bucket_key(F.seed, F.salt + static_cast<unsigned long long>(pass));
+        long long pass_moves = 0;
+        for (int b = 0; b < F.K; ++b) {
+            P.bucket = b;
+            P.mv_count = F.ctr + b;
+            direct_tier<8, MODE, VC>(P, TIER_G8, F.chunk[0], key, gw, nw, scratch[wid], q, st_n, st_e);
+            direct_tier<16, MODE, VC>(P, TIER_G16, F.chunk[1], key, gw, nw, scratch[wid], q, st_n, st_e);
+            direct_tier<32, MODE, VC>(P, TIER_G32, F.chunk[2], key, gw, nw, scratch[wid], q, st_n, st_e);
+            warp_tier<MODE, VC>(P, F.chunk[3], key, gw, nw, skeys[wid], svals[wid], sdist[wid], scratch[wid], q,
+                                st_n, st_e);
+            q.flush(P);
+            q.flush_gain(P);
+            grid.sync();
+            const int64_t mc = F.ctr[b];
+            if (MODE == MODE_PLM) {  // H/louvain.hpp:121-125
+                for (int64_t i = gtid; i < mc; i += gsize) {
+                    const int2 m = P.mv[i];
+                    const int32_t c = P.z[m.x];
+                    const_cast<int32_t *>(P.z)[m.x] = m.y;
+                    const double vu = P.vol[m.x];
+                    atomicAdd(const_cast<double *>(&P.vols[m.y]), vu);
+                    atomicAdd(const_cast<double *>(&P.vols[c]), -vu);
+                    atomicAdd(const_cast<int32_t *>(&P.csize[m.y]), 1);
+                    atomicSub(const_cast<int32_t *>(&P.csize[c]), 1);
+                }
+            } else {
+                for (int64_t i = gtid; i < mc; i += gsize) {
+                    const int2 m = P.mv[i];
+                    const_cast<int32_t *>(P.z)[m.x] = m.y;
+                }
+            }
+            if (P.active) {  // H/plp.hpp:127-133 / pruning: the movers' neighbours wake up
+                if (mc > n / 16) {
+                    for (int64_t i = gtid; i < n; i += gsize)
+                        P.active[i] = 1;
+                } else {
+                    for (int64_t i = gw; i < mc; i += nw) {
+                        const int32_t u = P.mv[i].x;
+                        for (int64_t e = P.off[u] + lane; e < P.off[u + 1]; e += 32)
+                            P.active[P.col[e]] = 1;
+                    }
+                }
+            }
+            pass_moves += mc;
+            grid.sync();
+        }
+        if (pass < F.trace_cap && gtid == 0) {
+            F.trace[pass] = pass_moves;
+            F.stamp[pass] = global_ns();
+        }
+        ++passes;
+        moves_total += pass_moves;
+        if (F.print && gtid == 0)
+            printf("[cd] %s(fused) n=%lld pass=%d moved=%lld\n", MODE == MODE_PLP ? "plp" : "move",
+                   static_cast<long long>(n), pass, pass_moves);
+        bool stop = false;
+        if (MODE == MODE_PLP) {
+            stop = pass_moves <= F.theta;  // H/plp.hpp:98
+        } else if (pass_moves == 0) {
+            stop = true;
+        } else {
+            changed = true;
+            if (pass_moves <= F.theta)
+                stop = true;
+            else if (F.stall > 0.0 && pass >= 8 && static_cast<double>(pass_moves) > F.stall * static_cast<double>(hist0))
+                stop = true;
+            if (!stop) {
+                const long long pass_fx = *F.gain;
+                cum_fx += pass_fx;
+                if (F.qtol > 0.0 && static_cast<double>(pass_fx) <= F.qtol * static_cast<double>(cum_fx))
+                    stop = true;
+            }
+            hist0 = hist1;
+            hist1 = pass_moves;
+        }
+        grid.sync();  // every thread has read the counters and the gain
+        if (gtid < 8)
+            F.ctr[gtid] = 0;
+        if (gtid == 0)
+            *F.gain = 0;
+        grid.sync();
+        if (stop)
+            break;
+    }
+    flush_stats(P, st_n, st_e);
+    if (gtid == 0) {
+        F.result[0] = passes;
+        F.result[1] = moves_total;
+        F.result[2] = changed ? 1 : 0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -2042,6 +2210,142 @@ void Sweeper::pass(uint64_t key) {
     }
     CD_CUDA(cudaGraphLaunch(exec_, ctx_->stream));
     ctx_->launches += kernels_per_pass_;
+}
+
+// Eligible: one device (no exchange), every degree within the warp tiers,
+// and few enough entries (CD_FUSED_MAX_D, default 2^23) that per-sub-sweep
+// launch and join latency, not the work, dominates: on C2's level 0 (18 M
+// entries) the separate, concurrently running tier kernels are faster.
+bool fused_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c) {
+    static const int64_t max_d = [] {
+        const char *e = std::getenv("CD_FUSED_MAX_D");
+        return e ? std::atoll(e) : (int64_t(1) << 23);
+    }();
+    return ctx->comm == nullptr && !c.dense_best && g->n > 0 && g->D <= max_d && g->max_degree <= 256 &&
+           c.buckets >= 1 && c.buckets <= 8;
+}
+
+template <int MODE, int VC>
+static void launch_fused(cd_ctx *ctx, SweepParams &P, FusedPhase &F) {
+    auto kfn = k_fused_phase<MODE, VC>;
+    int per_sm = 0;
+    CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, FUSED_THREADS, 0));
+    if (per_sm < 1)
+        fail(CD_EINTERNAL, "fused phase: kernel does not fit an SM");
+    const int grid = per_sm * ctx->num_sms;
+    const int64_t warps = int64_t(grid) * (FUSED_THREADS / 32);
+    // candidates per warp and round, as launch_tiers sizes them
+    const int npw[4] = {4, 2, 1, 1};
+    const int tiers[4] = {TIER_G8, TIER_G16, TIER_G32, TIER_WARP};
+    for (int i = 0; i < 4; ++i) {
+        const int64_t nodes = P.tend[tiers[i]] - P.tbeg[tiers[i]];
+        const int64_t hi = std::min<int64_t>(32, 2LL * npw[i] * F.K);
+        const int64_t lo = std::min<int64_t>(hi, static_cast<int64_t>(npw[i]) * F.K);
+        F.chunk[i] = static_cast<int>(std::max(lo, std::min(hi, (nodes + warps - 1) / warps)));
+    }
+    void *args[] = {&P, &F};
+    LaunchScope ls(ctx, MODE == MODE_PLP ? "plp_sweep.fused" : "plm_move.fused");
+    CD_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kfn), dim3(grid), dim3(FUSED_THREADS), args,
+                                        0, ctx->stream));
+}
+
+int64_t fused_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
+                    int64_t theta, double stall, double qtol, FusedResult &out) {
+    graph_ensure_bins(ctx, g);
+    const int64_t cap = std::max<int64_t>(max_passes, 1);
+    DBuf<int32_t> ctr(ctx, 8);
+    DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
+    DBuf<long long> result(ctx, 4), gain(ctx, 1), trace(ctx, cap);
+    DBuf<unsigned long long> stamp(ctx, cap + 1);
+    ctr.zero();
+    gain.zero();
+    SweepParams P{};
+    P.off = g->off.p;
+    P.col = g->col.p;
+    P.w = g->weighted ? g->w.p : nullptr;
+    P.vol = g->vol.p;
+    P.z = c.z;
+    P.active = c.active;
+    P.vols = c.vols;
+    P.csize = c.csize;
+    P.gamma = c.gamma;
+    P.inv_total = g->total > 0 ? 1.0 / g->total : 0.0;
+    P.inv_sq2 = g->total > 0 ? 1.0 / (2.0 * g->total * g->total) : 0.0;
+    P.guard = c.guard;
+    P.buckets = c.buckets;
+    P.tlist = g->tlist.p;
+    for (int t = 0; t < NUM_TIERS; ++t) {
+        P.tbeg[t] = g->tier_start[t];
+        P.tend[t] = g->tier_start[t + 1];
+    }
+    P.own_lo = 0;
+    P.own_hi = static_cast<int32_t>(g->n);
+    P.pre_mask = 0;
+    P.mv = mv.p;
+    P.stats = ctx->dstats + (c.mode == MODE_PLP ? 0 : 3);
+    P.gain_fx = c.mode == MODE_PLM ? gain.p : nullptr;
+    FusedPhase F{};
+    F.K = c.buckets;
+    F.seed = seed;
+    F.salt = salt;
+    F.max_passes = static_cast<int>(max_passes);
+    F.theta = theta;
+    F.stall = stall;
+    F.qtol = qtol;
+    F.ctr = ctr.p;
+    F.gain = gain.p;
+    F.result = result.p;
+    F.trace = trace.p;
+    F.stamp = stamp.p;
+    F.trace_cap = static_cast<int>(cap);
+    F.print = std::getenv("CD_TRACE") != nullptr;
+    unsigned long long t0 = 0;
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int vc = !g->weighted ? VC_COUNT : (g->int_weights ? VC_INT : VC_REAL);
+    const auto wall0 = std::chrono::steady_clock::now();
+    if (c.mode == MODE_PLP) {
+        if (vc == VC_COUNT)
+            launch_fused<MODE_PLP, VC_COUNT>(ctx, P, F);
+        else if (vc == VC_INT)
+            launch_fused<MODE_PLP, VC_INT>(ctx, P, F);
+        else
+            launch_fused<MODE_PLP, VC_REAL>(ctx, P, F);
+    } else {
+        if (vc == VC_COUNT)
+            launch_fused<MODE_PLM, VC_COUNT>(ctx, P, F);
+        else if (vc == VC_INT)
+            launch_fused<MODE_PLM, VC_INT>(ctx, P, F);
+        else
+            launch_fused<MODE_PLM, VC_REAL>(ctx, P, F);
+    }
+    long long h[3];
+    CD_CUDA(cudaMemcpyAsync(h, result.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    out.trace.assign(static_cast<size_t>(std::min<long long>(h[0], cap)), 0);
+    std::vector<unsigned long long> st(out.trace.size());
+    if (!out.trace.empty()) {
+        CD_CUDA(cudaMemcpyAsync(out.trace.data(), trace.p, out.trace.size() * sizeof(long long),
+                                cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaMemcpyAsync(st.data(), stamp.p, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+    }
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - wall0).count();
+    // per-pass times from the device clock (the first pass also carries the launch)
+    out.ms.assign(out.trace.size(), 0.0);
+    for (size_t i = 0; i < st.size(); ++i)
+        out.ms[i] = i ? static_cast<double>(st[i] - st[i - 1]) * 1e-6 : 0.0;
+    if (!st.empty()) {
+        double rest = 0.0;
+        for (size_t i = 1; i < st.size(); ++i)
+            rest += out.ms[i];
+        out.ms[0] = std::max(0.0, wall_ms - rest);
+    }
+    (void)t0;
+    out.passes = h[0];
+    out.moves = h[1];
+    out.changed = h[2] != 0;
+    return h[0];
 }
 
 // Eligible: one device (no exchange), no pruning, no hubs (the block

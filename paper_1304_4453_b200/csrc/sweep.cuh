@@ -78,6 +78,18 @@ class Sweeper {
     int64_t kernels_per_pass_ = 0;
 };
 
+// Whole PLP run / PLM move phase of a graph with degrees <= 256 in one
+// cooperative kernel (same decisions, order and stop rules as the Sweeper).
+struct FusedResult {
+    int64_t passes = 0, moves = 0;
+    bool changed = false;
+    std::vector<long long> trace;  // moves per pass
+    std::vector<double> ms;        // device time per pass
+};
+bool fused_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c);
+int64_t fused_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
+                    int64_t theta, double stall, double qtol, FusedResult &out);
+
 // Whole PLM move phase of a small graph in one cooperative kernel (same
 // decisions, order and stop rules as the Sweeper path); returns `changed`.
 bool small_move_eligible(const cd_ctx *ctx, const cd_graph *g, const SweepCall &c);
