@@ -2368,7 +2368,14 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
     CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, SMALL_THREADS, smem));
     if (per_sm < 1)
         fail(CD_EINTERNAL, "small move phase: kernel does not fit an SM");
-    const int grid = std::max(1, std::min<int>(per_sm * ctx->num_sms, static_cast<int>((S.nn + 1) / 2)));
+    // a grid barrier costs more with more blocks: tiny levels use few blocks
+    // (CD_SMALL_DIV nodes per block, default 2: measured best; fewer blocks
+    // only lengthen the per-block node queues)
+    static const int div = [] {
+        const char *e = std::getenv("CD_SMALL_DIV");
+        return e ? std::max(1, std::atoi(e)) : 2;
+    }();
+    const int grid = std::max(1, std::min<int>(per_sm * ctx->num_sms, static_cast<int>((S.nn + div - 1) / div)));
     SweepParams p = P;
     SmallPhase s = S;
     void *args[] = {&p, &s};
