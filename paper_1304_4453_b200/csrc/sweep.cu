@@ -2368,9 +2368,9 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
     CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, SMALL_THREADS, smem));
     if (per_sm < 1)
         fail(CD_EINTERNAL, "small move phase: kernel does not fit an SM");
-    // a grid barrier costs more with more blocks: tiny levels use few blocks
-    // (CD_SMALL_DIV nodes per block, default 2: measured best; fewer blocks
-    // only lengthen the per-block node queues)
+    // about CD_SMALL_DIV nodes per block (default 2, measured best: fewer,
+    // busier blocks lengthen the per-block node queues more than they save
+    // on the grid barriers)
     static const int div = [] {
         const char *e = std::getenv("CD_SMALL_DIV");
         return e ? std::max(1, std::atoi(e)) : 2;
