@@ -328,16 +328,24 @@ def bench_b200(args, wl):
     s = stats[fam]
     peak, peak_kind = measured_peak()
     achieved = s["bytes"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 and s["bytes"] > 0 else None
-    # bases ("plm_move", "coarsen") aggregate their ".warp/.sort/..." entries
+    # bases ("plm_move", "coarsen") aggregate their ".warp/.sort/..." entries;
+    # "<mode>.hub" is the sum of the hub kernels "<mode>.hub_*"
     bases = {k.split(".")[0] for k in stats if "." in k}
-    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in bases)
+    synthetic = {k for k in stats if k.endswith(".hub")}
+    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in bases and k not in synthetic)
     roofline = {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": None,
                 "peak_kind": peak_kind, "bytes_per_launch": s["bytes"] / max(s["launches"], 1),
                 "avg_launch_ms": s["total_ms"] / max(s["launches"], 1), "launches": s["launches"] // prof_steps,
                 "share_of_step": s["total_ms"] / prof_total if prof_total else None,
                 "families_ms_per_step": {k: round(v["total_ms"] / prof_steps, 4) for k, v in
-                                         sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])[:8]}}
+                                         sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])[:8]},
+                # every sweep kernel against the HBM roofline (per-tier work counters)
+                "kernels": {k: {"ms_per_step": round(v["total_ms"] / prof_steps, 4),
+                                "achieved": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9, 2),
+                                "frac": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9 / peak, 5)}
+                            for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])
+                            if "." in k and v["bytes"] > 0 and v["total_ms"] > 0}}
     prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:

@@ -277,15 +277,41 @@ cd_status cd_ctx_kernel_stats(cd_ctx *ctx, cd_kernel_stat *out, int32_t capacity
             for (auto &kv : agg)
                 ctx->stats[kv.first] = kv.second;
         }
-        if (ctx->stats.count("plp_sweep")) {
-            auto &s = ctx->stats["plp_sweep"];
-            s.items = static_cast<double>(ds[1] + ds[2]);
-            s.bytes = 17.0 * ds[0] + 8.0 * ds[1] + 12.0 * ds[2];
-        }
-        if (ctx->stats.count("plm_move")) {
-            auto &s = ctx->stats["plm_move"];
-            s.items = static_cast<double>(ds[4] + ds[5]);
-            s.bytes = 24.0 * ds[3] + 8.0 * ds[4] + 12.0 * ds[5];
+        // per-kernel algorithmic bytes (DESIGN.md byte model), from the
+        // per-tier work counters: plp 17 B / node, plm 24 B / node, plus
+        // 8 (unweighted) or 12 (weighted) B / entry
+        static const char *slot_name[STAT_SLOTS] = {"g8",     "g16",     "g32",     "warp",  "block", "block2",
+                                                    "block3", "cluster", "hub",     "small", "fused"};
+        for (int m = 0; m < 2; ++m) {
+            const std::string base = m == 0 ? "plp_sweep" : "plm_move";
+            const double per_node = m == 0 ? 17.0 : 24.0;
+            // the hub tier runs as several kernels: time it as one family
+            KStat hub;
+            for (auto &kv : ctx->stats)
+                if (kv.first.compare(0, base.size() + 5, base + ".hub_") == 0) {
+                    hub.launches = std::max(hub.launches, kv.second.launches);
+                    hub.total_ms += kv.second.total_ms;
+                }
+            if (hub.total_ms > 0)
+                ctx->stats[base + ".hub"] = hub;
+            double tb = 0.0, ti = 0.0;
+            for (int sl = 0; sl < STAT_SLOTS; ++sl) {
+                const unsigned long long *c = ds + m * STAT_MODE_STRIDE + 3 * sl;
+                const double bytes = per_node * c[0] + 8.0 * c[1] + 12.0 * c[2];
+                const double items = static_cast<double>(c[1] + c[2]);
+                tb += bytes;
+                ti += items;
+                auto it = ctx->stats.find(base + "." + slot_name[sl]);
+                if (it != ctx->stats.end()) {
+                    it->second.bytes = bytes;
+                    it->second.items = items;
+                }
+            }
+            auto it = ctx->stats.find(base);
+            if (it != ctx->stats.end()) {
+                it->second.bytes = tb;
+                it->second.items = ti;
+            }
         }
         int32_t i = 0;
         for (auto &kv : ctx->stats) {

@@ -66,9 +66,9 @@ struct cd_ctx {
     std::vector<cudaEvent_t> free_events;
     // small pinned staging area for scalar read-backs
     int64_t *pinned = nullptr;
-    // device work counters of the sweep families (algorithmic-byte model):
-    // [0] plp nodes, [1] plp entries (unweighted), [2] plp entries (weighted),
-    // [3] plm nodes, [4] plm entries (unweighted), [5] plm entries (weighted)
+    // device work counters of the sweep kernels (algorithmic-byte model):
+    // [mode * STAT_MODE_STRIDE + slot * 3 + {0: nodes, 1: entries unweighted,
+    // 2: entries weighted}], slot = degree tier, STAT_SLOT_SMALL or STAT_SLOT_FUSED
     unsigned long long *dstats = nullptr;
     // side streams + events used to capture independent kernels as parallel
     // branches of a CUDA graph
@@ -83,7 +83,11 @@ struct cd_ctx {
 
 namespace cdk {
 
-constexpr int DSTATS = 8;
+constexpr int STAT_SLOTS = 11;  // NUM_TIERS (9) + small + fused
+constexpr int STAT_SLOT_SMALL = 9;
+constexpr int STAT_SLOT_FUSED = 10;
+constexpr int STAT_MODE_STRIDE = 3 * STAT_SLOTS;
+constexpr int DSTATS = 2 * STAT_MODE_STRIDE;
 
 // ---------------------------------------------------------------------------
 // device buffers (stream-ordered pool allocations on the context stream)

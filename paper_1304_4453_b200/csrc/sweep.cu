@@ -343,13 +343,13 @@ __device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool 
 }
 
 // stats layout per mode: [0] nodes, [1] entries unweighted, [2] entries weighted
-__device__ __forceinline__ void flush_stats(const SweepParams &P, unsigned long long nodes,
+__device__ __forceinline__ void flush_stats(const SweepParams &P, int slot, unsigned long long nodes,
                                             unsigned long long entries) {
     nodes = warp_sum(nodes);
     entries = warp_sum(entries);
     if (lane_id() == 0 && (nodes | entries)) {
-        atomicAdd(&P.stats[0], nodes);
-        atomicAdd(&P.stats[P.w ? 2 : 1], entries);
+        atomicAdd(&P.stats[3 * slot], nodes);
+        atomicAdd(&P.stats[3 * slot + (P.w ? 2 : 1)], entries);
     }
 }
 
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, i
     direct_tier<G, MODE, VC>(P, tier, chunk, load_key(P), gw, nw, scratch[wid], q, st_n, st_e);
     q.flush(P);
     q.flush_gain(P);
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, tier, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
@@ -620,7 +620,7 @@ __global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
                         st_e);
     q.flush(P);
     q.flush_gain(P);
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, TIER_WARP, st_n, st_e);
 }
 
 #ifdef CD_PHASE_TIMING
@@ -846,7 +846,7 @@ __global__ void __launch_bounds__(NT) k_sweep_block(SweepParams P) {
         q.flush(P);
         q.flush_gain(P);
     }
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, TIER, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
@@ -1045,7 +1045,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         q.flush(P);
         q.flush_gain(P);
     }
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, TIER_CLUSTER, st_n, st_e);
 }
 
 // ---------------------------------------------------------------------------
@@ -1190,7 +1190,7 @@ __global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, Fu
         if (stop)
             break;
     }
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, STAT_SLOT_FUSED, st_n, st_e);
     if (gtid == 0) {
         F.result[0] = passes;
         F.result[1] = moves_total;
@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
         if (stop)
             break;
     }
-    flush_stats(P, st_n, st_e);
+    flush_stats(P, STAT_SLOT_SMALL, st_n, st_e);
     if (gtid == 0) {
         S.result[0] = passes;
         S.result[1] = moves_total;
@@ -1442,7 +1442,7 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
             }
         }
         if (threadIdx.x == 0)
-            atomicAdd(&P.stats[P.w ? 2 : 1], static_cast<unsigned long long>(e - s));
+            atomicAdd(&P.stats[3 * TIER_HUB + (P.w ? 2 : 1)], static_cast<unsigned long long>(e - s));
         return;
     }
     // scatter: one global reservation per (block, partition), then local slots
@@ -1596,7 +1596,7 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
             if (lane == 0) {
                 if (MODE == MODE_PLM)
                     P.hub_aux[h] = 0.0;
-                atomicAdd(&P.stats[0], 1ULL);
+                atomicAdd(&P.stats[3 * TIER_HUB], 1ULL);
             }
         }
         __syncthreads();
@@ -2098,7 +2098,7 @@ void Sweeper::enqueue(bool capture) {
     P.gain_fx = c_.mode == MODE_PLM ? gain_.p : nullptr;
     P.dense_best = c_.dense_best;
     P.dense_gain = c_.dense_gain;
-    P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : 3);
+    P.stats = ctx->dstats + (c_.mode == MODE_PLP ? 0 : STAT_MODE_STRIDE);
     P.hubs = g->hubs;
     P.chunk_hub = g->chunk_hub.p;
     P.chunk_part = g->chunk_part.p;
@@ -2282,7 +2282,7 @@ int64_t fused_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed,
     P.own_hi = static_cast<int32_t>(g->n);
     P.pre_mask = 0;
     P.mv = mv.p;
-    P.stats = ctx->dstats + (c.mode == MODE_PLP ? 0 : 3);
+    P.stats = ctx->dstats + (c.mode == MODE_PLP ? 0 : STAT_MODE_STRIDE);
     P.gain_fx = c.mode == MODE_PLM ? gain.p : nullptr;
     FusedPhase F{};
     F.K = c.buckets;
@@ -2420,7 +2420,7 @@ bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t see
     P.own_lo = 0;
     P.own_hi = static_cast<int32_t>(g->n);
     P.mv = mv.p;
-    P.stats = ctx->dstats + 3;
+    P.stats = ctx->dstats + STAT_MODE_STRIDE;
     P.gain_fx = gain.p;
     SmallPhase S{};
     S.order = order.p;
