@@ -295,6 +295,14 @@ CD_API cd_status cd_ctx_world(const cd_ctx *ctx, int32_t *rank, int32_t *size);
 CD_API cd_status cd_shard_bounds(int64_t n, const int64_t *off, int32_t nranks, int64_t *bounds);
 /* This rank's row shard of a whole graph (ranges of cd_shard_bounds). */
 CD_API cd_status cd_graph_shard(cd_ctx *ctx, const cd_graph *full, cd_graph **out);
+/* This rank's row shard of the seeded R-MAT graph (cd_graph_generate_rmat),
+ * built without ever holding the whole graph: rank r keeps the rows whose
+ * raw (pre-deduplication) adjacency splits the stream evenly, i.e.
+ * cd_shard_bounds over the raw adjacency lengths.  Collective over the
+ * context's ranks; with no communicator it is cd_graph_generate_rmat.  Both
+ * build in row chunks of bounded scratch (C5: scale 28 on one GPU). */
+CD_API cd_status cd_graph_generate_rmat_shard(cd_ctx *ctx, int32_t scale, int32_t edge_factor, double a, double b,
+                                              double c, int32_t weighted, uint64_t seed, cd_graph **out);
 
 #ifdef __cplusplus
 }

@@ -137,6 +137,7 @@ EXPORTS = [
     "cd_ensemble_config_default", "cd_ctx_create", "cd_ctx_destroy", "cd_ctx_synchronize", "cd_ctx_stream",
     "cd_ctx_set_profiling", "cd_ctx_reset_stats", "cd_ctx_kernel_stats", "cd_ctx_launch_count",
     "cd_graph_from_edges", "cd_graph_from_csr", "cd_graph_generate_planted", "cd_graph_generate_rmat",
+    "cd_graph_generate_rmat_shard",
     "cd_graph_generate_lfr", "cd_graph_get_info", "cd_graph_download", "cd_graph_destroy", "cd_modularity",
     "cd_community_volumes", "cd_compact", "cd_community_count", "cd_coarsen", "cd_prolong", "cd_combine_hashed",
     "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_plp_run", "cd_louvain_run", "cd_epp_run",
@@ -173,6 +174,7 @@ def load_library():
         "cd_graph_from_csr": [vp, i64, vp, vp, vp, vpp],
         "cd_graph_generate_planted": [vp, i64, i64, f64, f64, C.c_uint64, vpp, vp],
         "cd_graph_generate_rmat": [vp, i32, i32, f64, f64, f64, i32, C.c_uint64, vpp],
+        "cd_graph_generate_rmat_shard": [vp, i32, i32, f64, f64, f64, i32, C.c_uint64, vpp],
         "cd_graph_generate_lfr": [vp, C.POINTER(_LfrSpec), C.c_uint64, vpp, vp],
         "cd_graph_get_info": [vp, C.POINTER(_GraphInfo)], "cd_graph_download": [vp, vp, vp, vp, vp, vp],
         "cd_graph_destroy": [vp],
@@ -530,11 +532,13 @@ def generate_planted(n, k, p_in, p_out, seed=1, ctx=None):
     return Graph(h, ctx), truth[:n]
 
 
-def generate_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, weighted=False, seed=1, ctx=None):
+def generate_rmat(scale, edge_factor=16, a=0.57, b=0.19, c=0.19, weighted=False, seed=1, ctx=None, shard=False):
+    """Seeded R-MAT (DESIGN.md generators).  shard=True: collective over the
+    context's ranks; this rank's row shard, built without the whole graph."""
     ctx = _ctx(ctx)
     h = C.c_void_p()
-    _check(load_library().cd_graph_generate_rmat(ctx.h, scale, edge_factor, a, b, c, int(weighted), seed,
-                                                 C.byref(h)))
+    fn = load_library().cd_graph_generate_rmat_shard if shard else load_library().cd_graph_generate_rmat
+    _check(fn(ctx.h, scale, edge_factor, a, b, c, int(weighted), seed, C.byref(h)))
     return Graph(h, ctx)
 
 

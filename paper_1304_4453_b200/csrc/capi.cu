@@ -13,7 +13,7 @@ namespace cdk {
 cd_graph *generate_planted_dev(cd_ctx *ctx, int64_t n, int64_t k, double p_in, double p_out, uint64_t seed,
                                int32_t *truth_dev);
 cd_graph *generate_rmat_dev(cd_ctx *ctx, int scale, int edge_factor, double a, double b, double c, int weighted,
-                            uint64_t seed);
+                            uint64_t seed, bool shard);
 cd_graph *generate_lfr_dev(cd_ctx *ctx, const cd_lfr_spec &sp, uint64_t seed, int32_t *truth_dev);
 
 namespace {
@@ -421,7 +421,15 @@ cd_status cd_graph_generate_rmat(cd_ctx *ctx, int32_t scale, int32_t edge_factor
                                  int32_t weighted, uint64_t seed, cd_graph **out) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && out, CD_EINVAL, "invalid argument");
-        *out = generate_rmat_dev(ctx, scale, edge_factor, a, b, c, weighted, seed);
+        *out = generate_rmat_dev(ctx, scale, edge_factor, a, b, c, weighted, seed, false);
+    })
+}
+
+cd_status cd_graph_generate_rmat_shard(cd_ctx *ctx, int32_t scale, int32_t edge_factor, double a, double b, double c,
+                                       int32_t weighted, uint64_t seed, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out, CD_EINVAL, "invalid argument");
+        *out = generate_rmat_dev(ctx, scale, edge_factor, a, b, c, weighted, seed, true);
     })
 }
 

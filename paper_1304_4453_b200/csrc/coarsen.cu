@@ -69,6 +69,10 @@ __global__ void k_check_used(int64_t nc, const int32_t *csz, int *flag) {
 // ---------------------------------------------------------------------------
 constexpr int64_t COARSEN_DENSE_MAX = 8192;  // 64 KB of fp64 slots
 constexpr int DENSE_THREADS = 512;
+// fine entries per contraction batch (row engine scratch ~24-40 B each)
+constexpr int64_t COARSEN_CHUNK_ENTRIES = int64_t(1) << 29;
+// batched contraction: coarse rows kept from pass A up to this many bytes
+constexpr int64_t COARSEN_KEEP_BYTES = int64_t(16) << 30;
 
 __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
                                                               const int64_t *off, const int32_t *col, const float *w,
@@ -228,8 +232,81 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
     try {
         SrcCoarsen src{moff.p, mem.p, mpre.p, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, z};
         bool want_w = true;
-        cg->D = run_row_engine(ctx, src, nc, fpre.p, g->D, std::max<int64_t>(nc, 1), DUP_SUM, want_w, cg->off,
-                               cg->col, cg->w, nullptr, "coarsen");
+        const int64_t chunk = env_i64("CD_COARSEN_CHUNK_ENTRIES", COARSEN_CHUNK_ENTRIES);
+        if (g->D <= chunk) {
+            cg->D = run_row_engine(ctx, src, nc, fpre.p, g->D, std::max<int64_t>(nc, 1), DUP_SUM, want_w, cg->off,
+                                   cg->col, cg->w, nullptr, "coarsen");
+        } else {
+            // the engine's scratch is ~24-40 B per fine entry: contract in
+            // batches of coarse rows holding ~chunk fine entries each.  Pass
+            // A runs every batch, writes its row offsets and keeps its rows
+            // while they fit COARSEN_KEEP_BYTES; once the exact size is known
+            // the coarse CSR is allocated and pass B copies the kept batches
+            // and recomputes the others (a coarse graph about as large as the
+            // fine one -- R-MAT level 0 -- never exists twice)
+            const std::vector<int64_t> cut = split_rows(ctx, fpre.p, 0, nc, chunk);
+            const size_t nb = cut.size() - 1;
+            cg->off.alloc(ctx, nc + 1);
+            std::vector<DBuf<int32_t>> kcol(nb);
+            std::vector<DBuf<float>> kw(nb);
+            std::vector<int64_t> bD(nb, 0), bbase(nb, 0);
+            std::vector<char> kept(nb, 0);
+            int64_t kept_bytes = 0;
+            const int64_t keep_budget = env_i64("CD_COARSEN_KEEP_BYTES", COARSEN_KEEP_BYTES);
+            auto run_batch = [&](size_t b, DBuf<int64_t> &boff, DBuf<int32_t> &bcol, DBuf<float> &bw) {
+                const int64_t c0 = cut[b], rows = cut[b + 1] - c0;
+                int64_t pr[2];
+                CD_CUDA(cudaMemcpyAsync(&pr[0], fpre.p + c0, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+                CD_CUDA(cudaMemcpyAsync(&pr[1], fpre.p + c0 + rows, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                        ctx->stream));
+                CD_CUDA(cudaStreamSynchronize(ctx->stream));
+                DBuf<int64_t> bpre(ctx, rows + 1);
+                CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
+                          static_cast<const int64_t *>(fpre.p + c0), pr[0], int64_t(0), bpre.p);
+                SrcWindow<SrcCoarsen> win{src, c0, pr[0]};
+                bool bw_want = true;
+                return run_row_engine(ctx, win, rows, bpre.p, pr[1] - pr[0], std::max<int64_t>(nc, 1), DUP_SUM,
+                                      bw_want, boff, bcol, bw, nullptr, "coarsen");
+            };
+            int64_t D = 0;
+            for (size_t b = 0; b < nb; ++b) {
+                const int64_t c0 = cut[b], rows = cut[b + 1] - c0;
+                bbase[b] = D;
+                if (rows == 0)
+                    continue;
+                DBuf<int64_t> boff;
+                bD[b] = run_batch(b, boff, kcol[b], kw[b]);
+                CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
+                          static_cast<const int64_t *>(boff.p), int64_t(0), D, cg->off.p + c0);
+                const int64_t bytes = bD[b] * int64_t(sizeof(int32_t) + sizeof(float));
+                if (kept_bytes + bytes <= keep_budget) {
+                    kept[b] = 1;
+                    kept_bytes += bytes;
+                } else {
+                    kcol[b].release();
+                    kw[b].release();
+                }
+                D += bD[b];
+            }
+            cg->D = D;
+            cg->col.alloc(ctx, std::max<int64_t>(D, 1));
+            cg->w.alloc(ctx, std::max<int64_t>(D, 1));
+            for (size_t b = 0; b < nb; ++b) {
+                if (cut[b + 1] == cut[b] || bD[b] == 0)
+                    continue;
+                if (!kept[b]) {
+                    DBuf<int64_t> boff;
+                    run_batch(b, boff, kcol[b], kw[b]);
+                }
+                CD_CUDA(cudaMemcpyAsync(cg->col.p + bbase[b], kcol[b].p, bD[b] * sizeof(int32_t),
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+                CD_CUDA(cudaMemcpyAsync(cg->w.p + bbase[b], kw[b].p, bD[b] * sizeof(float), cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+                kcol[b].release();
+                kw[b].release();
+            }
+            CD_LAUNCH(ctx, "coarsen", k_fill_i64, 1, 32, 0, int64_t(1), D, cg->off.p + nc);
+        }
         graph_finalize(ctx, cg);
     } catch (...) {
         delete cg;

@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -118,12 +120,33 @@ struct DBuf {
         s = ctx->stream;
         n = count;
         if (count) {
+            static const bool trace = std::getenv("CD_TRACE_ALLOC") != nullptr;
+            if (trace && count * sizeof(T) >= (size_t(1) << 28)) {
+                size_t fr = 0, tot = 0;
+                cudaMemGetInfo(&fr, &tot);
+                std::fprintf(stderr, "[alloc] %.2f GB (free %.2f GB)\n", count * sizeof(T) / 1e9, fr / 1e9);
+            }
             cudaError_t e = cudaMallocAsync(reinterpret_cast<void **>(&p), count * sizeof(T), s);
+            if (e != cudaSuccess) {
+                // the pool keeps freed blocks (release threshold = max): hand
+                // them back to the device and retry once before failing
+                cudaGetLastError();
+                cudaMemPool_t pool;
+                int dev = 0;
+                if (cudaStreamSynchronize(s) == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+                    cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess &&
+                    cudaMemPoolTrimTo(pool, 0) == cudaSuccess)
+                    e = cudaMallocAsync(reinterpret_cast<void **>(&p), count * sizeof(T), s);
+            }
             if (e != cudaSuccess) {
                 p = nullptr;
                 n = 0;
                 cudaGetLastError();
-                fail(CD_ENOMEM, "device allocation of " + std::to_string(count * sizeof(T)) + " bytes failed");
+                size_t fr = 0, tot = 0;
+                cudaMemGetInfo(&fr, &tot);
+                cudaGetLastError();
+                fail(CD_ENOMEM, "device allocation of " + std::to_string(count * sizeof(T)) + " bytes failed (" +
+                                    std::to_string(fr) + " of " + std::to_string(tot) + " bytes free)");
             }
         }
     }
@@ -200,6 +223,16 @@ inline void add_stat_work(cd_ctx *ctx, const char *family, double bytes, double 
     auto &s = ctx->stats[family];
     s.bytes += bytes;
     s.items += items;
+}
+
+// integer tuning knob from the environment (default when unset / malformed)
+inline int64_t env_i64(const char *name, int64_t dflt) {
+    const char *e = std::getenv(name);
+    if (!e || !*e)
+        return dflt;
+    char *end = nullptr;
+    const long long v = std::strtoll(e, &end, 10);
+    return (end && *end == '\0') ? static_cast<int64_t>(v) : dflt;
 }
 
 inline int grid_for(int64_t items, int per_block, int cap_blocks) {

@@ -292,6 +292,8 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
     int64_t passes = 0, moves = 0;
     const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0), &passes, &moves);
     const double mv = t.stop_ms();
+    if (g->D >= BIG_GRAPH_ENTRIES)
+        graph_release_bins(g);  // room for the contraction and the coarse levels
     if (auto *L = rep.level(level)) {
         L->move_ms += mv;
         L->nodes = n;

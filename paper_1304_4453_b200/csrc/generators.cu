@@ -4,7 +4,9 @@
 //   definition is ported in oracle/commdet_oracle.c (cdo_generate_rmat /
 //   cdo_generate_lfr) so the CPU oracle sees identical bytes.
 #include <cmath>
+#include <cstring>
 
+#include "comm.cuh"
 #include "rows.cuh"
 
 namespace cdk {
@@ -116,46 +118,76 @@ cd_graph *generate_planted_dev(cd_ctx *ctx, int64_t n, int64_t k, double p_in, d
 // ---------------------------------------------------------------------------
 // R-MAT
 // ---------------------------------------------------------------------------
-__global__ void k_rmat(int64_t M, int scale, uint64_t key, uint64_t ta, uint64_t tab, uint64_t tabc, int32_t *eu,
-                       int32_t *ev, int32_t *count) {
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * blockDim.x; base < M;
-         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t e = base + threadIdx.x;
-        uint64_t u = 0, v = 0;
-        bool ok = e < M;
-        if (ok) {
-            for (int lvl = 0; lvl < scale; lvl += 2) {
-                const uint64_t r = splitmix64(key ^ (static_cast<uint64_t>(e) * 16u + static_cast<uint64_t>(lvl >> 1)));
-                for (int h = 0; h < 2 && lvl + h < scale; ++h) {
-                    const uint64_t r32 = h ? (r >> 32) : (r & 0xffffffffu);
-                    uint64_t bu, bv;
-                    if (r32 < ta) {
-                        bu = 0;
-                        bv = 0;
-                    } else if (r32 < tab) {
-                        bu = 0;
-                        bv = 1;
-                    } else if (r32 < tabc) {
-                        bu = 1;
-                        bv = 0;
-                    } else {
-                        bu = 1;
-                        bv = 1;
-                    }
-                    u = (u << 1) | bu;
-                    v = (v << 1) | bv;
-                }
-            }
-            ok = u != v;
+// Draw e of the R-MAT stream: `scale` quadrant choices from the 32-bit
+// halves of splitmix64 words (the oracle's cdo_generate_rmat).  Canonical
+// (u < v); false for a self-loop.
+struct RmatSpec {
+    int scale;
+    uint64_t key, ta, tab, tabc;
+};
+
+__device__ __forceinline__ bool rmat_draw(const RmatSpec &R, int64_t e, uint32_t &u, uint32_t &v) {
+    uint32_t a = 0, b = 0;
+    for (int lvl = 0; lvl < R.scale; lvl += 2) {
+        const uint64_t r = splitmix64(R.key ^ (static_cast<uint64_t>(e) * 16u + static_cast<uint64_t>(lvl >> 1)));
+        for (int h = 0; h < 2 && lvl + h < R.scale; ++h) {
+            const uint64_t r32 = h ? (r >> 32) : (r & 0xffffffffu);
+            const uint32_t bu = r32 >= R.tab, bv = (r32 >= R.ta && r32 < R.tab) || r32 >= R.tabc;
+            a = (a << 1) | bu;
+            b = (b << 1) | bv;
         }
-        const int32_t pos = warp_append(count, ok);
-        if (ok) {
-            eu[pos] = static_cast<int32_t>(u < v ? u : v);
-            ev[pos] = static_cast<int32_t>(u < v ? v : u);
+    }
+    u = a < b ? a : b;
+    v = a < b ? b : a;
+    return a != b;
+}
+
+// pass 1: raw adjacency length of every node (both directions, duplicates
+// included) -- an upper bound of its degree and the chunking / ownership key
+__global__ void k_rmat_degree(int64_t M, RmatSpec R, int32_t *deg) {
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < M;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t u, v;
+        if (rmat_draw(R, e, u, v)) {
+            atomicAdd(&deg[u], 1);
+            atomicAdd(&deg[v], 1);
         }
     }
 }
 
+// pass 2 (per row chunk [lo, hi)): regenerate the stream and scatter the raw
+// adjacency of the chunk's rows
+__global__ void k_rmat_scatter(int64_t M, RmatSpec R, int64_t lo, int64_t hi, unsigned long long *cursor,
+                               int32_t *rk) {
+    for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < M;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint32_t u, v;
+        if (!rmat_draw(R, e, u, v))
+            continue;
+        if (u >= lo && u < hi)
+            rk[atomicAdd(&cursor[u - lo], 1ULL)] = static_cast<int32_t>(v);
+        if (v >= lo && v < hi)
+            rk[atomicAdd(&cursor[v - lo], 1ULL)] = static_cast<int32_t>(u);
+    }
+}
+
+// global statistics of a row shard from the replicated node volumes
+__global__ void k_vol_stats(int64_t n, const double *vol, unsigned long long *acc) {
+    unsigned long long iso = 0, mx = 0;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const double x = vol[u];
+        iso += x == 0.0;
+        mx = max(mx, static_cast<unsigned long long>(__double_as_longlong(x)));  // x >= 0: bits are monotone
+    }
+    iso = __reduce_add_sync(0xffffffffu, static_cast<unsigned>(iso));
+    for (int o = 16; o > 0; o >>= 1)
+        mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane_id() == 0) {
+        atomicAdd(&acc[0], iso);
+        atomicMax(&acc[1], mx);
+    }
+}
 __global__ void k_pair_weights(int64_t n, const int64_t *off, const int32_t *col, uint64_t wkey, float *w) {
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -169,40 +201,177 @@ __global__ void k_pair_weights(int64_t n, const int64_t *off, const int32_t *col
         }
 }
 
+// Raw entries per build chunk: the row engine needs ~20 B of scratch per raw
+// entry (raw list, hash keys and values, chunk columns), so a chunk of 2^30
+// entries stays near 24 GB whatever the scale (C5: 8.6e9 entries, 9 chunks).
+constexpr int64_t RMAT_CHUNK_ENTRIES = int64_t(1) << 30;
+
+// The R-MAT graph, built in row chunks: pass 1 counts every node's raw
+// adjacency; each chunk of rows regenerates the stream, scatters its rows'
+// raw adjacency and reduces it (duplicates merged) with the row engine into
+// its slice of the CSR.  With `shard`, rank r of the context's communicator
+// builds only the rows it owns -- ranges splitting the raw adjacency evenly
+// (comm.cuh) -- with empty rows elsewhere and the global per-node state.
 cd_graph *generate_rmat_dev(cd_ctx *ctx, int scale, int edge_factor, double a, double b, double c, int weighted,
-                            uint64_t seed) {
+                            uint64_t seed, bool shard) {
     if (scale < 1 || scale > 30 || edge_factor < 1)
         fail(CD_EINVAL, "rmat: need 1 <= scale <= 30 and edge_factor >= 1");
     if (a < 0 || b < 0 || c < 0 || a + b + c > 1.0)
         fail(CD_EINVAL, "rmat: probabilities must be >= 0 with a + b + c <= 1");
     const int64_t n = int64_t(1) << scale;
     const int64_t M = static_cast<int64_t>(edge_factor) << scale;
-    const uint64_t ta = static_cast<uint64_t>(a * 4294967296.0);
-    const uint64_t tab = static_cast<uint64_t>((a + b) * 4294967296.0);
-    const uint64_t tabc = static_cast<uint64_t>((a + b + c) * 4294967296.0);
-    const uint64_t key = splitmix64(seed ^ RMAT_SALT);
-    DBuf<int32_t> eu(ctx, M), ev(ctx, M), cnt(ctx, 1);
-    cnt.zero();
-    CD_LAUNCH(ctx, "generate", k_rmat, grid_for(M, 256, ctx->num_sms * 16), 256, 0, M, scale, key, ta, tab, tabc, eu.p,
-              ev.p, cnt.p);
-    int32_t m = 0;
-    CD_CUDA(cudaMemcpyAsync(&m, cnt.p, sizeof(m), cudaMemcpyDeviceToHost, ctx->stream));
+    RmatSpec R;
+    R.scale = scale;
+    R.ta = static_cast<uint64_t>(a * 4294967296.0);
+    R.tab = static_cast<uint64_t>((a + b) * 4294967296.0);
+    R.tabc = static_cast<uint64_t>((a + b + c) * 4294967296.0);
+    R.key = splitmix64(seed ^ RMAT_SALT);
+    const int G = shard ? world_size(ctx) : 1, rank = shard ? world_rank(ctx) : 0;
+    const int gen_grid = ctx->num_sms * 16;
+
+    DBuf<int64_t> pre(ctx, n + 1);
+    {
+        DBuf<int32_t> deg(ctx, n);
+        deg.zero();
+        CD_LAUNCH(ctx, "generate", k_rmat_degree, gen_grid, 256, 0, M, R, deg.p);
+        exclusive_scan<int64_t>(ctx, n, ArrayGen<int32_t>{deg.p}, pre.p, pre.p + n);
+    }
+    int64_t lo = 0, hi = n;
+    if (G > 1) {
+        std::vector<int64_t> bnd(G + 1);
+        shard_bounds_dev(ctx, n, pre.p, G, bnd.data());
+        lo = bnd[rank];
+        hi = bnd[rank + 1];
+    }
+    int64_t praw[2];
+    CD_CUDA(cudaMemcpyAsync(&praw[0], pre.p + lo, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&praw[1], pre.p + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
-    cd_graph *g = graph_from_pairs(ctx, n, m, eu.p, ev.p, nullptr, DUP_ONE);
-    if (weighted) {
-        try {
-            g->w.alloc(ctx, std::max<int64_t>(g->D, 1));
+    const int64_t F = praw[1] - praw[0];
+    const std::vector<int64_t> cut =
+        split_rows(ctx, pre.p, lo, hi, env_i64("CD_BUILD_CHUNK_ENTRIES", RMAT_CHUNK_ENTRIES));
+    const int nchunks = static_cast<int>(cut.size()) - 1;
+
+    auto *g = new cd_graph();
+    try {
+        g->ctx = ctx;
+        g->n = n;
+        g->off.alloc(ctx, n + 1);
+        g->col.alloc(ctx, std::max<int64_t>(F, 1));  // raw bound; the merged rows fill a prefix
+        if (lo > 0)
+            CD_LAUNCH(ctx, "build", k_fill_i64, grid_for(lo, 256, ctx->num_sms * 8), 256, 0, lo, int64_t(0), g->off.p);
+        int64_t D = 0;
+        for (int k = 0; k < nchunks; ++k) {
+            const int64_t a0 = cut[k], a1 = cut[k + 1], rows = a1 - a0;
+            if (rows == 0)
+                continue;
+            int64_t pr[2];
+            CD_CUDA(cudaMemcpyAsync(&pr[0], pre.p + a0, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+            CD_CUDA(cudaMemcpyAsync(&pr[1], pre.p + a1, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+            CD_CUDA(cudaStreamSynchronize(ctx->stream));
+            const int64_t Fc = pr[1] - pr[0];
+            DBuf<int64_t> fpre(ctx, rows + 1);
+            CD_LAUNCH(ctx, "build", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
+                      static_cast<const int64_t *>(pre.p + a0), pr[0], int64_t(0), fpre.p);
+            DBuf<int32_t> rk(ctx, std::max<int64_t>(Fc, 1));
+            {
+                DBuf<int64_t> cursor(ctx, rows);
+                CD_CUDA(cudaMemcpyAsync(cursor.p, fpre.p, rows * sizeof(int64_t), cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+                CD_LAUNCH(ctx, "generate", k_rmat_scatter, gen_grid, 256, 0, M, R, a0, a1,
+                          reinterpret_cast<unsigned long long *>(cursor.p), rk.p);
+            }
+            DBuf<int64_t> off2;
+            DBuf<int32_t> col2;
+            DBuf<float> w2;
+            bool want_w = false;
+            const int64_t Dc = run_row_engine(ctx, SrcFlat{fpre.p, rk.p, nullptr}, rows, fpre.p, Fc, n, DUP_ONE,
+                                              want_w, off2, col2, w2, nullptr, "build");
+            CD_LAUNCH(ctx, "build", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
+                      static_cast<const int64_t *>(off2.p), int64_t(0), D, g->off.p + a0);
+            if (Dc)
+                CD_CUDA(cudaMemcpyAsync(g->col.p + D, col2.p, Dc * sizeof(int32_t), cudaMemcpyDeviceToDevice,
+                                        ctx->stream));
+            D += Dc;
+        }
+        CD_LAUNCH(ctx, "build", k_fill_i64, grid_for(n + 1 - hi, 256, ctx->num_sms * 8), 256, 0, n + 1 - hi, D,
+                  g->off.p + hi);
+        pre.release();
+        g->D = D;
+        if (weighted) {
+            g->w.alloc(ctx, std::max<int64_t>(D, 1));
             const uint64_t wkey = splitmix64(seed ^ WEIGHT_SALT);
             CD_LAUNCH(ctx, "generate", k_pair_weights, grid_for(n, 8, ctx->num_sms * 16), 256, 0, n,
                       static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p), wkey, g->w.p);
             g->weighted = true;
-            graph_finalize(ctx, g);
-        } catch (...) {
-            delete g;
-            throw;
         }
+        graph_finalize(ctx, g);
+        if (G > 1)
+            shard_globalize(ctx, g, lo, hi);
+    } catch (...) {
+        delete g;
+        throw;
     }
     return g;
+}
+
+// Turn a graph holding only rows [lo, hi) (finalized locally) into a row
+// shard: node volumes and loops summed over the ranks (each node's row lives
+// on one rank), m / total summed (each undirected entry is counted by the
+// rank owning its smaller endpoint), the maxima and isolated count taken from
+// the global volumes.
+void shard_globalize(cd_ctx *ctx, cd_graph *g, int64_t lo, int64_t hi) {
+    Comm *cm = ctx->comm;
+    const int G = world_size(ctx);
+    const int64_t n = g->n;
+    struct Local {
+        int64_t D, m, max_degree, nonint;
+        double total;
+    } mine{g->D, g->m, g->max_degree, g->int_weights ? 0 : 1, g->total};
+    DBuf<Local> all(ctx, G), one(ctx, 1);
+    CD_CUDA(cudaMemcpyAsync(one.p, &mine, sizeof(Local), cudaMemcpyHostToDevice, ctx->stream));
+    cm->allgather(ctx, one.p, all.p, sizeof(Local));
+    std::vector<Local> h(G);
+    CD_CUDA(cudaMemcpyAsync(h.data(), all.p, G * sizeof(Local), cudaMemcpyDeviceToHost, ctx->stream));
+    if (n) {
+        cm->allreduce_sum_f64(ctx, g->vol.p, n);
+        cm->allreduce_sum_f64(ctx, g->loop.p, n);
+    }
+    DBuf<unsigned long long> acc(ctx, 2);
+    acc.zero();
+    if (n)
+        CD_LAUNCH(ctx, "finalize", k_vol_stats, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
+                  static_cast<const double *>(g->vol.p), acc.p);
+    unsigned long long ha[2];
+    CD_CUDA(cudaMemcpyAsync(ha, acc.p, sizeof(ha), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t Dg = 0, m = 0, maxd = 0;
+    bool nonint = false;
+    double total = 0.0;
+    for (const Local &l : h) {
+        Dg += l.D;
+        m += l.m;
+        maxd = std::max(maxd, l.max_degree);
+        total += l.total;
+    }
+    // integral weights: every rank's rows integral and the global max volume
+    // below 2^31 (a local overflow implies the global one)
+    for (const Local &l : h)
+        nonint |= l.nonint != 0;
+    double max_vol;
+    std::memcpy(&max_vol, &ha[1], sizeof(double));
+    g->isolated = static_cast<int64_t>(ha[0]);
+    g->max_vol = max_vol;
+    g->m = m;
+    g->total = total;
+    g->max_degree = maxd;
+    g->int_weights = !nonint && max_vol < 2147483648.0;
+    g->rows_local = true;
+    g->shard_rank = world_rank(ctx);
+    g->shard_size = G;
+    g->own_lo = lo;
+    g->own_hi = hi;
+    g->D_global = Dg;
 }
 
 // ---------------------------------------------------------------------------

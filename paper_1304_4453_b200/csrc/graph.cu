@@ -172,6 +172,66 @@ cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, 
 }
 
 // ---------------------------------------------------------------------------
+// row batching helpers (chunked builders and contraction)
+// ---------------------------------------------------------------------------
+// chunk boundaries: first row whose raw prefix reaches an even split of
+// [pre[lo], pre[hi]) into k parts
+__global__ void k_split_rows(const int64_t *pre, int64_t lo, int64_t hi, int k, int64_t *cut) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > k)
+        return;
+    if (i == 0 || i == k) {
+        cut[i] = i == 0 ? lo : hi;
+        return;
+    }
+    const int64_t p0 = pre[lo];
+    const int64_t target = p0 + static_cast<int64_t>((static_cast<__int128>(pre[hi] - p0) * i) / k);
+    int64_t a = lo, b = hi;
+    while (a < b) {
+        const int64_t mid = (a + b) >> 1;
+        if (pre[mid] < target)
+            a = mid + 1;
+        else
+            b = mid;
+    }
+    cut[i] = a;
+}
+
+__global__ void k_rebase(int64_t cnt, const int64_t *src, int64_t sub, int64_t add, int64_t *dst) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = src[i] - sub + add;
+}
+
+__global__ void k_fill_i64(int64_t cnt, int64_t value, int64_t *dst) {
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[i] = value;
+}
+
+std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo, int64_t hi, int64_t chunk) {
+    int64_t pr[2];
+    CD_CUDA(cudaMemcpyAsync(&pr[0], pre_dev + lo, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&pr[1], pre_dev + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    chunk = std::max<int64_t>(chunk, 1);
+    const int k = static_cast<int>(std::max<int64_t>(1, (pr[1] - pr[0] + chunk - 1) / chunk));
+    std::vector<int64_t> cut(k + 1);
+    DBuf<int64_t> dcut(ctx, k + 1);
+    CD_LAUNCH(ctx, "build", k_split_rows, (k + 256) / 256, 256, 0, pre_dev, lo, hi, k, dcut.p);
+    CD_CUDA(cudaMemcpyAsync(cut.data(), dcut.p, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    // drop empty batches
+    std::vector<int64_t> out{cut[0]};
+    for (int i = 1; i <= k; ++i)
+        if (cut[i] > out.back())
+            out.push_back(cut[i]);
+    if (out.size() == 1)
+        out.push_back(hi);
+    return out;
+}
+
+// ---------------------------------------------------------------------------
 // validation of an input CSR (ranges, strictly ascending rows, weights > 0)
 // ---------------------------------------------------------------------------
 __global__ void k_validate_csr(int64_t n, int64_t D, const int64_t *off, const int32_t *col, const float *w,
@@ -366,6 +426,26 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
         g->hub_aux.zero();
     }
     g->binned = true;
+}
+
+// Drop the work decomposition (tier lists, hub scratch: ~12 B per hub entry)
+// of a graph whose move phases are over for now; graph_ensure_bins rebuilds it
+// on the next use (PLMR refinement).  Used for graphs near the device's
+// capacity, where the next level's contraction needs the room.
+void graph_release_bins(cd_graph *g) {
+    g->binned = false;
+    g->tier.release();
+    g->tlist.release();
+    g->hubs = nullptr;
+    g->n_hubs = g->n_hub_chunks = g->n_hub_parts = g->hub_entries = 0;
+    for (auto *b : {&g->chunk_hub, &g->chunk_part, &g->hub_pbits, &g->part_hub, &g->hp_cnt, &g->hp_cur,
+                    &g->hp_best_key, &g->hp_flag})
+        b->release();
+    for (auto *b : {&g->hub_pbase, &g->hp_start, &g->hp_scan})
+        b->release();
+    for (auto *b : {&g->hp_val, &g->hp_best_val, &g->hub_aux})
+        b->release();
+    g->hp_key.release();
 }
 
 }  // namespace cdk

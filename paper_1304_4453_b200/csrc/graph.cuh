@@ -136,6 +136,20 @@ enum DupMode : int { DUP_ERROR = 0, DUP_SUM = 1, DUP_ONE = 2 };
 
 // graph.cu
 void graph_finalize(cd_ctx *ctx, cd_graph *g);  // vol, loop, m, total, max degree
+// row batching: cut[i] = first row in [lo, hi] whose prefix reaches an even
+// split of [pre[lo], pre[hi]) into k parts (cut has k+1 entries)
+__global__ void k_split_rows(const int64_t *pre, int64_t lo, int64_t hi, int k, int64_t *cut);
+// dst[i] = src[i] - sub + add
+__global__ void k_rebase(int64_t cnt, const int64_t *src, int64_t sub, int64_t add, int64_t *dst);
+__global__ void k_fill_i64(int64_t cnt, int64_t value, int64_t *dst);
+// host: the row batches of [lo, hi) holding at most ~`chunk` prefix units each
+std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo, int64_t hi, int64_t chunk);
+// free the tier lists and hub scratch (rebuilt on demand by graph_ensure_bins)
+void graph_release_bins(cd_graph *g);
+// graphs at least this large drop their work decomposition between phases
+constexpr int64_t BIG_GRAPH_ENTRIES = int64_t(1) << 31;
+// rows [lo, hi) built and finalized locally -> row shard with global node state
+void shard_globalize(cd_ctx *ctx, cd_graph *g, int64_t lo, int64_t hi);
 void graph_ensure_bins(cd_ctx *ctx, cd_graph *g);
 cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, const int32_t *v, const float *w,
                            DupMode mode);  // device arrays; symmetrises

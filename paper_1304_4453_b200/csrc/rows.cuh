@@ -120,6 +120,21 @@ struct SrcCoarsen {
     }
 };
 
+// rows [r0, r0 + rows) of another source, renumbered from 0, with flat
+// entry indices rebased by f0 (= the source's prefix at r0): one batch of a
+// row engine run split to bound its scratch
+template <class Src>
+struct SrcWindow {
+    Src s;
+    int64_t r0, f0;
+    using Cursor = typename Src::Cursor;
+    __device__ Cursor init(int64_t r, int64_t f) const { return s.init(r + r0, f + f0); }
+    __device__ void load(int64_t r, int64_t f, int64_t fend, Cursor &cur, int32_t &k, double &wt,
+                         bool &valid) const {
+        s.load(r + r0, f + f0, fend + f0, cur, k, wt, valid);
+    }
+};
+
 // -------------------------------------------------------------------------
 // warp aggregation: lanes with equal keys combine; the lowest lane of each
 // group is the leader and receives the group's weight sum (summed in lane

@@ -212,3 +212,59 @@ def test_sharded_tiny_graphs_more_ranks_than_nodes(dev, layout):
         for res in run_ranks(dev, 4, fn):
             for a in z1:
                 assert np.array_equal(res[a], z1[a]), (n, a)
+
+
+def _info(g):
+    return (g.node_count(), g.edge_count(), g.total_edge_weight(), g.max_degree, g.isolated)
+
+
+@pytest.mark.parametrize("weighted", [False, True])
+def test_rmat_chunked_builder(dev, monkeypatch, weighted):
+    """The R-MAT builder in many row chunks (CD_BUILD_CHUNK_ENTRIES) gives the
+    same CSR as the one-chunk build (which the oracle pins bit-exactly)."""
+    ctx = dev.Context(0)
+    try:
+        ref = dev.generate_rmat(12, 8, weighted=weighted, seed=4, ctx=ctx).csr()
+        for chunk in ("7000", "1"):
+            monkeypatch.setenv("CD_BUILD_CHUNK_ENTRIES", chunk)
+            c = dev.generate_rmat(12, 8, weighted=weighted, seed=4, ctx=ctx).csr()
+            for key in ref:
+                np.testing.assert_array_equal(c[key], ref[key], err_msg=f"{key} chunk={chunk}")
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_generated_rmat_shard(dev, monkeypatch, G):
+    """cd_graph_generate_rmat_shard: every rank builds only its rows (in
+    several chunks here); the rows, node state and graph totals equal the
+    whole graph's, and PLM / PLP over the generated shards give the one-device
+    labels."""
+    monkeypatch.setenv("CD_BUILD_CHUNK_ENTRIES", "20000")
+    ctx0 = dev.Context(0)
+    g1 = dev.generate_rmat(13, 8, seed=6, ctx=ctx0)
+    full, info1 = g1.csr(), _info(g1)
+    zm, _ = dev.run_plm(g1, dev.LouvainConfig(seed=7))
+    zp, _ = dev.run_plp(g1, dev.PlpConfig(randomize_order=True, seed=7))
+    zm, zp = np.array(zm), np.array(zp)
+    ctx0.close()
+
+    def fn(ctx, r):
+        g = dev.generate_rmat(13, 8, seed=6, ctx=ctx, shard=True)
+        assert g.is_shard
+        lo, hi = g.owned_range
+        c = g.csr()
+        deg = np.diff(c["off"])
+        assert np.all(deg[:lo] == 0) and np.all(deg[hi:] == 0)
+        assert np.array_equal(c["col"], full["col"][full["off"][lo]:full["off"][hi]])
+        np.testing.assert_array_equal(c["vol"], full["vol"])
+        assert _info(g) == info1
+        z1 = np.array(dev.run_plm(g, dev.LouvainConfig(seed=7))[0])
+        z2 = np.array(dev.run_plp(g, dev.PlpConfig(randomize_order=True, seed=7))[0])
+        return lo, hi, z1, z2
+
+    res = run_ranks(dev, G, fn)
+    assert res[0][0] == 0 and res[-1][1] == info1[0]
+    assert all(res[i][1] == res[i + 1][0] for i in range(G - 1))
+    for _, _, z1, z2 in res:
+        assert np.array_equal(z1, zm) and np.array_equal(z2, zp)
