@@ -62,9 +62,17 @@ WORKLOADS = {
                             desc="PLMR on weighted R-MAT scale 22 ef 16"),
     "c4_rmat22w_epp": dict(gen="rmat", scale=22, weighted=True, algo="epp", seed=1,
                            desc="EPP(4,PLP,PLMR) on weighted R-MAT scale 22 ef 16"),
+    # BASELINE.json configs[4]: 8.5e9 entries; fits one B200 through the
+    # chunked builder / batched contraction, row shards built per rank at N > 1
+    "c5_rmat28_plm": dict(gen="rmat", scale=28, weighted=False, algo="plm", seed=1, cpu=False,
+                          desc="PLM on R-MAT scale 28 ef 16 (0.57,0.19,0.19,0.05), int64 offsets"),
+    "c5_rmat28_plp": dict(gen="rmat", scale=28, weighted=False, algo="plp", seed=1, cpu=False,
+                          desc="PLP on R-MAT scale 28 ef 16"),
 }
 # graphs whose multi-GPU mode is one sharded graph rather than replicas
-SHARDED_BY_DEFAULT = {"c3_rmat24_plp", "c3_rmat24_plm"}
+SHARDED_BY_DEFAULT = {"c3_rmat24_plp", "c3_rmat24_plm", "c5_rmat28_plm", "c5_rmat28_plp"}
+# the reference is infeasible there (~240 GB RAM, hours)
+NO_CPU_REASON = "reference infeasible at R-MAT scale 28 (SURVEY.md 8(d): ~240 GB host RAM, hours per run)"
 
 
 def parse():
@@ -147,7 +155,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def make_device_graph(P, ctx, wl):
+def make_device_graph(P, ctx, wl, shard=False):
+    """shard: this rank's row shard (R-MAT shards are generated directly,
+    never holding the whole graph; other graphs are cut from the whole)."""
+    if shard and wl["gen"] == "rmat":
+        return P.generate_rmat(wl["scale"], 16, 0.57, 0.19, 0.19, weighted=wl["weighted"], seed=wl["seed"], ctx=ctx,
+                               shard=True)
+    if shard:
+        return make_device_graph(P, ctx, wl).shard(ctx)
     if wl["gen"] == "lfr":
         g, _ = P.generate_lfr(seed=wl["seed"], ctx=ctx, **LFR_C2)
     elif wl["gen"] == "planted":
@@ -205,6 +220,9 @@ def bench_reference(args, wl):
     if not O.ref_available():
         emit({"impl": "reference", "unavailable": "oracle/_ref/libcommdet_ref.so not built"})
         return 0
+    if wl.get("cpu") is False:
+        emit({"impl": "reference", "unavailable": NO_CPU_REASON})
+        return 0
     og = make_oracle_graph(O, wl)
     rg = O.RefGraph.from_csr(og)
     threads = cpu_threads()
@@ -260,10 +278,8 @@ def bench_b200(args, wl):
         if dist:
             dist.broadcast_object_list(uid, src=0)
         ctx.attach_nccl(world, rank, uid[0])
-    g = make_device_graph(P, ctx, wl)
-    if mode == "rows":
-        g = g.shard(ctx)
-    n, m = g.node_count(), g.edge_count()
+    g = make_device_graph(P, ctx, wl, shard=mode == "rows")
+    n, m, entries = g.node_count(), g.edge_count(), g.entries
     units = 1 if sharded else world  # graphs processed per step, all ranks
     out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
@@ -356,6 +372,8 @@ def bench_b200(args, wl):
     # ---- end to end through the C ABI with host buffers ----------------------------
     # (a row shard uploads the whole CSR and cuts its rows on the device)
     c = make_device_graph(P, ctx, wl).csr() if mode == "rows" else g.csr()
+    if entries >= 1 << 31:  # C5: room on the device for the uploaded copy
+        g = None
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
     h_off, h_col = pin(c["off"]), pin(c["col"])
     h_w = pin(c["w"]) if c["w"] is not None else None
@@ -387,7 +405,10 @@ def bench_b200(args, wl):
 
     # ---- CPU baseline: the reference on identical bytes (rank 0, N = 1) -----------
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if wl.get("cpu") is False:
+        cpu = {"value": None, "unit": "edges/s", "cores": cpu_threads(), "kind": "reference",
+               "sample": "skipped: " + NO_CPU_REASON}
+    elif rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             from oracle import oracle as O
             if O.ref_available():
@@ -416,7 +437,7 @@ def bench_b200(args, wl):
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "int32+f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "desc": wl["desc"], "n": n, "m": m, "entries": g.entries,
+            "config": {"workload": args.workload, "desc": wl["desc"], "n": n, "m": m, "entries": entries,
                        "algo": wl["algo"], "seed": wl["seed"],
                        "parallelism": f"{mode} x{world}" if mode != "1gpu" else "1gpu",
                        "l2": "flushed (256 MiB write) before every timed step",
