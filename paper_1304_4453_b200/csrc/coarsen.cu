@@ -171,7 +171,7 @@ __global__ void k_dense_copy(int64_t nc, const int64_t *fpre, const int64_t *off
     }
 }
 
-cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc) {
+cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
     const int64_t n = g->n;
     const int grid = grid_for(n, 256, ctx->num_sms * 8);
     DBuf<int32_t> csz(ctx, std::max<int64_t>(nc, 1));
@@ -235,7 +235,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
         const int64_t chunk = env_i64("CD_COARSEN_CHUNK_ENTRIES", COARSEN_CHUNK_ENTRIES);
         if (g->D <= chunk) {
             cg->D = run_row_engine(ctx, src, nc, fpre.p, g->D, std::max<int64_t>(nc, 1), DUP_SUM, want_w, cg->off,
-                                   cg->col, cg->w, nullptr, "coarsen");
+                                   cg->col, cg->w, nullptr, "coarsen", sorted);
         } else {
             // the engine's scratch is ~24-40 B per fine entry: contract in
             // batches of coarse rows holding ~chunk fine entries each.  Pass
@@ -266,7 +266,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
                 SrcWindow<SrcCoarsen> win{src, c0, pr[0]};
                 bool bw_want = true;
                 return run_row_engine(ctx, win, rows, bpre.p, pr[1] - pr[0], std::max<int64_t>(nc, 1), DUP_SUM,
-                                      bw_want, boff, bcol, bw, nullptr, "coarsen");
+                                      bw_want, boff, bcol, bw, nullptr, "coarsen", sorted);
             };
             int64_t D = 0;
             for (size_t b = 0; b < nb; ++b) {

@@ -306,7 +306,7 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
         const int64_t k = compact_dev(ctx, n, z, n, zc.p);  // :248
         if (k < n) {                                        // :249
             t.start();
-            cd_graph *coarse = coarsen_sharded_dev(ctx, g, zc.p, k);  // :251
+            cd_graph *coarse = coarsen_sharded_dev(ctx, g, zc.p, k, false);  // :251 (rows unsorted)
             const double cm = t.stop_ms();
             if (auto *L = rep.level(level))
                 L->coarsen_ms += cm;
@@ -402,7 +402,7 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     const double combine_ms = t.stop_ms();
     // coarsen (:167-169)
     t.start();
-    cd_graph *coarse = coarsen_sharded_dev(ctx, g, core.p, k);
+    cd_graph *coarse = coarsen_sharded_dev(ctx, g, core.p, k, false);
     const double coarsen_ms = t.stop_ms();
     double final_ms = 0.0;
     try {

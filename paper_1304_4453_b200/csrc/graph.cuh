@@ -165,7 +165,7 @@ void graph_ensure_transpose(cd_ctx *ctx, cd_graph *g);         // toff / tcol of
 // ownership range of this rank on a replicated graph (whole graph on one device)
 void owned_range(cd_ctx *ctx, const cd_graph *g, int64_t &lo, int64_t &hi);
 // sum of the row-shard partial coarse graphs of all ranks (replicated result)
-cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc);
+cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted = true);
 
 // quality.cu
 void community_volumes_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, double *vols, int64_t ub);
@@ -183,7 +183,9 @@ void prolong_dev(cd_ctx *ctx, int64_t nc, const int32_t *zc, int64_t n, const in
 int64_t combine_hashed_dev(cd_ctx *ctx, int64_t b, int64_t n, const int32_t *const *sols_dev, int32_t *out);
 void iota_dev(cd_ctx *ctx, int32_t *z, int64_t n);
 
-// coarsen.cu
-cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc);
+// coarsen.cu.  sorted: rows ascending (the reference's CSR convention, the
+// API); the detectors pass false -- their tallies do not depend on row order
+// and the per-row sort is a third of a large contraction
+cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted = true);
 
 }  // namespace cdk

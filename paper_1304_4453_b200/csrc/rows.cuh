@@ -340,7 +340,15 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
     }
 }
 
-// global tier: grid over chunks of ENG_GLOBAL_CHUNK entries of the big rows
+// global tier: grid over chunks of ENG_GLOBAL_CHUNK entries of the big rows.
+// A block first combines its chunk in a small shared-memory table (a row
+// with few distinct keys -- a coarse level's giant communities -- would
+// otherwise hammer the same global slots with atomics from every block),
+// then inserts each distinct key once into the row's global table.  Keys
+// that find no smem slot within a few probes go to the global table directly.
+constexpr int ENG_PRE_CAP = 2048;
+constexpr int ENG_PRE_PROBES = 8;
+
 template <class Src>
 static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src, const int64_t *fpre,
                                                                   const int32_t *rows, int64_t nrows,
@@ -348,6 +356,9 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
                                                                   const int64_t *tab_cap, int32_t *gkeys,
                                                                   double *gvals, uint32_t *gcnts) {
     __shared__ double scratch[8][32];
+    __shared__ int32_t pk[ENG_PRE_CAP];
+    __shared__ double pv[ENG_PRE_CAP];
+    __shared__ uint32_t pc[ENG_PRE_CAP];
     const int wid = threadIdx.x >> 5;
     const int64_t j = blockIdx.x;
     // row index: largest i with chunk_pre[i] <= j
@@ -359,6 +370,12 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
         else
             hi = mid - 1;
     }
+    for (int t = threadIdx.x; t < ENG_PRE_CAP; t += blockDim.x) {
+        pk[t] = EMPTY_KEY;
+        pv[t] = 0.0;
+        pc[t] = 0;
+    }
+    __syncthreads();
     const int64_t r = rows[lo];
     const int64_t f1r = fpre[r + 1];
     const int64_t cstart = fpre[r] + (j - chunk_pre[lo]) * ENG_GLOBAL_CHUNK;
@@ -366,23 +383,40 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
     const int64_t per = ENG_GLOBAL_CHUNK / 8;
     const int64_t a = cstart + wid * per;
     const int64_t b = min(cend, a + per);
-    if (a >= b)
-        return;
     int32_t *keys = gkeys + tab_off[lo];
     double *vals = gvals + tab_off[lo];
     uint32_t *cnts = gcnts + tab_off[lo];
     const uint32_t mask = static_cast<uint32_t>(tab_cap[lo] - 1);
-    auto cur = src.init(r, a);
-    for (int64_t f = a; f < b; f += 32) {
-        int32_t k;
-        double w;
-        bool valid;
-        src.load(r, f, b, cur, k, w, valid);
-        double sum;
-        uint32_t cnt;
-        if (warp_aggregate(k, w, valid, 0xffffffffu, scratch[wid], sum, cnt))
-            table_insert(keys, vals, cnts, mask, k, sum, cnt);
+    if (a < b) {
+        auto cur = src.init(r, a);
+        for (int64_t f = a; f < b; f += 32) {
+            int32_t k;
+            double w;
+            bool valid;
+            src.load(r, f, b, cur, k, w, valid);
+            double sum;
+            uint32_t cnt;
+            if (warp_aggregate(k, w, valid, 0xffffffffu, scratch[wid], sum, cnt)) {
+                uint32_t sl = hash_slot(k, ENG_PRE_CAP - 1);
+                bool done = false;
+                for (int p = 0; p < ENG_PRE_PROBES && !done; ++p) {
+                    const int32_t old = atomicCAS(&pk[sl], EMPTY_KEY, k);
+                    if (old == EMPTY_KEY || old == k) {
+                        atomicAdd(&pv[sl], sum);
+                        atomicAdd(&pc[sl], cnt);
+                        done = true;
+                    }
+                    sl = (sl + 1) & (ENG_PRE_CAP - 1);
+                }
+                if (!done)
+                    table_insert(keys, vals, cnts, mask, k, sum, cnt);
+            }
+        }
     }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ENG_PRE_CAP; t += blockDim.x)
+        if (pk[t] != EMPTY_KEY)
+            table_insert(keys, vals, cnts, mask, pk[t], pv[t], pc[t]);
 }
 
 static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const int64_t *fpre, const int32_t *rows,
@@ -692,6 +726,48 @@ static __global__ void __launch_bounds__(1024) k_eng_sort_radix(const int64_t *f
     }
 }
 
+// Unsorted output (contraction inside the detectors, where row order is
+// irrelevant): the reduced rows are copied as they are.  Blocks own
+// ENG_COPY_CHUNK consecutive output entries; each thread finds its row by a
+// binary search over the block's row range.
+constexpr int64_t ENG_COPY_CHUNK = 4096;
+
+static __global__ void __launch_bounds__(256) k_eng_copy_rows(int64_t nrows, const int64_t *fpre, const int64_t *off2,
+                                                              int64_t D2, const int32_t *tkey, const double *tval,
+                                                              int32_t *col, float *wout) {
+    __shared__ int64_t rng[2];
+    const int64_t begin = static_cast<int64_t>(blockIdx.x) * ENG_COPY_CHUNK;
+    const int64_t end = min(D2, begin + ENG_COPY_CHUNK);
+    if (threadIdx.x < 2) {
+        // last row with off2[row] <= (begin | end - 1)
+        const int64_t target = threadIdx.x == 0 ? begin : end - 1;
+        int64_t lo = 0, hi = nrows - 1;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (off2[mid] <= target)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        rng[threadIdx.x] = lo;
+    }
+    __syncthreads();
+    for (int64_t i = begin + threadIdx.x; i < end; i += blockDim.x) {
+        int64_t lo = rng[0], hi = rng[1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi + 1) >> 1;
+            if (off2[mid] <= i)
+                lo = mid;
+            else
+                hi = mid - 1;
+        }
+        const int64_t src = fpre[lo] + (i - off2[lo]);
+        col[i] = tkey[src];
+        if (wout)
+            wout[i] = static_cast<float>(tval[src]);
+    }
+}
+
 // ---- row classification ------------------------------------------------------
 
 // classify rows by source length (reduce) or distinct length (sort)
@@ -764,7 +840,7 @@ static __global__ void k_cap_from_prefix(int64_t m, const int64_t *pre, const in
 template <class Src>
 int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t *fpre, int64_t F_total,
                        int64_t key_bound, DupMode mode, bool &want_w, DBuf<int64_t> &off2, DBuf<int32_t> &col,
-                       DBuf<float> &wout, bool *dup, const char *family) {
+                       DBuf<float> &wout, bool *dup, const char *family, bool sort_rows = true) {
     // per-phase profiler families "<family>.<phase>" (cd_ctx_kernel_stats sums them)
     const std::string fam(family);
     const std::string f_cls = fam + ".classify", f_red = fam + ".reduce", f_glob = fam + ".reduce_global",
@@ -857,6 +933,14 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         wout.alloc(ctx, std::max<int64_t>(D2, 1));
     else
         wout.alloc(ctx, 0);
+    if (!sort_rows) {
+        if (D2 > 0)
+            CD_LAUNCH(ctx, f_sort.c_str(), k_eng_copy_rows, static_cast<int>((D2 + ENG_COPY_CHUNK - 1) / ENG_COPY_CHUNK),
+                      256, 0, nrows, fpre, static_cast<const int64_t *>(off2.p), D2,
+                      static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p), col.p,
+                      want_w ? wout.p : static_cast<float *>(nullptr));
+        return D2;
+    }
     // sort phase: classify by distinct length
     counts.zero();
     CD_LAUNCH(ctx, f_cls.c_str(), k_eng_classify, cls_blocks, 256, 0, nrows, static_cast<const int64_t *>(nullptr),

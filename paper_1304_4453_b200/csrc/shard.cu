@@ -186,12 +186,12 @@ __global__ void k_stack_fpre(int64_t nc, const int64_t *roff, int G, int64_t ost
     }
 }
 
-cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc) {
+cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
     Comm *comm = ctx->comm;
     const int G = world_size(ctx);
     if (!g->rows_local || G == 1)
-        return coarsen_dev(ctx, g, z, nc);
-    cd_graph *part = coarsen_dev(ctx, g, z, nc);  // this rank's rows only
+        return coarsen_dev(ctx, g, z, nc, sorted);
+    cd_graph *part = coarsen_dev(ctx, g, z, nc, false);  // this rank's rows only (merged below)
     cd_graph *cg = nullptr;
     try {
         DBuf<int64_t> dcount(ctx, 1), rcount(ctx, G);
@@ -230,7 +230,7 @@ cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, 
         SrcStack src{roff.p, rcol.p, rw.p, fpre.p, G, ostride, maxd};
         bool want_w = true;
         cg->D = run_row_engine(ctx, src, nc, fpre.p, ftotal, std::max<int64_t>(nc, 1), DUP_SUM, want_w, cg->off,
-                               cg->col, cg->w, nullptr, "coarsen");
+                               cg->col, cg->w, nullptr, "coarsen", sorted);
         graph_finalize(ctx, cg);
     } catch (...) {
         delete part;

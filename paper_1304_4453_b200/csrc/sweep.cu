@@ -1937,29 +1937,37 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const int grid = warps_grid_k(kfn, per, 128, ch);
         CD_TIER_LAUNCH(kfn, grid, 128, 0, P, ch);
     }
-    if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
-        fam = names[MODE][TIER_BLOCK];
-        const size_t smem = size_t(BLOCK_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(BLOCK_TABLE_CAP / 2) * sizeof(uint16_t);
-        static bool attr = false;
+    // block tiers: one block per node; the block size trades threads per
+    // node against nodes in flight per SM (env CD_BLOCK_NT / CD_BLOCK2_NT)
+    auto block_tier = [&](auto kfn, int tier, int nt, uint32_t cap, bool &attr) {
+        fam = names[MODE][tier];
+        const size_t smem = size_t(cap) * (sizeof(V) + sizeof(int32_t)) + size_t(cap / 2) * sizeof(uint16_t);
         if (!attr) {
-            set_smem(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>, smem);
+            set_smem(kfn, smem);
             attr = true;
         }
-        const int nb = grid_for(pre_count(P, TIER_BLOCK, P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK]), 1,
-                                wave((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), SW_BLOCK_THREADS, smem));
-        CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK>), nb, SW_BLOCK_THREADS, smem, P);
+        const int nb = grid_for(pre_count(P, tier, P.tend[tier] - P.tbeg[tier]), 1, wave(kfn, nt, smem));
+        CD_TIER_LAUNCH(kfn, nb, nt, smem, P);
+    };
+    static const int block_nt = static_cast<int>(env_i64("CD_BLOCK_NT", 256));
+    static const int block2_nt = static_cast<int>(env_i64("CD_BLOCK2_NT", 512));
+    if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
+        static bool a128 = false, a256 = false;
+        if (block_nt == 128)
+            block_tier(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK, 128>, TIER_BLOCK, 128, BLOCK_TABLE_CAP,
+                       a128);
+        else
+            block_tier(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK, 256>, TIER_BLOCK, 256, BLOCK_TABLE_CAP,
+                       a256);
     }
     if ((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2])) {
-        fam = names[MODE][TIER_BLOCK2];
-        const size_t smem = size_t(BLOCK2_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(BLOCK2_TABLE_CAP / 2) * sizeof(uint16_t);
-        static bool attr2 = false;
-        if (!attr2) {
-            set_smem(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>, smem);
-            attr2 = true;
-        }
-        const int nb = grid_for(pre_count(P, TIER_BLOCK2, P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2]), 1,
-                                wave((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), SW_BLOCK_THREADS, smem));
-        CD_TIER_LAUNCH((k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2>), nb, SW_BLOCK_THREADS, smem, P);
+        static bool a256 = false, a512 = false;
+        if (block2_nt == 512)
+            block_tier(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2, 512>, TIER_BLOCK2, 512,
+                       BLOCK2_TABLE_CAP, a512);
+        else
+            block_tier(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2, 256>, TIER_BLOCK2, 256,
+                       BLOCK2_TABLE_CAP, a256);
     }
     if ((P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3])) {
         fam = names[MODE][TIER_BLOCK3];
