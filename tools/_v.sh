@@ -1,4 +1,6 @@
-for v in "X=1" "CD_BLOCK_NT=128" "CD_BLOCK2_NT=512" "CD_BLOCK_NT=128 CD_BLOCK2_NT=512"; do
-  echo "=== $v"
-  env $v python tools/prof_run.py --workload c3_rmat24_plm --runs 3 --families 2>&1 | grep -E "run 2|plm_move\.(block|block2) "
+for lib in build/libh4.so "" build/libh1.so; do
+  echo "=== ${lib:-fmix}"
+  for w in c2_lfr_plm c3_rmat24_plm c3_rmat24_plp c4_rmat22w_plmr c1_planted_plm; do
+    COMMDET_CUDA_LIB=$lib python tools/prof_run.py --workload $w --runs 4 2>&1 | grep "run 3" | awk '{print $1, $9, $10, $11, $12}'
+  done
 done
