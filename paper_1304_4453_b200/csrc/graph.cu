@@ -318,12 +318,6 @@ struct HubChunkGen {
     }
 };
 
-__host__ __device__ inline int hub_pbits_of(int64_t d) {
-    int b = 0;
-    while ((int64_t(HUB_PART) << b) < d && b < HUB_MAX_PBITS)
-        ++b;
-    return b;
-}
 
 struct HubPartGen {
     const int32_t *hubs;

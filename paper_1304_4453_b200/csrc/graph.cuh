@@ -39,6 +39,13 @@ constexpr int HUB_CHUNK = 4096;         // entries per hub chunk block
 constexpr int HUB_PART = 512;           // target pairs per hub partition
 constexpr int HUB_PART_CAP = 2048;      // smem slots of a partition block (4x HUB_PART)
 constexpr int HUB_MAX_PBITS = 13;       // partitions per hub <= 8192 (smem histogram)
+// partitions of a hub of degree d: 2^bits with HUB_PART << bits >= d
+__host__ __device__ inline int hub_pbits_of(int64_t d) {
+    int b = 0;
+    while ((int64_t(HUB_PART) << b) < d && b < HUB_MAX_PBITS)
+        ++b;
+    return b;
+}
 
 constexpr int64_t CLUSTER_MAX_DEG = 32768;
 

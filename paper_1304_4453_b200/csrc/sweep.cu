@@ -2012,14 +2012,18 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if (P.tend[TIER_HUB] > P.tbeg[TIER_HUB]) {
         fam = names[MODE][TIER_HUB];
+        // histograms sized for this graph's largest hub (the attribute once
+        // for the largest possible): the scatter kernel's occupancy is set
+        // by its shared memory
         const int max_np = 1 << HUB_MAX_PBITS;
-        const size_t smem_count = size_t(max_np) * sizeof(int32_t);
-        const size_t smem_scatter = size_t(HUB_PAIRS_SMEM) + 2 * size_t(max_np) * sizeof(int32_t);
+        const int np = 1 << hub_pbits_of(g->max_degree);
+        const size_t smem_count = size_t(np) * sizeof(int32_t);
+        const size_t smem_scatter = size_t(HUB_PAIRS_SMEM) + 2 * size_t(np) * sizeof(int32_t);
         const size_t smem_part = size_t(HUB_PART_CAP) * (sizeof(V) + sizeof(int32_t));
         static bool attr = false;
         if (!attr) {
-            set_smem(k_hub_pairs<MODE, VC, false>, smem_count);
-            set_smem(k_hub_pairs<MODE, VC, true>, smem_scatter);
+            set_smem(k_hub_pairs<MODE, VC, false>, size_t(max_np) * sizeof(int32_t));
+            set_smem(k_hub_pairs<MODE, VC, true>, size_t(HUB_PAIRS_SMEM) + 2 * size_t(max_np) * sizeof(int32_t));
             set_smem(k_hub_part<MODE, VC>, smem_part);
             attr = true;
         }

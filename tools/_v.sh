@@ -1,6 +1,6 @@
-for lib in build/libh4.so "" build/libh1.so; do
-  echo "=== ${lib:-fmix}"
-  for w in c2_lfr_plm c3_rmat24_plm c3_rmat24_plp c4_rmat22w_plmr c1_planted_plm; do
-    COMMDET_CUDA_LIB=$lib python tools/prof_run.py --workload $w --runs 4 2>&1 | grep "run 3" | awk '{print $1, $9, $10, $11, $12}'
+for v in "move_qtol=1e-3" "move_qtol=3e-4" "move_qtol=3e-3" "move_qtol=1e-2"; do
+  echo "=== $v"
+  for w in c3_rmat24_plm c2_lfr_plm c4_rmat22w_plmr; do
+    python tools/prof_run.py --workload $w --runs 3 --set $v 2>&1 | grep "run 2" | cut -c1-260
   done
 done
