@@ -75,9 +75,10 @@ constexpr int64_t COARSEN_CHUNK_ENTRIES = int64_t(1) << 29;
 constexpr int64_t COARSEN_KEEP_BYTES = int64_t(16) << 30;
 
 __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
-                                                              const int64_t *off, const int32_t *col, const float *w,
-                                                              const int32_t *z, const int64_t *fpre, int32_t *tkey,
-                                                              double *tval, int64_t *deg2) {
+                                                              const int64_t *mpre, const int64_t *off,
+                                                              const int32_t *col, const float *w, const int32_t *z,
+                                                              const int64_t *fpre, int32_t *tkey, double *tval,
+                                                              int64_t *deg2) {
     extern __shared__ double acc[];
     __shared__ int wsum[DENSE_THREADS / 32 + 1];
     __shared__ double scr[DENSE_THREADS / 32][32];
@@ -93,19 +94,22 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const 
         // (most entries: the community's internal weight) is summed in
         // registers; other labels combine per warp (match_any) before the
         // shared-memory atomic.
+        // The members' rows are enumerated flat (SrcCoarsen): a warp takes 32
+        // consecutive entries of the concatenated rows per step, so short
+        // member rows do not leave most lanes idle behind a chain of
+        // dependent loads per member.
         double self = 0.0;
-        for (int64_t p = moff[c] + wid; p < moff[c + 1]; p += NW) {
-            const int32_t u = mem[p];
-            const int64_t e0 = off[u], e1 = off[u + 1];
-            for (int64_t base = e0; base < e1; base += 32) {
-                const int64_t e = base + lane;
-                bool valid = e < e1;
-                const int32_t v = valid ? col[e] : 0;
-                const int32_t k = valid ? z[v] : -1;
-                const double wt = valid ? (w ? static_cast<double>(w[e]) : 1.0) : 0.0;
-                if (k == static_cast<int32_t>(c)) {
-                    if (v >= u)
-                        self += wt;
+        const SrcCoarsen src{moff, mem, mpre, off, col, w, z};
+        const int64_t fb = fpre[c], fe = fpre[c + 1];
+        if (fb + wid * 32 < fe) {
+            auto cur = src.init(c, fb + wid * 32);
+            for (int64_t f0 = fb + wid * 32; f0 < fe; f0 += NW * 32) {
+                int32_t k;
+                double wt;
+                bool valid;
+                src.load(c, f0, fe, cur, k, wt, valid);
+                if (valid && k == static_cast<int32_t>(c)) {
+                    self += wt;
                     valid = false;
                 }
                 double sum;
@@ -209,7 +213,8 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
             CD_LAUNCH(ctx, "coarsen.dense", k_dense_rows,
                       grid_for(nc, 1, std::max(1, per_sm) * ctx->num_sms), DENSE_THREADS, smem, nc,
                       static_cast<const int64_t *>(moff.p), static_cast<const int32_t *>(mem.p),
-                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                      static_cast<const int64_t *>(mpre.p), static_cast<const int64_t *>(g->off.p),
+                      static_cast<const int32_t *>(g->col.p),
                       static_cast<const float *>(g->weighted ? g->w.p : nullptr), z,
                       static_cast<const int64_t *>(fpre.p), tkey.p, tval.p, deg2.p);
             cg->off.alloc(ctx, nc + 1);
