@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -81,6 +82,11 @@ struct cd_ctx {
     bool use_graphs = true;
     // sharded execution (comm.cuh); nullptr = one device, no exchange
     cdk::Comm *comm = nullptr;
+    // child context of a concurrent run on the same device (EPP bases): the
+    // per-sub-sweep hub scratch is private to the context, keyed by graph
+    // (graph.cuh hub_scratch_for); everything else a run writes is its own
+    bool private_hubs = false;
+    std::map<const void *, std::shared_ptr<void>> hub_scratch;
 };
 
 namespace cdk {

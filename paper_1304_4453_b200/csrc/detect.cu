@@ -12,6 +12,8 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <exception>
+#include <thread>
 
 #include "detect.cuh"
 
@@ -361,18 +363,29 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     const bool base_parallel = G > 1 && !g->rows_local;
     const int64_t slots = base_parallel ? (b + G - 1) / G * G : b;
     DBuf<int32_t> bases(ctx, std::max<int64_t>(n * slots, 1));
-    auto run_base = [&](int64_t i, int32_t *zi) {
+    auto run_base_on = [&](cd_ctx *c, int64_t i, int32_t *zi) {
         if (cfg.base == CD_ALGO_PLP) {
             cd_plp_config pc = cfg.base_plp;
             pc.seed = cfg.seed + static_cast<uint64_t>(i);
-            plp_run_dev(ctx, g, pc, nullptr, zi, Report{nullptr});
+            plp_run_dev(c, g, pc, nullptr, zi, Report{nullptr});
         } else {
             cd_louvain_config lc = cfg.final_louvain;
             lc.seed = cfg.seed + static_cast<uint64_t>(i);
             lc.refine = cfg.base == CD_ALGO_PLMR;
-            louvain_run_dev(ctx, g, lc, zi, Report{nullptr});
+            louvain_run_dev(c, g, lc, zi, Report{nullptr});
         }
     };
+    auto run_base = [&](int64_t i, int32_t *zi) { run_base_on(ctx, i, zi); };
+    // One device: the bases are independent runs of latency-bound kernels, so
+    // they run concurrently -- one host thread and child context (own stream,
+    // counters, hub scratch) each; the graph's shared work decomposition is
+    // built first and only read.  PLP bases on graphs the tiered kernels run
+    // (the one-kernel cooperative phases -- fused PLP for max degree <= 256,
+    // the small PLM levels -- each want the whole GPU); not under profiling
+    // (per-launch timing wants the kernels serialised) nor for graphs that
+    // drop their bins between phases (BIG_GRAPH_ENTRIES).
+    const bool concurrent = G == 1 && b > 1 && cfg.base == CD_ALGO_PLP && g->max_degree > 256 &&
+                            !ctx->profiling && g->D < BIG_GRAPH_ENTRIES && env_i64("CD_EPP_CONCURRENT", 1) != 0;
     if (base_parallel) {
         for (int64_t j = 0; j < slots; j += G) {
             const int64_t i = j + rank;
@@ -385,6 +398,37 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
             }
             ctx->comm->allgather(ctx, zi, bases.p + j * n, n * sizeof(int32_t));  // in place
         }
+    } else if (concurrent) {
+        graph_ensure_bins(ctx, g);
+        ctx_sync(ctx);  // bases allocated, graph ready for every stream
+        std::vector<cd_ctx *> kids(b, nullptr);
+        std::vector<std::exception_ptr> errs(b);
+        try {
+            for (int64_t i = 0; i < b; ++i)
+                kids[i] = ctx_child(ctx);
+            std::vector<std::thread> th;
+            for (int64_t i = 0; i < b; ++i)
+                th.emplace_back([&, i] {
+                    try {
+                        CD_CUDA(cudaSetDevice(ctx->device));
+                        run_base_on(kids[i], i, bases.p + i * n);
+                        CD_CUDA(cudaStreamSynchronize(kids[i]->stream));
+                    } catch (...) {
+                        errs[i] = std::current_exception();
+                    }
+                });
+            for (auto &x : th)
+                x.join();
+        } catch (...) {
+            for (auto *k : kids)
+                ctx_child_destroy(ctx, k);
+            throw;
+        }
+        for (auto *k : kids)
+            ctx_child_destroy(ctx, k);
+        for (auto &e : errs)
+            if (e)
+                std::rethrow_exception(e);
     } else {
         for (int64_t i = 0; i < b; ++i)
             run_base(i, bases.p + i * n);

@@ -442,4 +442,71 @@ void graph_release_bins(cd_graph *g) {
     g->hp_key.release();
 }
 
+HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g) {
+    if (!ctx->private_hubs || !g->n_hubs)
+        return nullptr;
+    auto &slot = ctx->hub_scratch[g];
+    if (!slot) {
+        auto *h = new HubScratch();
+        slot = std::shared_ptr<void>(h, [](void *p) { delete static_cast<HubScratch *>(p); });
+        h->hp_cnt.alloc(ctx, g->n_hub_parts);
+        h->hp_cur.alloc(ctx, g->n_hub_parts);
+        h->hp_start.alloc(ctx, g->n_hub_parts + 1);
+        h->hp_key.alloc(ctx, g->hub_entries);
+        h->hp_val.alloc(ctx, g->hub_entries);
+        h->hp_best_val.alloc(ctx, g->n_hub_parts);
+        h->hp_best_key.alloc(ctx, g->n_hub_parts);
+        h->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));
+        h->hp_flag.alloc(ctx, 1);
+        h->hp_flag.zero();
+        h->hub_aux.alloc(ctx, g->n_hubs);
+        h->hub_aux.zero();
+    }
+    return static_cast<HubScratch *>(slot.get());
+}
+
+cd_ctx *ctx_child(const cd_ctx *parent) {
+    auto *c = new cd_ctx();
+    try {
+        c->device = parent->device;
+        c->pool = parent->pool;
+        c->num_sms = parent->num_sms;
+        c->smem_optin = parent->smem_optin;
+        c->use_graphs = parent->use_graphs;
+        c->private_hubs = true;
+        CD_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        CD_CUDA(cudaMalloc(reinterpret_cast<void **>(&c->dstats), DSTATS * sizeof(unsigned long long)));
+        CD_CUDA(cudaMemsetAsync(c->dstats, 0, DSTATS * sizeof(unsigned long long), c->stream));
+    } catch (...) {
+        if (c->stream)
+            cudaStreamDestroy(c->stream);
+        delete c;
+        throw;
+    }
+    return c;
+}
+
+void ctx_child_destroy(cd_ctx *parent, cd_ctx *child) {
+    if (!child)
+        return;
+    cudaStreamSynchronize(child->stream);
+    child->hub_scratch.clear();  // frees on the child stream
+    cudaStreamSynchronize(child->stream);
+    parent->launches += child->launches;
+    for (auto e : child->free_events)
+        cudaEventDestroy(e);
+    for (auto &st : child->side)
+        if (st)
+            cudaStreamDestroy(st);
+    if (child->fork_ev)
+        cudaEventDestroy(child->fork_ev);
+    for (auto e : child->join_ev)
+        if (e)
+            cudaEventDestroy(e);
+    if (child->dstats)
+        cudaFree(child->dstats);
+    cudaStreamDestroy(child->stream);
+    delete child;
+}
+
 }  // namespace cdk

@@ -151,6 +151,19 @@ __global__ void k_rebase(int64_t cnt, const int64_t *src, int64_t sub, int64_t a
 __global__ void k_fill_i64(int64_t cnt, int64_t value, int64_t *dst);
 // host: the row batches of [lo, hi) holding at most ~`chunk` prefix units each
 std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo, int64_t hi, int64_t chunk);
+// The hub tier's per-sub-sweep scratch.  A graph owns one (its hp_* fields);
+// a child context running concurrently with others on the same graph gets a
+// private copy (nullptr: use the graph's).
+struct HubScratch {
+    DBuf<int32_t> hp_cnt, hp_cur, hp_key, hp_best_key, hp_flag;
+    DBuf<int64_t> hp_start, hp_scan;
+    DBuf<double> hp_val, hp_best_val, hub_aux;
+};
+HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g);
+// a context for one concurrent run on the parent's device (own stream,
+// counters and hub scratch); ctx_child_destroy adds its launches to the parent
+cd_ctx *ctx_child(const cd_ctx *parent);
+void ctx_child_destroy(cd_ctx *parent, cd_ctx *child);
 // free the tier lists and hub scratch (rebuilt on demand by graph_ensure_bins)
 void graph_release_bins(cd_graph *g);
 // graphs at least this large drop their work decomposition between phases

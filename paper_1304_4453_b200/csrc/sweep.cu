@@ -82,6 +82,7 @@ struct SweepParams {
     int32_t *hp_best_key;
     int32_t *hp_flag;
     double *hub_aux;
+    int64_t *hp_scan;  // host-side scan scratch of hp_cnt (never read by kernels)
     int64_t n_hubs, n_parts;
 };
 
@@ -2033,8 +2034,8 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const int ndec = static_cast<int>(std::min<int64_t>(g->n_hubs, sms * 8));
         go([&](cudaStream_t s) {
             cudaStream_t st = s ? s : ctx->stream;
-            CD_CUDA(cudaMemsetAsync(g->hp_cnt.p, 0, g->n_hub_parts * sizeof(int32_t), st));
-            CD_CUDA(cudaMemsetAsync(g->hp_cur.p, 0, g->n_hub_parts * sizeof(int32_t), st));
+            CD_CUDA(cudaMemsetAsync(P.hp_cnt, 0, g->n_hub_parts * sizeof(int32_t), st));
+            CD_CUDA(cudaMemsetAsync(P.hp_cur, 0, g->n_hub_parts * sizeof(int32_t), st));
             const int64_t tiles = (g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1;
             // per-step profiler families: <mode>.hub_count / _scatter / _part / _decide
             static const std::string sub[2][5] = {
@@ -2045,8 +2046,10 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             const std::string *nm = sub[MODE];
             auto run = [&](auto launch_one) {
                 launch_one((k_hub_pairs<MODE, VC, false>), nchunks, smem_count, nm[0].c_str());
-                exclusive_scan_on<int64_t>(ctx, st, g->n_hub_parts, CountGen{g->hp_cnt.p}, g->hp_start.p,
-                                           g->hp_start.p + g->n_hub_parts, g->hp_scan.p, g->hp_scan.p + tiles,
+                exclusive_scan_on<int64_t>(ctx, st, g->n_hub_parts, CountGen{P.hp_cnt},
+                                           const_cast<int64_t *>(P.hp_start),
+                                           const_cast<int64_t *>(P.hp_start) + g->n_hub_parts, P.hp_scan,
+                                           P.hp_scan + tiles,
                                            nm[1].c_str());
                 launch_one((k_hub_pairs<MODE, VC, true>), nchunks, smem_scatter, nm[2].c_str());
                 launch_one((k_hub_part<MODE, VC>), npart, smem_part, nm[3].c_str());
@@ -2117,15 +2120,17 @@ void Sweeper::enqueue(bool capture) {
     P.hub_pbits = g->hub_pbits.p;
     P.hub_pbase = g->hub_pbase.p;
     P.part_hub = g->part_hub.p;
-    P.hp_cnt = g->hp_cnt.p;
-    P.hp_cur = g->hp_cur.p;
-    P.hp_start = g->hp_start.p;
-    P.hp_key = g->hp_key.p;
-    P.hp_val = g->hp_val.p;
-    P.hp_best_val = g->hp_best_val.p;
-    P.hp_best_key = g->hp_best_key.p;
-    P.hp_flag = g->hp_flag.p;
-    P.hub_aux = g->hub_aux.p;
+    HubScratch *hs = hub_scratch_for(ctx, g);  // private in a concurrent child context
+    P.hp_cnt = hs ? hs->hp_cnt.p : g->hp_cnt.p;
+    P.hp_cur = hs ? hs->hp_cur.p : g->hp_cur.p;
+    P.hp_start = hs ? hs->hp_start.p : g->hp_start.p;
+    P.hp_key = hs ? hs->hp_key.p : g->hp_key.p;
+    P.hp_val = hs ? hs->hp_val.p : g->hp_val.p;
+    P.hp_best_val = hs ? hs->hp_best_val.p : g->hp_best_val.p;
+    P.hp_best_key = hs ? hs->hp_best_key.p : g->hp_best_key.p;
+    P.hp_flag = hs ? hs->hp_flag.p : g->hp_flag.p;
+    P.hub_aux = hs ? hs->hub_aux.p : g->hub_aux.p;
+    P.hp_scan = hs ? hs->hp_scan.p : g->hp_scan.p;
     P.n_hubs = g->n_hubs;
     P.n_parts = g->n_hub_parts;
     const bool plp = c_.mode == MODE_PLP;
@@ -2479,8 +2484,11 @@ int64_t Sweeper::take_moves() {
         ctx_->comm->allreduce_sum_i64(ctx_, reinterpret_cast<int64_t *>(gain_.p), 1);
     CD_CUDA(cudaMemcpyAsync(&gfx, gain_.p, sizeof(gfx), cudaMemcpyDeviceToHost, ctx_->stream));
     CD_CUDA(cudaMemsetAsync(gain_.p, 0, sizeof(long long), ctx_->stream));
-    if (g_->n_hubs)
-        CD_CUDA(cudaMemcpyAsync(&overflow, g_->hp_flag.p, sizeof(overflow), cudaMemcpyDeviceToHost, ctx_->stream));
+    if (g_->n_hubs) {
+        const HubScratch *hs = hub_scratch_for(ctx_, g_);
+        CD_CUDA(cudaMemcpyAsync(&overflow, hs ? hs->hp_flag.p : g_->hp_flag.p, sizeof(overflow),
+                                cudaMemcpyDeviceToHost, ctx_->stream));
+    }
     CD_CUDA(cudaStreamSynchronize(ctx_->stream));
     if (overflow)
         fail(CD_EINTERNAL, "hub partition table overflow (more distinct labels per partition than slots)");

@@ -1,4 +1,4 @@
-for w in c2_lfr_plm c1_planted_plm c4_rmat22w_epp; do
-  python tools/prof_run.py --workload $w --runs 4 2>&1 | grep "run 3" | cut -c1-220
+for v in 1 0; do
+  CD_EPP_CONCURRENT=$v python tools/epp_anatomy.py 2>&1 | tail -3 | sed "s/^/conc=$v /"
 done
-timeout 600 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
