@@ -1413,7 +1413,11 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
             if (!SCATTER && MODE == MODE_PLM && valid && kk[c] == cur)
                 wc += wt;
             double agg;
-            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
+            // PLM: the own community is never a candidate (its weight w_c is
+            // summed into hub_aux above), so it gets no pairs -- it was the
+            // hottest key of every hub partition table
+            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg) &&
+                !(MODE == MODE_PLM && kk[c] == cur)) {
                 const int32_t p = hub_part(kk[c], pbits);
                 atomicAdd(&hist[p], 1);
                 if (SCATTER) {
@@ -1470,6 +1474,7 @@ __global__ void __launch_bounds__(256) k_hub_part(SweepParams P) {
     int32_t *keys = reinterpret_cast<int32_t *>(vals + HUB_PART_CAP);
     __shared__ double red_v[8];
     __shared__ int32_t red_k[8];
+    __shared__ double scratch[8][32];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     for (int64_t q = blockIdx.x; q < P.n_parts; q += gridDim.x) {
         const int32_t nq = P.hp_cnt[q];
@@ -1492,9 +1497,17 @@ __global__ void __launch_bounds__(256) k_hub_part(SweepParams P) {
         }
         __syncthreads();
         const int64_t st = P.hp_start[q];
-        for (int32_t i = threadIdx.x; i < nq; i += blockDim.x) {
-            const int32_t key = P.hp_key[st + i];
-            const V w = static_cast<V>(P.hp_val[st + i]);
+        // a warp's 32 consecutive pairs combine equal labels first (a hub's
+        // pairs repeat its popular labels once per chunk warp)
+        for (int32_t i0 = wid * 32; i0 < nq; i0 += blockDim.x) {
+            const int32_t i = i0 + lane;
+            const bool valid = i < nq;
+            const int32_t key = valid ? P.hp_key[st + i] : 0;
+            const double pv = valid ? P.hp_val[st + i] : 0.0;
+            double agg;
+            if (!aggregate<VC_REAL>(key, pv, valid, 0xffffffffu, scratch[wid], agg))
+                continue;
+            const V w = static_cast<V>(agg);
             uint32_t sl = hash_slot(key, cap - 1);
             bool done = false;
             for (uint32_t probe = 0; probe < cap; ++probe) {

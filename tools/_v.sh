@@ -1,4 +1,4 @@
-for v in 1 0; do
-  CD_EPP_CONCURRENT=$v python tools/epp_anatomy.py 2>&1 | tail -3 | sed "s/^/conc=$v /"
+for w in c4_rmat22w_plmr c4_rmat22w_epp c3_rmat24_plm c3_rmat24_plp; do
+  python tools/prof_run.py --workload $w --runs 3 2>&1 | grep "run 2" | cut -c1-250
 done
 timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
