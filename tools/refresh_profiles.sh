@@ -1,3 +1,5 @@
+# Re-measure every bench workload and the C2 launch list on a GPU box (outputs in gpurun_out/r/).
+# Usage: gpurun -- bash tools/refresh_profiles.sh
 set -x
 mkdir -p gpurun_out/r
 python bench.py > gpurun_out/r/c2.json 2> gpurun_out/r/c2.err
