@@ -279,12 +279,15 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
     }
 }
 
-template <class Src>
+// Block tier, instantiated per table capacity: the rows of the block list
+// with fmin < F <= fmax (fmax <= CAP / 2).  The small instance (rows of at
+// most 1024 entries, 32 KB of tables) runs 4 blocks per SM where the 4096-row
+// instance (128 KB) runs one.
+template <class Src, int CAP = 2 * ENG_BLOCK_F>
 static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const int64_t *fpre, const int32_t *rows,
                                                           int64_t nrows, int64_t key_bound, int mode,
-                                                          EngineOut out) {
+                                                          EngineOut out, int64_t fmin, int64_t fmax) {
     extern __shared__ unsigned char smem_raw[];
-    constexpr int CAP = 2 * ENG_BLOCK_F;
     double *vals = reinterpret_cast<double *>(smem_raw);
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
     uint32_t *cnts = reinterpret_cast<uint32_t *>(keys + CAP);
@@ -294,6 +297,8 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
     for (int64_t i = blockIdx.x; i < nrows; i += gridDim.x) {
         const int64_t r = rows[i];
         const int64_t f0 = fpre[r], f1 = fpre[r + 1];
+        if (f1 - f0 <= fmin || f1 - f0 > fmax)
+            continue;
         const uint32_t cap = table_cap_for(f1 - f0, key_bound, CAP);
         for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
             keys[s] = EMPTY_KEY;
@@ -882,11 +887,17 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_warp<Src>), grid_for(hc[1], 4, sms * 8), 128, 0, src, fpre, L[1],
                   int64_t(hc[1]), key_bound, int(mode), eo);
     if (hc[2]) {
-        const size_t smem = size_t(2 * ENG_BLOCK_F) * (sizeof(double) + sizeof(int32_t) + sizeof(uint32_t));
+        constexpr int CAP_S = 2048;
+        const size_t slot = sizeof(double) + sizeof(int32_t) + sizeof(uint32_t);
+        const size_t smem_s = size_t(CAP_S) * slot, smem = size_t(2 * ENG_BLOCK_F) * slot;
+        CD_CUDA(cudaFuncSetAttribute(k_eng_reduce_block<Src, CAP_S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem_s)));
         CD_CUDA(cudaFuncSetAttribute(k_eng_reduce_block<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(smem)));
+        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_block<Src, CAP_S>), grid_for(hc[2], 1, sms * 4), 512, smem_s, src,
+                  fpre, L[2], int64_t(hc[2]), key_bound, int(mode), eo, int64_t(0), int64_t(CAP_S / 2));
         CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_block<Src>), grid_for(hc[2], 1, sms * 2), 512, smem, src, fpre, L[2],
-                  int64_t(hc[2]), key_bound, int(mode), eo);
+                  int64_t(hc[2]), key_bound, int(mode), eo, int64_t(CAP_S / 2), int64_t(ENG_BLOCK_F));
     }
     if (hc[3]) {
         const int64_t nb = hc[3];
