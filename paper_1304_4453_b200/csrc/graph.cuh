@@ -47,7 +47,11 @@ __host__ __device__ inline int hub_pbits_of(int64_t d) {
     return b;
 }
 
-constexpr int64_t CLUSTER_MAX_DEG = 32768;
+#ifndef CD_CLUSTER_N
+#define CD_CLUSTER_N 4
+#endif
+constexpr int CLUSTER_CTAS = CD_CLUSTER_N;                      // CTAs per node (16384 slots each)
+constexpr int64_t CLUSTER_MAX_DEG = int64_t(CLUSTER_CTAS) * 8192;  // <= 50 % table load
 
 // cluster_max: CLUSTER_MAX_DEG, or 0 when the cluster tier is not used
 __host__ __device__ inline int tier_of_degree(int64_t d, int64_t cluster_max = CLUSTER_MAX_DEG) {

@@ -2000,7 +2000,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if ((P.tend[TIER_CLUSTER] - P.tbeg[TIER_CLUSTER])) {
         fam = names[MODE][TIER_CLUSTER];
-        constexpr int CLN = 4;  // 4 x 16384 slots: <= 50 % load at deg 32768
+        constexpr int CLN = CLUSTER_CTAS;  // CLN x 16384 slots: <= 50 % load at CLUSTER_MAX_DEG
         auto kfn = k_sweep_cluster<MODE, VC, CLN>;
         const size_t smem = size_t(CL_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(CL_CAP / 2) * sizeof(uint16_t);
         static int max_clusters = 0;
