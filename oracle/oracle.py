@@ -452,7 +452,7 @@ def plp_bucketed(g: CSR, theta=-1, max_iterations=100, seed=1, buckets=4, initia
 
 
 def louvain_cfg(gamma=1.0, max_move_iterations=32, max_levels=64, seed=1, buckets=4, refine=False,
-                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True, move_qtol=1e-3):
+                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True, move_qtol=2e-3):
     return _LouvainCfg(gamma, max_move_iterations, max_levels, seed, buckets, int(refine), int(singleton_guard),
                        move_theta, move_tol, move_stall, int(prune), move_qtol)
 

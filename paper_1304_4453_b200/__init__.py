@@ -631,7 +631,7 @@ class LouvainConfig:
     move_tol: float = 1e-3
     move_stall: float = 0.95
     prune: int = 1
-    move_qtol: float = 1e-3
+    move_qtol: float = 2e-3
 
     def _c(self):
         return _LouvainConfig(self.gamma, self.max_move_iterations, self.max_levels, self.seed, self.workers,

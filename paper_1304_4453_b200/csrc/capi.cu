@@ -144,7 +144,7 @@ void cd_louvain_config_default(cd_louvain_config *c) {
     c->move_tol = 1e-3;  // stop a level's passes below 0.1% movers
     c->move_stall = 0.95;  // ... or once the movers stop shrinking (oscillating tail)
     c->prune = 1;          // ... and skip nodes whose neighbourhood did not change
-    c->move_qtol = 1e-3;   // ... or once a pass adds < 0.1% of the phase's modularity gain
+    c->move_qtol = 2e-3;   // ... or once a pass adds < 0.2% of the phase's modularity gain
 }
 
 void cd_ensemble_config_default(cd_ensemble_config *c) {

@@ -68,7 +68,7 @@ def plp_sharded(g, rank, G, allgather, seed=3, buckets=4, max_iterations=100):
 
 
 def move_phase_sharded(g, rank, G, allgather, seed=3, buckets=4, max_move_iterations=32, move_tol=1e-3,
-                       move_stall=0.95, move_qtol=1e-3):
+                       move_stall=0.95, move_qtol=2e-3):
     from oracle import oracle as O
     b = _bounds(g.off, G)
     lo, hi = int(b[rank]), int(b[rank + 1])
