@@ -257,7 +257,23 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
             std::vector<int64_t> bD(nb, 0), bbase(nb, 0);
             std::vector<char> kept(nb, 0);
             int64_t kept_bytes = 0;
-            const int64_t keep_budget = env_i64("CD_COARSEN_KEEP_BYTES", COARSEN_KEEP_BYTES);
+            // keep what the device can hold next to the final CSR (bounded by
+            // the fine entry count): free memory plus the pool's idle reserve
+            int64_t keep_default = COARSEN_KEEP_BYTES;
+            {
+                size_t fr = 0, tot = 0;
+                uint64_t reserved = 0, used = 0;
+                if (cudaMemGetInfo(&fr, &tot) == cudaSuccess &&
+                    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+                    cudaMemPoolGetAttribute(ctx->pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess) {
+                    const int64_t avail = static_cast<int64_t>(fr) + static_cast<int64_t>(reserved - used);
+                    const int64_t room = avail - g->D * int64_t(sizeof(int32_t) + sizeof(float)) -
+                                         2 * chunk * int64_t(24) - (int64_t(8) << 30);
+                    keep_default = std::max(keep_default, room);
+                }
+                cudaGetLastError();
+            }
+            const int64_t keep_budget = env_i64("CD_COARSEN_KEEP_BYTES", keep_default);
             auto run_batch = [&](size_t b, DBuf<int64_t> &boff, DBuf<int32_t> &bcol, DBuf<float> &bw) {
                 const int64_t c0 = cut[b], rows = cut[b + 1] - c0;
                 int64_t pr[2];
