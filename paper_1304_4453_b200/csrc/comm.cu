@@ -36,6 +36,10 @@ struct NcclApi {
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 
 NcclApi &nccl() {
@@ -63,6 +67,10 @@ NcclApi &nccl() {
     api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
     api.Broadcast = reinterpret_cast<decltype(api.Broadcast)>(sym("ncclBroadcast"));
     api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.GroupStart = reinterpret_cast<decltype(api.GroupStart)>(sym("ncclGroupStart"));
+    api.GroupEnd = reinterpret_cast<decltype(api.GroupEnd)>(sym("ncclGroupEnd"));
+    api.Send = reinterpret_cast<decltype(api.Send)>(sym("ncclSend"));
+    api.Recv = reinterpret_cast<decltype(api.Recv)>(sym("ncclRecv"));
     api.loaded = true;
     return api;
 }
@@ -100,6 +108,19 @@ class NcclComm final : public Comm {
     }
     void broadcast(cd_ctx *ctx, void *buf, size_t bytes, int root) override {
         CD_NCCL(nccl().Broadcast(buf, buf, bytes, ncclInt8, root, comm_, ctx->stream));
+    }
+    void alltoallv(cd_ctx *ctx, const void *send, const size_t *sdispl, const size_t *scount, void *recv,
+                   const size_t *rdispl, const size_t *rcount) override {
+        CD_NCCL(nccl().GroupStart());
+        for (int p = 0; p < size; ++p) {
+            if (scount[p])
+                CD_NCCL(nccl().Send(static_cast<const unsigned char *>(send) + sdispl[p], scount[p], ncclInt8, p,
+                                    comm_, ctx->stream));
+            if (rcount[p])
+                CD_NCCL(nccl().Recv(static_cast<unsigned char *>(recv) + rdispl[p], rcount[p], ncclInt8, p, comm_,
+                                    ctx->stream));
+        }
+        CD_NCCL(nccl().GroupEnd());
     }
 
   private:
@@ -154,6 +175,27 @@ class LoopbackComm final : public Comm {
             CD_CUDA(cudaMemcpyAsync(buf, g_->slot[root], bytes, cudaMemcpyDeviceToDevice, ctx->stream));
         CD_CUDA(cudaStreamSynchronize(ctx->stream));
         g_->barrier();
+    }
+    void alltoallv(cd_ctx *ctx, const void *send, const size_t *sdispl, const size_t *scount, void *recv,
+                   const size_t *rdispl, const size_t *rcount) override {
+        // peers pull their blocks from the published send buffers; the send
+        // displacements travel as a host array next to the device pointer
+        struct Pub {
+            const void *send;
+            const size_t *sdispl;
+        } mine{send, sdispl};
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        publish(&mine);
+        for (int p = 0; p < size; ++p) {
+            const Pub *pp = static_cast<const Pub *>(g_->slot[p]);
+            if (rcount[p])
+                CD_CUDA(cudaMemcpyAsync(static_cast<unsigned char *>(recv) + rdispl[p],
+                                        static_cast<const unsigned char *>(pp->send) + pp->sdispl[rank], rcount[p],
+                                        cudaMemcpyDeviceToDevice, ctx->stream));
+        }
+        (void)scount;
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        g_->barrier();  // peers may reuse their send buffers (and `mine` goes out of scope) after this
     }
 
   private:

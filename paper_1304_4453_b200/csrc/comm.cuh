@@ -45,6 +45,11 @@ class Comm {
     virtual void allreduce_sum_i64(cd_ctx *ctx, int64_t *buf, size_t count) = 0;
     virtual void allreduce_sum_f64(cd_ctx *ctx, double *buf, size_t count) = 0;
     virtual void broadcast(cd_ctx *ctx, void *buf, size_t bytes, int root) = 0;
+    // personalised exchange: bytes [sdispl[p], +scount[p]) of send go to rank
+    // p, which receives them at [rdispl[me], +rcount[me]) of its recv (host
+    // arrays of G byte counts / offsets; every pair's counts must agree)
+    virtual void alltoallv(cd_ctx *ctx, const void *send, const size_t *sdispl, const size_t *scount, void *recv,
+                           const size_t *rdispl, const size_t *rcount) = 0;
 };
 
 Comm *comm_nccl_create(int nranks, int rank, const uint8_t id[128]);

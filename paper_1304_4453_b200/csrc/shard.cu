@@ -186,6 +186,126 @@ __global__ void k_stack_fpre(int64_t nc, const int64_t *roff, int G, int64_t ost
     }
 }
 
+__global__ void k_row_len(int64_t n, const int64_t *off, int64_t *len) {
+    for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+         c += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        len[c] = off[c + 1] - off[c];
+}
+
+struct Len64Gen {
+    const int64_t *a;
+    __device__ int64_t operator()(int64_t i) const { return a[i]; }
+};
+
+// Coarse graphs too large to replicate (C5's level 1 keeps ~98 % of the
+// entries) stay row-sharded: coarse rows are owned by degree-balanced ranges
+// of the summed partial row lengths, every rank sends each owner the slab of
+// its partial in the owner's range (one all-to-all for the row lengths, two
+// for the entries), and the owner merges its G slabs with the row engine.
+// The result is a row shard exactly like cd_graph_shard's (global node state
+// summed over the ranks by shard_globalize).
+static int64_t shard_coarse_min_entries() { return env_i64("CD_SHARD_COARSE_MIN_ENTRIES", int64_t(1) << 30); }
+
+static cd_graph *coarse_shard_from_partials(cd_ctx *ctx, cd_graph *part, int64_t nc, bool sorted) {
+    Comm *comm = ctx->comm;
+    const int G = world_size(ctx), me = world_rank(ctx);
+    const int grid = grid_for(std::max<int64_t>(nc, 1), 256, ctx->num_sms * 8);
+    // ownership of coarse rows
+    std::vector<int64_t> cb(G + 1);
+    {
+        DBuf<int64_t> len(ctx, std::max<int64_t>(nc, 1)), pre(ctx, nc + 1);
+        if (nc)
+            CD_LAUNCH(ctx, "coarsen", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), len.p);
+        comm->allreduce_sum_i64(ctx, len.p, static_cast<size_t>(std::max<int64_t>(nc, 1)));
+        exclusive_scan<int64_t>(ctx, nc, Len64Gen{len.p}, pre.p, pre.p + nc);
+        shard_bounds_dev(ctx, nc, pre.p, G, cb.data());
+    }
+    const int64_t clo = cb[me], chi = cb[me + 1], nloc = chi - clo;
+    // my partial's slab offsets at every owner boundary
+    std::vector<int64_t> ob(G + 1);
+    for (int d = 0; d <= G; ++d)
+        CD_CUDA(cudaMemcpyAsync(&ob[d], part->off.p + cb[d], sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    // G x G entry counts: row s = what rank s sends to each owner
+    std::vector<int64_t> mat(size_t(G) * G);
+    {
+        DBuf<int64_t> mine(ctx, G), all(ctx, size_t(G) * G);
+        std::vector<int64_t> cnt(G);
+        for (int d = 0; d < G; ++d)
+            cnt[d] = ob[d + 1] - ob[d];
+        CD_CUDA(cudaMemcpyAsync(mine.p, cnt.data(), G * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+        comm->allgather(ctx, mine.p, all.p, G * sizeof(int64_t));
+        CD_CUDA(cudaMemcpyAsync(mat.data(), all.p, mat.size() * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    int64_t cstride = 1, floc = 0;
+    for (int s = 0; s < G; ++s) {
+        cstride = std::max(cstride, mat[size_t(s) * G + me]);
+        floc += mat[size_t(s) * G + me];
+    }
+    const int64_t ostride = nloc + 1;
+    // row lengths of every source's slab for my rows; entries padded to cstride
+    DBuf<int64_t> slen(ctx, std::max<int64_t>(nc, 1)), rlen(ctx, size_t(G) * std::max<int64_t>(nloc, 1));
+    if (nc)
+        CD_LAUNCH(ctx, "coarsen", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), slen.p);
+    DBuf<int32_t> rcol(ctx, size_t(G) * cstride);
+    DBuf<float> rw(ctx, size_t(G) * cstride);
+    {
+        std::vector<size_t> sd(G), sc(G), rd(G), rc(G);
+        for (int d = 0; d < G; ++d) {
+            sd[d] = size_t(cb[d]) * sizeof(int64_t);
+            sc[d] = size_t(cb[d + 1] - cb[d]) * sizeof(int64_t);
+            rd[d] = size_t(d) * std::max<int64_t>(nloc, 1) * sizeof(int64_t);
+            rc[d] = size_t(nloc) * sizeof(int64_t);
+        }
+        comm->alltoallv(ctx, slen.p, sd.data(), sc.data(), rlen.p, rd.data(), rc.data());
+        for (int d = 0; d < G; ++d) {
+            sd[d] = size_t(ob[d]) * sizeof(int32_t);
+            sc[d] = size_t(ob[d + 1] - ob[d]) * sizeof(int32_t);
+            rd[d] = size_t(d) * cstride * sizeof(int32_t);
+            rc[d] = size_t(mat[size_t(d) * G + me]) * sizeof(int32_t);
+        }
+        comm->alltoallv(ctx, part->col.p, sd.data(), sc.data(), rcol.p, rd.data(), rc.data());
+        comm->alltoallv(ctx, part->w.p, sd.data(), sc.data(), rw.p, rd.data(), rc.data());  // float = int32 size
+    }
+    slen.release();
+    // per-source exclusive prefixes -> SrcStack layout [G][nloc+1]
+    DBuf<int64_t> roff(ctx, size_t(G) * ostride), fpre(ctx, ostride);
+    for (int s = 0; s < G; ++s)
+        exclusive_scan<int64_t>(ctx, nloc, Len64Gen{rlen.p + size_t(s) * std::max<int64_t>(nloc, 1)},
+                                roff.p + size_t(s) * ostride, roff.p + size_t(s) * ostride + nloc);
+    CD_LAUNCH(ctx, "coarsen", k_stack_fpre, grid_for(ostride, 256, ctx->num_sms * 8), 256, 0, nloc,
+              static_cast<const int64_t *>(roff.p), G, ostride, fpre.p);
+    auto *cg = new cd_graph();
+    try {
+        cg->ctx = ctx;
+        cg->n = nc;
+        cg->weighted = true;
+        DBuf<int64_t> loff;
+        bool want_w = true;
+        SrcStack src{roff.p, rcol.p, rw.p, fpre.p, G, ostride, cstride};
+        const int64_t dloc = run_row_engine(ctx, src, nloc, fpre.p, floc, std::max<int64_t>(nc, 1), DUP_SUM, want_w,
+                                            loff, cg->col, cg->w, nullptr, "coarsen", sorted);
+        cg->D = dloc;
+        cg->off.alloc(ctx, nc + 1);
+        if (clo > 0)
+            CD_LAUNCH(ctx, "coarsen", k_fill_i64, grid_for(clo, 256, ctx->num_sms * 8), 256, 0, clo, int64_t(0),
+                      cg->off.p);
+        if (nloc > 0)
+            CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(nloc, 256, ctx->num_sms * 8), 256, 0, nloc,
+                      static_cast<const int64_t *>(loff.p), int64_t(0), int64_t(0), cg->off.p + clo);
+        CD_LAUNCH(ctx, "coarsen", k_fill_i64, grid_for(nc + 1 - chi, 256, ctx->num_sms * 8), 256, 0, nc + 1 - chi,
+                  dloc, cg->off.p + chi);
+        graph_finalize(ctx, cg);
+        shard_globalize(ctx, cg, clo, chi);
+    } catch (...) {
+        delete cg;
+        throw;
+    }
+    return cg;
+}
+
 cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
     Comm *comm = ctx->comm;
     const int G = world_size(ctx);
@@ -204,6 +324,11 @@ cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, 
         for (int r = 0; r < G; ++r) {
             maxd = std::max(maxd, hc[r]);
             ftotal += hc[r];
+        }
+        if (ftotal >= shard_coarse_min_entries()) {
+            cg = coarse_shard_from_partials(ctx, part, nc, sorted);
+            delete part;
+            return cg;
         }
         const int64_t ostride = nc + 1;
         DBuf<int64_t> roff(ctx, G * ostride);

@@ -268,3 +268,56 @@ def test_generated_rmat_shard(dev, monkeypatch, G):
     assert all(res[i][1] == res[i + 1][0] for i in range(G - 1))
     for _, _, z1, z2 in res:
         assert np.array_equal(z1, zm) and np.array_equal(z2, zp)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("kind,algo", [("rmat", "plm"), ("lfr", "plm"), ("planted", "plmr"), ("rmat_int", "plmr"),
+                                       ("rmat", "epp")])
+def test_sharded_coarse_levels(dev, monkeypatch, G, kind, algo):
+    """Coarse graphs too large to replicate stay row-sharded (C5): every
+    rank sends each coarse-row owner its partial slab (all-to-all) and the
+    owner merges them.  Forced at every level here; labels must equal the
+    one-device run."""
+    z1, q1 = single(dev, kind, algo)
+    monkeypatch.setenv("CD_SHARD_COARSE_MIN_ENTRIES", "0")
+
+    def fn(ctx, r):
+        return detect(dev, algo, build(dev, kind, ctx).shard(ctx))
+
+    for r, (z, q) in enumerate(run_ranks(dev, G, fn)):
+        assert np.array_equal(z, z1), f"rank {r}: labels differ from the one-device run"
+        assert q == pytest.approx(q1, rel=1e-9, abs=1e-12)
+
+
+def test_sharded_coarse_graph_layout(dev, monkeypatch):
+    """The sharded coarse graph of a row shard: each rank's rows equal the
+    whole coarse graph's rows (as sets per row: detector-internal contraction
+    leaves rows unsorted), node state and totals global."""
+    ctx0 = dev.Context(0)
+    g1 = build(dev, "lfr", ctx0)
+    z1, _ = dev.run_plm(g1, dev.LouvainConfig(seed=1))
+    cg1 = dev.coarsen(g1, z1)[0]
+    full = cg1.csr()
+    tot1 = (cg1.edge_count(), cg1.total_edge_weight(), cg1.max_degree, cg1.isolated)
+    ctx0.close()
+    monkeypatch.setenv("CD_SHARD_COARSE_MIN_ENTRIES", "0")
+
+    def fn(ctx, r):
+        cg = dev.coarsen(build(dev, "lfr", ctx).shard(ctx), z1)[0]
+        assert cg.is_shard
+        lo, hi = cg.owned_range
+        c = cg.csr()
+        deg = np.diff(c["off"])
+        assert np.all(deg[:lo] == 0) and np.all(deg[hi:] == 0)
+        np.testing.assert_array_equal(c["vol"], full["vol"])
+        assert (cg.edge_count(), cg.total_edge_weight(), cg.max_degree, cg.isolated) == tot1
+        for u in range(lo, hi):
+            a = slice(c["off"][u], c["off"][u + 1])
+            b = slice(full["off"][u], full["off"][u + 1])
+            assert np.array_equal(c["col"][a], full["col"][b])  # the API contraction is sorted
+            np.testing.assert_array_equal(c["w"][a], full["w"][b])
+        return lo, hi
+
+    res = run_ranks(dev, 3, fn)
+    assert res[0][0] == 0 and res[-1][1] == full["off"].shape[0] - 1
+    assert all(res[i][1] == res[i + 1][0] for i in range(2))
