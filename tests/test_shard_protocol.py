@@ -156,6 +156,96 @@ def test_gloo_two_ranks_match_single_process(kind):
         assert np.array_equal(z, ref_z)
 
 
+def _row_shard(g, lo, hi):
+    """The oracle CSR holding only rows [lo, hi) (global column ids)."""
+    from oracle import oracle as O
+    idx = np.arange(g.n + 1)
+    off = np.where(idx <= lo, 0, np.where(idx >= hi, g.off[hi] - g.off[lo], g.off[np.minimum(idx, g.n)] - g.off[lo]))
+    return O.from_csr(g.n, off, g.col[g.off[lo]:g.off[hi]], g.w[g.off[lo]:g.off[hi]])
+
+
+def coarse_shard_sharded(g, zc, rank, G, allgather):
+    """The sharded contraction (csrc/shard.cu coarse_shard_from_partials):
+    partial coarse graph of this rank's rows; coarse-row owners from the
+    summed partial row lengths (cd_shard_bounds); every rank sends each owner
+    its slab; the owner merges (sum by label, rows ascending)."""
+    from oracle import oracle as O
+    b = _bounds(g.off, G)
+    part = O.coarsen(_row_shard(g, int(b[rank]), int(b[rank + 1])), zc)
+    nc = part.n
+    lens = sum(allgather(np.diff(part.off)))
+    cb = _bounds(np.concatenate([[0], np.cumsum(lens)]).astype(np.int64), G)
+    # slabs for every owner (all_gather_object stands in for the all-to-all)
+    slabs = allgather([(part.off[cb[d]:cb[d + 1] + 1] - part.off[cb[d]],
+                        part.col[part.off[cb[d]]:part.off[cb[d + 1]]],
+                        part.w[part.off[cb[d]]:part.off[cb[d + 1]]]) for d in range(G)])
+    lo, hi = int(cb[rank]), int(cb[rank + 1])
+    rows = []
+    for c in range(lo, hi):
+        acc = {}
+        for s in range(G):
+            roff, col, w = slabs[s][rank]
+            i = c - lo
+            for k, x in zip(col[roff[i]:roff[i + 1]], w[roff[i]:roff[i + 1]]):
+                acc[int(k)] = acc.get(int(k), 0.0) + float(x)
+        rows.append(sorted(acc.items()))
+    return lo, hi, nc, rows
+
+
+def _worker_coarse(rank, port, q):
+    try:
+        import torch.distributed as dist
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+
+        def allgather(obj):
+            out = [None] * WORLD
+            dist.all_gather_object(out, obj)
+            return out
+
+        from oracle import oracle as O
+        g = O.generate_rmat(10, 8, seed=4)
+        z, _ = O.move_phase_bucketed(g, np.arange(g.n), salt=0, seed=3, buckets=4)
+        zc, _ = O.compact(z)
+        out = coarse_shard_sharded(g, zc, rank, WORLD, allgather)
+        dist.barrier()
+        dist.destroy_process_group()
+        q.put((rank, out, None))
+    except BaseException as e:  # noqa: BLE001 -- reported to the parent
+        q.put((rank, None, repr(e)))
+
+
+def test_gloo_sharded_contraction_matches_whole():
+    """Two processes build the sharded coarse graph; the owners' rows, put
+    together, are the whole graph's contraction (oracle coarsen)."""
+    from oracle import oracle as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_coarse, args=(r, port, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(WORLD):
+        r, out, err = q.get(timeout=240)
+        assert err is None, f"rank {r}: {err}"
+        res[r] = out
+    for p in procs:
+        p.join(60)
+    g = O.generate_rmat(10, 8, seed=4)
+    z, _ = O.move_phase_bucketed(g, np.arange(g.n), salt=0, seed=3, buckets=4)
+    zc, _ = O.compact(z)
+    cg = O.coarsen(g, zc)
+    assert res[0][0] == 0 and res[WORLD - 1][1] == cg.n and res[0][1] == res[1][0]
+    for r in range(WORLD):
+        lo, hi, nc, rows = res[r]
+        assert nc == cg.n
+        for c, row in zip(range(lo, hi), rows):
+            seg = slice(cg.off[c], cg.off[c + 1])
+            assert [k for k, _ in row] == cg.col[seg].tolist()
+            np.testing.assert_allclose([x for _, x in row], cg.w[seg], rtol=1e-12)
+
+
 def test_shard_bounds_host():
     """cd_shard_bounds: first node whose offset reaches D*r/G (no GPU)."""
     import paper_1304_4453_b200 as P
