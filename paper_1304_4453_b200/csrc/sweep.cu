@@ -23,6 +23,8 @@
 // the whole move phase in one cooperative kernel (k_small_move).
 #include "sweep.cuh"
 
+#include <atomic>
+
 #include <cooperative_groups.h>
 
 #include <cmath>
@@ -1953,12 +1955,14 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     // block tiers: one block per node; the block size trades threads per
     // node against nodes in flight per SM (env CD_BLOCK_NT / CD_BLOCK2_NT)
-    auto block_tier = [&](auto kfn, int tier, int nt, uint32_t cap, bool &attr) {
+    // (the once-per-kernel attribute flags are atomics: concurrent EPP bases
+    // launch from several host threads)
+    auto block_tier = [&](auto kfn, int tier, int nt, uint32_t cap, std::atomic<bool> &attr) {
         fam = names[MODE][tier];
         const size_t smem = size_t(cap) * (sizeof(V) + sizeof(int32_t)) + size_t(cap / 2) * sizeof(uint16_t);
-        if (!attr) {
+        if (!attr.load(std::memory_order_acquire)) {
             set_smem(kfn, smem);
-            attr = true;
+            attr.store(true, std::memory_order_release);
         }
         const int nb = grid_for(pre_count(P, tier, P.tend[tier] - P.tbeg[tier]), 1, wave(kfn, nt, smem));
         CD_TIER_LAUNCH(kfn, nb, nt, smem, P);
@@ -1966,7 +1970,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     static const int block_nt = static_cast<int>(env_i64("CD_BLOCK_NT", 256));
     static const int block2_nt = static_cast<int>(env_i64("CD_BLOCK2_NT", 512));
     if ((P.tend[TIER_BLOCK] - P.tbeg[TIER_BLOCK])) {
-        static bool a128 = false, a256 = false;
+        static std::atomic<bool> a128{false}, a256{false};
         if (block_nt == 128)
             block_tier(k_sweep_block<MODE, VC, BLOCK_TABLE_CAP, TIER_BLOCK, 128>, TIER_BLOCK, 128, BLOCK_TABLE_CAP,
                        a128);
@@ -1975,7 +1979,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
                        a256);
     }
     if ((P.tend[TIER_BLOCK2] - P.tbeg[TIER_BLOCK2])) {
-        static bool a256 = false, a512 = false;
+        static std::atomic<bool> a256{false}, a512{false};
         if (block2_nt == 512)
             block_tier(k_sweep_block<MODE, VC, BLOCK2_TABLE_CAP, TIER_BLOCK2, 512>, TIER_BLOCK2, 512,
                        BLOCK2_TABLE_CAP, a512);
@@ -1989,10 +1993,10 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         auto kfn = k_sweep_block<MODE, VC, BLOCK3_TABLE_CAP, TIER_BLOCK3, NT3>;
         const size_t smem = size_t(BLOCK3_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) +
                             size_t(BLOCK3_TABLE_CAP / 2) * sizeof(uint16_t);
-        static bool attr3 = false;
-        if (!attr3) {
+        static std::atomic<bool> attr3{false};
+        if (!attr3.load(std::memory_order_acquire)) {
             set_smem(kfn, smem);
-            attr3 = true;
+            attr3.store(true, std::memory_order_release);
         }
         const int nb = grid_for(pre_count(P, TIER_BLOCK3, P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3]), 1,
                                 wave(kfn, NT3, smem));
@@ -2003,7 +2007,8 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         constexpr int CLN = CLUSTER_CTAS;  // CLN x 16384 slots: <= 50 % load at CLUSTER_MAX_DEG
         auto kfn = k_sweep_cluster<MODE, VC, CLN>;
         const size_t smem = size_t(CL_CAP) * (sizeof(V) + sizeof(int32_t)) + size_t(CL_CAP / 2) * sizeof(uint16_t);
-        static int max_clusters = 0;
+        static std::atomic<int> max_clusters_once{0};
+        int max_clusters = max_clusters_once.load(std::memory_order_acquire);
         if (!max_clusters) {
             set_smem(kfn, smem);
             cudaLaunchConfig_t lc = {};
@@ -2019,6 +2024,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             lc.numAttrs = 1;
             CD_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, reinterpret_cast<const void *>(kfn), &lc));
             max_clusters = std::max(1, max_clusters);
+            max_clusters_once.store(max_clusters, std::memory_order_release);
         }
         const int64_t nodes = pre_count(P, TIER_CLUSTER, P.tend[TIER_CLUSTER] - P.tbeg[TIER_CLUSTER]);
         const int ncl = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(max_clusters, nodes)));
@@ -2034,12 +2040,12 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const size_t smem_count = size_t(np) * sizeof(int32_t);
         const size_t smem_scatter = size_t(HUB_PAIRS_SMEM) + 2 * size_t(np) * sizeof(int32_t);
         const size_t smem_part = size_t(HUB_PART_CAP) * (sizeof(V) + sizeof(int32_t));
-        static bool attr = false;
-        if (!attr) {
+        static std::atomic<bool> attr{false};
+        if (!attr.load(std::memory_order_acquire)) {
             set_smem(k_hub_pairs<MODE, VC, false>, size_t(max_np) * sizeof(int32_t));
             set_smem(k_hub_pairs<MODE, VC, true>, size_t(HUB_PAIRS_SMEM) + 2 * size_t(max_np) * sizeof(int32_t));
             set_smem(k_hub_part<MODE, VC>, smem_part);
-            attr = true;
+            attr.store(true, std::memory_order_release);
         }
         const int nchunks = static_cast<int>(g->n_hub_chunks);
         const int npart = static_cast<int>(std::min<int64_t>(
