@@ -603,7 +603,9 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
 }
 
 template <int MODE, int VC>
-__global__ void __launch_bounds__(128) k_sweep_warp(SweepParams P, int chunk) {
+// count tallies fit 64 registers without spills: 8 blocks (32 warps) per SM
+// instead of 7 (C2 level 0 -3 %); the weighted instances would spill
+__global__ void __launch_bounds__(128, VC == VC_COUNT ? 8 : 1) k_sweep_warp(SweepParams P, int chunk) {
     using V = TallyT<VC>;
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][SW_WARP_CAP];
