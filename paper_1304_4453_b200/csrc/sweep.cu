@@ -426,7 +426,9 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
 }
 
 template <int G, int MODE, int VC>
-__global__ void __launch_bounds__(256) k_sweep_direct(SweepParams P, int tier, int chunk) {
+// count tallies: 32 registers (8-16 B of spill), 8 blocks per SM instead of 6
+// (C2 level 0 -6 %)
+__global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_sweep_direct(SweepParams P, int tier, int chunk) {
     __shared__ double scratch[8][32];
     const int wid = threadIdx.x >> 5;
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
