@@ -222,7 +222,7 @@ __device__ __forceinline__ uint32_t table_cap_for(int64_t F, int64_t key_bound, 
     return cap;
 }
 
-template <class Src>
+template <class Src, bool TRACK = true>
 static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const int64_t *fpre, const int32_t *rows,
                                                          int64_t nrows, int64_t key_bound, int mode,
                                                          EngineOut out) {
@@ -230,13 +230,13 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
     __shared__ double scratch[4][32];
     __shared__ int32_t skeys[4][CAP];
     __shared__ double svals[4][CAP];
-    __shared__ uint32_t scnts[4][CAP];
+    __shared__ uint32_t scnts[4][TRACK ? CAP : 1];  // duplicate counts only when tracked
     const int wid = threadIdx.x >> 5, lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     int32_t *keys = skeys[wid];
     double *vals = svals[wid];
-    uint32_t *cnts = scnts[wid];
+    uint32_t *cnts = TRACK ? scnts[wid] : nullptr;
     for (int64_t i = gw; i < nrows; i += nw) {
         const int64_t r = rows[i];
         const int64_t f0 = fpre[r], f1 = fpre[r + 1];
@@ -244,7 +244,8 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
         for (uint32_t s = lane; s < cap; s += 32) {
             keys[s] = EMPTY_KEY;
             vals[s] = 0.0;
-            cnts[s] = 0;
+            if (TRACK)
+                cnts[s] = 0;
         }
         __syncwarp();
         auto cur = src.init(r, f0);
@@ -268,7 +269,7 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
                 const int64_t pos = f0 + base + __popc(bm & lanemask_lt());
                 out.tkey[pos] = keys[s];
                 out.tval[pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1 && out.flag && !*out.flag)
+                if (TRACK && cnts[s] > 1 && out.flag && !*out.flag)
                     *out.flag = 1;
             }
             base += __popc(bm);
@@ -283,14 +284,14 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
 // with fmin < F <= fmax (fmax <= CAP / 2).  The small instance (rows of at
 // most 1024 entries, 32 KB of tables) runs 4 blocks per SM where the 4096-row
 // instance (128 KB) runs one.
-template <class Src, int CAP = 2 * ENG_BLOCK_F>
+template <class Src, int CAP = 2 * ENG_BLOCK_F, bool TRACK = true>
 static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const int64_t *fpre, const int32_t *rows,
                                                           int64_t nrows, int64_t key_bound, int mode,
                                                           EngineOut out, int64_t fmin, int64_t fmax) {
     extern __shared__ unsigned char smem_raw[];
     double *vals = reinterpret_cast<double *>(smem_raw);
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CAP);
-    uint32_t *cnts = reinterpret_cast<uint32_t *>(keys + CAP);
+    uint32_t *cnts = TRACK ? reinterpret_cast<uint32_t *>(keys + CAP) : nullptr;
     __shared__ double scratch[16][32];
     __shared__ int32_t counter;
     const int wid = threadIdx.x >> 5, nwarps = blockDim.x >> 5, lane = lane_id();
@@ -303,7 +304,8 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
         for (uint32_t s = threadIdx.x; s < cap; s += blockDim.x) {
             keys[s] = EMPTY_KEY;
             vals[s] = 0.0;
-            cnts[s] = 0;
+            if (TRACK)
+                cnts[s] = 0;
         }
         if (threadIdx.x == 0)
             counter = 0;
@@ -334,7 +336,7 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const 
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1 && out.flag && !*out.flag)
+                if (TRACK && cnts[s] > 1 && out.flag && !*out.flag)
                     *out.flag = 1;
             }
         }
@@ -883,21 +885,32 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
     if (hc[0])
         CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_direct<Src>), grid_for(hc[0], 8, sms * 8), 256, 0, src, fpre, L[0],
                   int64_t(hc[0]), int(mode), eo);
-    if (hc[1])
-        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_warp<Src>), grid_for(hc[1], 4, sms * 8), 128, 0, src, fpre, L[1],
-                  int64_t(hc[1]), key_bound, int(mode), eo);
+    // contraction (no duplicate tracking) drops the per-slot counts: 25 % less
+    // shared memory per table, more resident warps / blocks
+    if (hc[1]) {
+        if (track)
+            CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_warp<Src, true>), grid_for(hc[1], 4, sms * 8), 128, 0, src,
+                      fpre, L[1], int64_t(hc[1]), key_bound, int(mode), eo);
+        else
+            CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_warp<Src, false>), grid_for(hc[1], 4, sms * 8), 128, 0, src,
+                      fpre, L[1], int64_t(hc[1]), key_bound, int(mode), eo);
+    }
     if (hc[2]) {
-        constexpr int CAP_S = 2048;
-        const size_t slot = sizeof(double) + sizeof(int32_t) + sizeof(uint32_t);
-        const size_t smem_s = size_t(CAP_S) * slot, smem = size_t(2 * ENG_BLOCK_F) * slot;
-        CD_CUDA(cudaFuncSetAttribute(k_eng_reduce_block<Src, CAP_S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem_s)));
-        CD_CUDA(cudaFuncSetAttribute(k_eng_reduce_block<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
-        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_block<Src, CAP_S>), grid_for(hc[2], 1, sms * 4), 512, smem_s, src,
-                  fpre, L[2], int64_t(hc[2]), key_bound, int(mode), eo, int64_t(0), int64_t(CAP_S / 2));
-        CD_LAUNCH(ctx, f_red.c_str(), (k_eng_reduce_block<Src>), grid_for(hc[2], 1, sms * 2), 512, smem, src, fpre, L[2],
-                  int64_t(hc[2]), key_bound, int(mode), eo, int64_t(CAP_S / 2), int64_t(ENG_BLOCK_F));
+        constexpr int CAP_S = 2048, CAP_L = 2 * ENG_BLOCK_F;
+        const size_t slot = sizeof(double) + sizeof(int32_t) + (track ? sizeof(uint32_t) : 0);
+        const size_t smem_s = size_t(CAP_S) * slot, smem = size_t(CAP_L) * slot;
+        auto launch = [&](auto ks, auto kl) {
+            CD_CUDA(cudaFuncSetAttribute(ks, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem_s)));
+            CD_CUDA(cudaFuncSetAttribute(kl, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            CD_LAUNCH(ctx, f_red.c_str(), ks, grid_for(hc[2], 1, sms * 4), 512, smem_s, src, fpre, L[2],
+                      int64_t(hc[2]), key_bound, int(mode), eo, int64_t(0), int64_t(CAP_S / 2));
+            CD_LAUNCH(ctx, f_red.c_str(), kl, grid_for(hc[2], 1, sms * 2), 512, smem, src, fpre, L[2], int64_t(hc[2]),
+                      key_bound, int(mode), eo, int64_t(CAP_S / 2), int64_t(ENG_BLOCK_F));
+        };
+        if (track)
+            launch(k_eng_reduce_block<Src, CAP_S, true>, k_eng_reduce_block<Src, CAP_L, true>);
+        else
+            launch(k_eng_reduce_block<Src, CAP_S, false>, k_eng_reduce_block<Src, CAP_L, false>);
     }
     if (hc[3]) {
         const int64_t nb = hc[3];
