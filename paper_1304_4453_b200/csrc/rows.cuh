@@ -158,6 +158,23 @@ __device__ __forceinline__ bool warp_aggregate(int32_t key, double w, bool valid
     return leader;
 }
 
+// open-addressing insert (linear probing) into a table of any `cap` slots
+// (the global tier sizes tables at exactly 2x the row's entries)
+__device__ __forceinline__ void table_insert_n(int32_t *keys, double *vals, uint32_t *cnts, uint32_t cap,
+                                               int32_t key, double w, uint32_t c) {
+    uint32_t s = hash_slot(key, cap - 1);  // multiply-high by cap: any table size
+    while (true) {
+        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
+        if (old == EMPTY_KEY || old == key) {
+            atomicAdd(&vals[s], w);
+            if (cnts)
+                atomicAdd(&cnts[s], c);
+            return;
+        }
+        s = (s + 1 == cap) ? 0 : s + 1;
+    }
+}
+
 // open-addressing insert (linear probing) into a table with 2^k slots
 __device__ __forceinline__ void table_insert(int32_t *keys, double *vals, uint32_t *cnts, uint32_t mask,
                                              int32_t key, double w, uint32_t c) {
@@ -392,8 +409,8 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
     const int64_t b = min(cend, a + per);
     int32_t *keys = gkeys + tab_off[lo];
     double *vals = gvals + tab_off[lo];
-    uint32_t *cnts = gcnts + tab_off[lo];
-    const uint32_t mask = static_cast<uint32_t>(tab_cap[lo] - 1);
+    uint32_t *cnts = gcnts ? gcnts + tab_off[lo] : nullptr;
+    const uint32_t cap = static_cast<uint32_t>(tab_cap[lo]);
     if (a < b) {
         auto cur = src.init(r, a);
         for (int64_t f = a; f < b; f += 32) {
@@ -416,14 +433,14 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
                     sl = (sl + 1) & (ENG_PRE_CAP - 1);
                 }
                 if (!done)
-                    table_insert(keys, vals, cnts, mask, k, sum, cnt);
+                    table_insert_n(keys, vals, cnts, cap, k, sum, cnt);
             }
         }
     }
     __syncthreads();
     for (int t = threadIdx.x; t < ENG_PRE_CAP; t += blockDim.x)
         if (pk[t] != EMPTY_KEY)
-            table_insert(keys, vals, cnts, mask, pk[t], pv[t], pc[t]);
+            table_insert_n(keys, vals, cnts, cap, pk[t], pv[t], pc[t]);
 }
 
 static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const int64_t *fpre, const int32_t *rows,
@@ -438,7 +455,7 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const in
         const int64_t f0 = fpre[r];
         const int32_t *keys = gkeys + tab_off[i];
         const double *vals = gvals + tab_off[i];
-        const uint32_t *cnts = gcnts + tab_off[i];
+        const uint32_t *cnts = gcnts ? gcnts + tab_off[i] : nullptr;
         const int64_t cap = tab_cap[i];
         if (threadIdx.x == 0)
             counter = 0;
@@ -450,7 +467,7 @@ static __global__ void __launch_bounds__(512) k_eng_reduce_global_flush(const in
             if (has) {
                 out.tkey[f0 + pos] = keys[s];
                 out.tval[f0 + pos] = mode == DUP_ONE ? 1.0 : vals[s];
-                if (cnts[s] > 1 && out.flag && !*out.flag)
+                if (out.flag && cnts && cnts[s] > 1 && !*out.flag)
                     *out.flag = 1;
             }
         }
@@ -509,7 +526,7 @@ static __global__ void __launch_bounds__(256) k_eng_flush_chunked(const int64_t 
             const int64_t pos = fpre[r] + base + __popc(peers & lanemask_lt());
             out.tkey[pos] = gkeys[s];
             out.tval[pos] = mode == DUP_ONE ? 1.0 : gvals[s];
-            if (gcnts[s] > 1 && out.flag && !*out.flag)
+            if (out.flag && gcnts && gcnts[s] > 1 && !*out.flag)
                 *out.flag = 1;
         }
     }
@@ -812,10 +829,7 @@ struct CapGen {
         const int64_t r = rows[i];
         const int64_t F = fpre[r + 1] - fpre[r];
         const int64_t need = 2 * (F < key_bound ? F : key_bound);
-        int64_t c = 64;
-        while (c < need)
-            c <<= 1;
-        return c;
+        return need < 64 ? 64 : need;  // load factor <= 1/2, no power-of-two rounding
     }
 };
 struct ChunkGen {
@@ -925,10 +939,11 @@ int64_t run_row_engine(cd_ctx *ctx, const Src &src, int64_t nrows, const int64_t
         CD_CUDA(cudaStreamSynchronize(ctx->stream));
         DBuf<int32_t> gk(ctx, ht[0]);
         DBuf<double> gv(ctx, ht[0]);
-        DBuf<uint32_t> gc(ctx, ht[0]);
+        DBuf<uint32_t> gc(ctx, track ? ht[0] : 0);  // duplicate counts only when tracked
         gk.fill_bytes(0xff);
         gv.zero();
-        gc.zero();
+        if (track)
+            gc.zero();
         CD_LAUNCH(ctx, f_glob.c_str(), (k_eng_reduce_global_insert<Src>), static_cast<int>(ht[1]), 256, 0, src, fpre, L[3],
                   nb, static_cast<const int64_t *>(chunk_pre.p), static_cast<const int64_t *>(tab_off.p),
                   static_cast<const int64_t *>(tab_cap.p), gk.p, gv.p, gc.p);
