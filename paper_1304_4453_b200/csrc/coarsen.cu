@@ -74,12 +74,17 @@ constexpr int64_t COARSEN_CHUNK_ENTRIES = int64_t(1) << 29;
 // batched contraction: coarse rows kept from pass A up to this many bytes
 constexpr int64_t COARSEN_KEEP_BYTES = int64_t(16) << 30;
 
+// A: the slot type -- uint32 when every weight is integral and every volume
+// below 2^31 (graph int_weights: exact, native shared-memory atomics, half the
+// shared memory), else fp64 (shared-memory fp64 adds are CAS loops).
+template <class A>
 __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
                                                               const int64_t *mpre, const int64_t *off,
                                                               const int32_t *col, const float *w, const int32_t *z,
                                                               const int64_t *fpre, int32_t *tkey, double *tval,
                                                               int64_t *deg2) {
-    extern __shared__ double acc[];
+    extern __shared__ __align__(8) unsigned char dense_smem[];
+    A *acc = reinterpret_cast<A *>(dense_smem);
     __shared__ int wsum[DENSE_THREADS / 32 + 1];
     __shared__ double scr[DENSE_THREADS / 32][32];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
@@ -87,7 +92,7 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const 
     const int per = static_cast<int>((nc + DENSE_THREADS - 1) / DENSE_THREADS);  // slots per thread
     for (int64_t c = blockIdx.x; c < nc; c += gridDim.x) {
         for (int64_t k = threadIdx.x; k < nc; k += DENSE_THREADS)
-            acc[k] = 0.0;
+            acc[k] = A(0);
         __syncthreads();
         // tally: entry (u -> v) of a member u adds w to slot z[v]; intra-community
         // entries once (v >= u), H/louvain.hpp:180-186.  The row's own slot
@@ -114,18 +119,18 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const 
                 }
                 double sum;
                 if (warp_aggregate_sum(k, wt, valid, scr[wid], sum))
-                    atomicAdd(&acc[k], sum);
+                    atomicAdd(&acc[k], static_cast<A>(sum));
             }
         }
         self = warp_sum(self);
         if (lane == 0 && self != 0.0)
-            atomicAdd(&acc[c], self);
+            atomicAdd(&acc[c], static_cast<A>(self));
         __syncthreads();
         // emit the nonzero slots in index order at the row's scratch offset
         const int64_t k0 = static_cast<int64_t>(threadIdx.x) * per;
         int mine = 0;
         for (int i = 0; i < per; ++i)
-            mine += (k0 + i < nc && acc[k0 + i] != 0.0) ? 1 : 0;
+            mine += (k0 + i < nc && acc[k0 + i] != A(0)) ? 1 : 0;
         int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -149,9 +154,9 @@ __global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const 
         int64_t pos = fpre[c] + wsum[wid] + incl - mine;
         for (int i = 0; i < per; ++i) {
             const int64_t k = k0 + i;
-            if (k < nc && acc[k] != 0.0) {
+            if (k < nc && acc[k] != A(0)) {
                 tkey[pos] = static_cast<int32_t>(k);
-                tval[pos] = acc[k];
+                tval[pos] = static_cast<double>(acc[k]);
                 ++pos;
             }
         }
@@ -205,18 +210,24 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
             DBuf<int32_t> tkey(ctx, std::max<int64_t>(g->D, 1));
             DBuf<double> tval(ctx, std::max<int64_t>(g->D, 1));
             DBuf<int64_t> deg2(ctx, nc);
-            const size_t smem = size_t(nc) * sizeof(double);
-            CD_CUDA(cudaFuncSetAttribute(k_dense_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(std::max<size_t>(smem, 1))));
-            int per_sm = 0;
-            CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_rows, DENSE_THREADS, smem));
-            CD_LAUNCH(ctx, "coarsen.dense", k_dense_rows,
-                      grid_for(nc, 1, std::max(1, per_sm) * ctx->num_sms), DENSE_THREADS, smem, nc,
-                      static_cast<const int64_t *>(moff.p), static_cast<const int32_t *>(mem.p),
-                      static_cast<const int64_t *>(mpre.p), static_cast<const int64_t *>(g->off.p),
-                      static_cast<const int32_t *>(g->col.p),
-                      static_cast<const float *>(g->weighted ? g->w.p : nullptr), z,
-                      static_cast<const int64_t *>(fpre.p), tkey.p, tval.p, deg2.p);
+            auto launch = [&](auto kfn, size_t slot) {
+                const size_t smem = size_t(nc) * slot;
+                CD_CUDA(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(std::max<size_t>(smem, 1))));
+                int per_sm = 0;
+                CD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, DENSE_THREADS, smem));
+                CD_LAUNCH(ctx, "coarsen.dense", kfn, grid_for(nc, 1, std::max(1, per_sm) * ctx->num_sms),
+                          DENSE_THREADS, smem, nc, static_cast<const int64_t *>(moff.p),
+                          static_cast<const int32_t *>(mem.p), static_cast<const int64_t *>(mpre.p),
+                          static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                          static_cast<const float *>(g->weighted ? g->w.p : nullptr), z,
+                          static_cast<const int64_t *>(fpre.p), tkey.p, tval.p, deg2.p);
+            };
+            // integral weights whose total volume fits uint32: every slot sum does
+            if (g->int_weights && 2.0 * g->total < 4294967296.0)
+                launch(k_dense_rows<uint32_t>, sizeof(uint32_t));
+            else
+                launch(k_dense_rows<double>, sizeof(double));
             cg->off.alloc(ctx, nc + 1);
             exclusive_scan<int64_t>(ctx, nc, ArrayGen<int64_t>{deg2.p}, cg->off.p, cg->off.p + nc);
             CD_CUDA(cudaMemcpyAsync(&cg->D, cg->off.p + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
