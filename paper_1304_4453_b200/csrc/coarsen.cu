@@ -186,7 +186,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
     DBuf<int32_t> csz(ctx, std::max<int64_t>(nc, 1));
     csz.zero();
     if (n > 0)
-        CD_LAUNCH(ctx, "coarsen", k_member_count, grid, 256, 0, n, z, csz.p);
+        CD_LAUNCH(ctx, "coarsen.prep", k_member_count, grid, 256, 0, n, z, csz.p);
     DBuf<int64_t> moff(ctx, nc + 1);
     exclusive_scan<int64_t>(ctx, nc, CszGen{csz.p}, moff.p, moff.p + nc);
     DBuf<int32_t> mem(ctx, std::max<int64_t>(n, 1));
@@ -194,12 +194,12 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
         DBuf<int64_t> cursor(ctx, nc + 1);
         CD_CUDA(cudaMemcpyAsync(cursor.p, moff.p, (nc + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
         if (n > 0)
-            CD_LAUNCH(ctx, "coarsen", k_member_scatter, grid, 256, 0, n, z, cursor.p, mem.p);
+            CD_LAUNCH(ctx, "coarsen.prep", k_member_scatter, grid, 256, 0, n, z, cursor.p, mem.p);
     }
     DBuf<int64_t> mpre(ctx, n + 1);
     exclusive_scan<int64_t>(ctx, n, MemDegGen{mem.p, g->off.p}, mpre.p, mpre.p + n);
     DBuf<int64_t> fpre(ctx, nc + 1);
-    CD_LAUNCH(ctx, "coarsen", k_row_fpre, grid_for(nc + 1, 256, ctx->num_sms * 8), 256, 0, nc,
+    CD_LAUNCH(ctx, "coarsen.prep", k_row_fpre, grid_for(nc + 1, 256, ctx->num_sms * 8), 256, 0, nc,
               static_cast<const int64_t *>(moff.p), static_cast<const int64_t *>(mpre.p), fpre.p);
     auto *cg = new cd_graph();
     cg->ctx = ctx;
@@ -293,7 +293,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
                                         ctx->stream));
                 CD_CUDA(cudaStreamSynchronize(ctx->stream));
                 DBuf<int64_t> bpre(ctx, rows + 1);
-                CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
+                CD_LAUNCH(ctx, "coarsen.prep", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
                           static_cast<const int64_t *>(fpre.p + c0), pr[0], int64_t(0), bpre.p);
                 SrcWindow<SrcCoarsen> win{src, c0, pr[0]};
                 bool bw_want = true;
@@ -308,7 +308,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
                     continue;
                 DBuf<int64_t> boff;
                 bD[b] = run_batch(b, boff, kcol[b], kw[b]);
-                CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
+                CD_LAUNCH(ctx, "coarsen.prep", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
                           static_cast<const int64_t *>(boff.p), int64_t(0), D, cg->off.p + c0);
                 const int64_t bytes = bD[b] * int64_t(sizeof(int32_t) + sizeof(float));
                 if (kept_bytes + bytes <= keep_budget) {
@@ -337,7 +337,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
                 kcol[b].release();
                 kw[b].release();
             }
-            CD_LAUNCH(ctx, "coarsen", k_fill_i64, 1, 32, 0, int64_t(1), D, cg->off.p + nc);
+            CD_LAUNCH(ctx, "coarsen.prep", k_fill_i64, 1, 32, 0, int64_t(1), D, cg->off.p + nc);
         }
         graph_finalize(ctx, cg);
     } catch (...) {
@@ -354,8 +354,8 @@ bool is_compact_dev(cd_ctx *ctx, int64_t n, const int32_t *z, int64_t nc) {
     DBuf<int> flag(ctx, 1);
     flag.zero();
     if (n > 0)
-        CD_LAUNCH(ctx, "coarsen", k_member_count, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z, csz.p);
-    CD_LAUNCH(ctx, "coarsen", k_check_used, grid_for(nc, 256, ctx->num_sms * 8), 256, 0, nc,
+        CD_LAUNCH(ctx, "coarsen.prep", k_member_count, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n, z, csz.p);
+    CD_LAUNCH(ctx, "coarsen.prep", k_check_used, grid_for(nc, 256, ctx->num_sms * 8), 256, 0, nc,
               static_cast<const int32_t *>(csz.p), flag.p);
     int h = 0;
     CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));

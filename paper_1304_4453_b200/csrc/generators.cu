@@ -259,7 +259,7 @@ cd_graph *generate_rmat_dev(cd_ctx *ctx, int scale, int edge_factor, double a, d
         g->off.alloc(ctx, n + 1);
         g->col.alloc(ctx, std::max<int64_t>(F, 1));  // raw bound; the merged rows fill a prefix
         if (lo > 0)
-            CD_LAUNCH(ctx, "build", k_fill_i64, grid_for(lo, 256, ctx->num_sms * 8), 256, 0, lo, int64_t(0), g->off.p);
+            CD_LAUNCH(ctx, "build.prep", k_fill_i64, grid_for(lo, 256, ctx->num_sms * 8), 256, 0, lo, int64_t(0), g->off.p);
         int64_t D = 0;
         for (int k = 0; k < nchunks; ++k) {
             const int64_t a0 = cut[k], a1 = cut[k + 1], rows = a1 - a0;
@@ -271,7 +271,7 @@ cd_graph *generate_rmat_dev(cd_ctx *ctx, int scale, int edge_factor, double a, d
             CD_CUDA(cudaStreamSynchronize(ctx->stream));
             const int64_t Fc = pr[1] - pr[0];
             DBuf<int64_t> fpre(ctx, rows + 1);
-            CD_LAUNCH(ctx, "build", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
+            CD_LAUNCH(ctx, "build.prep", k_rebase, grid_for(rows + 1, 256, ctx->num_sms * 8), 256, 0, rows + 1,
                       static_cast<const int64_t *>(pre.p + a0), pr[0], int64_t(0), fpre.p);
             DBuf<int32_t> rk(ctx, std::max<int64_t>(Fc, 1));
             {
@@ -287,14 +287,14 @@ cd_graph *generate_rmat_dev(cd_ctx *ctx, int scale, int edge_factor, double a, d
             bool want_w = false;
             const int64_t Dc = run_row_engine(ctx, SrcFlat{fpre.p, rk.p, nullptr}, rows, fpre.p, Fc, n, DUP_ONE,
                                               want_w, off2, col2, w2, nullptr, "build");
-            CD_LAUNCH(ctx, "build", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
+            CD_LAUNCH(ctx, "build.prep", k_rebase, grid_for(rows, 256, ctx->num_sms * 8), 256, 0, rows,
                       static_cast<const int64_t *>(off2.p), int64_t(0), D, g->off.p + a0);
             if (Dc)
                 CD_CUDA(cudaMemcpyAsync(g->col.p + D, col2.p, Dc * sizeof(int32_t), cudaMemcpyDeviceToDevice,
                                         ctx->stream));
             D += Dc;
         }
-        CD_LAUNCH(ctx, "build", k_fill_i64, grid_for(n + 1 - hi, 256, ctx->num_sms * 8), 256, 0, n + 1 - hi, D,
+        CD_LAUNCH(ctx, "build.prep", k_fill_i64, grid_for(n + 1 - hi, 256, ctx->num_sms * 8), 256, 0, n + 1 - hi, D,
                   g->off.p + hi);
         pre.release();
         g->D = D;

@@ -131,7 +131,7 @@ cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, 
     deg.zero();
     const int blocks = ctx->num_sms * 8;
     if (m > 0)
-        CD_LAUNCH(ctx, "build", k_pair_degree, grid_for(m, 256, blocks), 256, 0, m, u, v, deg.p);
+        CD_LAUNCH(ctx, "build.prep", k_pair_degree, grid_for(m, 256, blocks), 256, 0, m, u, v, deg.p);
     DBuf<int64_t> fpre(ctx, n + 1);
     exclusive_scan<int64_t>(ctx, n, DegGen{deg.p}, fpre.p, fpre.p + n);
     int64_t F = 0;
@@ -147,7 +147,7 @@ cd_graph *graph_from_pairs(cd_ctx *ctx, int64_t n, int64_t m, const int32_t *u, 
         DBuf<int64_t> cursor(ctx, n + 1);
         CD_CUDA(cudaMemcpyAsync(cursor.p, fpre.p, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, ctx->stream));
         if (m > 0)
-            CD_LAUNCH(ctx, "build", k_pair_scatter, grid_for(m, 256, blocks), 256, 0, m, u, v,
+            CD_LAUNCH(ctx, "build.prep", k_pair_scatter, grid_for(m, 256, blocks), 256, 0, m, u, v,
                       weighted ? w : static_cast<const float *>(nullptr), cursor.p, rk.p, weighted ? rw.p : nullptr);
     }
     auto *g = new cd_graph();
@@ -218,7 +218,7 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
     const int k = static_cast<int>(std::max<int64_t>(1, (pr[1] - pr[0] + chunk - 1) / chunk));
     std::vector<int64_t> cut(k + 1);
     DBuf<int64_t> dcut(ctx, k + 1);
-    CD_LAUNCH(ctx, "build", k_split_rows, (k + 256) / 256, 256, 0, pre_dev, lo, hi, k, dcut.p);
+    CD_LAUNCH(ctx, "build.prep", k_split_rows, (k + 256) / 256, 256, 0, pre_dev, lo, hi, k, dcut.p);
     CD_CUDA(cudaMemcpyAsync(cut.data(), dcut.p, (k + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
     // drop empty batches

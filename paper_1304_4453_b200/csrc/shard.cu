@@ -215,7 +215,7 @@ static cd_graph *coarse_shard_from_partials(cd_ctx *ctx, cd_graph *part, int64_t
     {
         DBuf<int64_t> len(ctx, std::max<int64_t>(nc, 1)), pre(ctx, nc + 1);
         if (nc)
-            CD_LAUNCH(ctx, "coarsen", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), len.p);
+            CD_LAUNCH(ctx, "coarsen.prep", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), len.p);
         comm->allreduce_sum_i64(ctx, len.p, static_cast<size_t>(std::max<int64_t>(nc, 1)));
         exclusive_scan<int64_t>(ctx, nc, Len64Gen{len.p}, pre.p, pre.p + nc);
         shard_bounds_dev(ctx, nc, pre.p, G, cb.data());
@@ -248,7 +248,7 @@ static cd_graph *coarse_shard_from_partials(cd_ctx *ctx, cd_graph *part, int64_t
     // row lengths of every source's slab for my rows; entries padded to cstride
     DBuf<int64_t> slen(ctx, std::max<int64_t>(nc, 1)), rlen(ctx, size_t(G) * std::max<int64_t>(nloc, 1));
     if (nc)
-        CD_LAUNCH(ctx, "coarsen", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), slen.p);
+        CD_LAUNCH(ctx, "coarsen.prep", k_row_len, grid, 256, 0, nc, static_cast<const int64_t *>(part->off.p), slen.p);
     DBuf<int32_t> rcol(ctx, size_t(G) * cstride);
     DBuf<float> rw(ctx, size_t(G) * cstride);
     {
@@ -275,7 +275,7 @@ static cd_graph *coarse_shard_from_partials(cd_ctx *ctx, cd_graph *part, int64_t
     for (int s = 0; s < G; ++s)
         exclusive_scan<int64_t>(ctx, nloc, Len64Gen{rlen.p + size_t(s) * std::max<int64_t>(nloc, 1)},
                                 roff.p + size_t(s) * ostride, roff.p + size_t(s) * ostride + nloc);
-    CD_LAUNCH(ctx, "coarsen", k_stack_fpre, grid_for(ostride, 256, ctx->num_sms * 8), 256, 0, nloc,
+    CD_LAUNCH(ctx, "coarsen.prep", k_stack_fpre, grid_for(ostride, 256, ctx->num_sms * 8), 256, 0, nloc,
               static_cast<const int64_t *>(roff.p), G, ostride, fpre.p);
     auto *cg = new cd_graph();
     try {
@@ -290,12 +290,12 @@ static cd_graph *coarse_shard_from_partials(cd_ctx *ctx, cd_graph *part, int64_t
         cg->D = dloc;
         cg->off.alloc(ctx, nc + 1);
         if (clo > 0)
-            CD_LAUNCH(ctx, "coarsen", k_fill_i64, grid_for(clo, 256, ctx->num_sms * 8), 256, 0, clo, int64_t(0),
+            CD_LAUNCH(ctx, "coarsen.prep", k_fill_i64, grid_for(clo, 256, ctx->num_sms * 8), 256, 0, clo, int64_t(0),
                       cg->off.p);
         if (nloc > 0)
-            CD_LAUNCH(ctx, "coarsen", k_rebase, grid_for(nloc, 256, ctx->num_sms * 8), 256, 0, nloc,
+            CD_LAUNCH(ctx, "coarsen.prep", k_rebase, grid_for(nloc, 256, ctx->num_sms * 8), 256, 0, nloc,
                       static_cast<const int64_t *>(loff.p), int64_t(0), int64_t(0), cg->off.p + clo);
-        CD_LAUNCH(ctx, "coarsen", k_fill_i64, grid_for(nc + 1 - chi, 256, ctx->num_sms * 8), 256, 0, nc + 1 - chi,
+        CD_LAUNCH(ctx, "coarsen.prep", k_fill_i64, grid_for(nc + 1 - chi, 256, ctx->num_sms * 8), 256, 0, nc + 1 - chi,
                   dloc, cg->off.p + chi);
         graph_finalize(ctx, cg);
         shard_globalize(ctx, cg, clo, chi);
@@ -346,7 +346,7 @@ cd_graph *coarsen_sharded_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, 
         comm->allgather(ctx, scol.p, rcol.p, maxd * sizeof(int32_t));
         comm->allgather(ctx, sw.p, rw.p, maxd * sizeof(float));
         DBuf<int64_t> fpre(ctx, nc + 1);
-        CD_LAUNCH(ctx, "coarsen", k_stack_fpre, grid_for(nc + 1, 256, ctx->num_sms * 8), 256, 0, nc,
+        CD_LAUNCH(ctx, "coarsen.prep", k_stack_fpre, grid_for(nc + 1, 256, ctx->num_sms * 8), 256, 0, nc,
                   static_cast<const int64_t *>(roff.p), G, ostride, fpre.p);
         cg = new cd_graph();
         cg->ctx = ctx;
