@@ -368,6 +368,13 @@ def bench_b200(args, wl):
             ps = json.load(f).get(args.workload, {}).get(fam)
         if ps and ps.get("dram_bytes_per_launch"):
             roofline["traffic"] = ps["dram_bytes_per_launch"]
+            # DRAM bytes the hardware moved (ncu, per launch) over this run's
+            # average launch time: the sector-level view of the same kernels
+            # (label gathers move 32 B sectors for 4 B)
+            avg_s = roofline["avg_launch_ms"] / 1e3
+            if avg_s > 0:
+                roofline["traffic_gbs"] = ps["dram_bytes_per_launch"] / avg_s / 1e9
+                roofline["traffic_frac"] = roofline["traffic_gbs"] / peak
 
     # ---- end to end through the C ABI with host buffers ----------------------------
     # (a row shard uploads the whole CSR and cuts its rows on the device)
