@@ -411,6 +411,9 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
         g->hp_start.alloc(ctx, g->n_hub_parts + 1);
         g->hp_key.alloc(ctx, g->hub_entries);
         g->hp_val.alloc(ctx, g->hub_entries);
+        g->st_key.alloc(ctx, g->hub_entries);
+        g->st_val.alloc(ctx, g->hub_entries);
+        g->chunk_np.alloc(ctx, g->n_hub_chunks);
         g->hp_best_val.alloc(ctx, g->n_hub_parts);
         g->hp_best_key.alloc(ctx, g->n_hub_parts);
         g->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));
@@ -440,6 +443,9 @@ void graph_release_bins(cd_graph *g) {
     for (auto *b : {&g->hp_val, &g->hp_best_val, &g->hub_aux})
         b->release();
     g->hp_key.release();
+    g->st_key.release();
+    g->st_val.release();
+    g->chunk_np.release();
 }
 
 HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g) {
@@ -454,6 +460,9 @@ HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g) {
         h->hp_start.alloc(ctx, g->n_hub_parts + 1);
         h->hp_key.alloc(ctx, g->hub_entries);
         h->hp_val.alloc(ctx, g->hub_entries);
+        h->st_key.alloc(ctx, g->hub_entries);
+        h->st_val.alloc(ctx, g->hub_entries);
+        h->chunk_np.alloc(ctx, g->n_hub_chunks);
         h->hp_best_val.alloc(ctx, g->n_hub_parts);
         h->hp_best_key.alloc(ctx, g->n_hub_parts);
         h->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));

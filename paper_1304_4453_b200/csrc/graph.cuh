@@ -118,6 +118,9 @@ struct cd_graph {
     cdk::DBuf<int64_t> hp_start;    // [n_hub_parts + 1]
     cdk::DBuf<int32_t> hp_key;      // [hub_entries] partitioned (label, weight) pairs
     cdk::DBuf<double> hp_val;       // [hub_entries]
+    cdk::DBuf<int32_t> st_key;      // [hub_entries] the count pass's pairs, chunk-major (staging)
+    cdk::DBuf<double> st_val;       // [hub_entries]
+    cdk::DBuf<int32_t> chunk_np;    // [n_hub_chunks] pairs staged per chunk
     cdk::DBuf<double> hp_best_val;  // [n_hub_parts] per-partition best candidate
     cdk::DBuf<int32_t> hp_best_key; // [n_hub_parts]
     cdk::DBuf<int64_t> hp_scan;     // scan scratch (2 x tiles)
@@ -159,9 +162,9 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
 // a child context running concurrently with others on the same graph gets a
 // private copy (nullptr: use the graph's).
 struct HubScratch {
-    DBuf<int32_t> hp_cnt, hp_cur, hp_key, hp_best_key, hp_flag;
+    DBuf<int32_t> hp_cnt, hp_cur, hp_key, hp_best_key, hp_flag, st_key, chunk_np;
     DBuf<int64_t> hp_start, hp_scan;
-    DBuf<double> hp_val, hp_best_val, hub_aux;
+    DBuf<double> hp_val, hp_best_val, hub_aux, st_val;
 };
 HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g);
 // a context for one concurrent run on the parent's device (own stream,

@@ -85,6 +85,9 @@ struct SweepParams {
     int32_t *hp_flag;
     double *hub_aux;
     int64_t *hp_scan;  // host-side scan scratch of hp_cnt (never read by kernels)
+    int32_t *st_key;   // count pass -> scatter: staged pairs (chunk-major) and their counts
+    double *st_val;
+    int32_t *chunk_np;
     int64_t n_hubs, n_parts;
 };
 
@@ -1348,15 +1351,16 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
 }
 
 // ---------------------------------------------------------------------------
-// tier HUB (deg > 4096): hash-partitioned tally.
-//   count   chunk blocks (HUB_CHUNK entries) pre-aggregate with match_any and
-//           count pairs per partition p = top pbits of (label * phi)
+// tier HUB (largest degrees): hash-partitioned tally.
+//   count   chunk blocks (HUB_CHUNK entries) pre-aggregate with match_any,
+//           count pairs per partition p = top pbits of (label * phi) and
+//           stage the pairs chunk-major
 //   scan    partition offsets
-//   scatter the same pairs, written contiguously per partition
+//   scatter the staged pairs, written contiguously per partition
 //   part    one block per partition aggregates its pairs in a smem hash and
 //           keeps the partition's best candidate
 //   decide  one block per hub reduces its partitions' candidates
-// A pass streams the hub's entries twice; there are no global hash tables.
+// A pass streams the hub's entries once; there are no global hash tables.
 // ---------------------------------------------------------------------------
 struct CountGen {
     const int32_t *c;
@@ -1367,15 +1371,13 @@ __device__ __forceinline__ int32_t hub_part(int32_t key, int pbits) {
     return pbits ? static_cast<int32_t>((static_cast<uint32_t>(key) * 0x9E3779B1u) >> (32 - pbits)) : 0;
 }
 
-constexpr int HUB_PAIRS_SMEM = HUB_CHUNK * (sizeof(int32_t) + sizeof(double));
-
-template <int MODE, int VC, bool SCATTER>
+// Count pass: chunk blocks pre-aggregate their slice of the hub's row per
+// warp (match_any), count pairs per partition and stage the pairs
+// (chunk-major) for k_hub_scatter_staged; PLM also sums w(u, C) into hub_aux.
+template <int MODE, int VC>
 __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
     extern __shared__ unsigned char hub_smem[];
-    // count: hist[np]; scatter: pair list (HUB_CHUNK) + hist[np] + base[np]
-    double *pv = reinterpret_cast<double *>(hub_smem);
-    int32_t *pk = reinterpret_cast<int32_t *>(pv + (SCATTER ? HUB_CHUNK : 0));
-    int32_t *hist = pk + (SCATTER ? HUB_CHUNK : 0);
+    int32_t *hist = reinterpret_cast<int32_t *>(hub_smem);  // [np]
     __shared__ double scratch[8][32];
     __shared__ double red_wc[8];
     __shared__ int32_t npairs;
@@ -1386,7 +1388,6 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
         return;
     const int pbits = P.hub_pbits[h];
     const int np = 1 << pbits;
-    int32_t *hbase = hist + np;
     const int64_t pbase = P.hub_pbase[h];
     const int64_t s0 = P.off[u], e0 = P.off[u + 1];
     const int64_t s = s0 + static_cast<int64_t>(P.chunk_part[blockIdx.x]) * HUB_CHUNK;
@@ -1416,59 +1417,78 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
             if (MODE == MODE_PLM)
                 valid = valid && vv[c] != u;
             const double wt = static_cast<double>(ww[c]);
-            if (!SCATTER && MODE == MODE_PLM && valid && kk[c] == cur)
+            if (MODE == MODE_PLM && valid && kk[c] == cur)
                 wc += wt;
             double agg;
             // PLM: the own community is never a candidate (its weight w_c is
-            // summed into hub_aux above), so it gets no pairs -- it was the
-            // hottest key of every hub partition table
+            // summed into hub_aux), so it gets no pairs -- it was the hottest
+            // key of every hub partition table
             if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg) &&
                 !(MODE == MODE_PLM && kk[c] == cur)) {
-                const int32_t p = hub_part(kk[c], pbits);
-                atomicAdd(&hist[p], 1);
-                if (SCATTER) {
-                    const int32_t i = atomicAdd(&npairs, 1);
-                    pk[i] = kk[c];
-                    pv[i] = agg;
-                }
+                atomicAdd(&hist[hub_part(kk[c], pbits)], 1);
+                const int64_t at = static_cast<int64_t>(blockIdx.x) * HUB_CHUNK + atomicAdd(&npairs, 1);
+                P.st_key[at] = kk[c];
+                P.st_val[at] = agg;
             }
         }
     }
     __syncthreads();
-    if (!SCATTER) {
-        for (int q = threadIdx.x; q < np; q += blockDim.x)
-            if (hist[q])
-                atomicAdd(&P.hp_cnt[pbase + q], hist[q]);
-        if (MODE == MODE_PLM) {
-            wc = warp_sum(wc);
-            if (lane == 0)
-                red_wc[wid] = wc;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                double t = 0.0;
-                for (int q = 0; q < 8; ++q)
-                    t += red_wc[q];
-                if (t != 0.0)
-                    atomicAdd(&P.hub_aux[h], t);
-            }
+    if (threadIdx.x == 0)
+        P.chunk_np[blockIdx.x] = npairs;
+    for (int q = threadIdx.x; q < np; q += blockDim.x)
+        if (hist[q])
+            atomicAdd(&P.hp_cnt[pbase + q], hist[q]);
+    if (MODE == MODE_PLM) {
+        wc = warp_sum(wc);
+        if (lane == 0)
+            red_wc[wid] = wc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int q = 0; q < 8; ++q)
+                t += red_wc[q];
+            if (t != 0.0)
+                atomicAdd(&P.hub_aux[h], t);
         }
-        if (threadIdx.x == 0)
-            atomicAdd(&P.stats[3 * TIER_HUB + (P.w ? 2 : 1)], static_cast<unsigned long long>(e - s));
-        return;
     }
-    // scatter: one global reservation per (block, partition), then local slots
+    if (threadIdx.x == 0)
+        atomicAdd(&P.stats[3 * TIER_HUB + (P.w ? 2 : 1)], static_cast<unsigned long long>(e - s));
+}
+
+// The scatter pass from the count pass's staged pairs: one block per chunk
+// reads its pairs back (coalesced, recently written), reserves each
+// partition's range once and writes -- instead of re-reading the row and
+// re-gathering its labels.
+__global__ void __launch_bounds__(256) k_hub_scatter_staged(SweepParams P) {
+    extern __shared__ unsigned char hub_smem[];
+    int32_t *hist = reinterpret_cast<int32_t *>(hub_smem);
+    const int32_t h = P.chunk_hub[blockIdx.x];
+    const int32_t u = P.hubs[h];
+    if (!selected(P, load_key(P), u))
+        return;
+    const int pbits = P.hub_pbits[h];
+    const int np = 1 << pbits;
+    int32_t *hbase = hist + np;
+    const int64_t pbase = P.hub_pbase[h];
+    const int32_t n = P.chunk_np[blockIdx.x];
+    const int64_t cbase = static_cast<int64_t>(blockIdx.x) * HUB_CHUNK;
+    for (int q = threadIdx.x; q < np; q += blockDim.x)
+        hist[q] = 0;
+    __syncthreads();
+    for (int32_t i = threadIdx.x; i < n; i += blockDim.x)
+        atomicAdd(&hist[hub_part(P.st_key[cbase + i], pbits)], 1);
+    __syncthreads();
     for (int q = threadIdx.x; q < np; q += blockDim.x) {
         hbase[q] = hist[q] ? atomicAdd(&P.hp_cur[pbase + q], hist[q]) : 0;
         hist[q] = 0;
     }
     __syncthreads();
-    const int32_t n = npairs;
     for (int32_t i = threadIdx.x; i < n; i += blockDim.x) {
-        const int32_t key = pk[i];
+        const int32_t key = P.st_key[cbase + i];
         const int32_t p = hub_part(key, pbits);
         const int64_t pos = P.hp_start[pbase + p] + hbase[p] + atomicAdd(&hist[p], 1);
         P.hp_key[pos] = key;
-        P.hp_val[pos] = pv[i];
+        P.hp_val[pos] = P.st_val[cbase + i];
     }
 }
 
@@ -2042,12 +2062,12 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
         const int max_np = 1 << HUB_MAX_PBITS;
         const int np = 1 << hub_pbits_of(g->max_degree);
         const size_t smem_count = size_t(np) * sizeof(int32_t);
-        const size_t smem_scatter = size_t(HUB_PAIRS_SMEM) + 2 * size_t(np) * sizeof(int32_t);
+        const size_t smem_scatter = 2 * size_t(np) * sizeof(int32_t);  // staged: histogram + bases
         const size_t smem_part = size_t(HUB_PART_CAP) * (sizeof(V) + sizeof(int32_t));
         static std::atomic<bool> attr{false};
         if (!attr.load(std::memory_order_acquire)) {
-            set_smem(k_hub_pairs<MODE, VC, false>, size_t(max_np) * sizeof(int32_t));
-            set_smem(k_hub_pairs<MODE, VC, true>, size_t(HUB_PAIRS_SMEM) + 2 * size_t(max_np) * sizeof(int32_t));
+            set_smem(k_hub_pairs<MODE, VC>, size_t(max_np) * sizeof(int32_t));
+            set_smem(k_hub_scatter_staged, 2 * size_t(max_np) * sizeof(int32_t));
             set_smem(k_hub_part<MODE, VC>, smem_part);
             attr.store(true, std::memory_order_release);
         }
@@ -2068,13 +2088,13 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
                  "plm_move.hub_decide"}};
             const std::string *nm = sub[MODE];
             auto run = [&](auto launch_one) {
-                launch_one((k_hub_pairs<MODE, VC, false>), nchunks, smem_count, nm[0].c_str());
+                launch_one((k_hub_pairs<MODE, VC>), nchunks, smem_count, nm[0].c_str());
                 exclusive_scan_on<int64_t>(ctx, st, g->n_hub_parts, CountGen{P.hp_cnt},
                                            const_cast<int64_t *>(P.hp_start),
                                            const_cast<int64_t *>(P.hp_start) + g->n_hub_parts, P.hp_scan,
                                            P.hp_scan + tiles,
                                            nm[1].c_str());
-                launch_one((k_hub_pairs<MODE, VC, true>), nchunks, smem_scatter, nm[2].c_str());
+                launch_one(k_hub_scatter_staged, nchunks, smem_scatter, nm[2].c_str());
                 launch_one((k_hub_part<MODE, VC>), npart, smem_part, nm[3].c_str());
                 launch_one((k_hub_decide<MODE>), ndec, size_t(0), nm[4].c_str());
             };
@@ -2154,6 +2174,9 @@ void Sweeper::enqueue(bool capture) {
     P.hp_flag = hs ? hs->hp_flag.p : g->hp_flag.p;
     P.hub_aux = hs ? hs->hub_aux.p : g->hub_aux.p;
     P.hp_scan = hs ? hs->hp_scan.p : g->hp_scan.p;
+    P.st_key = hs ? hs->st_key.p : g->st_key.p;
+    P.st_val = hs ? hs->st_val.p : g->st_val.p;
+    P.chunk_np = hs ? hs->chunk_np.p : g->chunk_np.p;
     P.n_hubs = g->n_hubs;
     P.n_parts = g->n_hub_parts;
     const bool plp = c_.mode == MODE_PLP;
