@@ -1115,12 +1115,21 @@ __global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, Fu
     long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
     int passes = 0;
     bool changed = false;
+    // pass counters (per-bucket moves, summed gain) are double-buffered by
+    // pass parity: the buffer of pass p+1 is reset after pass p's first grid
+    // barrier (every thread has read pass p-1's values by then), so the end
+    // of a pass needs no extra barriers
+    const bool has_gain = P.gain_fx != nullptr;
     for (int pass = 0; pass < F.max_passes; ++pass) {
         const unsigned long long key = bucket_key(F.seed, F.salt + static_cast<unsigned long long>(pass));
+        int32_t *ctr = F.ctr + 8 * (pass & 1);
+        long long *gain = F.gain + (pass & 1);
+        if (has_gain)
+            P.gain_fx = gain;
         long long pass_moves = 0;
         for (int b = 0; b < F.K; ++b) {
             P.bucket = b;
-            P.mv_count = F.ctr + b;
+            P.mv_count = ctr + b;
             direct_tier<8, MODE, VC>(P, TIER_G8, F.chunk[0], key, gw, nw, scratch[wid], q, st_n, st_e);
             direct_tier<16, MODE, VC>(P, TIER_G16, F.chunk[1], key, gw, nw, scratch[wid], q, st_n, st_e);
             direct_tier<32, MODE, VC>(P, TIER_G32, F.chunk[2], key, gw, nw, scratch[wid], q, st_n, st_e);
@@ -1129,7 +1138,13 @@ __global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, Fu
             q.flush(P);
             q.flush_gain(P);
             grid.sync();
-            const int64_t mc = F.ctr[b];
+            if (b == 0) {  // the next pass's counters (read by everyone before this barrier)
+                if (gtid < 8)
+                    F.ctr[8 * ((pass + 1) & 1) + gtid] = 0;
+                if (gtid == 0)
+                    F.gain[(pass + 1) & 1] = 0;
+            }
+            const int64_t mc = ctr[b];
             if (MODE == MODE_PLM) {  // H/louvain.hpp:121-125
                 for (int64_t i = gtid; i < mc; i += gsize) {
                     const int2 m = P.mv[i];
@@ -1183,7 +1198,7 @@ __global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, Fu
             else if (F.stall > 0.0 && pass >= 8 && static_cast<double>(pass_moves) > F.stall * static_cast<double>(hist0))
                 stop = true;
             if (!stop) {
-                const long long pass_fx = *F.gain;
+                const long long pass_fx = *gain;
                 cum_fx += pass_fx;
                 if (F.qtol > 0.0 && static_cast<double>(pass_fx) <= F.qtol * static_cast<double>(cum_fx))
                     stop = true;
@@ -1191,12 +1206,6 @@ __global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, Fu
             hist0 = hist1;
             hist1 = pass_moves;
         }
-        grid.sync();  // every thread has read the counters and the gain
-        if (gtid < 8)
-            F.ctr[gtid] = 0;
-        if (gtid == 0)
-            *F.gain = 0;
-        grid.sync();
         if (stop)
             break;
     }
@@ -1251,21 +1260,30 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
     const int wid = threadIdx.x >> 5;
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int64_t gsize = static_cast<int64_t>(gridDim.x) * blockDim.x;
-    int32_t *ctr = S.ctr;
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
     block_table_init(vals, keys, S.cap_max, sh);
     long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
     int passes = 0;
     bool changed = false;
+    // the 32 pass counters and the gain are double-buffered by pass parity:
+    // pass p+1's buffer is reset after pass p's first grid barrier (everyone
+    // has read pass p-1's values by then), so a pass ends without barriers
     for (int pass = 0; pass < S.max_passes; ++pass) {
         const unsigned long long key = bucket_key(S.seed, S.salt + static_cast<unsigned long long>(pass));
+        int32_t *ctr = S.ctr + 32 * (pass & 1);
+        long long *gain = S.gain + (pass & 1);
+        P.gain_fx = gain;
         for (int64_t i = gtid; i < S.nn; i += gsize) {
             const int b = S.K > 1 ? bucket_of(key, S.order[i], S.K) : 0;
             S.bsel[i] = b;
             atomicAdd(&ctr[b], 1);
         }
         grid.sync();
+        if (blockIdx.x == 0 && threadIdx.x < 32)
+            S.ctr[32 * ((pass + 1) & 1) + threadIdx.x] = 0;
+        if (gtid == 0)
+            S.gain[(pass + 1) & 1] = 0;
         for (int64_t i = gtid; i < S.nn; i += gsize) {
             const int b = S.bsel[i];
             int off = 0;
@@ -1325,7 +1343,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
             else if (S.stall > 0.0 && pass >= 8 && static_cast<double>(pass_moves) > S.stall * static_cast<double>(hist0))
                 stop = true;
             if (!stop) {
-                const long long pass_fx = *S.gain;
+                const long long pass_fx = *gain;
                 cum_fx += pass_fx;
                 if (S.qtol > 0.0 && static_cast<double>(pass_fx) <= S.qtol * static_cast<double>(cum_fx))
                     stop = true;
@@ -1333,12 +1351,6 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
             hist0 = hist1;
             hist1 = pass_moves;
         }
-        grid.sync();  // every thread has read this pass's counters and gain
-        if (blockIdx.x == 0 && threadIdx.x < 32)
-            ctr[threadIdx.x] = 0;
-        if (gtid == 0)
-            *S.gain = 0;
-        grid.sync();
         if (stop)
             break;
     }
@@ -2316,9 +2328,9 @@ int64_t fused_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed,
                     int64_t theta, double stall, double qtol, FusedResult &out) {
     graph_ensure_bins(ctx, g);
     const int64_t cap = std::max<int64_t>(max_passes, 1);
-    DBuf<int32_t> ctr(ctx, 8);
+    DBuf<int32_t> ctr(ctx, 16);  // two passes' per-bucket counters (parity)
     DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
-    DBuf<long long> result(ctx, 4), gain(ctx, 1), trace(ctx, cap);
+    DBuf<long long> result(ctx, 4), gain(ctx, 2), trace(ctx, cap);
     DBuf<unsigned long long> stamp(ctx, cap + 1);
     ctr.zero();
     gain.zero();
@@ -2452,9 +2464,9 @@ bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t see
     graph_ensure_bins(ctx, g);
     const int64_t nn = g->tier_start[NUM_TIERS];
     DBuf<int32_t> order(ctx, std::max<int64_t>(nn, 1)), bsel(ctx, std::max<int64_t>(nn, 1)),
-        blist(ctx, std::max<int64_t>(nn, 1)), ctr(ctx, 32);
+        blist(ctx, std::max<int64_t>(nn, 1)), ctr(ctx, 64);  // two passes' counters (parity)
     DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
-    DBuf<long long> result(ctx, 4), gain(ctx, 1);
+    DBuf<long long> result(ctx, 4), gain(ctx, 2);
     ctr.zero();
     gain.zero();
     // heaviest tiers first (longest-processing-time first over the work counter)
