@@ -78,7 +78,7 @@ constexpr int64_t COARSEN_KEEP_BYTES = int64_t(16) << 30;
 // below 2^31 (graph int_weights: exact, native shared-memory atomics, half the
 // shared memory), else fp64 (shared-memory fp64 adds are CAS loops).
 template <class A>
-__global__ void __launch_bounds__(DENSE_THREADS) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
+__global__ void __launch_bounds__(DENSE_THREADS, 4) k_dense_rows(int64_t nc, const int64_t *moff, const int32_t *mem,
                                                               const int64_t *mpre, const int64_t *off,
                                                               const int32_t *col, const float *w, const int32_t *z,
                                                               const int64_t *fpre, int32_t *tkey, double *tval,
