@@ -250,6 +250,8 @@ def test_c1_louvain_quality_vs_reference(dev, ctx, c1, refine):
 def test_c1_epp_quality_vs_reference(dev, ctx, c1):
     rg, _ = c1
     g, _ = dev.generate_planted(100000, 1000, 0.1, 2 / 99900, 1)
-    _, rrep = rg.run_epp(workers=0)
+    # one worker: the reference's multi-threaded EPP varies from run to run
+    # (racing PLP bases), which made this comparison flaky
+    _, rrep = rg.run_epp(workers=1)
     z, rep = dev.run_epp(g)
     assert abs(rep.modularity - rrep["modularity"]) <= E2E_Q
