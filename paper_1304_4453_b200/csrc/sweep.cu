@@ -1505,7 +1505,7 @@ __global__ void __launch_bounds__(256) k_hub_scatter_staged(SweepParams P) {
 }
 
 template <int MODE, int VC>
-__global__ void __launch_bounds__(256) k_hub_part(SweepParams P) {
+__global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepParams P) {
     using V = TallyT<VC>;
     extern __shared__ unsigned char hub_smem[];
     V *vals = reinterpret_cast<V *>(hub_smem);
