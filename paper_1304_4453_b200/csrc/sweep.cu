@@ -1092,7 +1092,7 @@ __device__ __forceinline__ unsigned long long global_ns() {
 constexpr int FUSED_THREADS = 128;
 
 template <int MODE, int VC>
-__global__ void __launch_bounds__(FUSED_THREADS) k_fused_phase(SweepParams P, FusedPhase F) {
+__global__ void __launch_bounds__(FUSED_THREADS, 8) k_fused_phase(SweepParams P, FusedPhase F) {
     namespace cg = cooperative_groups;
     using V = TallyT<VC>;
     cg::grid_group grid = cg::this_grid();
