@@ -302,7 +302,7 @@ static __global__ void __launch_bounds__(128) k_eng_reduce_warp(Src src, const i
 // most 1024 entries, 32 KB of tables) runs 4 blocks per SM where the 4096-row
 // instance (128 KB) runs one.
 template <class Src, int CAP = 2 * ENG_BLOCK_F, bool TRACK = true>
-static __global__ void __launch_bounds__(512) k_eng_reduce_block(Src src, const int64_t *fpre, const int32_t *rows,
+static __global__ void __launch_bounds__(512, CAP <= 2048 ? 4 : 1) k_eng_reduce_block(Src src, const int64_t *fpre, const int32_t *rows,
                                                           int64_t nrows, int64_t key_bound, int mode,
                                                           EngineOut out, int64_t fmin, int64_t fmax) {
     extern __shared__ unsigned char smem_raw[];
