@@ -416,7 +416,7 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
         g->chunk_np.alloc(ctx, g->n_hub_chunks);
         g->hp_best_val.alloc(ctx, g->n_hub_parts);
         g->hp_best_key.alloc(ctx, g->n_hub_parts);
-        g->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));
+        g->hp_scan.alloc(ctx, 2 * scan_scratch_elems(g->n_hub_parts));
         g->hp_flag.alloc(ctx, 1);
         g->hp_flag.zero();
         g->hub_aux.alloc(ctx, nh);
@@ -465,7 +465,7 @@ HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g) {
         h->chunk_np.alloc(ctx, g->n_hub_chunks);
         h->hp_best_val.alloc(ctx, g->n_hub_parts);
         h->hp_best_key.alloc(ctx, g->n_hub_parts);
-        h->hp_scan.alloc(ctx, 2 * ((g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1));
+        h->hp_scan.alloc(ctx, 2 * scan_scratch_elems(g->n_hub_parts));
         h->hp_flag.alloc(ctx, 1);
         h->hp_flag.zero();
         h->hub_aux.alloc(ctx, g->n_hubs);

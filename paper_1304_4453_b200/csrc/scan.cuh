@@ -92,22 +92,33 @@ struct ArrayGen {
 };
 
 // Two-level exclusive scan on an explicit stream with caller-provided
-// scratch (no allocation: safe inside CUDA-graph capture).  n <= SCAN_TILE^2.
-// partial / pscan: >= ceil(n / SCAN_TILE) elements each.
+// Scratch elements exclusive_scan_on needs in EACH of `partial` and `pscan`
+// for n items (the tile partials of every recursion level).
+inline int64_t scan_scratch_elems(int64_t n) {
+    int64_t s = 0, t = (n + SCAN_TILE - 1) / SCAN_TILE;
+    while (t > 1) {
+        s += t;
+        t = (t + SCAN_TILE - 1) / SCAN_TILE;
+    }
+    return s + 1;
+}
+
+// scratch (no allocation: safe inside CUDA-graph capture); any n.
+// partial / pscan: >= scan_scratch_elems(n) elements each.
 template <class T, class F>
 void exclusive_scan_on(cd_ctx *ctx, cudaStream_t s, int64_t n, F f, T *out, T *total, T *partial, T *pscan,
                        const char *family) {
     const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (tiles > SCAN_TILE)
-        fail(CD_EINTERNAL, "exclusive_scan_on: input too large");
     if (tiles <= 1) {
         CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, F>), 1, SCAN_THREADS, 0, n, f, static_cast<const T *>(nullptr),
                     out, total);
         return;
     }
     CD_LAUNCH_S(ctx, s, family, (k_scan_reduce<T, F>), static_cast<int>(tiles), SCAN_THREADS, 0, n, f, partial);
-    CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, ArrayGen<T>>), 1, SCAN_THREADS, 0, tiles,
-                ArrayGen<T>{partial}, static_cast<const T *>(nullptr), pscan, static_cast<T *>(nullptr));
+    // the tile partials: one block, or (beyond SCAN_TILE tiles) recursively
+    // with the scratch that follows this level's
+    exclusive_scan_on<T>(ctx, s, tiles, ArrayGen<T>{partial}, pscan, static_cast<T *>(nullptr), partial + tiles,
+                         pscan + tiles, family);
     CD_LAUNCH_S(ctx, s, family, (k_scan_apply<T, F>), static_cast<int>(tiles), SCAN_THREADS, 0, n, f,
                 static_cast<const T *>(pscan), out, total);
 }

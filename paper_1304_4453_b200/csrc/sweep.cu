@@ -2091,7 +2091,7 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
             cudaStream_t st = s ? s : ctx->stream;
             CD_CUDA(cudaMemsetAsync(P.hp_cnt, 0, g->n_hub_parts * sizeof(int32_t), st));
             CD_CUDA(cudaMemsetAsync(P.hp_cur, 0, g->n_hub_parts * sizeof(int32_t), st));
-            const int64_t tiles = (g->n_hub_parts + SCAN_TILE - 1) / SCAN_TILE + 1;
+            const int64_t tiles = scan_scratch_elems(g->n_hub_parts);  // per scratch half
             // per-step profiler families: <mode>.hub_count / _scatter / _part / _decide
             static const std::string sub[2][5] = {
                 {"plp_sweep.hub_count", "plp_sweep.hub_scan", "plp_sweep.hub_scatter", "plp_sweep.hub_part",
