@@ -4,22 +4,33 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl b200|reference]
 
 One "step" = one complete detector run (the reference's RunReport.total_ms
-region, H/louvain.hpp:277-279) over one synthetic graph resident in HBM.
-Metric: edges/s = m (undirected edges, the reference CLI bench's
-edge_count(), P/tools/commdet.cpp:241-245) / step time.  Default workload =
-BASELINE.json configs[1]: PLM (gamma 1) on the LFR-shaped n=1e6 graph.
+region, H/plp.hpp:70-142, H/louvain.hpp:277-279) over one synthetic graph
+resident in HBM.  Metric: edges/s = m (undirected edges, the reference CLI
+bench's edge_count(), P/tools/commdet.cpp:241-245) / step time.  Default
+workload = the largest single-GPU config, BASELINE.json configs[2] (C3):
+PLP on R-MAT scale 24 (520.8M CSR entries); c3_rmat24_plm is the same graph
+under PLM.
 
 value      device time (CUDA events on the library stream), graph + output in HBM,
            L2 flushed (256 MiB write) before every timed step.
 e2e        the same metric through the public C ABI with HOST buffers: pinned
            host CSR -> cd_graph_from_csr (H2D + validation + finalize) ->
-           cd_louvain_run with a host output (D2H of the labels).
-roofline   dominant kernel family (per-launch CUDA events on a profiled pass of
-           the same workload), algorithmic bytes per DESIGN.md's byte model vs
-           MEASURED_PEAKS.json hbm_gbs.
+           cd_plp_run / cd_louvain_run with a host output (D2H of the labels).
+roofline   the dominant kernel family (the sweep: every tier kernel of a
+           sub-sweep, run as concurrent branches exactly as in the timed step,
+           timed as one unit with CUDA events around the group, so family time
+           <= step time), algorithmic bytes per DESIGN.md's byte model vs
+           MEASURED_PEAKS.json hbm_gbs; "kernels" = each tier kernel timed
+           alone on a serialised pass (diagnostic).
+quality    modularity / communities of the device run vs the reference: the
+           live CPU baseline run (default order, all threads) and, for PLP, the
+           named parity setting (randomize_order, seed 1, 1 worker; SURVEY.md
+           8(c)) cached by tests/golden/make_ref_quality.py on the same bytes.
 cpu_baseline  the unmodified reference (oracle/_ref) on identical bytes (the C
            port of the generator), all host threads, rank 0 at N=1.
 --impl reference  the reference arm: the same metric from oracle/_ref only.
+--gpus N   without a torchrun environment, re-launches itself under
+           torch.distributed.run with N ranks (127.0.0.1).
 Multi-GPU (torchrun), --parallel:
   replicas   one independent graph per rank, no collective (weak scaling);
              value = all ranks' edges / max-over-ranks time.  Default for the
@@ -54,6 +65,9 @@ WORKLOADS = {
     "c1_planted_plp": dict(gen="planted", algo="plp", seed=1,
                            desc="PLP on planted partition n=1e5, k=1000, p_in=0.1, p_out=2/99900"),
     "c1_planted_plm": dict(gen="planted", algo="plm", seed=1, desc="PLM on config-1 planted graph"),
+    # a seconds-sized planted graph for the contract tests (not a bench config)
+    "t0_planted_plp": dict(gen="planted", algo="plp", seed=3, n=2000, k=8, p_in=0.05, p_out=0.002,
+                           desc="PLP on a planted partition n=2000, k=8 (test workload)"),
     "c3_rmat24_plp": dict(gen="rmat", scale=24, weighted=False, algo="plp", seed=1,
                           desc="PLP on R-MAT scale 24 ef 16 (0.57,0.19,0.19,0.05)"),
     "c3_rmat24_plm": dict(gen="rmat", scale=24, weighted=False, algo="plm", seed=1,
@@ -80,7 +94,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2_lfr_plm", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3_rmat24_plp", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--parallel", default=None, choices=["replicas", "rows", "replicated"],
                     help="multi-GPU mode (default: rows for C3, replicas otherwise)")
@@ -155,6 +169,10 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def planted_args(wl):
+    return (wl.get("n", 100000), wl.get("k", 1000), wl.get("p_in", 0.1), wl.get("p_out", 2 / 99900), wl["seed"])
+
+
 def make_device_graph(P, ctx, wl, shard=False):
     """shard: this rank's row shard (R-MAT shards are generated directly,
     never holding the whole graph; other graphs are cut from the whole)."""
@@ -166,7 +184,7 @@ def make_device_graph(P, ctx, wl, shard=False):
     if wl["gen"] == "lfr":
         g, _ = P.generate_lfr(seed=wl["seed"], ctx=ctx, **LFR_C2)
     elif wl["gen"] == "planted":
-        g, _ = P.generate_planted(100000, 1000, 0.1, 2 / 99900, wl["seed"], ctx=ctx)
+        g, _ = P.generate_planted(*planted_args(wl), ctx=ctx)
     else:
         g = P.generate_rmat(wl["scale"], 16, 0.57, 0.19, 0.19, weighted=wl["weighted"], seed=wl["seed"], ctx=ctx)
     return g
@@ -177,7 +195,7 @@ def make_oracle_graph(O, wl):
     if wl["gen"] == "lfr":
         return O.generate_lfr(seed=wl["seed"], **LFR_C2)[0]
     if wl["gen"] == "planted":
-        rg, _ = O.RefGraph.planted(100000, 1000, 0.1, 2 / 99900, wl["seed"], workers=0)
+        rg, _ = O.RefGraph.planted(*planted_args(wl), workers=0)
         return rg.csr()
     return O.generate_rmat(wl["scale"], 16, 0.57, 0.19, 0.19, weighted=wl["weighted"], seed=wl["seed"])
 
@@ -210,6 +228,43 @@ def cpu_threads():
 
 
 # ---------------------------------------------------------------------------
+# shared pieces of both arms' lines
+# ---------------------------------------------------------------------------
+def workload_config(args, wl, n, m, entries):
+    """The workload-identifying config: identical keys and values in both arms."""
+    return {"workload": args.workload, "desc": wl["desc"], "algo": wl["algo"], "seed": wl["seed"], "n": int(n),
+            "m": int(m), "entries": int(entries)}
+
+
+def cached_reference_quality(workload, digest=None):
+    """tests/golden/ref_quality.json: the reference's results on the same bytes
+    (tests/golden/make_ref_quality.py), keyed by workload/setting."""
+    path = os.path.join(ROOT, "tests", "golden", "ref_quality.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as f:
+        cache = json.load(f)
+    out = {}
+    for key, v in cache.items():
+        wk, setting = key.split("/")
+        if wk == workload and (digest is None or v["graph"]["digest"] == digest):
+            out[setting] = {"modularity": v["modularity"], "communities": v["communities"], "workers": v["workers"],
+                            "randomize_order": v["randomize_order"], "runs": v["runs"], "total_ms": v["total_ms"],
+                            "host": v["host"]}
+    return out
+
+
+def graph_digest(off, col):
+    import hashlib
+
+    import numpy as np
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(off, dtype=np.int64).tobytes())
+    h.update(np.ascontiguousarray(col, dtype=np.int32).tobytes())
+    return h.hexdigest()[:16]
+
+
+# ---------------------------------------------------------------------------
 # reference arm
 # ---------------------------------------------------------------------------
 def bench_reference(args, wl):
@@ -228,19 +283,22 @@ def bench_reference(args, wl):
     threads = cpu_threads()
     for _ in range(args.warmup):
         run_reference(O, rg, wl["algo"], threads)
-    times, qs = [], []
+    times, qs, ks = [], [], []
     for _ in range(args.steps):
         rep = run_reference(O, rg, wl["algo"], threads)
         times.append(rep["total_ms"] / 1e3)
         qs.append(rep["modularity"])
+        ks.append(rep["community_count"])
     total = sum(times)
     value = og.m * args.steps / total
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": args.workload, "desc": wl["desc"], "m": og.m, "n": og.n,
-                   "modularity": statistics.median(qs), "parallelism": "openmp"},
+        "config": workload_config(args, wl, og.n, og.m, og.D),
+        "parallelism": f"openmp x{threads}",
+        "quality": {"modularity": statistics.median(qs), "communities": int(statistics.median(ks)),
+                    "setting": f"reference defaults (ascending order), OMP workers={threads}"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
                          "sample": f"{args.steps} complete runs of the reference {wl['algo']} (oracle/_ref, "
                                    f"OMP workers={threads}) on the identical graph"},
@@ -253,6 +311,33 @@ def bench_reference(args, wl):
 # ---------------------------------------------------------------------------
 # B200 arm
 # ---------------------------------------------------------------------------
+SWEEP_FAMILY = {"plp": "plp_sweep", "plm": "plm_move", "plmr": "plm_move", "epp": "plp_sweep"}
+
+
+def profile_pass(P, ctx, step, flush, mode, reps):
+    """`reps` profiled runs (ctx profiling mode 1: every launch timed, sweep
+    tiers serialised; 2: tiers concurrent as in the timed run, each
+    sub-sweep's group timed as one unit).  Returns (kernel stats, total
+    device ms of the profiled runs measured around each run)."""
+    import torch
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    ctx.reset_stats()
+    ctx.set_profiling(mode)
+    tot = 0.0
+    for _ in range(reps):
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step()
+        e1.record(stream)
+        e1.synchronize()
+        tot += e0.elapsed_time(e1)
+    ctx.set_profiling(0)
+    return ctx.kernel_stats(), tot
+
+
 def bench_b200(args, wl):
     import numpy as np
     import torch
@@ -279,7 +364,8 @@ def bench_b200(args, wl):
             dist.broadcast_object_list(uid, src=0)
         ctx.attach_nccl(world, rank, uid[0])
     g = make_device_graph(P, ctx, wl, shard=mode == "rows")
-    n, m, entries = g.node_count(), g.edge_count(), g.entries
+    n, m = g.node_count(), g.edge_count()
+    entries = g.entries if mode != "rows" else g._info.D_global
     units = 1 if sharded else world  # graphs processed per step, all ranks
     out = torch.empty(max(n, 1), dtype=torch.int32, device=f"cuda:{local}")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
@@ -328,62 +414,61 @@ def bench_b200(args, wl):
                           for l in rep.levels],
                "iterations": len(rep.iterations), "run_ms": rep.total_ms}
 
-    # ---- roofline: profiled pass of the same workload ---------------------------
-    ctx.reset_stats()
-    ctx.set_profiling(True)
-    prof_steps = max(1, min(3, args.steps))
-    for _ in range(prof_steps):
-        flush.fill_(1.0)
-        torch.cuda.synchronize()
-        step()
-    ctx.set_profiling(False)
-    stats = ctx.kernel_stats()
-    fam = "plp_sweep" if wl["algo"] == "plp" else ("plm_move" if wl["algo"] in ("plm", "plmr") else None)
-    if fam is None or fam not in stats:
-        fam = max(stats, key=lambda k: stats[k]["total_ms"])
-    s = stats[fam]
+    # ---- roofline: profiled passes of the same workload ---------------------------
     peak, peak_kind = measured_peak()
+    fam = SWEEP_FAMILY[wl["algo"]]
+    prof_steps = max(1, min(3, args.steps))
+    # (a) the sweep family as it runs in the timed step: tier kernels concurrent,
+    #     each sub-sweep's group timed as one unit (+ the one-kernel phases)
+    gst, gstep_ms = profile_pass(P, ctx, step, flush, 2, prof_steps)
+    # (b) every kernel timed alone (tiers serialised): per-tier diagnostics
+    sst, sstep_ms = profile_pass(P, ctx, step, flush, 1, prof_steps)
+    s = gst.get(fam) or {"total_ms": 0.0, "bytes": 0.0, "launches": 0}
     achieved = s["bytes"] / (s["total_ms"] / 1e3) / 1e9 if s["total_ms"] > 0 and s["bytes"] > 0 else None
-    # bases ("plm_move", "coarsen") aggregate their ".warp/.sort/..." entries;
-    # "<mode>.hub" is the sum of the hub kernels "<mode>.hub_*"
-    bases = {k.split(".")[0] for k in stats if "." in k}
-    synthetic = {k for k in stats if k.endswith(".hub")}
-    prof_total = sum(v["total_ms"] for k, v in stats.items() if k not in bases and k not in synthetic)
     roofline = {"bound": "hbm", "kernel": fam, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": None,
-                "peak_kind": peak_kind, "bytes_per_launch": s["bytes"] / max(s["launches"], 1),
+                "frac": (achieved / peak) if achieved else None, "traffic": None, "peak_kind": peak_kind,
+                "unit_of_launch": "one sub-sweep: its tier kernels as concurrent branches (as timed), "
+                                  "or one cooperative phase kernel",
+                "bytes_per_launch": s["bytes"] / max(s["launches"], 1),
                 "avg_launch_ms": s["total_ms"] / max(s["launches"], 1), "launches": s["launches"] // prof_steps,
-                "share_of_step": s["total_ms"] / prof_total if prof_total else None,
+                "family_ms_per_step": s["total_ms"] / prof_steps,
+                "profiled_step_ms": gstep_ms / prof_steps,
+                "share_of_step": s["total_ms"] / gstep_ms if gstep_ms else None,
                 "families_ms_per_step": {k: round(v["total_ms"] / prof_steps, 4) for k, v in
-                                         sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])[:8]},
-                # every sweep kernel against the HBM roofline (per-tier work counters)
+                                         sorted(gst.items(), key=lambda kv: -kv[1]["total_ms"])[:10]},
+                # every sweep tier kernel timed alone (serialised pass) against the roofline
+                "kernels_serialised_step_ms": sstep_ms / prof_steps,
                 "kernels": {k: {"ms_per_step": round(v["total_ms"] / prof_steps, 4),
                                 "achieved": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9, 2),
                                 "frac": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9 / peak, 5)}
-                            for k, v in sorted(stats.items(), key=lambda kv: -kv[1]["total_ms"])
+                            for k, v in sorted(sst.items(), key=lambda kv: -kv[1]["total_ms"])
                             if "." in k and v["bytes"] > 0 and v["total_ms"] > 0}}
     prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:
             ps = json.load(f).get(args.workload, {}).get(fam)
-        if ps and ps.get("dram_bytes_per_launch"):
-            roofline["traffic"] = ps["dram_bytes_per_launch"]
-            # DRAM bytes the hardware moved (ncu, per launch) over this run's
-            # average launch time: the sector-level view of the same kernels
-            # (label gathers move 32 B sectors for 4 B)
-            avg_s = roofline["avg_launch_ms"] / 1e3
-            if avg_s > 0:
-                roofline["traffic_gbs"] = ps["dram_bytes_per_launch"] / avg_s / 1e9
-                roofline["traffic_frac"] = roofline["traffic_gbs"] / peak
+        if ps and ps.get("dram_bytes_per_step"):
+            # ncu DRAM bytes of the family's kernels per step, over the sub-sweeps
+            roofline["traffic"] = ps["dram_bytes_per_step"] / max(roofline["launches"], 1)
+            roofline["traffic_source"] = ps.get("source")
 
     # ---- end to end through the C ABI with host buffers ----------------------------
-    # (a row shard uploads the whole CSR and cuts its rows on the device)
-    c = make_device_graph(P, ctx, wl).csr() if mode == "rows" else g.csr()
+    # (rows mode: every rank uploads the offsets and only its own rows)
+    c = (make_device_graph(P, ctx, wl) if mode == "rows" else g).csr()
+    bounds = P.shard_bounds(c["off"], world) if mode == "rows" else None
     if entries >= 1 << 31:  # C5: room on the device for the uploaded copy
         g = None
     pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
-    h_off, h_col = pin(c["off"]), pin(c["col"])
-    h_w = pin(c["w"]) if c["w"] is not None else None
+    h_off = pin(c["off"])
+    if mode == "rows":
+        lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+        e0_, e1_ = int(c["off"][lo]), int(c["off"][hi])
+        h_col = pin(c["col"][e0_:e1_])
+        h_w = pin(c["w"][e0_:e1_]) if c["w"] is not None else None
+    else:
+        h_col = pin(c["col"])
+        h_w = pin(c["w"]) if c["w"] is not None else None
+    digest = graph_digest(c["off"], c["col"]) if mode != "rows" else None
     h_out = torch.empty(max(n, 1), dtype=torch.int32).pin_memory().numpy()
     e2e_ms = 0.0
     e2e_steps = max(1, min(args.steps, 5))
@@ -392,9 +477,10 @@ def bench_b200(args, wl):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        gh = P.Graph.from_csr(n, h_off, h_col, h_w, ctx=ctx)
         if mode == "rows":
-            gh = gh.shard(ctx)
+            gh = P.Graph.from_csr_rows(n, h_off, lo, hi, h_col, h_w, ctx=ctx)
+        else:
+            gh = P.Graph.from_csr(n, h_off, h_col, h_w, ctx=ctx)
         run_device(P, gh, wl["algo"], h_out, report=False)
         e1.record(stream)
         e1.synchronize()
@@ -408,9 +494,16 @@ def bench_b200(args, wl):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": units * m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": int(4 * n), "ms_per_step": e2e_ms}
+           "d2h_bytes_per_step": int(4 * n), "ms_per_step": e2e_ms,
+           "path": "pinned host CSR -> cd_graph_from_csr" + ("_rows (own rows)" if mode == "rows" else "")
+                   + " -> detector -> host labels"}
 
-    # ---- CPU baseline: the reference on identical bytes (rank 0, N = 1) -----------
+    # ---- the reference on the same bytes: cached parity setting + live baseline ----
+    cached = cached_reference_quality(args.workload, digest)
+    if cached:
+        quality["reference_cached"] = cached
+        for setting, v in cached.items():
+            quality[f"abs_diff_{setting}"] = abs(quality["modularity"] - v["modularity"])
     cpu = None
     if wl.get("cpu") is False:
         cpu = {"value": None, "unit": "edges/s", "cores": cpu_threads(), "kind": "reference",
@@ -419,9 +512,15 @@ def bench_b200(args, wl):
         try:
             from oracle import oracle as O
             if O.ref_available():
-                og = make_oracle_graph(O, wl)
-                assert og.m == m and np.array_equal(og.col, c["col"]), "oracle graph differs from device graph"
+                if cached:
+                    # these bytes' digest equals the one the C port of the
+                    # generator produced for the cached reference runs
+                    og = O.from_csr(n, c["off"], c["col"], None if c["w"] is None else c["w"].astype(np.float64))
+                else:
+                    og = make_oracle_graph(O, wl)
+                assert og.m == m and graph_digest(og.off, og.col) == digest, "oracle graph differs from device graph"
                 rg = O.RefGraph.from_csr(og)
+                del og
                 threads = cpu_threads()
                 ts, qs = [], []
                 t0 = time.time()
@@ -431,24 +530,24 @@ def bench_b200(args, wl):
                     qs.append(r["modularity"])
                 cpu = {"value": m / statistics.median(ts), "unit": "edges/s", "cores": threads, "kind": "reference",
                        "sample": f"{len(ts)} complete reference {wl['algo']} runs (oracle/_ref, OMP workers="
-                                 f"{threads}) on the identical graph, median total_ms"}
+                                 f"{threads}, default order) on the identical graph, median total_ms"}
                 quality["ref_modularity"] = statistics.median(qs)
                 quality["abs_diff"] = abs(quality["modularity"] - quality["ref_modularity"])
         except Exception as exc:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": "edges/s", "cores": cpu_threads(), "kind": "reference",
                    "sample": f"failed: {exc}"}
 
+    del c
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "int32+f64",
             "data": "synthetic",
-            "config": {"workload": args.workload, "desc": wl["desc"], "n": n, "m": m, "entries": entries,
-                       "algo": wl["algo"], "seed": wl["seed"],
-                       "parallelism": f"{mode} x{world}" if mode != "1gpu" else "1gpu",
-                       "l2": "flushed (256 MiB write) before every timed step",
-                       "quality": quality},
+            "config": workload_config(args, wl, n, m, entries),
+            "parallelism": f"{mode} x{world}" if mode != "1gpu" else "1gpu",
+            "l2": "flushed (256 MiB write) before every timed step",
+            "quality": quality,
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
         }
         emit(line)
@@ -464,6 +563,21 @@ def emit(line):
     print(json.dumps(line), file=_OUT or sys.stdout, flush=True)
 
 
+def spawn_ranks(n):
+    """--gpus N outside torchrun: re-launch this command with N ranks (one per
+    GPU) under torch.distributed.run on 127.0.0.1; rank 0 prints the line."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) on stderr
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env, stdout=_OUT, stderr=sys.stderr)
+
+
 def main():
     global _OUT
     # Libraries (NCCL's version banner, ...) may write to fd 1; keep stdout
@@ -473,6 +587,8 @@ def main():
     os.dup2(2, 1)
     args = parse()
     wl = WORKLOADS[args.workload]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return bench_reference(args, wl)
     return bench_b200(args, wl)

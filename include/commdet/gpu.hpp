@@ -359,6 +359,12 @@ struct LouvainConfig {
     std::uint64_t seed = 1;
     int workers = 1;
     bool refine = false;
+    // device only (not in the reference): false = the device's default early
+    // stopping and pruning (cd_louvain_config_default: move_tol 1e-3,
+    // move_stall 0.95, move_qtol 2e-3, prune 1); true = the reference's rule
+    // alone, a move phase ends after a pass without moves or at
+    // max_move_iterations (cd_louvain_config_reference)
+    bool reference_stopping = false;
 };
 
 enum class Algo { plp, plm, plmr };
@@ -569,11 +575,15 @@ struct RunReport {
 };
 
 namespace detail {
+// the reference's caps are uint64 counts; the C ABI takes int64: saturate
+inline int64_t sat64(count c) {
+    return c > static_cast<count>(INT64_MAX) ? INT64_MAX : static_cast<int64_t>(c);
+}
 inline cd_plp_config plp_c(const PlpConfig &c) {
     cd_plp_config o;
     cd_plp_config_default(&o);
     o.theta = c.theta;
-    o.max_iterations = static_cast<int64_t>(c.max_iterations);
+    o.max_iterations = sat64(c.max_iterations);
     o.randomize_order = c.randomize_order ? 1 : 0;
     o.seed = c.seed;
     o.workers = c.workers;
@@ -581,10 +591,13 @@ inline cd_plp_config plp_c(const PlpConfig &c) {
 }
 inline cd_louvain_config louvain_c(const LouvainConfig &c) {
     cd_louvain_config o;
-    cd_louvain_config_default(&o);
+    if (c.reference_stopping)
+        cd_louvain_config_reference(&o);
+    else
+        cd_louvain_config_default(&o);
     o.gamma = c.gamma;
-    o.max_move_iterations = static_cast<int64_t>(c.max_move_iterations);
-    o.max_levels = static_cast<int64_t>(c.max_levels);
+    o.max_move_iterations = sat64(c.max_move_iterations);
+    o.max_levels = sat64(c.max_levels);
     o.seed = c.seed;
     o.workers = c.workers;
     o.refine = c.refine ? 1 : 0;

@@ -84,7 +84,7 @@ typedef struct cd_louvain_config {
                                 input graph's move phases, 2 on every level, 0 never */
     int32_t reserved;
     double move_qtol;        /* device: ... or once a pass's summed gain is <= move_qtol x the
-                                phase's summed gain so far (0 disables; default 1e-3) */
+                                phase's summed gain so far (0 disables; default 2e-3) */
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */
@@ -168,6 +168,11 @@ CD_API const char *cd_last_error(void);
 CD_API const char *cd_version(void);
 CD_API void cd_plp_config_default(cd_plp_config *cfg);
 CD_API void cd_louvain_config_default(cd_louvain_config *cfg);
+/* The reference's stopping rule only (H/louvain.hpp:78, :136-137): a move
+ * phase ends after a pass without moves or at max_move_iterations; every
+ * non-isolated node is evaluated in every pass (no pruning).  The device
+ * update order (buckets, singleton guard) is kept. */
+CD_API void cd_louvain_config_reference(cd_louvain_config *cfg);
 CD_API void cd_ensemble_config_default(cd_ensemble_config *cfg);
 CD_API cd_status cd_ctx_create(int device, cd_ctx **out);
 CD_API cd_status cd_ctx_destroy(cd_ctx *ctx);
@@ -295,6 +300,15 @@ CD_API cd_status cd_ctx_world(const cd_ctx *ctx, int32_t *rank, int32_t *size);
 CD_API cd_status cd_shard_bounds(int64_t n, const int64_t *off, int32_t nranks, int64_t *bounds);
 /* This rank's row shard of a whole graph (ranges of cd_shard_bounds). */
 CD_API cd_status cd_graph_shard(cd_ctx *ctx, const cd_graph *full, cd_graph **out);
+/* This rank's row shard straight from its own rows (no rank ever holds the
+ * whole CSR): off = the whole graph's offsets (n+1, host or device), [lo, hi)
+ * = this rank's range, which must equal cd_shard_bounds(off, world)[rank..];
+ * col / w = the off[hi] - off[lo] entries of rows [lo, hi) (w NULL =
+ * unweighted).  Rows are validated as in cd_graph_from_csr; node volumes,
+ * loops, m and w(E) are summed over the ranks.  Collective over the
+ * context's ranks; with no communicator it is cd_graph_from_csr. */
+CD_API cd_status cd_graph_from_csr_rows(cd_ctx *ctx, int64_t n, const int64_t *off, int64_t lo, int64_t hi,
+                                        const int32_t *col, const float *w, cd_graph **out);
 /* This rank's row shard of the seeded R-MAT graph (cd_graph_generate_rmat),
  * built without ever holding the whole graph: rank r keeps the rows whose
  * raw (pre-deduplication) adjacency splits the stream evenly, i.e.

@@ -133,7 +133,7 @@ _lib = None
 
 # every symbol include/commdet_cuda.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "cd_last_error", "cd_version", "cd_plp_config_default", "cd_louvain_config_default",
+    "cd_last_error", "cd_version", "cd_plp_config_default", "cd_louvain_config_default", "cd_louvain_config_reference",
     "cd_ensemble_config_default", "cd_ctx_create", "cd_ctx_destroy", "cd_ctx_synchronize", "cd_ctx_stream",
     "cd_ctx_set_profiling", "cd_ctx_reset_stats", "cd_ctx_kernel_stats", "cd_ctx_launch_count",
     "cd_graph_from_edges", "cd_graph_from_csr", "cd_graph_generate_planted", "cd_graph_generate_rmat",
@@ -142,7 +142,7 @@ EXPORTS = [
     "cd_community_volumes", "cd_compact", "cd_community_count", "cd_coarsen", "cd_prolong", "cd_combine_hashed",
     "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_plp_run", "cd_louvain_run", "cd_epp_run",
     "cd_nccl_unique_id", "cd_ctx_attach_nccl", "cd_loopback_create", "cd_loopback_destroy",
-    "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard",
+    "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard", "cd_graph_from_csr_rows",
     "cd_graph_read_metis", "cd_graph_read_edge_list", "cd_graph_load_metis", "cd_graph_load_edge_list",
     "cd_graph_original_ids", "cd_rand_index",
 ]
@@ -193,6 +193,7 @@ def load_library():
         "cd_loopback_create": [i32, vpp], "cd_loopback_destroy": [vp], "cd_ctx_attach_loopback": [vp, vp, i32],
         "cd_ctx_detach": [vp], "cd_ctx_world": [vp, C.POINTER(i32), C.POINTER(i32)],
         "cd_shard_bounds": [i64, vp, i32, vp], "cd_graph_shard": [vp, vp, vpp],
+        "cd_graph_from_csr_rows": [vp, i64, vp, i64, i64, vp, vp, vpp],
         "cd_graph_read_metis": [vp, vp, i64, vpp], "cd_graph_read_edge_list": [vp, vp, i64, i32, vpp],
         "cd_graph_load_metis": [vp, C.c_char_p, vpp], "cd_graph_load_edge_list": [vp, C.c_char_p, i32, vpp],
         "cd_graph_original_ids": [vp, vp], "cd_rand_index": [vp, vp, vp, vp, C.POINTER(f64)],
@@ -205,6 +206,8 @@ def load_library():
     L.cd_plp_config_default.restype = None
     L.cd_louvain_config_default.argtypes = [C.POINTER(_LouvainConfig)]
     L.cd_louvain_config_default.restype = None
+    L.cd_louvain_config_reference.argtypes = [C.POINTER(_LouvainConfig)]
+    L.cd_louvain_config_reference.restype = None
     L.cd_ensemble_config_default.argtypes = [C.POINTER(_EnsembleConfig)]
     L.cd_ensemble_config_default.restype = None
     _lib = L
@@ -426,6 +429,19 @@ class Graph:
         _check(load_library().cd_graph_from_csr(ctx.h, n, po, pc, pw, C.byref(h)))
         return cls(h, ctx)
 
+    @classmethod
+    def from_csr_rows(cls, n, off, lo, hi, col_rows, w_rows=None, ctx=None):
+        """This rank's row shard from its own rows only (cd_graph_from_csr_rows):
+        off = the whole graph's offsets, [lo, hi) = shard_bounds(off, world)[r:r+2],
+        col_rows / w_rows = the entries of rows [lo, hi).  Collective."""
+        ctx = _ctx(ctx)
+        po, ko = _ptr(off, np.int64)
+        pc, kc = _ptr(col_rows, np.int32)
+        pw, kw = _ptr(w_rows, np.float32)
+        h = C.c_void_p()
+        _check(load_library().cd_graph_from_csr_rows(ctx.h, n, po, int(lo), int(hi), pc, pw, C.byref(h)))
+        return cls(h, ctx)
+
     # --- reference accessors (H/graph.hpp:105-123) ---------------------------
     def node_count(self) -> int:
         return self._info.n
@@ -603,6 +619,11 @@ def read_edge_list(source, merge_duplicates=False, ctx=None) -> Graph:
 # ---------------------------------------------------------------------------
 # configs / reports (H/plp.hpp:16-22, H/louvain.hpp:15-22, H/ensemble.hpp:19-31)
 # ---------------------------------------------------------------------------
+def _sat64(v):
+    """The reference's caps are uint64 counts; the C ABI takes int64: saturate."""
+    return min(int(v), (1 << 63) - 1)
+
+
 @dataclass
 class PlpConfig:
     theta: int = -1
@@ -613,7 +634,7 @@ class PlpConfig:
     buckets: int = 4
 
     def _c(self):
-        return _PlpConfig(self.theta, self.max_iterations, int(self.randomize_order), self.workers, self.seed,
+        return _PlpConfig(self.theta, _sat64(self.max_iterations), int(self.randomize_order), self.workers, self.seed,
                           self.buckets, 0)
 
 
@@ -633,8 +654,16 @@ class LouvainConfig:
     prune: int = 1
     move_qtol: float = 2e-3
 
+    @classmethod
+    def reference(cls, **kw):
+        """The reference's stopping rule alone (cd_louvain_config_reference):
+        no early stops, no pruning; buckets and the singleton guard kept."""
+        d = dict(move_theta=0, move_tol=0.0, move_stall=0.0, prune=0, move_qtol=0.0)
+        d.update(kw)
+        return cls(**d)
+
     def _c(self):
-        return _LouvainConfig(self.gamma, self.max_move_iterations, self.max_levels, self.seed, self.workers,
+        return _LouvainConfig(self.gamma, _sat64(self.max_move_iterations), _sat64(self.max_levels), self.seed, self.workers,
                               int(self.refine), self.buckets, int(self.singleton_guard), self.move_theta,
                               self.move_tol, self.move_stall, int(self.prune), 0, self.move_qtol)
 

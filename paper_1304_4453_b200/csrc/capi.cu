@@ -147,6 +147,15 @@ void cd_louvain_config_default(cd_louvain_config *c) {
     c->move_qtol = 2e-3;   // ... or once a pass adds < 0.2% of the phase's modularity gain
 }
 
+void cd_louvain_config_reference(cd_louvain_config *c) {
+    cd_louvain_config_default(c);
+    c->move_theta = 0;
+    c->move_tol = 0.0;
+    c->move_stall = 0.0;
+    c->prune = 0;
+    c->move_qtol = 0.0;
+}
+
 void cd_ensemble_config_default(cd_ensemble_config *c) {
     std::memset(c, 0, sizeof(*c));
     c->ensemble_size = 4;
@@ -243,7 +252,7 @@ cd_status cd_ctx_stream(cd_ctx *ctx, void **stream) {
 }
 
 cd_status cd_ctx_set_profiling(cd_ctx *ctx, int enabled) {
-    CD_GUARD(ctx, CD_REQUIRE(ctx, CD_EINVAL, "null context"); ctx_flush_stats(ctx); ctx->profiling = enabled != 0)
+    CD_GUARD(ctx, CD_REQUIRE(ctx, CD_EINVAL, "null context"); ctx_flush_stats(ctx); ctx->profiling = enabled < 0 ? 0 : (enabled > 2 ? 1 : enabled))
 }
 
 cd_status cd_ctx_reset_stats(cd_ctx *ctx) {
@@ -864,6 +873,15 @@ cd_status cd_graph_shard(cd_ctx *ctx, const cd_graph *full, cd_graph **out) {
     CD_GUARD(ctx, {
         CD_REQUIRE(ctx && full && out, CD_EINVAL, "invalid argument");
         *out = graph_shard_dev(ctx, full);
+    })
+}
+
+cd_status cd_graph_from_csr_rows(cd_ctx *ctx, int64_t n, const int64_t *off, int64_t lo, int64_t hi,
+                                 const int32_t *col, const float *w, cd_graph **out) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && out && off && n >= 0 && n < INT32_MAX, CD_EINVAL, "invalid argument");
+        CD_REQUIRE(0 <= lo && lo <= hi && hi <= n, CD_EINVAL, "row range out of bounds");
+        *out = graph_from_rows_dev(ctx, n, off, lo, hi, col, w);
     })
 }
 

@@ -64,5 +64,7 @@ inline int world_rank(const cd_ctx *ctx) { return ctx->comm ? ctx->comm->rank : 
 // each range holds about D*r/G CSR entries (binary search on off[]).
 void shard_bounds_host(int64_t n, const int64_t *off_host, int nranks, int64_t *bounds);
 void shard_bounds_dev(cd_ctx *ctx, int64_t n, const int64_t *off_dev, int nranks, int64_t *bounds);
+cd_graph *graph_from_rows_dev(cd_ctx *ctx, int64_t n, const int64_t *off, int64_t lo, int64_t hi,
+                              const int32_t *col, const float *w);
 
 }  // namespace cdk

@@ -62,7 +62,10 @@ struct cd_ctx {
     cudaMemPool_t pool = nullptr;
     int num_sms = 148;
     size_t smem_optin = 0;
-    bool profiling = false;
+    // 0 off; 1 every launch timed, sweep tiers serialised on the library
+    // stream; 2 sweep tiers as concurrent branches (as in the timed run), one
+    // event pair around each sub-sweep's tier group ("<mode>.group")
+    int profiling = 0;
     int64_t launches = 0;
     std::map<std::string, cdk::KStat> stats;
     std::vector<cdk::PendingEvent> pending;

@@ -78,6 +78,55 @@ cd_graph *graph_shard_dev(cd_ctx *ctx, const cd_graph *full) {
     return sh;
 }
 
+cd_graph *graph_from_rows_dev(cd_ctx *ctx, int64_t n, const int64_t *off, int64_t lo, int64_t hi,
+                              const int32_t *col, const float *w) {
+    const int G = world_size(ctx), r = world_rank(ctx);
+    DBuf<int64_t> full(ctx, n + 1);
+    CD_CUDA(cudaMemcpyAsync(full.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, ctx->stream));
+    std::vector<int64_t> bounds(G + 1);
+    shard_bounds_dev(ctx, n, full.p, G, bounds.data());
+    if (bounds[r] != lo || bounds[r + 1] != hi)
+        fail(CD_EINVAL, "row range [" + std::to_string(lo) + ", " + std::to_string(hi) + ") is not this rank's " +
+                            "shard range [" + std::to_string(bounds[r]) + ", " + std::to_string(bounds[r + 1]) + ")");
+    int64_t e[3] = {0, 0, 0};
+    CD_CUDA(cudaMemcpyAsync(&e[0], full.p + lo, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&e[1], full.p + hi, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaMemcpyAsync(&e[2], full.p + n, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    const int64_t D = e[1] - e[0];
+    if (D < 0 || e[0] < 0 || e[2] < e[1])
+        fail(CD_EINPUT, "malformed CSR offsets");
+    if (D && !col)
+        fail(CD_EINVAL, "null column array");
+    auto *g = new cd_graph();
+    try {
+        g->ctx = ctx;
+        g->n = n;
+        g->D = D;
+        g->weighted = w != nullptr;
+        g->off.alloc(ctx, n + 1);
+        CD_LAUNCH(ctx, "shard", k_shard_off, grid_for(n + 1, 256, ctx->num_sms * 8), 256, 0, n,
+                  static_cast<const int64_t *>(full.p), lo, hi, g->off.p);
+        full.release();
+        g->col.alloc(ctx, std::max<int64_t>(D, 1));
+        if (D)
+            CD_CUDA(cudaMemcpyAsync(g->col.p, col, D * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
+        if (w) {
+            g->w.alloc(ctx, std::max<int64_t>(D, 1));
+            if (D)
+                CD_CUDA(cudaMemcpyAsync(g->w.p, w, D * sizeof(float), cudaMemcpyDefault, ctx->stream));
+        }
+        graph_validate_csr(ctx, n, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, D);
+        graph_finalize(ctx, g);  // over the owned rows: each edge counted once, by its smaller endpoint's owner
+        if (G > 1)
+            shard_globalize(ctx, g, lo, hi);
+    } catch (...) {
+        delete g;
+        throw;
+    }
+    return g;
+}
+
 // transposed block: for every node v, the owned u with (u, v) an entry
 __global__ void k_tcount(int64_t lo, int64_t hi, const int64_t *off, const int32_t *col, int32_t *cnt) {
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;

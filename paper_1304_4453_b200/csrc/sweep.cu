@@ -2200,6 +2200,13 @@ void Sweeper::enqueue(bool capture) {
         P.bucket = b;
         P.mv_count = cnt_.p + b;
         int branch = 0;
+        // profiling mode 2: the sub-sweep's concurrent tier group is the unit
+        // timed (non-overlapping: its kernels run as in the timed run)
+        cudaEvent_t ga = nullptr;
+        if (capture && ctx->profiling == 2) {
+            ga = ctx_event(ctx);
+            CD_CUDA(cudaEventRecord(ga, ctx->stream));
+        }
         if (capture)
             CD_CUDA(cudaEventRecord(ctx->fork_ev, ctx->stream));
         if (plp)
@@ -2208,6 +2215,11 @@ void Sweeper::enqueue(bool capture) {
             launch_tiers_vc<MODE_PLM>(ctx, g, P, capture, branch);
         for (int i = 0; i < branch; ++i)
             CD_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[i], 0));
+        if (ga) {
+            cudaEvent_t gb = ctx_event(ctx);
+            CD_CUDA(cudaEventRecord(gb, ctx->stream));
+            ctx->pending.push_back({plp ? "plp_sweep.group" : "plm_move.group", ga, gb});
+        }
         if (c_.dense_best)
             continue;
         if (exchange_)
@@ -2256,6 +2268,11 @@ void Sweeper::exchange_and_apply(int b) {
 void Sweeper::pass(uint64_t key) {
     unsigned long long k = key;
     CD_CUDA(cudaMemcpyAsync(key_.p, &k, sizeof(k), cudaMemcpyHostToDevice, ctx_->stream));
+    if (ctx_->profiling == 2 && !exchange_) {
+        ensure_side_streams(ctx_);
+        enqueue(true);  // concurrent tier branches, eagerly, group-timed
+        return;
+    }
     if (ctx_->profiling || !ctx_->use_graphs || exchange_) {
         enqueue(false);
         return;
@@ -2327,7 +2344,10 @@ static void launch_fused(cd_ctx *ctx, SweepParams &P, FusedPhase &F) {
 int64_t fused_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
                     int64_t theta, double stall, double qtol, FusedResult &out) {
     graph_ensure_bins(ctx, g);
-    const int64_t cap = std::max<int64_t>(max_passes, 1);
+    // the reference's caps are uint64 counts: saturate, never wrap; the
+    // per-pass trace holds at most the report's record capacity
+    max_passes = std::min<int64_t>(std::max<int64_t>(max_passes, 0), INT32_MAX);
+    const int64_t cap = std::max<int64_t>(std::min<int64_t>(max_passes, CD_MAX_ITERATION_RECORDS), 1);
     DBuf<int32_t> ctr(ctx, 16);  // two passes' per-bucket counters (parity)
     DBuf<int2> mv(ctx, std::max<int64_t>(g->n, 1));
     DBuf<long long> result(ctx, 4), gain(ctx, 2), trace(ctx, cap);
@@ -2462,6 +2482,7 @@ static void launch_small(cd_ctx *ctx, const SweepParams &P, const SmallPhase &S,
 bool small_move_phase(cd_ctx *ctx, cd_graph *g, const SweepCall &c, uint64_t seed, uint64_t salt, int64_t max_passes,
                       int64_t theta, double stall, double qtol, int64_t *passes, int64_t *moves) {
     graph_ensure_bins(ctx, g);
+    max_passes = std::min<int64_t>(std::max<int64_t>(max_passes, 0), INT32_MAX);  // saturate (uint64 caps)
     const int64_t nn = g->tier_start[NUM_TIERS];
     DBuf<int32_t> order(ctx, std::max<int64_t>(nn, 1)), bsel(ctx, std::max<int64_t>(nn, 1)),
         blist(ctx, std::max<int64_t>(nn, 1)), ctr(ctx, 64);  // two passes' counters (parity)

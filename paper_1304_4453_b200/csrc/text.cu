@@ -32,6 +32,15 @@ namespace cdk {
 
 namespace {
 
+// Weights are stored as fp32 (rounded to nearest).  A positive fp64 weight
+// below the smallest fp32 subnormal would round to 0 and one above FLT_MAX to
+// inf; both break the w > 0 invariant (H/graph.hpp:52-53), so they are
+// rejected like a nonpositive weight.
+__device__ __host__ __forceinline__ bool fp32_weight_ok(double w) {
+    const float f = static_cast<float>(w);
+    return f > 0.0f && f <= 3.402823466e38f;
+}
+
 __device__ __host__ __forceinline__ bool is_ws(char c) {
     return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r';
 }
@@ -381,6 +390,8 @@ __global__ void k_metis_entries(int64_t nadj, int64_t n, MetisLines M, const cha
                     code = 3;
                 else if (!(w > 0.0))
                     code = 4;
+                else if (!fp32_weight_ok(w))
+                    code = 6;
             }
             if (code) {
                 const unsigned long long tok = static_cast<unsigned long long>(j * stride + which + 1);
@@ -567,6 +578,8 @@ cd_graph *read_metis_dev(cd_ctx *ctx, const char *text, int64_t len, const std::
             fail(CD_EINPUT, where + ": neighbor id " + tok + " out of range");
         if (code == 3)
             fail(CD_EINPUT, "malformed weight '" + tok + "' in " + where);
+        if (code == 6)
+            fail(CD_EINPUT, "weight '" + tok + "' in " + where + " is not a positive finite fp32 value");
         fail(CD_EINPUT, where + ": nonpositive edge weight");
     }
     if (nc - 1 < nn)
@@ -668,6 +681,9 @@ __global__ void k_el_parse(int64_t nlines, const int64_t *line_tok, const int64_
             tok = 3;
         } else if (!(wt > 0.0)) {
             code = 4;
+        } else if (!fp32_weight_ok(wt)) {
+            code = 6;  // parsed and positive, but the stored fp32 weight would be 0 or inf
+            tok = 3;
         }
         if (code)
             atomicMin(err, (static_cast<unsigned long long>(l) << 24) | (static_cast<unsigned long long>(tok) << 4) |
@@ -754,6 +770,8 @@ cd_graph *read_edge_list_dev(cd_ctx *ctx, const char *text, int64_t len, bool me
             fail(CD_EINPUT, "malformed integer '" + tok + "' in " + where);
         if (code == 3)
             fail(CD_EINPUT, "malformed weight '" + tok + "' in " + where);
+        if (code == 6)
+            fail(CD_EINPUT, "weight '" + tok + "' in " + where + " is not a positive finite fp32 value");
         fail(CD_EINPUT, where + ": nonpositive edge weight");
     }
     const bool weighted = read1(ctx, any_w.p) != 0;

@@ -255,3 +255,16 @@ def test_c1_epp_quality_vs_reference(dev, ctx, c1):
     _, rrep = rg.run_epp(workers=1)
     z, rep = dev.run_epp(g)
     assert abs(rep.modularity - rrep["modularity"]) <= E2E_Q
+
+
+@pytest.mark.parametrize("name", ["planted", "lfr", "rmat_w"])
+def test_louvain_reference_stopping_bit_exact(dev, ctx, oracle, e2e_graphs, name):
+    """cd_louvain_config_reference: the reference's stopping rule alone
+    (H/louvain.hpp:78, :136-137), no pruning -- bit-exact vs the port."""
+    og = e2e_graphs[name]
+    g = _dev_of(dev, name, og)
+    kw = dict(move_theta=0, move_tol=0.0, move_stall=0.0, prune=False, move_qtol=0.0)
+    z_ref, k_ref, lv_ref = oracle.louvain_bucketed(og, seed=3, **kw)
+    z, rep = dev.run_louvain(g, dev.LouvainConfig.reference(seed=3))
+    assert np.array_equal(z, z_ref)
+    assert rep.community_count == k_ref and len(rep.levels) == lv_ref

@@ -51,6 +51,7 @@ def main():
     ap.add_argument("--workload", required=True)
     ap.add_argument("--out", required=True)
     ap.add_argument("--cmd", default="")
+    ap.add_argument("--runs", type=int, default=1, help="detector runs in the capture (per-step = total / runs)")
     a = ap.parse_args()
     rows = []
     with open(a.csv) as f:
@@ -101,7 +102,8 @@ def main():
         with open(path) as f:
             js = json.load(f)
     js[a.workload] = {fam: {"dram_bytes_per_launch": b / max(n, 1), "ms_per_launch": ms / max(n, 1),
-                            "launches": n, "share": ms / tot_ms}
+                            "launches": n, "share": ms / tot_ms, "dram_bytes_per_step": b / max(a.runs, 1),
+                            "ms_per_step": ms / max(a.runs, 1), "source": a.cmd or a.csv}
                       for fam, (ms, n, b) in by_f.items()}
     with open(path, "w") as f:
         json.dump(js, f, indent=1, sort_keys=True)

@@ -39,7 +39,8 @@ def main():
         print(a.workload, "run", i, "m", g.edge_count(), "Q", round(rep.modularity, 6), "k", rep.community_count,
               "ms", round(rep.total_ms, 3),
               "levels", [(l["nodes"], l["passes"], round(l["move_ms"], 2), round(l["coarsen_ms"], 2))
-                         for l in rep.levels], "iters", len(rep.iterations), flush=True)
+                         for l in rep.levels], "iters", [(it["updated"], round(it["ms"], 3)) for it in rep.iterations],
+              flush=True)
     if a.families:
         ctx.reset_stats()
         ctx.set_profiling(True)
