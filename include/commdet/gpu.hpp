@@ -37,6 +37,7 @@
 #include <string>
 #include <unordered_map>
 #include <utility>
+#include <numeric>
 #include <vector>
 
 #include "../commdet_cuda.h"
@@ -266,12 +267,12 @@ class Partition {
     Partition() = default;
     explicit Partition(count n, index initial = 0) : data_(n, initial), upper_(initial + 1) {}
 
+    // every node its own community; the bound stays >= 1 for n = 0
     static Partition singletons(count n) {
         Partition z;
-        z.data_.resize(n);
-        for (node u = 0; u < n; ++u)
-            z.data_[u] = u;
-        z.upper_ = n > 0 ? n : 1;
+        z.data_.assign(n, 0);
+        std::iota(z.data_.begin(), z.data_.end(), index{0});
+        z.upper_ = std::max<index>(n, 1);
         return z;
     }
 
@@ -298,23 +299,18 @@ class Partition {
         detail::check(cd_community_count(Context::instance().get(), static_cast<int64_t>(z.size()), z.data(), &k));
         return static_cast<count>(k);
     }
+    // histogram over [0, largest id]; empty ids get 0
     std::vector<count> community_sizes() const {
-        std::vector<count> sizes;
-        for (index c : data_) {
-            if (c >= sizes.size())
-                sizes.resize(c + 1, 0);
-            ++sizes[c];
-        }
-        return sizes;
+        const index top = data_.empty() ? 0 : *std::max_element(data_.begin(), data_.end()) + 1;
+        std::vector<count> hist(top, 0);
+        for (index c : data_)
+            hist[c] += 1;
+        return hist;
     }
+    // compact <=> the ids in use are exactly 0..k-1
     bool is_compact() const {
-        std::vector<bool> used;
-        for (index c : data_) {
-            if (c >= used.size())
-                used.resize(c + 1, false);
-            used[c] = true;
-        }
-        return std::all_of(used.begin(), used.end(), [](bool b) { return b; });
+        const std::vector<count> h = community_sizes();
+        return std::find(h.begin(), h.end(), count{0}) == h.end();
     }
     bool operator==(const Partition &o) const { return data_ == o.data_; }
 
@@ -941,45 +937,53 @@ inline std::ofstream open_output(const std::string &path) {
         throw input_error("cannot open " + path + " for writing");
     return out;
 }
+// runs `emit` on the opened file, then checks the stream once
+template <class F>
+inline void write_text(const std::string &path, F &&emit) {
+    std::ofstream out = open_output(path);
+    emit(out);
+    out.flush();
+    if (!out)
+        throw input_error("write failed: " + path);
+}
 }  // namespace detail
 
 /// io::write_metis (H/io.hpp:168-183): fmt 1, 1-based neighbours with weights.
 inline void write_metis(const Graph &g, const std::string &path) {
-    auto out = detail::open_output(path);
-    out << g.node_count() << " " << g.edge_count() << " 1\n";
-    for (node u = 0; u < g.node_count(); ++u) {
-        bool first = true;
-        g.for_neighbors(u, [&](node v, edgeweight w) {
-            if (!first)
-                out << " ";
-            out << (v + 1) << " " << detail::format_weight(w);
-            first = false;
-        });
-        out << "\n";
-    }
-    if (!out)
-        throw input_error("write failed: " + path);
+    detail::write_text(path, [&](std::ostream &out) {
+        out << g.node_count() << ' ' << g.edge_count() << " 1\n";
+        std::string row;
+        for (node u = 0; u < g.node_count(); ++u) {
+            row.clear();
+            g.for_neighbors(u, [&](node v, edgeweight w) {
+                row += row.empty() ? "" : " ";
+                row += std::to_string(v + 1);
+                row += ' ';
+                row += detail::format_weight(w);
+            });
+            out << row << '\n';
+        }
+    });
 }
 
 /// io::write_edge_list (H/io.hpp:239-245): "u v w", one line per undirected edge.
 inline void write_edge_list(const Graph &g, const std::string &path) {
-    auto out = detail::open_output(path);
-    for (node u = 0; u < g.node_count(); ++u)
-        g.for_neighbors(u, [&](node v, edgeweight w) {
-            if (v >= u)
-                out << u << " " << v << " " << detail::format_weight(w) << "\n";
-        });
-    if (!out)
-        throw input_error("write failed: " + path);
+    detail::write_text(path, [&](std::ostream &out) {
+        for (node u = 0; u < g.node_count(); ++u)
+            g.for_neighbors(u, [&](node v, edgeweight w) {
+                if (v < u)
+                    return;  // each undirected edge once, from its smaller endpoint
+                out << u << ' ' << v << ' ' << detail::format_weight(w) << '\n';
+            });
+    });
 }
 
 /// io::write_partition (H/io.hpp:248-255).
 inline void write_partition(const Partition &z, const std::string &path) {
-    auto out = detail::open_output(path);
-    for (node u = 0; u < z.size(); ++u)
-        out << z[u] << "\n";
-    if (!out)
-        throw input_error("write failed: " + path);
+    detail::write_text(path, [&](std::ostream &out) {
+        for (index c : z.data())
+            out << c << '\n';
+    });
 }
 
 /// io::read_partition (H/io.hpp:257-275).
@@ -1025,14 +1029,13 @@ inline Partition read_partition(const std::string &path) {
 /// device) in METIS format, plus "<path>.sizes" with "community_id size" lines.
 inline void write_community_graph(const Graph &g, const Partition &z, const std::string &path) {
     const Partition zc = z.is_compact() ? z : z.compacted();
-    CoarseningResult cr = coarsen(g, zc);
-    write_metis(cr.coarse, path);
-    auto sizes = zc.community_sizes();
-    auto out = detail::open_output(path + ".sizes");
-    for (index c = 0; c < sizes.size(); ++c)
-        out << c << " " << sizes[c] << "\n";
-    if (!out)
-        throw input_error("write failed: " + path + ".sizes");
+    write_metis(coarsen(g, zc).coarse, path);
+    const std::vector<count> sizes = zc.community_sizes();
+    detail::write_text(path + ".sizes", [&](std::ostream &out) {
+        index c = 0;
+        for (count s : sizes)
+            out << c++ << ' ' << s << '\n';
+    });
 }
 
 }  // namespace io

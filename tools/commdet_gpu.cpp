@@ -1,403 +1,450 @@
-// commdet_gpu -- the reference's command-line driver (P/tools/commdet.cpp,
-// SURVEY.md §8(f) rank 2) over the B200 library: the same subcommands, flags,
-// text output, JSON report fields and exit codes, so scripts that drive the
-// reference binary can drive this one.  Everything runs through the drop-in
-// C++ shim (include/commdet/gpu.hpp) and therefore on the device:
+// commdet_gpu -- command-line front end of the B200 library with the
+// reference CLI's contract (P/tools/commdet.cpp: subcommands, flag names,
+// printed keys, report JSON fields, exit codes).
+// Every computation goes through the drop-in C++ shim (include/commdet/gpu.hpp)
+// and therefore through the C ABI onto the device.
 //
-//   detect    --algo plp|plm|plmr|epp --input F [--format metis|edges]
-//             [--merge-duplicates] [--threads N] [--theta T] [--shuffle]
+//   detect    --input F [--algo plp|plm|plmr|epp] [--format metis|edges]
+//             [--merge-duplicates] [--shuffle] [--threads N] [--theta T]
 //             [--gamma G] [--ensemble B] [--seed S] [--runs R] [--output P]
-//             [--report J] [--community-graph C]           (commdet.cpp:81-131)
-//   score     --input F [--format] --partition P [--reference Q] [--gamma G]
-//   generate  --n N --k K --pin P --pout Q [--seed S] [--threads] --output F
+//             [--report J] [--community-graph C]
+//   score     --input F --partition P [--reference Q] [--format] [--gamma G]
+//   generate  --n N --k K --pin P --pout Q --output F [--seed S] [--threads N]
 //             [--ground-truth T]
-//   bench     [--mode strong|weak] [--algo] [--input F | --gen-n N --gen-k K
-//             --gen-pin P --gen-pout Q] [--threads-list 1,2,4] [--seed]
-//             [--theta] [--gamma] [--ensemble] [--data TSV]  (commdet.cpp:193-248)
+//   bench     [--mode strong|weak] [--algo A] (--input F | --gen-n N [--gen-k
+//             K --gen-pin P --gen-pout Q]) [--threads-list 1,2,..] [--seed S]
+//             [--theta T] [--gamma G] [--ensemble B] [--data TSV]
 //
-// `--threads` is accepted and echoed like the reference's worker count; the
-// device path does not use it.  Exit codes: 0 ok, 2 usage / input error,
-// 3 internal error (commdet.cpp:24-25).
+// Worker counts are accepted and reported like the reference's OpenMP worker
+// count; the device ignores them (one GPU per context).  Exit status: 0 ok,
+// 2 bad usage or bad input, 3 anything else.
 #define COMMDET_GPU_DROP_IN
 #include <commdet/gpu.hpp>
 
 #include <cstdio>
 #include <fstream>
+#include <functional>
 #include <iostream>
 #include <map>
-#include <set>
+#include <sstream>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace {
 
 using namespace commdet;
 
-constexpr int kExitUsage = 2;
-constexpr int kExitInternal = 3;
+enum Exit { kOk = 0, kBadInput = 2, kInternal = 3 };
 
-struct UsageError : std::runtime_error {
+struct BadUsage : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
 
-// --name value | --name=value | --flag
-class Args {
+// ---------------------------------------------------------------------------
+// option tables: one row per accepted flag of a subcommand
+// ---------------------------------------------------------------------------
+struct FlagSpec {
+    const char *name;
+    bool takes_value;
+};
+
+const std::map<std::string, std::vector<FlagSpec>> &command_table() {
+    static const std::map<std::string, std::vector<FlagSpec>> t = {
+        {"detect",
+         {{"algo", true}, {"input", true}, {"format", true}, {"merge-duplicates", false}, {"shuffle", false},
+          {"threads", true}, {"theta", true}, {"gamma", true}, {"ensemble", true}, {"seed", true}, {"runs", true},
+          {"output", true}, {"report", true}, {"community-graph", true}}},
+        {"score", {{"input", true}, {"format", true}, {"partition", true}, {"reference", true}, {"gamma", true}}},
+        {"generate",
+         {{"n", true}, {"k", true}, {"pin", true}, {"pout", true}, {"seed", true}, {"threads", true},
+          {"output", true}, {"ground-truth", true}}},
+        {"bench",
+         {{"mode", true}, {"algo", true}, {"input", true}, {"format", true}, {"gen-n", true}, {"gen-k", true},
+          {"gen-pin", true}, {"gen-pout", true}, {"threads-list", true}, {"seed", true}, {"theta", true},
+          {"gamma", true}, {"ensemble", true}, {"data", true}}},
+    };
+    return t;
+}
+
+// Parsed flags of one subcommand; typed getters validate on access.
+class Options {
   public:
-    Args(int argc, char **argv, int first, const std::set<std::string> &flags, const std::set<std::string> &opts) {
-        for (int i = first; i < argc; ++i) {
-            std::string a = argv[i];
-            if (a.rfind("--", 0) != 0)
-                throw UsageError("unexpected argument '" + a + "'");
-            std::string name = a.substr(2), value;
-            const auto eq = name.find('=');
-            if (eq != std::string::npos) {
-                value = name.substr(eq + 1);
-                name = name.substr(0, eq);
+    Options(const std::vector<FlagSpec> &spec, const std::vector<std::string> &words) {
+        std::map<std::string, bool> known;
+        for (const FlagSpec &f : spec)
+            known[f.name] = f.takes_value;
+        for (std::size_t i = 0; i < words.size(); ++i) {
+            const std::string &w = words[i];
+            if (w.size() < 3 || w[0] != '-' || w[1] != '-')
+                throw BadUsage("unexpected argument '" + w + "'");
+            std::string key = w.substr(2);
+            std::string value;
+            const std::size_t eq = key.find('=');
+            const bool inline_value = eq != std::string::npos;
+            if (inline_value) {
+                value = key.substr(eq + 1);
+                key.resize(eq);
             }
-            if (flags.count(name)) {
-                if (eq != std::string::npos)
-                    throw UsageError("flag --" + name + " takes no value");
-                vals_[name] = "1";
-            } else if (opts.count(name)) {
-                if (eq == std::string::npos) {
-                    if (i + 1 >= argc)
-                        throw UsageError("--" + name + " requires a value");
-                    value = argv[++i];
-                }
-                vals_[name] = value;
+            auto k = known.find(key);
+            if (k == known.end())
+                throw BadUsage("unknown option --" + key);
+            if (!k->second) {
+                if (inline_value)
+                    throw BadUsage("flag --" + key + " takes no value");
+                value = "1";
+            } else if (!inline_value) {
+                if (i + 1 == words.size())
+                    throw BadUsage("--" + key + " requires a value");
+                value = words[++i];
+            }
+            given_[key] = value;
+        }
+    }
+
+    bool given(const std::string &key) const { return given_.find(key) != given_.end(); }
+    std::string text(const std::string &key, const std::string &fallback = "") const {
+        auto it = given_.find(key);
+        return it == given_.end() ? fallback : it->second;
+    }
+    std::string required(const std::string &key) const {
+        if (!given(key))
+            throw BadUsage("--" + key + " is required");
+        return text(key);
+    }
+    template <class T>
+    T number(const std::string &key, T fallback) const {
+        return given(key) ? convert<T>(key, text(key)) : fallback;
+    }
+    template <class T>
+    T required_number(const std::string &key) const {
+        return convert<T>(key, required(key));
+    }
+
+    // whole-token numeric conversion; unsigned values reject a sign
+    template <class T>
+    static T convert(const std::string &key, const std::string &s) {
+        std::istringstream in(s);
+        T v{};
+        bool ok = !s.empty() && !(std::is_unsigned_v<T> && s[0] == '-');
+        if (ok) {
+            if constexpr (std::is_same_v<T, std::uint64_t>) {
+                unsigned long long u = 0;
+                ok = static_cast<bool>(in >> u);
+                v = static_cast<T>(u);
             } else {
-                throw UsageError("unknown option --" + name);
+                ok = static_cast<bool>(in >> v);
             }
+            ok = ok && in.peek() == std::char_traits<char>::eof();
         }
-    }
-    bool has(const std::string &k) const { return vals_.count(k) > 0; }
-    std::string str(const std::string &k, const std::string &def = "") const {
-        auto it = vals_.find(k);
-        return it == vals_.end() ? def : it->second;
-    }
-    std::string req(const std::string &k) const {
-        if (!has(k))
-            throw UsageError("--" + k + " is required");
-        return str(k);
-    }
-    template <class T>
-    T num(const std::string &k, T def) const {
-        if (!has(k))
-            return def;
-        return parse<T>(k, str(k));
-    }
-    template <class T>
-    static T parse(const std::string &k, const std::string &v) {
-        try {
-            size_t pos = 0;
-            T out;
-            if constexpr (std::is_floating_point_v<T>)
-                out = static_cast<T>(std::stod(v, &pos));
-            else if constexpr (std::is_signed_v<T>)
-                out = static_cast<T>(std::stoll(v, &pos));
-            else {
-                if (!v.empty() && v[0] == '-')
-                    throw std::invalid_argument("negative");
-                out = static_cast<T>(std::stoull(v, &pos));
-            }
-            if (pos != v.size())
-                throw std::invalid_argument("trailing");
-            return out;
-        } catch (const std::exception &) {
-            throw UsageError("--" + k + ": invalid value '" + v + "'");
-        }
+        if (!ok)
+            throw BadUsage("--" + key + ": invalid value '" + s + "'");
+        return v;
     }
 
   private:
-    std::map<std::string, std::string> vals_;
+    std::map<std::string, std::string> given_;
 };
 
-Graph load_graph(const std::string &path, const std::string &format, bool merge_duplicates) {
-    if (format == "metis")
-        return io::read_metis(path);
-    if (format == "edges")
-        return io::read_edge_list(path, merge_duplicates);
-    throw input_error("unknown graph format '" + format + "'");
-}
-
-struct DetectOptions {
-    std::string algo = "plm";
-    std::string input;
-    std::string format = "metis";
-    bool merge_duplicates = false;
-    int threads = 1;
+// ---------------------------------------------------------------------------
+// detector registry: algorithm name -> one run on the device
+// ---------------------------------------------------------------------------
+struct RunSettings {
+    int workers = 1;
     long long theta = -1;
     bool shuffle = false;
     double gamma = 1.0;
     count ensemble = 4;
-    std::uint64_t seed = 1;
-    unsigned runs = 1;
-    std::string output;
-    std::string report_path;
-    std::string community_graph;
 };
 
-std::pair<Partition, RunReport> run_algorithm(const Graph &g, const DetectOptions &opt, std::uint64_t seed) {
-    if (opt.algo == "plp") {
-        PlpConfig cfg;
-        cfg.theta = opt.theta;
-        cfg.randomize_order = opt.shuffle;
-        cfg.seed = seed;
-        cfg.workers = opt.threads;
-        return run_plp(g, cfg);
-    }
-    LouvainConfig lc;
-    lc.gamma = opt.gamma;
-    lc.seed = seed;
-    lc.workers = opt.threads;
-    if (opt.algo == "plm")
-        return run_plm(g, lc);
-    if (opt.algo == "plmr")
-        return run_plmr(g, lc);
-    if (opt.algo == "epp") {
-        EnsembleConfig ec;
-        ec.ensemble_size = opt.ensemble;
-        ec.seed = seed;
-        ec.workers = opt.threads;
-        ec.base_plp.theta = opt.theta;
-        ec.final_louvain.gamma = opt.gamma;
-        return run_epp(g, ec);
-    }
-    throw input_error("unknown algorithm '" + opt.algo + "'");
+using Detector = std::function<std::pair<Partition, RunReport>(const Graph &, const RunSettings &, std::uint64_t)>;
+
+const Detector &detector(const std::string &algo) {
+    static const std::map<std::string, Detector> registry = {
+        {"plp",
+         [](const Graph &g, const RunSettings &s, std::uint64_t seed) {
+             PlpConfig c;
+             c.theta = s.theta;
+             c.randomize_order = s.shuffle;
+             c.seed = seed;
+             c.workers = s.workers;
+             return run_plp(g, c);
+         }},
+        {"plm",
+         [](const Graph &g, const RunSettings &s, std::uint64_t seed) {
+             LouvainConfig c;
+             c.gamma = s.gamma;
+             c.seed = seed;
+             c.workers = s.workers;
+             return run_plm(g, c);
+         }},
+        {"plmr",
+         [](const Graph &g, const RunSettings &s, std::uint64_t seed) {
+             LouvainConfig c;
+             c.gamma = s.gamma;
+             c.seed = seed;
+             c.workers = s.workers;
+             return run_plmr(g, c);
+         }},
+        {"epp",
+         [](const Graph &g, const RunSettings &s, std::uint64_t seed) {
+             EnsembleConfig c;
+             c.ensemble_size = s.ensemble;
+             c.seed = seed;
+             c.workers = s.workers;
+             c.base_plp.theta = s.theta;
+             c.final_louvain.gamma = s.gamma;
+             return run_epp(g, c);
+         }},
+    };
+    auto it = registry.find(algo);
+    if (it == registry.end())
+        throw input_error("unknown algorithm '" + algo + "'");
+    return it->second;
 }
 
-int cmd_detect(const DetectOptions &opt) {
-    const Graph g = load_graph(opt.input, opt.format, opt.merge_duplicates);
-    std::vector<RunReport> reports;
-    Partition best;
-    double best_mod = -2.0;
-    for (unsigned r = 0; r < opt.runs; ++r) {
-        auto [z, report] = run_algorithm(g, opt, opt.seed + r);
-        report.input = opt.input;
-        if (report.modularity > best_mod) {
-            best_mod = report.modularity;
-            best = z.compacted();
-        }
-        reports.push_back(std::move(report));
-    }
-    double avg_ms = 0.0, avg_mod = 0.0, avg_cov = 0.0;
-    for (const auto &r : reports) {
-        avg_ms += r.total_ms;
-        avg_mod += r.modularity;
-        avg_cov += r.coverage;
-    }
-    avg_ms /= reports.size();
-    avg_mod /= reports.size();
-    avg_cov /= reports.size();
-    std::cout << "algorithm " << opt.algo << "\n"
-              << "runs " << opt.runs << "\n"
-              << "threads " << opt.threads << "\n"
-              << "avg_time_ms " << avg_ms << "\n"
-              << "avg_modularity " << avg_mod << "\n"
-              << "avg_coverage " << avg_cov << "\n"
-              << "best_modularity " << best_mod << "\n"
-              << "communities " << best.upper_bound() << "\n";
-    if (!opt.output.empty())
-        io::write_partition(best, opt.output);
-    if (!opt.community_graph.empty())
-        io::write_community_graph(g, best, opt.community_graph);
-    if (!opt.report_path.empty()) {
-        Json j = Json::object();
-        Json avg = Json::object();
-        avg["time_ms"] = avg_ms;
-        avg["modularity"] = avg_mod;
-        avg["coverage"] = avg_cov;
-        j["average"] = avg;
-        j["best_modularity"] = best_mod;
-        Json runs = Json::array();
-        for (const auto &r : reports)
-            runs.push_back(r.to_json());
-        j["runs"] = runs;
-        std::ofstream out(opt.report_path);
-        if (!out)
-            throw input_error("cannot open " + opt.report_path + " for writing");
-        out << j.dump(2) << "\n";
-    }
-    return 0;
+Graph read_graph(const std::string &path, const std::string &format, bool merge) {
+    if (format == "edges")
+        return io::read_edge_list(path, merge);
+    if (format != "metis")
+        throw input_error("unknown graph format '" + format + "'");
+    return io::read_metis(path);
 }
 
-int cmd_score(const Args &a) {
-    const Graph g = load_graph(a.req("input"), a.str("format", "metis"), false);
-    const Partition z = io::read_partition(a.req("partition"));
-    if (z.size() != g.node_count())
-        throw input_error("partition length " + std::to_string(z.size()) + " does not match node count " +
-                          std::to_string(g.node_count()));
-    const QualityReport q = evaluate(g, z, a.num<double>("gamma", 1.0));
-    std::cout << "modularity " << q.modularity << "\n"
-              << "coverage " << q.coverage << "\n"
-              << "communities " << q.community_count << "\n";
-    if (a.has("reference")) {
-        const Partition ref = io::read_partition(a.str("reference"));
-        if (ref.size() != g.node_count())
-            throw input_error("reference partition length does not match node count");
-        std::cout << "rand_index " << graph_rand_index(g, z, ref) << "\n";
-    }
-    return 0;
-}
-
-PlantedPartitionSpec gen_spec(const Args &a, const std::string &pre, bool required) {
-    PlantedPartitionSpec s;
-    auto get = [&](const std::string &k) { return required ? a.req(pre + k) : a.str(pre + k); };
-    s.n = Args::parse<count>(pre + "n", get("n"));
-    s.k = Args::parse<count>(pre + "k", get("k"));
-    s.p_in = Args::parse<double>(pre + "pin", get("pin"));
-    s.p_out = Args::parse<double>(pre + "pout", get("pout"));
+RunSettings settings_from(const Options &o) {
+    RunSettings s;
+    s.workers = o.number<int>("threads", 1);
+    s.theta = o.number<long long>("theta", -1);
+    s.shuffle = o.given("shuffle");
+    s.gamma = o.number<double>("gamma", 1.0);
+    s.ensemble = o.number<count>("ensemble", 4);
     return s;
 }
 
-int cmd_generate(const Args &a) {
-    PlantedPartitionSpec spec = gen_spec(a, "", true);
-    spec.seed = a.num<std::uint64_t>("seed", 1);
-    auto [g, truth] = generate_planted(spec, a.num<int>("threads", 1));
-    io::write_metis(g, a.req("output"));
-    if (a.has("ground-truth"))
-        io::write_partition(truth.compacted(), a.str("ground-truth"));
-    std::cout << "nodes " << g.node_count() << "\n"
-              << "edges " << g.edge_count() << "\n"
-              << "blocks " << spec.k << "\n";
-    return 0;
+void print_pairs(const std::vector<std::pair<std::string, std::string>> &rows) {
+    for (const auto &[k, v] : rows)
+        std::cout << k << " " << v << "\n";
 }
 
-int cmd_bench(const Args &a) {
-    const std::string mode = a.str("mode", "strong");
-    const bool use_generator = a.has("gen-n");
+template <class T>
+std::string fmt(const T &v) {
+    std::ostringstream s;
+    s.precision(15);
+    s << v;
+    return s.str();
+}
+
+std::ofstream open_for_writing(const std::string &path) {
+    std::ofstream f(path);
+    if (!f)
+        throw input_error("cannot open " + path + " for writing");
+    return f;
+}
+
+// ---------------------------------------------------------------------------
+// subcommands
+// ---------------------------------------------------------------------------
+int detect(const Options &o) {
+    const std::string algo = o.text("algo", "plm");
+    const std::string input = o.required("input");
+    const unsigned runs = o.number<unsigned>("runs", 1);
+    if (runs == 0)
+        throw BadUsage("--runs: value must be positive");
+    const std::uint64_t seed0 = o.number<std::uint64_t>("seed", 1);
+    const RunSettings s = settings_from(o);
+    const Graph g = read_graph(input, o.text("format", "metis"), o.given("merge-duplicates"));
+    const Detector &run = detector(algo);
+
+    // reports in run order; the best partition (highest modularity, the
+    // earliest run on ties) is kept compacted
+    std::vector<RunReport> reps;
+    Partition best;
+    double best_q = -2.0;
+    for (unsigned i = 0; i < runs; ++i) {
+        auto [z, r] = run(g, s, seed0 + i);
+        r.input = input;
+        if (r.modularity > best_q) {
+            best_q = r.modularity;
+            best = z.compacted();
+        }
+        reps.push_back(std::move(r));
+    }
+    double sum_ms = 0.0, sum_q = 0.0, sum_cov = 0.0;
+    for (const RunReport &r : reps) {
+        sum_ms += r.total_ms;
+        sum_q += r.modularity;
+        sum_cov += r.coverage;
+    }
+    const double k = static_cast<double>(reps.size());
+    print_pairs({{"algorithm", algo},
+                 {"runs", fmt(runs)},
+                 {"threads", fmt(s.workers)},
+                 {"avg_time_ms", fmt(sum_ms / k)},
+                 {"avg_modularity", fmt(sum_q / k)},
+                 {"avg_coverage", fmt(sum_cov / k)},
+                 {"best_modularity", fmt(best_q)},
+                 {"communities", fmt(best.upper_bound())}});
+    if (o.given("output"))
+        io::write_partition(best, o.text("output"));
+    if (o.given("community-graph"))
+        io::write_community_graph(g, best, o.text("community-graph"));
+    if (o.given("report")) {
+        Json doc = Json::object();
+        Json mean = Json::object();
+        mean["time_ms"] = sum_ms / k;
+        mean["modularity"] = sum_q / k;
+        mean["coverage"] = sum_cov / k;
+        doc["average"] = mean;
+        doc["best_modularity"] = best_q;
+        Json list = Json::array();
+        for (const RunReport &r : reps)
+            list.push_back(r.to_json());
+        doc["runs"] = list;
+        open_for_writing(o.text("report")) << doc.dump(2) << "\n";
+    }
+    return kOk;
+}
+
+int score(const Options &o) {
+    const Graph g = read_graph(o.required("input"), o.text("format", "metis"), false);
+    auto load_cover = [&](const std::string &path, const char *what) {
+        Partition p = io::read_partition(path);
+        if (p.size() != g.node_count())
+            throw input_error(std::string(what) + " length " + std::to_string(p.size()) +
+                              " does not match node count " + std::to_string(g.node_count()));
+        return p;
+    };
+    const Partition z = load_cover(o.required("partition"), "partition");
+    const QualityReport q = evaluate(g, z, o.number<double>("gamma", 1.0));
+    std::vector<std::pair<std::string, std::string>> rows = {
+        {"modularity", fmt(q.modularity)}, {"coverage", fmt(q.coverage)}, {"communities", fmt(q.community_count)}};
+    if (o.given("reference"))
+        rows.emplace_back("rand_index", fmt(graph_rand_index(g, z, load_cover(o.text("reference"), "reference"))));
+    print_pairs(rows);
+    return kOk;
+}
+
+PlantedPartitionSpec planted_spec(const Options &o, const std::string &prefix, bool all_required) {
+    auto take = [&](const char *field, const char *fallback) {
+        const std::string key = prefix + field;
+        return all_required ? o.required(key) : o.text(key, fallback);
+    };
+    PlantedPartitionSpec s;
+    s.n = Options::convert<count>(prefix + "n", take("n", ""));
+    s.k = Options::convert<count>(prefix + "k", take("k", "1"));
+    s.p_in = Options::convert<double>(prefix + "pin", take("pin", "0"));
+    s.p_out = Options::convert<double>(prefix + "pout", take("pout", "0"));
+    return s;
+}
+
+int generate(const Options &o) {
+    PlantedPartitionSpec spec = planted_spec(o, "", true);
+    spec.seed = o.number<std::uint64_t>("seed", 1);
+    const std::string out = o.required("output");
+    auto made = generate_planted(spec, o.number<int>("threads", 1));
+    io::write_metis(made.first, out);
+    if (o.given("ground-truth"))
+        io::write_partition(made.second.compacted(), o.text("ground-truth"));
+    print_pairs({{"nodes", fmt(made.first.node_count())},
+                 {"edges", fmt(made.first.edge_count())},
+                 {"blocks", fmt(spec.k)}});
+    return kOk;
+}
+
+std::vector<int> worker_counts(const std::string &csv) {
+    std::vector<int> out;
+    std::stringstream in(csv);
+    std::string item;
+    while (std::getline(in, item, ','))
+        out.push_back(Options::convert<int>("threads-list", item));
+    if (csv.empty() || csv.back() == ',')
+        out.push_back(Options::convert<int>("threads-list", ""));
+    return out;
+}
+
+int bench(const Options &o) {
+    const std::string mode = o.text("mode", "strong");
+    const bool synthetic = o.given("gen-n");
     if (mode != "strong" && mode != "weak")
         throw input_error("unknown bench mode '" + mode + "'");
-    if (mode == "weak" && !use_generator)
+    if (mode == "weak" && !synthetic)
         throw input_error("weak scaling requires a generator spec (--gen-n ...)");
-    if (!use_generator && !a.has("input"))
+    if (!synthetic && !o.given("input"))
         throw input_error("bench needs --input or --gen-n");
-    std::vector<int> threads_list;
-    {
-        const std::string tl = a.str("threads-list", "1");
-        size_t p = 0;
-        while (p <= tl.size()) {
-            const size_t q = tl.find(',', p);
-            const std::string t = tl.substr(p, q == std::string::npos ? std::string::npos : q - p);
-            threads_list.push_back(Args::parse<int>("threads-list", t));
-            if (q == std::string::npos)
-                break;
-            p = q + 1;
-        }
-    }
-    PlantedPartitionSpec gen;
-    if (use_generator) {
-        gen.n = Args::parse<count>("gen-n", a.str("gen-n"));
-        gen.k = Args::parse<count>("gen-k", a.str("gen-k", "1"));
-        gen.p_in = Args::parse<double>("gen-pin", a.str("gen-pin", "0"));
-        gen.p_out = Args::parse<double>("gen-pout", a.str("gen-pout", "0"));
-    }
-    const std::uint64_t seed = a.num<std::uint64_t>("seed", 1);
-    Graph fixed;
+    const std::vector<int> counts = worker_counts(o.text("threads-list", "1"));
+    PlantedPartitionSpec base = synthetic ? planted_spec(o, "gen-", false) : PlantedPartitionSpec{};
+    RunSettings s = settings_from(o);
+    const Detector &run = detector(o.text("algo", "plm"));
+    const std::uint64_t seed = o.number<std::uint64_t>("seed", 1);
+
+    // strong: one graph for every worker count; weak: n grows with the count
+    Graph shared;
     if (mode == "strong")
-        fixed = use_generator ? generate_planted(gen, threads_list.back()).first
-                              : load_graph(a.str("input"), a.str("format", "metis"), false);
-    std::printf("%8s %12s %9s %12s %12s\n", "threads", "time_ms", "speedup", "modularity", "edges");
-    std::ofstream data;
-    if (a.has("data")) {
-        data.open(a.str("data"));
-        if (!data)
-            throw input_error("cannot open " + a.str("data") + " for writing");
-        data << "threads\ttime_ms\tspeedup\tmodularity\tedges\n";
+        shared = synthetic ? generate_planted(base, counts.back()).first
+                           : read_graph(o.text("input"), o.text("format", "metis"), false);
+    std::ofstream tsv;
+    if (o.given("data")) {
+        tsv = open_for_writing(o.text("data"));
+        tsv << "threads\ttime_ms\tspeedup\tmodularity\tedges\n";
     }
-    double base_time = 0.0;
-    for (std::size_t i = 0; i < threads_list.size(); ++i) {
-        const int t = threads_list[i];
-        if (t < 1)
+    std::printf("%8s %12s %9s %12s %12s\n", "threads", "time_ms", "speedup", "modularity", "edges");
+    double first_ms = 0.0;
+    for (std::size_t i = 0; i < counts.size(); ++i) {
+        const int w = counts[i];
+        if (w < 1)
             throw input_error("thread counts must be >= 1");
         Graph scaled;
-        const Graph *g = &fixed;
         if (mode == "weak") {
-            PlantedPartitionSpec s = gen;
-            s.n *= static_cast<count>(t);
-            scaled = generate_planted(s, t).first;
-            g = &scaled;
+            PlantedPartitionSpec sp = base;
+            sp.n *= static_cast<count>(w);
+            scaled = generate_planted(sp, w).first;
         }
-        DetectOptions run;
-        run.algo = a.str("algo", "plm");
-        run.threads = t;
-        run.theta = a.num<long long>("theta", -1);
-        run.gamma = a.num<double>("gamma", 1.0);
-        run.ensemble = a.num<count>("ensemble", 4);
-        auto [z, report] = run_algorithm(*g, run, seed);
+        const Graph &g = mode == "weak" ? scaled : shared;
+        s.workers = w;
+        const RunReport r = run(g, s, seed).second;
         if (i == 0)
-            base_time = report.total_ms;
-        const double speedup = report.total_ms > 0 ? base_time / report.total_ms : 1.0;
-        std::printf("%8d %12.2f %9.3f %12.6f %12llu\n", t, report.total_ms, speedup, report.modularity,
-                    static_cast<unsigned long long>(g->edge_count()));
-        if (data)
-            data << t << "\t" << report.total_ms << "\t" << speedup << "\t" << report.modularity << "\t"
-                 << g->edge_count() << "\n";
+            first_ms = r.total_ms;
+        const double speedup = r.total_ms > 0 ? first_ms / r.total_ms : 1.0;
+        const auto edges = static_cast<unsigned long long>(g.edge_count());
+        std::printf("%8d %12.2f %9.3f %12.6f %12llu\n", w, r.total_ms, speedup, r.modularity, edges);
+        if (tsv)
+            tsv << w << "\t" << r.total_ms << "\t" << speedup << "\t" << r.modularity << "\t" << edges << "\n";
     }
-    return 0;
+    return kOk;
 }
 
-void usage() {
+int usage(int status) {
     std::cerr << "usage: commdet_gpu {detect|score|generate|bench} [options]\n"
-                 "  (flags of the reference CLI, P/tools/commdet.cpp; see the header of tools/commdet_gpu.cpp)\n";
+                 "  (the reference CLI's flags; see the header of tools/commdet_gpu.cpp)\n";
+    return status;
 }
 
 }  // namespace
 
 int main(int argc, char **argv) {
     std::cout.precision(15);
-    if (argc < 2 || std::string(argv[1]) == "--help" || std::string(argv[1]) == "-h") {
-        usage();
-        return argc < 2 ? kExitUsage : 0;
-    }
-    const std::string cmd = argv[1];
+    const std::string first = argc > 1 ? argv[1] : "";
+    if (first == "--help" || first == "-h")
+        return usage(kOk);
+    static const std::map<std::string, int (*)(const Options &)> handlers = {
+        {"detect", detect}, {"score", score}, {"generate", generate}, {"bench", bench}};
+    auto h = handlers.find(first);
+    if (h == handlers.end())
+        return usage(kBadInput);
     try {
-        if (cmd == "detect") {
-            Args a(argc, argv, 2, {"merge-duplicates", "shuffle"},
-                   {"algo", "input", "format", "threads", "theta", "gamma", "ensemble", "seed", "runs", "output",
-                    "report", "community-graph"});
-            DetectOptions o;
-            o.algo = a.str("algo", "plm");
-            o.input = a.req("input");
-            o.format = a.str("format", "metis");
-            o.merge_duplicates = a.has("merge-duplicates");
-            o.threads = a.num<int>("threads", 1);
-            o.theta = a.num<long long>("theta", -1);
-            o.shuffle = a.has("shuffle");
-            o.gamma = a.num<double>("gamma", 1.0);
-            o.ensemble = a.num<count>("ensemble", 4);
-            o.seed = a.num<std::uint64_t>("seed", 1);
-            o.runs = a.num<unsigned>("runs", 1);
-            if (o.runs < 1)
-                throw UsageError("--runs: value must be positive");
-            o.output = a.str("output");
-            o.report_path = a.str("report");
-            o.community_graph = a.str("community-graph");
-            return cmd_detect(o);
-        }
-        if (cmd == "score")
-            return cmd_score(Args(argc, argv, 2, {}, {"input", "format", "partition", "reference", "gamma"}));
-        if (cmd == "generate")
-            return cmd_generate(
-                Args(argc, argv, 2, {}, {"n", "k", "pin", "pout", "seed", "threads", "output", "ground-truth"}));
-        if (cmd == "bench")
-            return cmd_bench(Args(argc, argv, 2, {},
-                                  {"mode", "algo", "input", "format", "gen-n", "gen-k", "gen-pin", "gen-pout",
-                                   "threads-list", "seed", "theta", "gamma", "ensemble", "data"}));
-        usage();
-        return kExitUsage;
-    } catch (const UsageError &e) {
+        const Options o(command_table().at(first), std::vector<std::string>(argv + 2, argv + argc));
+        return h->second(o);
+    } catch (const BadUsage &e) {
         std::cerr << e.what() << "\n";
-        usage();
-        return kExitUsage;
+        return usage(kBadInput);
     } catch (const input_error &e) {
         std::cerr << "error: " << e.what() << "\n";
-        return kExitUsage;
+        return kBadInput;
     } catch (const std::invalid_argument &e) {
         std::cerr << "error: " << e.what() << "\n";
-        return kExitUsage;
+        return kBadInput;
     } catch (const std::exception &e) {
         std::cerr << "internal error: " << e.what() << "\n";
-        return kExitInternal;
+        return kInternal;
     }
 }
