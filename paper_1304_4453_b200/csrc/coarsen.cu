@@ -238,7 +238,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
                       static_cast<const int64_t *>(fpre.p), static_cast<const int64_t *>(cg->off.p),
                       static_cast<const int32_t *>(tkey.p), static_cast<const double *>(tval.p), cg->col.p,
                       cg->w.p);
-            graph_finalize(ctx, cg);
+            graph_finalize(ctx, cg, g->int_weights);
         } catch (...) {
             delete cg;
             throw;
@@ -339,7 +339,7 @@ cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t 
             }
             CD_LAUNCH(ctx, "coarsen.prep", k_fill_i64, 1, 32, 0, int64_t(1), D, cg->off.p + nc);
         }
-        graph_finalize(ctx, cg);
+        graph_finalize(ctx, cg, g->int_weights);
     } catch (...) {
         delete cg;
         throw;

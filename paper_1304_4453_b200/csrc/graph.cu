@@ -62,13 +62,257 @@ __global__ void __launch_bounds__(256) k_finalize(int64_t n, const int64_t *off,
     }
 }
 
-void graph_finalize(cd_ctx *ctx, cd_graph *g) {
+// ---------------------------------------------------------------------------
+// entry-parallel passes over a CSR: a thread per CSR_CHUNK consecutive
+// entries finds its first row by binary search and walks the row boundaries,
+// so hubs and the many tiny / empty rows of R-MAT cost the same per entry
+// (a warp per row spent most of its time on 16.7M mostly short or empty rows:
+// C3 finalize 8.8 ms -> one read of the columns)
+// ---------------------------------------------------------------------------
+constexpr int CSR_CHUNK = 16;
+
+__device__ __forceinline__ int64_t row_of_entry(int64_t n, const int64_t *off, int64_t i) {
+    int64_t lo = 0, hi = n - 1;  // last r with off[r] <= i (clamped: offsets may be invalid here)
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (off[mid] <= i)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+// offsets: off[0] = 0, nondecreasing, off[n] = D
+__global__ void k_check_offsets(int64_t n, int64_t D, const int64_t *off, int64_t *flag) {
+    bool bad = false;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t s = off[u], e = off[u + 1];
+        bad |= s > e || s < 0 || e > D || (u == 0 && s != 0) || (u == n - 1 && e != D);
+    }
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
+        flag[0] = 1;
+}
+
+// ranges, strictly ascending rows, weights > 0; FIN (unweighted graphs): also
+// the self-loop count per row and the number of entries with v >= u (= m = w(E))
+template <bool FIN>
+__global__ void __launch_bounds__(256) k_csr_entries(int64_t n, int64_t D, const int64_t *off, const int32_t *col,
+                                                    const float *w, int64_t *flag, int32_t *loops,
+                                                    unsigned long long *m_acc) {
+    bool bad = false;
+    unsigned long long m_loc = 0;
+    for (int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * CSR_CHUNK; i0 < D;
+         i0 += static_cast<int64_t>(gridDim.x) * blockDim.x * CSR_CHUNK) {
+        int64_t r = row_of_entry(n, off, i0);
+        int64_t rs = off[r], re = off[r + 1];
+        const int64_t i1 = min(i0 + CSR_CHUNK, D);
+        int32_t prev = i0 > 0 ? col[i0 - 1] : 0;
+        for (int64_t i = i0; i < i1; ++i) {
+            for (int guard = 0; i >= re && r + 1 < n && guard < 64; ++guard) {  // next nonempty row
+                ++r;
+                rs = re;
+                re = off[r + 1];
+            }
+            if (i >= re) {  // more advance than the guard allows: finish by search
+                r = row_of_entry(n, off, i);
+                rs = off[r];
+                re = off[r + 1];
+            }
+            const int32_t c = col[i];
+            bad |= c < 0 || c >= n || (i > rs && prev >= c);
+            if (w)
+                bad |= !(w[i] > 0.0f);
+            if (FIN && c >= r) {
+                ++m_loc;
+                if (c == r)
+                    atomicAdd(&loops[r], 1);
+            }
+            prev = c;
+        }
+    }
+    if (__any_sync(0xffffffffu, bad) && lane_id() == 0)
+        flag[0] = 1;
+    if (FIN) {
+        m_loc = warp_sum(m_loc);
+        if (lane_id() == 0 && m_loc)
+            atomicAdd(m_acc, m_loc);
+    }
+}
+
+// integral weights (contractions of integer-weight graphs): per-row sums are
+// exact in fp64 in any order, so the same entry-parallel walk sums each run
+// of a row's entries in a register and adds it to the row once (rows split
+// across threads add one partial per thread)
+__global__ void __launch_bounds__(256) k_csr_entries_intw(int64_t n, int64_t D, const int64_t *off,
+                                                         const int32_t *col, const float *w, double *vsum,
+                                                         double *loop, unsigned long long *acc,
+                                                         double *tot_acc) {
+    unsigned long long m_loc = 0, frac = 0;
+    double tot = 0.0;
+    for (int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * CSR_CHUNK; i0 < D;
+         i0 += static_cast<int64_t>(gridDim.x) * blockDim.x * CSR_CHUNK) {
+        int64_t r = row_of_entry(n, off, i0);
+        int64_t re = off[r + 1];
+        const int64_t i1 = min(i0 + CSR_CHUNK, D);
+        double run = 0.0;
+        for (int64_t i = i0; i < i1; ++i) {
+            if (i >= re) {
+                if (run != 0.0)
+                    atomicAdd(&vsum[r], run);
+                run = 0.0;
+                for (int guard = 0; i >= re && r + 1 < n && guard < 64; ++guard)
+                    re = off[++r + 1];
+                if (i >= re) {
+                    r = row_of_entry(n, off, i);
+                    re = off[r + 1];
+                }
+            }
+            const int32_t c = col[i];
+            const double wt = static_cast<double>(w[i]);
+            frac |= wt != floor(wt);
+            run += wt;
+            if (c >= r) {
+                ++m_loc;
+                tot += wt;
+                if (c == r)
+                    atomicAdd(&loop[r], wt);
+            }
+        }
+        if (run != 0.0)
+            atomicAdd(&vsum[r], run);
+    }
+    m_loc = warp_sum(m_loc);
+    tot = warp_sum(tot);
+    frac = __any_sync(0xffffffffu, frac != 0);
+    if (lane_id() == 0) {
+        if (m_loc)
+            atomicAdd(&acc[0], m_loc);
+        if (frac)
+            atomicOr(&acc[3], 1ULL);
+        if (tot != 0.0)
+            atomicAdd(tot_acc, tot);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_finalize_nodes_w(int64_t n, const int64_t *off, double *vol,
+                                                          const double *loop, int64_t *acc_i) {
+    int64_t maxdeg = 0, iso = 0;
+    double maxvol = 0.0;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t d = off[u + 1] - off[u];
+        const double v = vol[u] + loop[u];  // the loop twice
+        vol[u] = v;
+        maxdeg = max(maxdeg, d);
+        maxvol = fmax(maxvol, v);
+        iso += d == 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        maxdeg = max(maxdeg, __shfl_xor_sync(0xffffffffu, maxdeg, o));
+        maxvol = fmax(maxvol, __shfl_xor_sync(0xffffffffu, maxvol, o));
+        iso += __shfl_xor_sync(0xffffffffu, iso, o);
+    }
+    if (lane_id() == 0) {
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[1]), static_cast<unsigned long long>(maxdeg));
+        atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[2]), static_cast<unsigned long long>(iso));
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[4]),
+                  static_cast<unsigned long long>(__double_as_longlong(maxvol)));
+    }
+}
+
+// unweighted finalize, per node: vol = degree + loop (the loop twice)
+__global__ void __launch_bounds__(256) k_finalize_unweighted(int64_t n, const int64_t *off, const int32_t *loops,
+                                                             double *vol, double *loop, int64_t *acc_i) {
+    int64_t maxdeg = 0, iso = 0;
+    double maxvol = 0.0;
+    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+         u += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t d = off[u + 1] - off[u];
+        const double lp = static_cast<double>(loops[u]);
+        vol[u] = static_cast<double>(d) + lp;
+        loop[u] = lp;
+        maxdeg = max(maxdeg, d);
+        maxvol = fmax(maxvol, static_cast<double>(d) + lp);
+        iso += d == 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        maxdeg = max(maxdeg, __shfl_xor_sync(0xffffffffu, maxdeg, o));
+        maxvol = fmax(maxvol, __shfl_xor_sync(0xffffffffu, maxvol, o));
+        iso += __shfl_xor_sync(0xffffffffu, iso, o);
+    }
+    if (lane_id() == 0) {
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[1]), static_cast<unsigned long long>(maxdeg));
+        atomicAdd(reinterpret_cast<unsigned long long *>(&acc_i[2]), static_cast<unsigned long long>(iso));
+        atomicMax(reinterpret_cast<unsigned long long *>(&acc_i[4]),
+                  static_cast<unsigned long long>(__double_as_longlong(maxvol)));
+    }
+}
+
+void graph_finalize(cd_ctx *ctx, cd_graph *g, bool integral_weights) {
     g->vol.alloc(ctx, std::max<int64_t>(g->n, 1));
     g->loop.alloc(ctx, std::max<int64_t>(g->n, 1));
     DBuf<int64_t> acc_i(ctx, 5);
     DBuf<double> acc_d(ctx, 1);
     acc_i.zero();
     acc_d.zero();
+    if (g->n > 0 && !g->weighted) {
+        // integer counts: order-free, so entry-parallel (m = w(E) = entries with v >= u)
+        DBuf<int32_t> loops(ctx, g->n);
+        loops.zero();
+        DBuf<int64_t> flag(ctx, 1);
+        const int eg = grid_for((g->D + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32);
+        if (g->D)
+            CD_LAUNCH(ctx, "finalize", k_csr_entries<true>, eg, 256, 0, g->n, g->D,
+                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                      static_cast<const float *>(nullptr), flag.p, loops.p,
+                      reinterpret_cast<unsigned long long *>(acc_i.p));
+        CD_LAUNCH(ctx, "finalize", k_finalize_unweighted, grid_for(g->n, 256, ctx->num_sms * 16), 256, 0, g->n,
+                  static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(loops.p), g->vol.p,
+                  g->loop.p, acc_i.p);
+        int64_t hi[5];
+        CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        g->m = hi[0];
+        g->max_degree = hi[1];
+        g->isolated = hi[2];
+        std::memcpy(&g->max_vol, &hi[4], sizeof(double));
+        g->int_weights = g->max_vol < 2147483648.0;
+        g->total = static_cast<double>(hi[0]);
+        g->binned = false;
+        return;
+    }
+    if (g->n > 0 && g->weighted && integral_weights) {
+        g->vol.zero();
+        g->loop.zero();
+        if (g->D)
+            CD_LAUNCH(ctx, "finalize", k_csr_entries_intw,
+                      grid_for((g->D + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32), 256, 0, g->n, g->D,
+                      static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
+                      static_cast<const float *>(g->w.p), g->vol.p, g->loop.p,
+                      reinterpret_cast<unsigned long long *>(acc_i.p), acc_d.p);
+        CD_LAUNCH(ctx, "finalize", k_finalize_nodes_w, grid_for(g->n, 256, ctx->num_sms * 16), 256, 0, g->n,
+                  static_cast<const int64_t *>(g->off.p), g->vol.p, static_cast<const double *>(g->loop.p), acc_i.p);
+        int64_t hi[5];
+        double hd;
+        CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaMemcpyAsync(&hd, acc_d.p, sizeof(hd), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (hi[3] == 0) {
+            g->m = hi[0];
+            g->max_degree = hi[1];
+            g->isolated = hi[2];
+            std::memcpy(&g->max_vol, &hi[4], sizeof(double));
+            g->int_weights = g->max_vol < 2147483648.0;
+            g->total = hd;
+            g->binned = false;
+            return;
+        }
+        // a fractional weight after all: the fixed-order path below
+        acc_i.zero();
+        acc_d.zero();
+    }
     if (g->n > 0)
         CD_LAUNCH(ctx, "finalize", k_finalize, grid_for(g->n, 8, ctx->num_sms * 16), 256, 0, g->n,
                   static_cast<const int64_t *>(g->off.p), static_cast<const int32_t *>(g->col.p),
@@ -234,40 +478,17 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
 // ---------------------------------------------------------------------------
 // validation of an input CSR (ranges, strictly ascending rows, weights > 0)
 // ---------------------------------------------------------------------------
-__global__ void k_validate_csr(int64_t n, int64_t D, const int64_t *off, const int32_t *col, const float *w,
-                               int64_t *flag) {
-    const int lane = lane_id();
-    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t u = gw; u < n; u += nw) {
-        const int64_t s = off[u], e = off[u + 1];
-        bool bad = (s > e) || (s < 0) || (e > D);
-        if (u == 0 && s != 0)
-            bad = true;
-        if (u == n - 1 && e != D)
-            bad = true;
-        if (!bad) {
-            for (int64_t i = s + lane; i < e; i += 32) {
-                const int32_t c = col[i];
-                if (c < 0 || c >= n)
-                    bad = true;
-                if (i > s && col[i - 1] >= c)
-                    bad = true;
-                if (w && !(w[i] > 0.0f))
-                    bad = true;
-            }
-        }
-        if (__any_sync(0xffffffffu, bad) && lane == 0)
-            flag[0] = 1;
-    }
-}
-
 void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D) {
     if (n == 0)
         return;
     DBuf<int64_t> flag(ctx, 1);
     flag.zero();
-    CD_LAUNCH(ctx, "validate", k_validate_csr, grid_for(n, 8, ctx->num_sms * 16), 256, 0, n, D, off, col, w, flag.p);
+    CD_LAUNCH(ctx, "validate", k_check_offsets, grid_for(n, 256, ctx->num_sms * 16), 256, 0, n, D, off, flag.p);
+    if (D)
+        CD_LAUNCH(ctx, "validate", k_csr_entries<false>, grid_for((D + CSR_CHUNK - 1) / CSR_CHUNK, 256,
+                                                                  ctx->num_sms * 32),
+                  256, 0, n, D, off, col, w, flag.p, static_cast<int32_t *>(nullptr),
+                  static_cast<unsigned long long *>(nullptr));
     int64_t h = 0;
     CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -149,7 +149,10 @@ namespace cdk {
 enum DupMode : int { DUP_ERROR = 0, DUP_SUM = 1, DUP_ONE = 2 };
 
 // graph.cu
-void graph_finalize(cd_ctx *ctx, cd_graph *g);  // vol, loop, m, total, max degree
+// vol, loop, m, total, max degree.  integral_weights: the caller knows every
+// weight is an integer (contraction of an integer-weight graph), so sums are
+// order-free and computed entry-parallel
+void graph_finalize(cd_ctx *ctx, cd_graph *g, bool integral_weights = false);
 // row batching: cut[i] = first row in [lo, hi] whose prefix reaches an even
 // split of [pre[lo], pre[hi]) into k parts (cut has k+1 entries)
 __global__ void k_split_rows(const int64_t *pre, int64_t lo, int64_t hi, int k, int64_t *cut);

@@ -171,6 +171,55 @@ __device__ __forceinline__ bool tinsert_claim(int32_t *keys, V *vals, uint32_t m
     }
 }
 
+// Count tallies (unweighted graphs): an empty slot already holds 1, so the
+// entry that claims a slot needs no add -- one shared-memory atomic per
+// distinct label instead of two (a shared atomic costs one L1 wavefront per
+// lane; tools/microbench/tally_bench.cu).  Other tallies start at 0.
+template <int VC>
+__device__ __forceinline__ TallyT<VC> tally_empty() {
+    return VC == VC_COUNT ? TallyT<VC>(1) : TallyT<VC>(0);
+}
+
+// insert one entry of weight w (1 for count tallies); true if it claimed the
+// key's slot (*slot = its index)
+template <int VC>
+__device__ __forceinline__ bool tinsert_entry(int32_t *keys, TallyT<VC> *vals, uint32_t mask, int32_t key,
+                                              TallyT<VC> w, uint32_t *slot) {
+    if (VC != VC_COUNT)
+        return tinsert_claim<TallyT<VC>>(keys, vals, mask, key, w, slot);
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
+        if (old == EMPTY_KEY) {
+            *slot = s;
+            return true;
+        }
+        if (old == key) {
+            atomicAdd(&vals[s], TallyT<VC>(1));
+            *slot = s;
+            return false;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// insert `cnt` equal entries (a match_any group) into a count table
+__device__ __forceinline__ bool tinsert_count_n(int32_t *keys, unsigned int *vals, uint32_t mask, int32_t key,
+                                                unsigned int cnt, uint32_t *slot) {
+    uint32_t s = hash_slot(key, mask);
+    while (true) {
+        const int32_t old = atomicCAS(&keys[s], EMPTY_KEY, key);
+        if (old == EMPTY_KEY || old == key) {
+            const unsigned int add = old == EMPTY_KEY ? cnt - 1u : cnt;  // an empty slot holds 1
+            if (add)
+                atomicAdd(&vals[s], add);
+            *slot = s;
+            return old == EMPTY_KEY;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
 template <int VC>
 __device__ __forceinline__ double load_w(const SweepParams &P, int64_t f, bool valid) {
     return (VC != VC_COUNT && valid) ? static_cast<double>(P.w[f]) : 1.0;
@@ -540,7 +589,7 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                         claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
                 } else if (valid) {
                     // integer tallies are order-free: insert directly
-                    claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(ww[c]), &slot);
+                    claimed = tinsert_entry<VC>(keys, vals, cap - 1, kk[c], static_cast<V>(ww[c]), &slot);
                 }
                 const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
                 if (claimed)
@@ -593,7 +642,7 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
             for (int j = lane; j < nd; j += 32) {
                 const uint32_t t = dist[j];
                 keys[t] = EMPTY_KEY;
-                vals[t] = V(0);
+                vals[t] = tally_empty<VC>();
             }
             __syncwarp();
             CD_PT(pt, 5);
@@ -619,7 +668,7 @@ __global__ void __launch_bounds__(128, VC == VC_COUNT ? 8 : 1) k_sweep_warp(Swee
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     for (int t = lane; t < SW_WARP_CAP; t += 32) {  // empty once; each node cleans up after itself
         skeys[wid][t] = EMPTY_KEY;
-        svals[wid][t] = V(0);
+        svals[wid][t] = tally_empty<VC>();
     }
     __syncwarp();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -728,11 +777,36 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
             const double wt = static_cast<double>(ww[c]);
             if (MODE == MODE_PLM && valid && kk[c] == cur)
                 wc += wt;
-            double agg;
             bool claimed = false;
             uint32_t slot = 0;
-            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, sh.scratch[wid], agg))
-                claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+            // integer tallies insert each entry directly (match_any costs about an
+            // atomic per lane when the labels differ), unless the round is flooded
+            // -- half its entries share the first one's label, whose slot every
+            // warp of the block would hit: then equal labels are combined first
+            bool combine = false;
+            if (VC != VC_REAL) {
+                const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+                const int32_t k0 = __shfl_sync(0xffffffffu, kk[c], vm ? __ffs(vm) - 1 : 0);
+                combine = __popc(__ballot_sync(0xffffffffu, valid && kk[c] == k0)) >= 16;
+            }
+            if (VC == VC_REAL) {
+                // fp64: equal labels combined in lane order first (one add per slot per round)
+                double agg;
+                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, sh.scratch[wid], agg))
+                    claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+            } else if (combine) {
+                double agg;
+                if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, sh.scratch[wid], agg)) {
+                    if (VC == VC_COUNT)
+                        claimed = tinsert_count_n(keys, reinterpret_cast<unsigned int *>(vals), cap - 1, kk[c],
+                                                  static_cast<unsigned int>(agg), &slot);
+                    else
+                        claimed = tinsert_claim<V>(keys, vals, cap - 1, kk[c], static_cast<V>(agg), &slot);
+                }
+            } else if (valid) {
+                // integer tallies are order-free: insert directly (tools/microbench/tally_bench.cu)
+                claimed = tinsert_entry<VC>(keys, vals, cap - 1, kk[c], static_cast<V>(ww[c]), &slot);
+            }
             // the claimers of new slots list them (one counter add per warp)
             const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
             int base = 0;
@@ -806,7 +880,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     for (int j = threadIdx.x; j < nd; j += NT) {
         const uint32_t t = dlist[j];
         keys[t] = EMPTY_KEY;
-        vals[t] = V(0);
+        vals[t] = tally_empty<VC>();
     }
     __syncthreads();
     if (threadIdx.x == 0)
@@ -816,11 +890,11 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
 
 // Empties a block evaluator's table once per kernel (nodes then clean up
 // after themselves); ends with a block barrier.
-template <class V, class SH>
-__device__ __forceinline__ void block_table_init(V *vals, int32_t *keys, uint32_t cap, SH &sh) {
+template <int VC, class SH>
+__device__ __forceinline__ void block_table_init(TallyT<VC> *vals, int32_t *keys, uint32_t cap, SH &sh) {
     for (uint32_t t = threadIdx.x; t < cap; t += blockDim.x) {
         keys[t] = EMPTY_KEY;
-        vals[t] = V(0);
+        vals[t] = tally_empty<VC>();
     }
     if (threadIdx.x == 0)
         sh.ndist = 0;
@@ -845,7 +919,7 @@ __global__ void __launch_bounds__(NT) k_sweep_block(SweepParams P) {
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
-    block_table_init(vals, keys, CAP, sh);
+    block_table_init<VC>(vals, keys, CAP, sh);
     const int64_t per_block = (count - blockIdx.x + gridDim.x - 1) / gridDim.x;  // candidates of this block
     for (int64_t k0 = 0; k0 < per_block; k0 += NT) {
         const int nsel = block_select<NT>(P, bkey, list, count, k0, sel, wcount, pre);
@@ -1103,7 +1177,7 @@ __global__ void __launch_bounds__(FUSED_THREADS, 8) k_fused_phase(SweepParams P,
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     for (int t = lane; t < SW_WARP_CAP; t += 32) {
         skeys[wid][t] = EMPTY_KEY;
-        svals[wid][t] = V(0);
+        svals[wid][t] = tally_empty<VC>();
     }
     __syncwarp();
     const int64_t gtid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1262,7 +1336,7 @@ __global__ void __launch_bounds__(SMALL_THREADS) k_small_move(SweepParams P, Sma
     const int64_t gsize = static_cast<int64_t>(gridDim.x) * blockDim.x;
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
-    block_table_init(vals, keys, S.cap_max, sh);
+    block_table_init<VC>(vals, keys, S.cap_max, sh);
     long long hist0 = -1, hist1 = -1, moves_total = 0, cum_fx = 0;
     int passes = 0;
     bool changed = false;
@@ -1697,6 +1771,20 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
                 for (int64_t j = 16 * i; j < n; ++j)
                     active[j] = 1;
         }
+    if (!active || dense) {
+        // labels only: a thread per move (coalesced move-list reads; a warp per
+        // move left 31 lanes idle -- C3 PLP iteration 1 moves 2.2M nodes per bucket)
+        for (int sg = 0; sg < nseg; ++sg) {
+            const int2 *m = mv + sg * stride;
+            const int64_t cnt = counts[sg];
+            for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+                 i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+                const int2 e2 = m[i];
+                z[e2.x] = e2.y;
+            }
+        }
+        return;
+    }
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t cnt = counts[sg];
@@ -1704,9 +1792,8 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
             const int2 e2 = m[i];
             if (lane == 0)
                 z[e2.x] = e2.y;
-            if (active && !dense)
-                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
-                    active[tcol[e]] = 1;
+            for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
+                active[tcol[e]] = 1;
         }
     }
 }

@@ -32,13 +32,14 @@ namespace cdk {
 
 namespace {
 
-// Weights are stored as fp32 (rounded to nearest).  A positive fp64 weight
-// below the smallest fp32 subnormal would round to 0 and one above FLT_MAX to
-// inf; both break the w > 0 invariant (H/graph.hpp:52-53), so they are
-// rejected like a nonpositive weight.
+// Weights are stored as fp32 (rounded to nearest).  A positive finite fp64
+// weight below the smallest fp32 subnormal would round to 0 (breaking the
+// w > 0 invariant, H/graph.hpp:52-53) and one beyond FLT_MAX to inf; both
+// are rejected like a nonpositive weight.  A literal inf is accepted, as the
+// reference's `w > 0` accepts it.
 __device__ __host__ __forceinline__ bool fp32_weight_ok(double w) {
     const float f = static_cast<float>(w);
-    return f > 0.0f && f <= 3.402823466e38f;
+    return f > 0.0f && (f <= 3.402823466e38f || isinf(w));
 }
 
 __device__ __host__ __forceinline__ bool is_ws(char c) {

@@ -46,6 +46,16 @@ def test_reader_matches_oracle(dev, ctx, name, kind, text, merge):
         np.testing.assert_array_equal(g.original_ids(), oids)
 
 
+@pytest.mark.parametrize("kind,text", [
+    ("metis", b"2 1 1\n2 1e-50\n1 1e-50\n"), ("metis", b"2 1 1\n2 1e300\n1 1e300\n"),
+    ("edges", b"0 1 1e-50\n"), ("edges", b"0 1 1e300\n")])
+def test_weight_not_fp32_representable(dev, ctx, kind, text):
+    """Weights are stored as fp32: a positive weight that would round to 0 or
+    overflow to inf is rejected with its line (the reference keeps fp64)."""
+    with pytest.raises(dev.InputError, match="not a positive finite fp32 value"):
+        _dev_read(dev, kind, text, False)
+
+
 def test_load_from_path_messages(dev, tmp_path):
     """cd_graph_load_*: the path prefixes messages like the reference's."""
     p = tmp_path / "g.metis"
