@@ -110,6 +110,16 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
         }
         return;
     }
+    // count tallies on one device: the margin-pruned active set (exact;
+    // DESIGN.md "Margin-pruned active set"); CD_PLP_MARGIN=0 keeps the flags
+    DBuf<int2> chg;
+    static const bool margins = env_i64("CD_PLP_MARGIN", 1) != 0;
+    if (margins && !g->weighted && world_size(ctx) == 1 && n > 0) {
+        chg.alloc(ctx, n);
+        chg.fill_bytes(0x20);  // (CHG_ALL, 0x20202020): every node is evaluated once
+        c.chg = chg.p;
+        c.active = nullptr;
+    }
     Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
     int64_t updated = n, iter = 0;

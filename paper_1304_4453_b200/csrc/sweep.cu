@@ -45,6 +45,7 @@ struct SweepParams {
     const double *vol;
     const int32_t *z;
     uint8_t *active;
+    int2 *chg;  // margin mode (PLP, count tallies): (changes, margin) per node; see evaluate_again
     const double *vols;
     const int32_t *csize;
     double gamma, inv_total, inv_sq2;
@@ -120,6 +121,34 @@ __device__ __forceinline__ void argmax_xor(double &v, int32_t &k) {
             v = ov;
             k = ok;
         }
+    }
+}
+
+// argmax that also keeps the runner-up's value s (over all other keys)
+template <int WIDTH>
+__device__ __forceinline__ void argmax2_xor(double &v, int32_t &k, double &s) {
+#pragma unroll
+    for (int o = WIDTH / 2; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int32_t ok = __shfl_xor_sync(0xffffffffu, k, o);
+        const double os = __shfl_xor_sync(0xffffffffu, s, o);
+        if (better(ov, ok, v, k)) {
+            s = fmax(os, v);
+            v = ov;
+            k = ok;
+        } else {
+            s = fmax(s, ov);
+        }
+    }
+}
+
+__device__ __forceinline__ void keep2(double val, int32_t key, double &v, int32_t &k, double &s) {
+    if (better(val, key, v, k)) {
+        s = fmax(s, v);
+        v = val;
+        k = key;
+    } else {
+        s = fmax(s, val);
     }
 }
 
@@ -225,12 +254,33 @@ __device__ __forceinline__ double load_w(const SweepParams &P, int64_t f, bool v
     return (VC != VC_COUNT && valid) ? static_cast<double>(P.w[f]) : 1.0;
 }
 
+// Margin-pruned active set (PLP, count tallies).  At its last evaluation u's
+// best label b led every other label by margin = T(b) - max_{l != b} T(l)
+// (T = neighbour label counts incl. the self-loop, H/plp.hpp:112-124); since
+// then chg[u] entries of its row changed label.  Each change moves one count
+// from one label to another, so b still wins -- and u, already labelled b,
+// would not move -- while 2 * chg < margin: evaluating it is skipped
+// (chg == 0 is the reference's inactive node, H/plp.hpp:131-132).  Labels,
+// update counts and iterations are exactly those of the flag rule.
+constexpr int32_t CHG_ALL = 0x20202020;  // "changed beyond counting": evaluate (a byte fill)
+
+__device__ __forceinline__ bool evaluate_again(const SweepParams &P, int32_t u) {
+    const int2 cm = P.chg[u];  // one 8-byte load
+    return cm.x > 0 && 2 * cm.x >= cm.y;
+}
+
+__device__ __forceinline__ bool is_active(const SweepParams &P, int32_t u) {
+    if (P.chg)
+        return evaluate_again(P, u);
+    return !P.active || P.active[u];
+}
+
 __device__ __forceinline__ bool selected(const SweepParams &P, unsigned long long key, int32_t u) {
     if (u < P.own_lo || u >= P.own_hi)
         return false;
     if (P.buckets > 1 && bucket_of(key, u, P.buckets) != P.bucket)
         return false;
-    return !P.active || P.active[u];
+    return is_active(P, u);
 }
 
 __device__ __forceinline__ unsigned long long load_key(const SweepParams &P) {
@@ -252,7 +302,7 @@ __device__ __forceinline__ bool tier_range(const SweepParams &P, int t, const in
 }
 
 __device__ __forceinline__ bool selected_in(const SweepParams &P, unsigned long long key, int32_t u, bool pre) {
-    return pre ? (!P.active || P.active[u]) : selected(P, key, u);
+    return pre ? is_active(P, u) : selected(P, key, u);
 }
 
 // Once per pass: stable partition of each pre-bucketed tier segment by bucket
@@ -367,9 +417,11 @@ struct MoveQueue {
 
 // Applies one decision.  Must be reached by all lanes of the warp (moves are
 // queued warp-collectively); only lanes with `act` carry a decision.
+// `margin`: PLP count tallies, best count minus the runner-up's (0 where a
+// tier does not track the runner-up: the node is re-evaluated on any change)
 template <int MODE>
 __device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool act, int32_t u, int32_t cur,
-                                       int32_t best, double val) {
+                                       int32_t best, double val, double margin = 0.0) {
     bool moved = false;
     if (act) {
         if (MODE == MODE_PLP) {
@@ -395,6 +447,9 @@ __device__ __forceinline__ void decide(const SweepParams &P, MoveQueue &q, bool 
     // until a neighbour moves
     if (act && !moved && P.active)
         P.active[u] = 0;
+    if (MODE == MODE_PLP && act && P.chg) {
+        P.chg[u] = make_int2(0, static_cast<int32_t>(margin));
+    }
 }
 
 // stats layout per mode: [0] nodes, [1] entries unweighted, [2] entries weighted
@@ -466,9 +521,16 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
                     ck = INT32_MAX;
                 }
             }
-            argmax_xor<G>(cv, ck);
+            double margin = 0.0;
+            if (MODE == MODE_PLP && P.chg) {
+                double cs = -1.0;
+                argmax2_xor<G>(cv, ck, cs);
+                margin = cv - fmax(cs, 0.0);
+            } else {
+                argmax_xor<G>(cv, ck);
+            }
             const bool act = has && k == 0;
-            decide<MODE>(P, q, act, u, cur, ck, cv);
+            decide<MODE>(P, q, act, u, cur, ck, cv, margin);
             if (act) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(d);
@@ -601,6 +663,7 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
             if (MODE == MODE_PLM)
                 wc = warp_sum(wc);
             double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+            double cs = -1.0;  // PLP margin mode: the runner-up's count
             int32_t ck = INT32_MAX;
             const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(vols_cur, vol_u) : 0.0;
             // the distinct labels in rounds of SW_ILP per lane: the vols[key]
@@ -625,15 +688,23 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                     if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
                         continue;
                     const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
-                    if (better(val, key[c], cv, ck)) {
+                    if (MODE == MODE_PLP && P.chg) {
+                        keep2(val, key[c], cv, ck, cs);
+                    } else if (better(val, key[c], cv, ck)) {
                         cv = val;
                         ck = key[c];
                     }
                 }
             }
             CD_PT(pt, 4);
-            argmax_xor<32>(cv, ck);
-            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+            double margin = 0.0;
+            if (MODE == MODE_PLP && P.chg) {
+                argmax2_xor<32>(cv, ck, cs);
+                margin = cv - fmax(cs, 0.0);
+            } else {
+                argmax_xor<32>(cv, ck);
+            }
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(e - s);
@@ -737,6 +808,7 @@ struct BlockShared {
     double scratch[NW][32];
     double red_v[NW];
     int32_t red_k[NW];
+    double red_s[NW];  // PLP margin mode: each warp's runner-up
     double red_wc[NW];
     int ndist;
 };
@@ -831,6 +903,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     }
     const int nd = sh.ndist;
     double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+    double cs = -1.0;
     int32_t ck = INT32_MAX;
     const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(volsc, vol_u) : 0.0;
     // candidates = the distinct labels only (not the whole table)
@@ -854,23 +927,37 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
             if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
                 continue;
             const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
-            if (better(val, key[c], cv, ck)) {
+            if (MODE == MODE_PLP && P.chg) {
+                keep2(val, key[c], cv, ck, cs);
+            } else if (better(val, key[c], cv, ck)) {
                 cv = val;
                 ck = key[c];
             }
         }
     }
-    argmax_xor<32>(cv, ck);
+    const bool two = MODE == MODE_PLP && P.chg != nullptr;
+    if (two)
+        argmax2_xor<32>(cv, ck, cs);
+    else
+        argmax_xor<32>(cv, ck);
     if (lane == 0) {
         sh.red_v[wid] = cv;
         sh.red_k[wid] = ck;
+        sh.red_s[wid] = cs;
     }
     __syncthreads();
     if (wid == 0) {
         cv = lane < NT / 32 ? sh.red_v[lane] : -INFINITY;
         ck = lane < NT / 32 ? sh.red_k[lane] : INT32_MAX;
-        argmax_xor<32>(cv, ck);
-        decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+        cs = lane < NT / 32 ? sh.red_s[lane] : -1.0;
+        double margin = 0.0;
+        if (two) {
+            argmax2_xor<32>(cv, ck, cs);
+            margin = cv - fmax(cs, 0.0);
+        } else {
+            argmax_xor<32>(cv, ck);
+        }
+        decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
         if (lane == 0) {
             ++st_n;
             st_e += static_cast<unsigned long long>(e - s);
@@ -1753,7 +1840,7 @@ __device__ __forceinline__ int64_t seg_total(const int32_t *counts, int nseg) {
 }
 
 __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
-                                                   int32_t *z, uint8_t *active, const int64_t *toff,
+                                                   int32_t *z, uint8_t *active, int2 *chg, const int64_t *toff,
                                                    const int32_t *tcol, long long *total, int64_t n) {
     const int64_t count = seg_total(counts, nseg);
     const int lane = lane_id();
@@ -1761,8 +1848,18 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     if (blockIdx.x == 0 && threadIdx.x == 0)
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
-    const bool dense = active && count > n / 16;
-    if (dense)
+    // margin mode: neighbours count the changes in their rows (each entry
+    // whose label changed); beyond n/16 movers every node is re-evaluated
+    const bool dense = (active || chg) && count > n / 16;
+    if (dense && chg)  // (the margins are recomputed at the next evaluation)
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 1) / 2;
+             i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+            if (2 * i + 2 <= n)
+                reinterpret_cast<int4 *>(chg)[i] = make_int4(CHG_ALL, 0, CHG_ALL, 0);
+            else
+                chg[2 * i] = make_int2(CHG_ALL, 0);
+        }
+    else if (dense)
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 15) / 16;
              i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
             if (16 * i + 16 <= n)
@@ -1771,7 +1868,7 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
                 for (int64_t j = 16 * i; j < n; ++j)
                     active[j] = 1;
         }
-    if (!active || dense) {
+    if ((!active && !chg) || dense) {
         // labels only: a thread per move (coalesced move-list reads; a warp per
         // move left 31 lanes idle -- C3 PLP iteration 1 moves 2.2M nodes per bucket)
         for (int sg = 0; sg < nseg; ++sg) {
@@ -1792,8 +1889,12 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
             const int2 e2 = m[i];
             if (lane == 0)
                 z[e2.x] = e2.y;
-            for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
-                active[tcol[e]] = 1;
+            if (chg)
+                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
+                    atomicAdd(&chg[tcol[e]].x, 1);
+            else
+                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
+                    active[tcol[e]] = 1;
         }
     }
 }
@@ -2230,6 +2331,7 @@ void Sweeper::enqueue(bool capture) {
     P.vol = g->vol.p;
     P.z = c_.z;
     P.active = c_.active;
+    P.chg = c_.chg;
     P.vols = c_.vols;
     P.csize = c_.csize;
     P.gamma = c_.gamma;
@@ -2322,7 +2424,7 @@ void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t str
     const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, ctx->num_sms * 4));
     if (c_.mode == MODE_PLP)
         CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
-                  c_.active, c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
+                  c_.active, c_.chg, c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
                   c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), total_.p, g->n);
     else
         CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,

@@ -13,6 +13,10 @@ struct SweepCall {
     int mode = MODE_PLP;
     int32_t *z = nullptr;
     uint8_t *active = nullptr;   // PLP active set (nullable: all active, no deactivation)
+    // PLP on count tallies, in place of `active`: neighbour label changes since
+    // the node's last evaluation and the margin of its decision then
+    // (DESIGN.md "Margin-pruned active set"); both nullable
+    int2 *chg = nullptr;  // (changes since the last evaluation, margin then)
     double *vols = nullptr;      // PLM community volumes
     int32_t *csize = nullptr;    // PLM community sizes (singleton guard; nullable)
     double gamma = 1.0;

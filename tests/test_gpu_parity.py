@@ -175,7 +175,8 @@ def e2e_graphs(oracle):
     pg, _ = oracle.generate_planted(2000, 8, 0.05, 0.002, 3)
     lg, _ = oracle.generate_lfr(seed=2, n=20000)
     rg = oracle.generate_rmat(14, 16, weighted=True, seed=9)
-    return {"planted": pg, "lfr": lg, "rmat_w": rg}
+    ru = oracle.generate_rmat(17, 16, weighted=False, seed=4)  # hubs; PLP's margin-pruned active set
+    return {"planted": pg, "lfr": lg, "rmat_w": rg, "rmat_u": ru}
 
 
 def _dev_of(dev, name, og):
@@ -183,10 +184,12 @@ def _dev_of(dev, name, og):
         return dev.generate_planted(2000, 8, 0.05, 0.002, 3)[0]
     if name == "lfr":
         return dev.generate_lfr(seed=2, n=20000)[0]
+    if name == "rmat_u":
+        return dev.generate_rmat(17, 16, weighted=False, seed=4)
     return dev.generate_rmat(14, 16, weighted=True, seed=9)
 
 
-@pytest.mark.parametrize("name", ["planted", "lfr", "rmat_w"])
+@pytest.mark.parametrize("name", ["planted", "lfr", "rmat_w", "rmat_u"])
 def test_plp_end_to_end_bit_exact(dev, ctx, oracle, e2e_graphs, name):
     og = e2e_graphs[name]
     g = _dev_of(dev, name, og)
