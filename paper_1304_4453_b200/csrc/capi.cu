@@ -239,6 +239,8 @@ cd_status cd_ctx_destroy(cd_ctx *ctx) {
         cudaEventDestroy(e);
     if (ctx->dstats)
         cudaFree(ctx->dstats);
+    if (ctx->copy_stream)
+        cudaStreamDestroy(ctx->copy_stream);
     delete ctx->comm;
     cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -397,15 +399,19 @@ cd_status cd_graph_from_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const in
             g->weighted = w != nullptr;
             g->off.alloc(ctx, n + 1);
             g->col.alloc(ctx, std::max<int64_t>(D, 1));
-            CD_CUDA(cudaMemcpyAsync(g->off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, ctx->stream));
-            if (D)
-                CD_CUDA(cudaMemcpyAsync(g->col.p, col, D * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
-            if (w) {
+            if (w)
                 g->w.alloc(ctx, std::max<int64_t>(D, 1));
+            CD_CUDA(cudaMemcpyAsync(g->off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, ctx->stream));
+            if (D && !is_device_ptr(col) && D >= UPLOAD_CHUNK) {
+                // host columns: chunked copies, each chunk validated while the next one copies
+                graph_upload_validate(ctx, n, D, g->off.p, g->col.p, col, w ? g->w.p : nullptr, w);
+            } else {
                 if (D)
+                    CD_CUDA(cudaMemcpyAsync(g->col.p, col, D * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
+                if (w && D)
                     CD_CUDA(cudaMemcpyAsync(g->w.p, w, D * sizeof(float), cudaMemcpyDefault, ctx->stream));
+                graph_validate_csr(ctx, n, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, D);
             }
-            graph_validate_csr(ctx, n, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, D);
             graph_finalize(ctx, g);
         } catch (...) {
             delete g;

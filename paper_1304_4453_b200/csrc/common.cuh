@@ -83,6 +83,8 @@ struct cd_ctx {
     cudaEvent_t fork_ev = nullptr;
     cudaEvent_t join_ev[NSIDE] = {};
     bool use_graphs = true;
+    // host -> device uploads in chunks, overlapped with their validation
+    cudaStream_t copy_stream = nullptr;
     // sharded execution (comm.cuh); nullptr = one device, no exchange
     cdk::Comm *comm = nullptr;
     // child context of a concurrent run on the same device (EPP bases): the

@@ -97,17 +97,20 @@ __global__ void k_check_offsets(int64_t n, int64_t D, const int64_t *off, int64_
 
 // ranges, strictly ascending rows, weights > 0; FIN (unweighted graphs): also
 // the self-loop count per row and the number of entries with v >= u (= m = w(E))
+// (entries [ib, ie) of D; one launch covers [0, D))
 template <bool FIN>
 __global__ void __launch_bounds__(256) k_csr_entries(int64_t n, int64_t D, const int64_t *off, const int32_t *col,
                                                     const float *w, int64_t *flag, int32_t *loops,
-                                                    unsigned long long *m_acc) {
+                                                    unsigned long long *m_acc, int64_t ib = 0, int64_t ie = -1) {
     bool bad = false;
     unsigned long long m_loc = 0;
-    for (int64_t i0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * CSR_CHUNK; i0 < D;
+    if (ie < 0)
+        ie = D;
+    for (int64_t i0 = ib + (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * CSR_CHUNK; i0 < ie;
          i0 += static_cast<int64_t>(gridDim.x) * blockDim.x * CSR_CHUNK) {
         int64_t r = row_of_entry(n, off, i0);
         int64_t rs = off[r], re = off[r + 1];
-        const int64_t i1 = min(i0 + CSR_CHUNK, D);
+        const int64_t i1 = min(i0 + CSR_CHUNK, ie);
         int32_t prev = i0 > 0 ? col[i0 - 1] : 0;
         for (int64_t i = i0; i < i1; ++i) {
             for (int guard = 0; i >= re && r + 1 < n && guard < 64; ++guard) {  // next nonempty row
@@ -478,6 +481,51 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
 // ---------------------------------------------------------------------------
 // validation of an input CSR (ranges, strictly ascending rows, weights > 0)
 // ---------------------------------------------------------------------------
+void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off_dev, int32_t *col_dev,
+                           const int32_t *col_host, float *w_dev, const float *w_host) {
+    if (!ctx->copy_stream)
+        CD_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    DBuf<int64_t> flag(ctx, 1);
+    flag.zero();
+    if (n)
+        CD_LAUNCH(ctx, "validate", k_check_offsets, grid_for(n, 256, ctx->num_sms * 16), 256, 0, n, D, off_dev,
+                  flag.p);
+    // the copies must not start before the destination buffers exist on the
+    // library stream (stream-ordered pool allocations)
+    cudaEvent_t ready = ctx_event(ctx);
+    CD_CUDA(cudaEventRecord(ready, ctx->stream));
+    CD_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+    const int64_t nchunks = (D + UPLOAD_CHUNK - 1) / UPLOAD_CHUNK;
+    std::vector<cudaEvent_t> done(static_cast<size_t>(nchunks));
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
+        CD_CUDA(cudaMemcpyAsync(col_dev + ib, col_host + ib, (ie - ib) * sizeof(int32_t), cudaMemcpyHostToDevice,
+                                ctx->copy_stream));
+        if (w_dev)
+            CD_CUDA(cudaMemcpyAsync(w_dev + ib, w_host + ib, (ie - ib) * sizeof(float), cudaMemcpyHostToDevice,
+                                    ctx->copy_stream));
+        done[c] = ctx_event(ctx);
+        CD_CUDA(cudaEventRecord(done[c], ctx->copy_stream));
+    }
+    // one entry of slack on each side: a chunk's first entry compares with the previous one
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
+        CD_CUDA(cudaStreamWaitEvent(ctx->stream, done[c], 0));
+        CD_LAUNCH(ctx, "validate", k_csr_entries<false>,
+                  grid_for((ie - ib + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32), 256, 0, n, D, off_dev,
+                  static_cast<const int32_t *>(col_dev), static_cast<const float *>(w_dev), flag.p,
+                  static_cast<int32_t *>(nullptr), static_cast<unsigned long long *>(nullptr), ib, ie);
+    }
+    int64_t h = 0;
+    CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->free_events.push_back(ready);
+    for (cudaEvent_t e : done)
+        ctx->free_events.push_back(e);
+    if (h)
+        fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
+}
+
 void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D) {
     if (n == 0)
         return;

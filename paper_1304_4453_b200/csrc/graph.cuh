@@ -153,6 +153,13 @@ enum DupMode : int { DUP_ERROR = 0, DUP_SUM = 1, DUP_ONE = 2 };
 // weight is an integer (contraction of an integer-weight graph), so sums are
 // order-free and computed entry-parallel
 void graph_finalize(cd_ctx *ctx, cd_graph *g, bool integral_weights = false);
+// Host columns (and weights) -> device in chunks of UPLOAD_CHUNK entries on
+// the context's copy stream, each chunk validated (graph_validate_csr's
+// checks) on the library stream while the next one copies; off_dev is already
+// enqueued on the library stream.  Throws CD_EINPUT like graph_validate_csr.
+constexpr int64_t UPLOAD_CHUNK = int64_t(1) << 25;
+void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off_dev, int32_t *col_dev,
+                           const int32_t *col_host, float *w_dev, const float *w_host);
 // row batching: cut[i] = first row in [lo, hi] whose prefix reaches an even
 // split of [pre[lo], pre[hi]) into k parts (cut has k+1 entries)
 __global__ void k_split_rows(const int64_t *pre, int64_t lo, int64_t hi, int k, int64_t *cut);

@@ -1,0 +1,51 @@
+"""cd_graph_from_csr with host arrays above UPLOAD_CHUNK (2^25) entries: the
+columns are copied in chunks, each validated while the next one copies
+(graph_upload_validate).  The graph must equal the device-built one, and a
+defect in any chunk -- or right at a chunk boundary -- must raise the same
+input error as the unchunked path (H/graph.hpp:48-81 semantics)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CHUNK = 1 << 25
+
+
+@pytest.fixture(scope="module")
+def big(dev, ctx):
+    g = dev.generate_rmat(21, 16, weighted=True, seed=2)  # ~63M entries: two chunks
+    c = g.csr()
+    assert len(c["col"]) > CHUNK
+    return g, c
+
+
+def test_chunked_upload_equals_device_graph(dev, big):
+    g, c = big
+    h = dev.Graph.from_csr(g.node_count(), c["off"], c["col"], c["w"])
+    d = h.csr()
+    assert np.array_equal(d["off"], c["off"]) and np.array_equal(d["col"], c["col"])
+    assert np.array_equal(d["w"], c["w"])
+    np.testing.assert_array_equal(d["vol"], c["vol"])
+    assert h.edge_count() == g.edge_count() and h.total_edge_weight() == g.total_edge_weight()
+
+
+@pytest.mark.parametrize("where", ["second_chunk", "boundary"])
+def test_chunked_upload_rejects_unsorted_row(dev, big, where):
+    g, c = big
+    off, col = c["off"], c["col"].copy()
+    target = CHUNK + 12345 if where == "second_chunk" else CHUNK
+    u = int(np.searchsorted(off, target, side="right") - 1)
+    while off[u + 1] - off[u] < 2:  # a row with two entries at or after the target
+        u += 1
+    i = max(int(off[u]) + 1, target) if target < off[u + 1] else int(off[u]) + 1
+    col[i - 1], col[i] = col[i], col[i - 1]  # breaks the strictly ascending order
+    with pytest.raises(dev.InputError, match="malformed CSR"):
+        dev.Graph.from_csr(g.node_count(), off, col, c["w"])
+
+
+def test_chunked_upload_rejects_out_of_range(dev, big):
+    g, c = big
+    col = c["col"].copy()
+    col[-1] = g.node_count()  # the last chunk
+    with pytest.raises(dev.InputError, match="malformed CSR"):
+        dev.Graph.from_csr(g.node_count(), c["off"], col, c["w"])
