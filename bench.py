@@ -443,6 +443,14 @@ def bench_b200(args, wl):
                                 "frac": round(v["bytes"] / (v["total_ms"] / 1e3) / 1e9 / peak, 5)}
                             for k, v in sorted(sst.items(), key=lambda kv: -kv[1]["total_ms"])
                             if "." in k and v["bytes"] > 0 and v["total_ms"] > 0}}
+    cs = gst.get("coarsen")
+    if cs and cs["total_ms"] > 0 and cs["bytes"] > 0:
+        # contraction (PLM / PLMR / EPP): the SURVEY.md 8(d) byte model per coarsening
+        # over the coarsen kernels' time (they run on the library stream, serially)
+        ca = cs["bytes"] / (cs["total_ms"] / 1e3) / 1e9
+        roofline["contraction"] = {"achieved": ca, "frac": ca / peak, "ms_per_step": cs["total_ms"] / prof_steps,
+                                   "bytes_per_step": cs["bytes"] / prof_steps,
+                                   "share_of_step": cs["total_ms"] / gstep_ms if gstep_ms else None}
     prof_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof_path):
         with open(prof_path) as f:

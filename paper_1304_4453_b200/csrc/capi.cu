@@ -287,6 +287,11 @@ cd_status cd_ctx_kernel_stats(cd_ctx *ctx, cd_kernel_stat *out, int32_t capacity
             }
             for (auto &kv : agg)
                 ctx->stats[kv.first] = kv.second;
+            auto model = ctx->stats.find("coarsen.model");  // contraction byte model (coarsen_dev)
+            if (model != ctx->stats.end() && ctx->stats.count("coarsen")) {
+                ctx->stats["coarsen"].bytes = model->second.bytes;
+                ctx->stats["coarsen"].items = model->second.items;
+            }
         }
         // per-kernel algorithmic bytes (DESIGN.md byte model), from the
         // per-tier work counters: plp 17 B / node, plm 24 B / node, plus

@@ -180,7 +180,7 @@ __global__ void k_dense_copy(int64_t nc, const int64_t *fpre, const int64_t *off
     }
 }
 
-cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
+static cd_graph *coarsen_dev_impl(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
     const int64_t n = g->n;
     const int grid = grid_for(n, 256, ctx->num_sms * 8);
     DBuf<int32_t> csz(ctx, std::max<int64_t>(nc, 1));
@@ -363,4 +363,19 @@ bool is_compact_dev(cd_ctx *ctx, int64_t n, const int32_t *z, int64_t nc) {
     return h == 0;
 }
 
+}  // namespace cdk
+
+namespace cdk {
+// Contraction with its algorithmic bytes: 12 B per fine node
+// (offsets + label), 8 (+4 weighted) B per fine entry (column + label gather
+// [+ weight]), 8 B per coarse entry (column + weight) and per coarse node
+// (offset), recorded as "coarsen.model" for the contraction roofline.
+cd_graph *coarsen_dev(cd_ctx *ctx, const cd_graph *g, const int32_t *z, int64_t nc, bool sorted) {
+    cd_graph *cg = coarsen_dev_impl(ctx, g, z, nc, sorted);
+    if (ctx->profiling)
+        add_stat_work(ctx, "coarsen.model",
+                      12.0 * g->n + (g->weighted ? 12.0 : 8.0) * g->D + 8.0 * cg->D + 8.0 * cg->n,
+                      static_cast<double>(g->D));
+    return cg;
+}
 }  // namespace cdk

@@ -75,3 +75,5 @@ def main():
 
 if __name__ == "__main__":
     main()
+    sys.stdout.flush()
+    os._exit(0)  # skip interpreter teardown: pinned torch tensors outlive the library context
