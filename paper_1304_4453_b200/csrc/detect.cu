@@ -120,6 +120,9 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
         c.chg = chg.p;
         c.active = nullptr;
     }
+    // from the node ids, on count tallies: the first sub-sweep needs no tally
+    c.identity_first = !initial && !g->weighted && world_size(ctx) == 1 &&
+                       env_i64("CD_PLP_IDENTITY", 1) != 0;
     Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
     int64_t updated = n, iter = 0;

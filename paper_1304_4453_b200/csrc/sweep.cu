@@ -1821,6 +1821,37 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// PLP's first sub-sweep from z = node ids (run_plp without `initial`,
+// H/plp.hpp:75) on count tallies.  Every label in a row is distinct (rows are
+// strictly ascending: no duplicate entries; a self-loop is u's own label
+// once), so each tallies 1 and the tie rule (H/plp.hpp:118-124) picks the
+// smallest: the row's first entry.  Same decision, margin and move as the
+// tally kernels; 8 bytes per node instead of the row and its label gathers.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_plp_identity(SweepParams P) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned long long key = load_key(P);
+    MoveQueue q;
+    for (int64_t base = P.own_lo + gw * 32; base < P.own_hi; base += nw * 32) {
+        const int64_t u = base + lane;
+        bool act = u < P.own_hi && selected(P, key, static_cast<int32_t>(u));
+        int64_t s = 0, d = 0;
+        if (act) {
+            s = P.off[u];
+            d = P.off[u + 1] - s;
+            act = d > 0;  // isolated nodes are never evaluated (H/plp.hpp:109)
+        }
+        const int32_t best = act ? P.col[s] : 0;
+        // a single label leads the (empty) runner-up by 1; two or more tie
+        decide<MODE_PLP>(P, q, act, static_cast<int32_t>(u), static_cast<int32_t>(u), best, 1.0,
+                         d == 1 ? 1.0 : 0.0);
+    }
+    q.flush(P);
+}
+
+// ---------------------------------------------------------------------------
 // apply: the bucket's moves become visible to the next sub-sweep
 // ---------------------------------------------------------------------------
 // A changed node activates its neighbours (H/plp.hpp:127-130).  When a
@@ -2003,6 +2034,7 @@ __global__ void k_tier_narrow(const int32_t *tlist, const int64_t *tstart, int64
 }
 
 Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g), c_(c) {
+    identity_pending_ = c.identity_first && c.mode == MODE_PLP && !g->weighted && !c.dense_best;
     graph_ensure_bins(ctx, g);
     cnt_.alloc(ctx, 8);
     mv_.alloc(ctx, std::max<int64_t>(g->n, 1));
@@ -2321,7 +2353,7 @@ static void launch_tiers_vc(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool
         launch_tiers<MODE, VC_REAL>(ctx, g, P, capture, branch);
 }
 
-void Sweeper::enqueue(bool capture) {
+void Sweeper::enqueue(bool capture, bool recording) {
     cd_ctx *ctx = ctx_;
     cd_graph *g = g_;
     SweepParams P;
@@ -2385,9 +2417,20 @@ void Sweeper::enqueue(bool capture) {
         CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
     if (n_pre_)
         CD_LAUNCH(ctx, "prebucket", k_prebucket, n_pre_, 1024, 0, P);
+    const bool identity = identity_pending_ && !recording && !exchange_;
+    if (!recording)
+        identity_pending_ = false;
     for (int b = 0; b < c_.buckets; ++b) {
         P.bucket = b;
         P.mv_count = cnt_.p + b;
+        if (b == 0 && identity) {
+            // labels are still the node ids: the tally is 1 for every neighbour,
+            // so the decision is the row's first (smallest) entry
+            const int64_t span = P.own_hi - P.own_lo;
+            CD_LAUNCH(ctx, "plp_first", k_plp_identity, grid_for((span + 31) / 32, 8, ctx->num_sms * 16), 256, 0, P);
+            apply(mv_.p, cnt_.p + b, 1, 0);
+            continue;
+        }
         int branch = 0;
         // profiling mode 2: the sub-sweep's concurrent tier group is the unit
         // timed (non-overlapping: its kernels run as in the timed run)
@@ -2475,7 +2518,7 @@ void Sweeper::pass(uint64_t key) {
         const int64_t l0 = ctx_->launches;
         CD_CUDA(cudaStreamBeginCapture(ctx_->stream, cudaStreamCaptureModeThreadLocal));
         try {
-            enqueue(true);
+            enqueue(true, true);
         } catch (...) {
             cudaGraph_t gtmp = nullptr;
             cudaStreamEndCapture(ctx_->stream, &gtmp);

@@ -17,6 +17,9 @@ struct SweepCall {
     // the node's last evaluation and the margin of its decision then
     // (DESIGN.md "Margin-pruned active set"); both nullable
     int2 *chg = nullptr;  // (changes since the last evaluation, margin then)
+    // PLP on count tallies from z = node ids over rows sorted ascending: the
+    // first sub-sweep takes each node's smallest neighbour (identity_subsweep)
+    bool identity_first = false;
     double *vols = nullptr;      // PLM community volumes
     int32_t *csize = nullptr;    // PLM community sizes (singleton guard; nullable)
     double gamma = 1.0;
@@ -54,7 +57,7 @@ class Sweeper {
     long long last_gain_fx() const { return last_gain_fx_; }  // the same in units of 2^-44 (exact)
 
   private:
-    void enqueue(bool capture);
+    void enqueue(bool capture, bool recording = false);
     void apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride);
     void exchange_and_apply(int b);
     cd_ctx *ctx_;
@@ -80,6 +83,7 @@ class Sweeper {
     cudaGraph_t graph_ = nullptr;
     cudaGraphExec_t exec_ = nullptr;
     int64_t kernels_per_pass_ = 0;
+    bool identity_pending_ = false;  // the first eager pass's bucket 0 (SweepCall::identity_first)
 };
 
 // Whole PLP run / PLM move phase of a graph with degrees <= 256 in one
