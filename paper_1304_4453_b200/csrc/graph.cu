@@ -684,6 +684,7 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
         g->st_val.alloc(ctx, g->hub_entries);
         g->chunk_np.alloc(ctx, g->n_hub_chunks);
         g->hp_best_val.alloc(ctx, g->n_hub_parts);
+        g->hp_second.alloc(ctx, g->n_hub_parts);
         g->hp_best_key.alloc(ctx, g->n_hub_parts);
         g->hp_scan.alloc(ctx, 2 * scan_scratch_elems(g->n_hub_parts));
         g->hp_flag.alloc(ctx, 1);
@@ -709,7 +710,7 @@ void graph_release_bins(cd_graph *g) {
         b->release();
     for (auto *b : {&g->hub_pbase, &g->hp_start, &g->hp_scan})
         b->release();
-    for (auto *b : {&g->hp_val, &g->hp_best_val, &g->hub_aux})
+    for (auto *b : {&g->hp_val, &g->hp_best_val, &g->hp_second, &g->hub_aux})
         b->release();
     g->hp_key.release();
     g->st_key.release();
@@ -733,6 +734,7 @@ HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g) {
         h->st_val.alloc(ctx, g->hub_entries);
         h->chunk_np.alloc(ctx, g->n_hub_chunks);
         h->hp_best_val.alloc(ctx, g->n_hub_parts);
+        h->hp_second.alloc(ctx, g->n_hub_parts);
         h->hp_best_key.alloc(ctx, g->n_hub_parts);
         h->hp_scan.alloc(ctx, 2 * scan_scratch_elems(g->n_hub_parts));
         h->hp_flag.alloc(ctx, 1);

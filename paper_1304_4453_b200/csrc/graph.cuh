@@ -122,6 +122,7 @@ struct cd_graph {
     cdk::DBuf<double> st_val;       // [hub_entries]
     cdk::DBuf<int32_t> chunk_np;    // [n_hub_chunks] pairs staged per chunk
     cdk::DBuf<double> hp_best_val;  // [n_hub_parts] per-partition best candidate
+    cdk::DBuf<double> hp_second;    // [n_hub_parts] its runner-up (PLP margins)
     cdk::DBuf<int32_t> hp_best_key; // [n_hub_parts]
     cdk::DBuf<int64_t> hp_scan;     // scan scratch (2 x tiles)
     cdk::DBuf<int32_t> hp_flag;     // partition table overflow (sticky)
@@ -174,7 +175,7 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
 struct HubScratch {
     DBuf<int32_t> hp_cnt, hp_cur, hp_key, hp_best_key, hp_flag, st_key, chunk_np;
     DBuf<int64_t> hp_start, hp_scan;
-    DBuf<double> hp_val, hp_best_val, hub_aux, st_val;
+    DBuf<double> hp_val, hp_best_val, hp_second, hub_aux, st_val;
 };
 HubScratch *hub_scratch_for(cd_ctx *ctx, const cd_graph *g);
 // a context for one concurrent run on the parent's device (own stream,

@@ -82,6 +82,7 @@ struct SweepParams {
     int32_t *hp_key;
     double *hp_val;
     double *hp_best_val;
+    double *hp_second;
     int32_t *hp_best_key;
     int32_t *hp_flag;
     double *hub_aux;
@@ -1047,12 +1048,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
     int32_t *keys = reinterpret_cast<int32_t *>(vals + CL_CAP);
     uint16_t *dlist = reinterpret_cast<uint16_t *>(keys + CL_CAP);
     __shared__ double scratch[CL_THREADS / 32][32];
-    __shared__ double red_v[CL_THREADS / 32];
+    __shared__ double red_v[CL_THREADS / 32], red_s[CL_THREADS / 32];
     __shared__ int32_t red_k[CL_THREADS / 32];
     __shared__ double red_wc[CL_THREADS / 32];
     __shared__ int ndist, overflow;
-    __shared__ double part_wc, best_v;
+    __shared__ double part_wc, best_v, best_s;
     __shared__ int32_t best_k;
+    const bool two = MODE == MODE_PLP && P.chg != nullptr;  // PLP margins: the runner-up too
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     constexpr int NW = CL_THREADS / 32;
     const int rank = static_cast<int>(cluster.block_rank());
@@ -1147,7 +1149,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
         const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
         const int nd = ndist;
-        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
+        double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY, cs = -1.0;
         int32_t ck = INT32_MAX;
         for (int j0 = threadIdx.x; j0 < nd; j0 += CL_THREADS * SW_ILP) {
             int32_t key[SW_ILP];
@@ -1169,33 +1171,51 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                 if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
                     continue;
                 const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc_all, vol_c, vd[c], vol_u, P);
-                if (better(val, key[c], cv, ck)) {
+                if (two) {
+                    keep2(val, key[c], cv, ck, cs);
+                } else if (better(val, key[c], cv, ck)) {
                     cv = val;
                     ck = key[c];
                 }
             }
         }
-        argmax_xor<32>(cv, ck);
+        if (two)
+            argmax2_xor<32>(cv, ck, cs);
+        else
+            argmax_xor<32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
+            red_s[wid] = cs;
         }
         __syncthreads();
         if (wid == 0) {
             cv = lane < NW ? red_v[lane] : -INFINITY;
             ck = lane < NW ? red_k[lane] : INT32_MAX;
-            argmax_xor<32>(cv, ck);
+            cs = lane < NW ? red_s[lane] : -1.0;
+            if (two)
+                argmax2_xor<32>(cv, ck, cs);
+            else
+                argmax_xor<32>(cv, ck);
             if (lane == 0) {
                 best_v = cv;
                 best_k = ck;
+                best_s = cs;
             }
         }
         cluster.sync();  // every CTA's best is visible
         if (rank == 0 && wid == 0) {
             cv = lane < CL ? *cluster.map_shared_rank(&best_v, lane < CL ? lane : 0) : -INFINITY;
             ck = lane < CL ? *cluster.map_shared_rank(&best_k, lane < CL ? lane : 0) : INT32_MAX;
-            argmax_xor<32>(cv, ck);
-            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+            cs = lane < CL ? *cluster.map_shared_rank(&best_s, lane < CL ? lane : 0) : -1.0;
+            double margin = 0.0;
+            if (two) {
+                argmax2_xor<32>(cv, ck, cs);
+                margin = cv - fmax(cs, 0.0);
+            } else {
+                argmax_xor<32>(cv, ck);
+            }
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
                 ++st_n;
                 st_e += static_cast<unsigned long long>(e - s);
@@ -1671,7 +1691,7 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
     extern __shared__ unsigned char hub_smem[];
     V *vals = reinterpret_cast<V *>(hub_smem);
     int32_t *keys = reinterpret_cast<int32_t *>(vals + HUB_PART_CAP);
-    __shared__ double red_v[8];
+    __shared__ double red_v[8], red_s[8];
     __shared__ int32_t red_k[8];
     __shared__ double scratch[8][32];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
@@ -1681,6 +1701,7 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
             if (threadIdx.x == 0) {
                 P.hp_best_val[q] = -INFINITY;
                 P.hp_best_key[q] = INT32_MAX;
+                P.hp_second[q] = -1.0;
             }
             continue;
         }
@@ -1725,8 +1746,9 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
         const double wc = (MODE == MODE_PLM) ? P.hub_aux[h] : 0.0;
         const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
         const double vol_c = (MODE == MODE_PLM) ? __dsub_rn(P.vols[cur], vol_u) : 0.0;
-        double cv = -INFINITY;
+        double cv = -INFINITY, cs = -1.0;
         int32_t ck = INT32_MAX;
+        const bool two = MODE == MODE_PLP && P.chg != nullptr;  // PLP margins: the runner-up too
         for (uint32_t t0 = threadIdx.x; t0 < cap; t0 += blockDim.x * SW_ILP) {
             int32_t key[SW_ILP];
             double aff[SW_ILP], vd[SW_ILP];
@@ -1746,28 +1768,40 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
                 if (key[c] == EMPTY_KEY || (MODE == MODE_PLM && key[c] == cur))
                     continue;
                 const double val = (MODE == MODE_PLP) ? aff[c] : plm_delta(aff[c], wc, vol_c, vd[c], vol_u, P);
-                if (better(val, key[c], cv, ck)) {
+                if (two) {
+                    keep2(val, key[c], cv, ck, cs);
+                } else if (better(val, key[c], cv, ck)) {
                     cv = val;
                     ck = key[c];
                 }
             }
         }
-        argmax_xor<32>(cv, ck);
+        if (two)
+            argmax2_xor<32>(cv, ck, cs);
+        else
+            argmax_xor<32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
+            red_s[wid] = cs;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
             cv = red_v[0];
             ck = red_k[0];
-            for (int w2 = 1; w2 < 8; ++w2)
+            cs = red_s[0];
+            for (int w2 = 1; w2 < 8; ++w2) {
                 if (better(red_v[w2], red_k[w2], cv, ck)) {
+                    cs = fmax(red_s[w2], cv);
                     cv = red_v[w2];
                     ck = red_k[w2];
+                } else {
+                    cs = fmax(cs, red_v[w2]);
                 }
+            }
             P.hp_best_val[q] = cv;
             P.hp_best_key[q] = ck;
+            P.hp_second[q] = cs;
         }
         __syncthreads();
     }
@@ -1775,37 +1809,58 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
 
 template <int MODE>
 __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
-    __shared__ double red_v[8];
+    __shared__ double red_v[8], red_s[8];
     __shared__ int32_t red_k[8];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const unsigned long long bkey = load_key(P);
+    const bool two = MODE == MODE_PLP && P.chg != nullptr;  // PLP margins
     MoveQueue mq;
     for (int64_t h = blockIdx.x; h < P.n_hubs; h += gridDim.x) {
         const int32_t u = P.hubs[h];
         if (!selected(P, bkey, u))
             continue;
-        double cv = -INFINITY;
+        double cv = -INFINITY, cs = -1.0;
         int32_t ck = INT32_MAX;
         for (int64_t q = P.hub_pbase[h] + threadIdx.x; q < P.hub_pbase[h + 1]; q += blockDim.x) {
             const double v = P.hp_best_val[q];
             const int32_t k = P.hp_best_key[q];
-            if (better(v, k, cv, ck)) {
+            if (two) {  // a partition's (best, runner-up) against the running pair
+                const double s = P.hp_second[q];
+                if (better(v, k, cv, ck)) {
+                    cs = fmax(s, cv);
+                    cv = v;
+                    ck = k;
+                } else {
+                    cs = fmax(cs, v);
+                }
+            } else if (better(v, k, cv, ck)) {
                 cv = v;
                 ck = k;
             }
         }
-        argmax_xor<32>(cv, ck);
+        if (two)
+            argmax2_xor<32>(cv, ck, cs);
+        else
+            argmax_xor<32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
+            red_s[wid] = cs;
         }
         __syncthreads();
         if (wid == 0) {
             cv = lane < 8 ? red_v[lane] : -INFINITY;
             ck = lane < 8 ? red_k[lane] : INT32_MAX;
-            argmax_xor<32>(cv, ck);
+            cs = lane < 8 ? red_s[lane] : -1.0;
+            double margin = 0.0;
+            if (two) {
+                argmax2_xor<32>(cv, ck, cs);
+                margin = cv - fmax(cs, 0.0);
+            } else {
+                argmax_xor<32>(cv, ck);
+            }
             const int32_t cur = P.z[u];
-            decide<MODE>(P, mq, lane == 0, u, cur, ck, cv);
+            decide<MODE>(P, mq, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
                 if (MODE == MODE_PLM)
                     P.hub_aux[h] = 0.0;
@@ -2403,6 +2458,7 @@ void Sweeper::enqueue(bool capture, bool recording) {
     P.hp_key = hs ? hs->hp_key.p : g->hp_key.p;
     P.hp_val = hs ? hs->hp_val.p : g->hp_val.p;
     P.hp_best_val = hs ? hs->hp_best_val.p : g->hp_best_val.p;
+    P.hp_second = hs ? hs->hp_second.p : g->hp_second.p;
     P.hp_best_key = hs ? hs->hp_best_key.p : g->hp_best_key.p;
     P.hp_flag = hs ? hs->hp_flag.p : g->hp_flag.p;
     P.hub_aux = hs ? hs->hub_aux.p : g->hub_aux.p;
