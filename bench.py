@@ -347,6 +347,7 @@ def bench_b200(args, wl):
     world, rank, local = dist_env()
     dist = None
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines (nranks) on stderr
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)

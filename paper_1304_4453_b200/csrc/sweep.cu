@@ -1927,7 +1927,8 @@ __device__ __forceinline__ int64_t seg_total(const int32_t *counts, int nseg) {
 
 __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, uint8_t *active, int2 *chg, const int64_t *toff,
-                                                   const int32_t *tcol, long long *total, int64_t n) {
+                                                   const int32_t *tcol, long long *total, int64_t n,
+                                                   int64_t dense_at) {
     const int64_t count = seg_total(counts, nseg);
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -1936,7 +1937,7 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count));
     // margin mode: neighbours count the changes in their rows (each entry
     // whose label changed); beyond n/16 movers every node is re-evaluated
-    const bool dense = (active || chg) && count > n / 16;
+    const bool dense = (active || chg) && count > dense_at;
     if (dense && chg)  // (the margins are recomputed at the next evaluation)
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 1) / 2;
              i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -2517,6 +2518,13 @@ void Sweeper::enqueue(bool capture, bool recording) {
     }
 }
 
+// movers in one PLP sub-sweep beyond which every node is re-evaluated instead
+// of counting per neighbour (CD_PLP_DENSE_DIV: n / div, default 16)
+static int64_t plp_dense_at(int64_t n) {
+    static const int64_t div = std::max<int64_t>(1, env_i64("CD_PLP_DENSE_DIV", 16));
+    return n / div;
+}
+
 void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride) {
     cd_ctx *ctx = ctx_;
     cd_graph *g = g_;
@@ -2524,7 +2532,7 @@ void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t str
     if (c_.mode == MODE_PLP)
         CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
                   c_.active, c_.chg, c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
-                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), total_.p, g->n);
+                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), total_.p, g->n, plp_dense_at(g->n));
     else
         CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
                   c_.vols, c_.csize, static_cast<const double *>(g->vol.p), c_.active,
