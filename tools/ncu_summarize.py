@@ -25,7 +25,7 @@ MODE_ARG = {"k_sweep_direct": 1, "k_sweep_warp": 0, "k_sweep_block": 0, "k_hub_p
 
 
 def family_of(name):
-    m = re.search(r"cdk::(k_\w+)(?:<([^>]*)>)?", name)
+    m = re.search(r"(?:cdk::)?\b(k_\w+)(?:<([^>]*)>)?", name)
     if not m:
         return None
     base, args = m.group(1), m.group(2)
