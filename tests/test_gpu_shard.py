@@ -321,3 +321,55 @@ def test_sharded_coarse_graph_layout(dev, monkeypatch):
     res = run_ranks(dev, 3, fn)
     assert res[0][0] == 0 and res[-1][1] == full["off"].shape[0] - 1
     assert all(res[i][1] == res[i + 1][0] for i in range(2))
+
+
+@pytest.mark.parametrize("G", [2, 3])
+@pytest.mark.parametrize("kind", ["rmat", "rmat_int", "planted"])
+def test_row_shard_from_own_rows(dev, G, kind):
+    """cd_graph_from_csr_rows: every rank uploads the offsets and only its own
+    rows (bench.py's multi-GPU e2e) and gets the same row shard as cutting
+    the whole graph (cd_graph_shard): layout, node state and totals, and the
+    same labels as one device."""
+    ctx0 = dev.Context(0)
+    g1 = build(dev, kind, ctx0)
+    full = g1.csr()
+    n, m, total = g1.node_count(), g1.edge_count(), g1.total_edge_weight()
+    z1, _ = detect(dev, "plm", g1)
+    p1, _ = detect(dev, "plp", g1)
+    ctx0.close()
+    bounds = dev.shard_bounds(full["off"], G)
+
+    def fn(ctx, r):
+        lo, hi = int(bounds[r]), int(bounds[r + 1])
+        e0, e1 = int(full["off"][lo]), int(full["off"][hi])
+        w = None if full["w"] is None else full["w"][e0:e1]
+        g = dev.Graph.from_csr_rows(n, full["off"], lo, hi, full["col"][e0:e1], w, ctx=ctx)
+        ref = build(dev, kind, ctx).shard(ctx)
+        a, b = g.csr(), ref.csr()
+        for key in ("off", "col", "vol", "loop"):
+            np.testing.assert_array_equal(a[key], b[key])
+        assert g.owned_range == ref.owned_range == (lo, hi)
+        assert (g.edge_count(), g.total_edge_weight()) == (m, total)
+        return detect(dev, "plm", g)[0], detect(dev, "plp", g)[0]
+
+    for z, p in run_ranks(dev, G, fn):
+        assert np.array_equal(z, z1) and np.array_equal(p, p1)
+
+
+def test_row_shard_from_own_rows_checks_range(dev):
+    """Every rank must pass exactly its cd_shard_bounds range (checked
+    before any collective, so a wrong range fails on each rank alone)."""
+    ctx0 = dev.Context(0)
+    full = build(dev, "rmat", ctx0).csr()
+    ctx0.close()
+    n = len(full["off"]) - 1
+    bounds = dev.shard_bounds(full["off"], 2)
+
+    def fn(ctx, r):
+        lo, hi = int(bounds[r]) + 1, int(bounds[r + 1])  # one row short
+        e0, e1 = int(full["off"][lo]), int(full["off"][hi])
+        with pytest.raises(dev.InvalidArgument, match="not this rank's shard range"):
+            dev.Graph.from_csr_rows(n, full["off"], lo, hi, full["col"][e0:e1], ctx=ctx)
+        return True
+
+    assert all(run_ranks(dev, 2, fn))
