@@ -540,6 +540,89 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
     }
 }
 
+// ---------------------------------------------------------------------------
+// tiers G8 / G16 (deg <= DM): a thread per node.  The row's <= DM labels are tallied in
+// registers (each label's first entry sums the equal ones after it, in entry
+// order -- the lane order of the group aggregate), so a warp evaluates 32
+// nodes at once with no shuffles, no __match_any_sync and no cross-lane
+// argmax; 8 lanes per node spent most of the round on those collectives.
+// ---------------------------------------------------------------------------
+template <int DM, int MODE, int VC>
+__global__ void __launch_bounds__(256) k_sweep_thread(SweepParams P, int tier) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const int32_t *list;
+    int64_t count;
+    const bool pre = tier_range(P, tier, list, count);
+    const unsigned long long bkey = load_key(P);
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    for (int64_t base = gw * 32; base < count; base += nw * 32) {
+        const int64_t i = base + lane;
+        const int32_t u = i < count ? list[i] : 0;
+        const bool act = i < count && selected_in(P, bkey, u, pre);
+        int32_t best = INT32_MAX, cur = 0;
+        double bv = (MODE == MODE_PLP) ? -1.0 : -INFINITY, sv = -1.0;
+        if (act) {
+            const int64_t s = P.off[u];
+            const int d = static_cast<int>(P.off[u + 1] - s);
+            cur = P.z[u];
+            int32_t kk[DM];
+            double ww[DM];
+#pragma unroll
+            for (int c = 0; c < DM; ++c) {
+                const bool valid = c < d;
+                const int32_t v = valid ? P.col[s + c] : -1;
+                ww[c] = (VC != VC_COUNT && valid) ? static_cast<double>(P.w[s + c]) : 1.0;
+                kk[c] = (valid && !(MODE == MODE_PLM && v == u)) ? v : -1;
+            }
+#pragma unroll
+            for (int c = 0; c < DM; ++c)
+                kk[c] = kk[c] >= 0 ? P.z[kk[c]] : EMPTY_KEY;
+            double wc = 0.0, vol_u = 0.0, vol_c = 0.0;
+            if (MODE == MODE_PLM) {
+#pragma unroll
+                for (int c = 0; c < DM; ++c)
+                    if (kk[c] != EMPTY_KEY && kk[c] == cur)
+                        wc += ww[c];
+                vol_u = P.vol[u];
+                vol_c = __dsub_rn(P.vols[cur], vol_u);
+            }
+            // candidates: each label's first entry; their volumes gathered together
+            bool head[DM];
+            double vd[DM];
+#pragma unroll
+            for (int c = 0; c < DM; ++c) {
+                head[c] = kk[c] != EMPTY_KEY && !(MODE == MODE_PLM && kk[c] == cur);
+#pragma unroll
+                for (int j = 0; j < c; ++j)
+                    head[c] = head[c] && kk[j] != kk[c];
+                vd[c] = (MODE == MODE_PLM && head[c]) ? P.vols[kk[c]] : 0.0;
+            }
+#pragma unroll
+            for (int c = 0; c < DM; ++c) {
+                if (!head[c])
+                    continue;
+                double agg = 0.0;
+#pragma unroll
+                for (int j = c; j < DM; ++j)
+                    if (kk[j] == kk[c])
+                        agg += ww[j];
+                const double val = (MODE == MODE_PLP) ? agg : plm_delta(agg, wc, vol_c, vd[c], vol_u, P);
+                keep2(val, kk[c], bv, best, sv);
+            }
+            ++st_n;
+            st_e += static_cast<unsigned long long>(d);
+        }
+        const double margin = (MODE == MODE_PLP && P.chg) ? bv - fmax(sv, 0.0) : 0.0;
+        decide<MODE>(P, q, act, u, cur, best, bv, margin);
+    }
+    q.flush(P);
+    q.flush_gain(P);
+    flush_stats(P, tier, st_n, st_e);
+}
+
 template <int G, int MODE, int VC>
 // count tallies: 32 registers (8-16 B of spill), 8 blocks per SM instead of 6
 // (C2 level 0 -6 %)
@@ -2233,17 +2316,24 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     })
     if ((P.tend[TIER_G8] - P.tbeg[TIER_G8])) {
         fam = names[MODE][TIER_G8];
-        auto kfn = k_sweep_direct<8, MODE, VC>;
-        const int ch = chunk_for(4, P.tend[TIER_G8] - P.tbeg[TIER_G8], int64_t(wave(kfn, 256, 0)) * (256 / 32));
-        const int grid = warps_grid_k(kfn, (P.tend[TIER_G8] - P.tbeg[TIER_G8]), 256, ch);
-        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G8), ch);
+        auto kfn = k_sweep_thread<8, MODE, VC>;  // a thread per node
+        const int64_t nodes = pre_count(P, TIER_G8, P.tend[TIER_G8] - P.tbeg[TIER_G8]);
+        const int grid = grid_for((nodes + 31) / 32, 8, wave(kfn, 256, 0));
+        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G8));
     }
     if ((P.tend[TIER_G16] - P.tbeg[TIER_G16])) {
         fam = names[MODE][TIER_G16];
-        auto kfn = k_sweep_direct<16, MODE, VC>;
-        const int ch = chunk_for(2, P.tend[TIER_G16] - P.tbeg[TIER_G16], int64_t(wave(kfn, 256, 0)) * (256 / 32));
-        const int grid = warps_grid_k(kfn, (P.tend[TIER_G16] - P.tbeg[TIER_G16]), 256, ch);
-        CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16), ch);
+        if (MODE == MODE_PLP) {  // a thread per node (PLM's 16 volume gathers per thread cost occupancy)
+            auto kfn = k_sweep_thread<16, MODE, VC>;
+            const int64_t nodes = pre_count(P, TIER_G16, P.tend[TIER_G16] - P.tbeg[TIER_G16]);
+            const int grid = grid_for((nodes + 31) / 32, 8, wave(kfn, 256, 0));
+            CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16));
+        } else {
+            auto kfn = k_sweep_direct<16, MODE, VC>;
+            const int ch = chunk_for(2, P.tend[TIER_G16] - P.tbeg[TIER_G16], int64_t(wave(kfn, 256, 0)) * (256 / 32));
+            const int grid = warps_grid_k(kfn, (P.tend[TIER_G16] - P.tbeg[TIER_G16]), 256, ch);
+            CD_TIER_LAUNCH(kfn, grid, 256, 0, P, int(TIER_G16), ch);
+        }
     }
     if ((P.tend[TIER_G32] - P.tbeg[TIER_G32])) {
         fam = names[MODE][TIER_G32];
