@@ -195,7 +195,7 @@ void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vol
 }
 
 bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt,
-                    int64_t *passes, int64_t *moves) {
+                    int64_t *passes, int64_t *moves, bool from_singletons) {
     const int64_t n = g->n;
     if (n == 0 || g->total == 0.0)  // H/louvain.hpp:67-68
         return false;
@@ -203,7 +203,7 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
         bool ch;
         {
             LocalScope local(ctx);
-            ch = move_phase_dev(ctx, g, z, cfg, salt, passes, moves);
+            ch = move_phase_dev(ctx, g, z, cfg, salt, passes, moves, from_singletons);
         }
         ctx->comm->broadcast(ctx, z, n * sizeof(int32_t), 0);
         int32_t chv = ch ? 1 : 0;
@@ -254,6 +254,9 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
             *moves += fr.moves;
         return fr.changed;
     }
+    // from singletons every neighbour is its own community: the first
+    // sub-sweep needs no tally (k_plm_identity)
+    c.identity_first = from_singletons && world_size(ctx) == 1 && env_i64("CD_PLM_IDENTITY", 1) != 0;
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;
@@ -305,7 +308,7 @@ static void louvain_recurse(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &c
     DevTimer t(ctx);
     t.start();
     int64_t passes = 0, moves = 0;
-    const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0), &passes, &moves);
+    const bool changed = move_phase_dev(ctx, g, z, cfg, louvain_salt(level, 0), &passes, &moves, true);
     const double mv = t.stop_ms();
     if (g->D >= BIG_GRAPH_ENTRIES)
         graph_release_bins(g);  // room for the contraction and the coarse levels

@@ -39,8 +39,9 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
 int64_t plp_sweep_sync_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z_in, int32_t *z_out);
 void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vols, double gamma, int32_t *best,
                    double *gain);
+// from_singletons: z holds the node ids (the recursion's every level, H/louvain.hpp:242)
 bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt,
-                    int64_t *passes = nullptr, int64_t *moves = nullptr);
+                    int64_t *passes = nullptr, int64_t *moves = nullptr, bool from_singletons = false);
 int64_t louvain_run_dev(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg, int32_t *z, Report rep);
 int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep);
 

@@ -1990,6 +1990,110 @@ __global__ void __launch_bounds__(256) k_plp_identity(SweepParams P) {
 }
 
 // ---------------------------------------------------------------------------
+// PLM's first sub-sweep of a move phase from singletons (every level of the
+// recursion, H/louvain.hpp:242).  Each neighbour v != u is its own
+// community, so its tally is exactly w(u, v); u's own community holds u
+// alone (w_c = 0, vol_c = vols[u] - vol_u); the candidates are the row's
+// entries and each gets the same plm_delta the tally kernels compute.  No
+// table: a gather of vols[v] per entry.  Nodes up to BLOCK3 degree: a warp
+// each; CLUSTER / HUB degrees: a block each.  (Not counted in the sweep
+// families' work counters or times: no tally runs.)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void plm_identity_scan(const SweepParams &P, int32_t u, int64_t s, int64_t e,
+                                                  double vol_u, double vol_c, int stride, int first, double &cv,
+                                                  int32_t &ck) {
+    for (int64_t f0 = s + first; f0 < e; f0 += int64_t(stride) * SW_ILP) {
+        int32_t vv[SW_ILP];
+        double ww[SW_ILP], vd[SW_ILP];
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            const int64_t f = f0 + int64_t(c) * stride;
+            vv[c] = f < e ? P.col[f] : -1;
+            ww[c] = (P.w && f < e) ? static_cast<double>(P.w[f]) : 1.0;
+        }
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            if (vv[c] == u)
+                vv[c] = -1;  // the self-loop is no candidate (H/louvain.hpp:96-97)
+            vd[c] = vv[c] >= 0 ? P.vols[vv[c]] : 0.0;
+        }
+#pragma unroll
+        for (int c = 0; c < SW_ILP; ++c) {
+            if (vv[c] < 0)
+                continue;
+            const double val = plm_delta(ww[c], 0.0, vol_c, vd[c], vol_u, P);
+            if (better(val, vv[c], cv, ck)) {
+                cv = val;
+                ck = vv[c];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_plm_identity_warp(SweepParams P) {
+    const int lane = lane_id();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    const unsigned long long key = load_key(P);
+    const int32_t *list = P.tlist + P.tbeg[TIER_G8];
+    const int64_t count = P.tend[TIER_BLOCK3] - P.tbeg[TIER_G8];
+    MoveQueue q;
+    for (int64_t i = gw; i < count; i += nw) {
+        const int32_t u = list[i];
+        if (!selected(P, key, u))
+            continue;
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        const double vol_u = P.vol[u];
+        const double vol_c = __dsub_rn(P.vols[u], vol_u);
+        double cv = -INFINITY;
+        int32_t ck = INT32_MAX;
+        plm_identity_scan(P, u, s, e, vol_u, vol_c, 32, lane, cv, ck);
+        argmax_xor<32>(cv, ck);
+        decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
+    }
+    q.flush(P);
+    q.flush_gain(P);
+}
+
+__global__ void __launch_bounds__(256) k_plm_identity_block(SweepParams P) {
+    __shared__ double red_v[8];
+    __shared__ int32_t red_k[8];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    const unsigned long long key = load_key(P);
+    const int32_t *list = P.tlist + P.tbeg[TIER_CLUSTER];
+    const int64_t count = P.tend[TIER_HUB] - P.tbeg[TIER_CLUSTER];
+    MoveQueue q;
+    for (int64_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const int32_t u = list[i];
+        if (!selected(P, key, u))  // uniform across the block
+            continue;
+        const int64_t s = P.off[u], e = P.off[u + 1];
+        const double vol_u = P.vol[u];
+        const double vol_c = __dsub_rn(P.vols[u], vol_u);
+        double cv = -INFINITY;
+        int32_t ck = INT32_MAX;
+        plm_identity_scan(P, u, s, e, vol_u, vol_c, 256, threadIdx.x, cv, ck);
+        argmax_xor<32>(cv, ck);
+        if (lane == 0) {
+            red_v[wid] = cv;
+            red_k[wid] = ck;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            cv = lane < 8 ? red_v[lane] : -INFINITY;
+            ck = lane < 8 ? red_k[lane] : INT32_MAX;
+            argmax_xor<32>(cv, ck);
+            decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
+        }
+        __syncthreads();
+    }
+    if (wid == 0) {
+        q.flush(P);
+        q.flush_gain(P);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // apply: the bucket's moves become visible to the next sub-sweep
 // ---------------------------------------------------------------------------
 // A changed node activates its neighbours (H/plp.hpp:127-130).  When a
@@ -2173,7 +2277,8 @@ __global__ void k_tier_narrow(const int32_t *tlist, const int64_t *tstart, int64
 }
 
 Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g), c_(c) {
-    identity_pending_ = c.identity_first && c.mode == MODE_PLP && !g->weighted && !c.dense_best;
+    // PLP needs count tallies (an unweighted graph); PLM's identity sub-sweep takes any weights
+    identity_pending_ = c.identity_first && !c.dense_best && (c.mode == MODE_PLM || !g->weighted);
     graph_ensure_bins(ctx, g);
     cnt_.alloc(ctx, 8);
     mv_.alloc(ctx, std::max<int64_t>(g->n, 1));
@@ -2571,10 +2676,21 @@ void Sweeper::enqueue(bool capture, bool recording) {
         P.bucket = b;
         P.mv_count = cnt_.p + b;
         if (b == 0 && identity) {
-            // labels are still the node ids: the tally is 1 for every neighbour,
-            // so the decision is the row's first (smallest) entry
-            const int64_t span = P.own_hi - P.own_lo;
-            CD_LAUNCH(ctx, "plp_first", k_plp_identity, grid_for((span + 31) / 32, 8, ctx->num_sms * 16), 256, 0, P);
+            if (plp) {
+                // labels are still the node ids: the tally is 1 for every neighbour,
+                // so the decision is the row's first (smallest) entry
+                const int64_t span = P.own_hi - P.own_lo;
+                CD_LAUNCH(ctx, "plp_first", k_plp_identity, grid_for((span + 31) / 32, 8, ctx->num_sms * 16), 256,
+                          0, P);
+            } else {
+                // singletons: every neighbour is its own community
+                const int64_t nw = P.tend[TIER_BLOCK3] - P.tbeg[TIER_G8];
+                const int64_t nb = P.tend[TIER_HUB] - P.tbeg[TIER_CLUSTER];
+                if (nw > 0)
+                    CD_LAUNCH(ctx, "plm_first", k_plm_identity_warp, grid_for(nw, 8, ctx->num_sms * 16), 256, 0, P);
+                if (nb > 0)
+                    CD_LAUNCH(ctx, "plm_first", k_plm_identity_block, grid_for(nb, 1, ctx->num_sms * 8), 256, 0, P);
+            }
             apply(mv_.p, cnt_.p + b, 1, 0);
             continue;
         }
