@@ -114,14 +114,14 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
     // DESIGN.md "Margin-pruned active set"); CD_PLP_MARGIN=0 keeps the flags
     DBuf<int2> chg;
     static const bool margins = env_i64("CD_PLP_MARGIN", 1) != 0;
-    if (margins && !g->weighted && world_size(ctx) == 1 && n > 0) {
+    if (margins && !g->weighted && n > 0) {
         chg.alloc(ctx, n);
         chg.fill_bytes(0x20);  // (CHG_ALL, 0x20202020): every node is evaluated once
         c.chg = chg.p;
         c.active = nullptr;
     }
     // from the node ids, on count tallies: the first sub-sweep needs no tally
-    c.identity_first = !initial && !g->weighted && world_size(ctx) == 1 &&
+    c.identity_first = !initial && !g->weighted &&
                        env_i64("CD_PLP_IDENTITY", 1) != 0;
     Sweeper sw(ctx, g, c);
     DevTimer it(ctx);
@@ -256,7 +256,7 @@ bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_confi
     }
     // from singletons every neighbour is its own community: the first
     // sub-sweep needs no tally (k_plm_identity)
-    c.identity_first = from_singletons && world_size(ctx) == 1 && env_i64("CD_PLM_IDENTITY", 1) != 0;
+    c.identity_first = from_singletons && env_i64("CD_PLM_IDENTITY", 1) != 0;
     Sweeper sw(ctx, g, c);
     bool changed = false;
     static const bool trace = std::getenv("CD_TRACE") != nullptr;

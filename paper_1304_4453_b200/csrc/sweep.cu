@@ -2669,7 +2669,7 @@ void Sweeper::enqueue(bool capture, bool recording) {
         CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
     if (n_pre_)
         CD_LAUNCH(ctx, "prebucket", k_prebucket, n_pre_, 1024, 0, P);
-    const bool identity = identity_pending_ && !recording && !exchange_;
+    const bool identity = identity_pending_ && !recording;
     if (!recording)
         identity_pending_ = false;
     for (int b = 0; b < c_.buckets; ++b) {
@@ -2691,7 +2691,10 @@ void Sweeper::enqueue(bool capture, bool recording) {
                 if (nb > 0)
                     CD_LAUNCH(ctx, "plm_first", k_plm_identity_block, grid_for(nb, 1, ctx->num_sms * 8), 256, 0, P);
             }
-            apply(mv_.p, cnt_.p + b, 1, 0);
+            if (exchange_)
+                exchange_and_apply(b);
+            else
+                apply(mv_.p, cnt_.p + b, 1, 0);
             continue;
         }
         int branch = 0;
