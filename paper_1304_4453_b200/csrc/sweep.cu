@@ -2428,7 +2428,9 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if ((P.tend[TIER_G16] - P.tbeg[TIER_G16])) {
         fam = names[MODE][TIER_G16];
-        if (MODE == MODE_PLP) {  // a thread per node (PLM's 16 volume gathers per thread cost occupancy)
+        // a thread per node for PLP count tallies (PLM's 16 volume gathers, or 16
+        // fp64 weights, per thread cost too many registers: 100-128)
+        if (MODE == MODE_PLP && VC == VC_COUNT) {
             auto kfn = k_sweep_thread<16, MODE, VC>;
             const int64_t nodes = pre_count(P, TIER_G16, P.tend[TIER_G16] - P.tbeg[TIER_G16]);
             const int grid = grid_for((nodes + 31) / 32, 8, wave(kfn, 256, 0));
