@@ -370,8 +370,6 @@ static __global__ void __launch_bounds__(512, CAP <= 2048 ? 4 : 1) k_eng_reduce_
 // otherwise hammer the same global slots with atomics from every block),
 // then inserts each distinct key once into the row's global table.  Keys
 // that find no smem slot within a few probes go to the global table directly.
-// A warp whose slice proves mostly distinct skips the combine after two
-// rounds (it cannot shrink such keys).
 constexpr int ENG_PRE_CAP = 2048;
 constexpr int ENG_PRE_PROBES = 8;
 
@@ -415,21 +413,13 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
     const uint32_t cap = static_cast<uint32_t>(tab_cap[lo]);
     if (a < b) {
         auto cur = src.init(r, a);
-        bool direct = false;
-        int rounds = 0, seen = 0, novel = 0;
         for (int64_t f = a; f < b; f += 32) {
             int32_t k;
             double w;
             bool valid;
             src.load(r, f, b, cur, k, w, valid);
-            if (direct) {
-                if (valid)
-                    table_insert_n(keys, vals, cnts, cap, k, w, 1u);
-                continue;
-            }
             double sum;
             uint32_t cnt;
-            bool fresh = false;  // this leader claimed a new smem slot
             if (warp_aggregate(k, w, valid, 0xffffffffu, scratch[wid], sum, cnt)) {
                 uint32_t sl = hash_slot(k, ENG_PRE_CAP - 1);
                 bool done = false;
@@ -438,24 +428,13 @@ static __global__ void __launch_bounds__(256) k_eng_reduce_global_insert(Src src
                     if (old == EMPTY_KEY || old == k) {
                         atomicAdd(&pv[sl], sum);
                         atomicAdd(&pc[sl], cnt);
-                        fresh = old == EMPTY_KEY;
                         done = true;
                     }
                     sl = (sl + 1) & (ENG_PRE_CAP - 1);
                 }
-                if (!done) {
+                if (!done)
                     table_insert_n(keys, vals, cnts, cap, k, sum, cnt);
-                    fresh = true;
-                }
             }
-            // a warp whose first two rounds combined (almost) nothing -- an
-            // R-MAT coarse level's big rows are 98.6 % distinct -- inserts the
-            // rest of its slice straight into the row's table: the combine
-            // costs a match_any and up to 8 shared CAS probes per entry
-            seen += __popc(__ballot_sync(0xffffffffu, valid));
-            novel += __popc(__ballot_sync(0xffffffffu, fresh));
-            if (++rounds == 2)
-                direct = 10 * novel >= 9 * seen;
         }
     }
     __syncthreads();
