@@ -271,3 +271,27 @@ def test_louvain_reference_stopping_bit_exact(dev, ctx, oracle, e2e_graphs, name
     z, rep = dev.run_louvain(g, dev.LouvainConfig.reference(seed=3))
     assert np.array_equal(z, z_ref)
     assert rep.community_count == k_ref and len(rep.levels) == lv_ref
+
+
+@pytest.mark.parametrize("kind", ["unit", "int", "dyadic"])
+def test_end_to_end_with_loops_and_isolated_nodes(dev, ctx, oracle, kind):
+    """Self-loops, isolated nodes and every weight kind through the first
+    sub-sweeps from singletons (PLP's row-first-entry rule, PLM's tally-free
+    evaluation) and the margin-pruned active set: bit-exact vs the port."""
+    from conftest import rand_edges
+    rng = np.random.default_rng(17)
+    n = 3000
+    eu, ev, ew = rand_edges(rng, n, 0.004, kind=kind, loop_p=0.2)
+    keep = (eu < n - 100) & (ev < n - 100)  # the last 100 nodes stay isolated
+    eu, ev, ew = eu[keep], ev[keep], ew[keep]
+    og = oracle.from_arrays(n, eu, ev, ew)
+    w = None if kind == "unit" else ew.astype(np.float32)
+    g = dev.Graph.from_edges(n, (eu, ev, w)) if w is not None else dev.Graph.from_edges(n, (eu, ev))
+    lab_ref, trace_ref = oracle.plp_bucketed(og, seed=4)
+    lab, rep = dev.run_plp(g, dev.PlpConfig(seed=4))
+    assert [it["updated"] for it in rep.iterations] == trace_ref.tolist()
+    assert np.array_equal(lab, lab_ref)
+    for refine in (False, True):
+        z_ref, k_ref, _ = oracle.louvain_bucketed(og, refine=refine, seed=4)
+        z, rep = dev.run_louvain(g, dev.LouvainConfig(refine=refine, seed=4))
+        assert np.array_equal(z, z_ref), refine
