@@ -104,8 +104,8 @@ struct SrcCoarsen {
         if (valid) {
             u = mem[p];
             const int64_t e = off[u] + (f - mpre[p]);
-            v = col[e];
-            wt = w ? static_cast<double>(w[e]) : 1.0;
+            v = __ldcs(col + e);  // streamed once: evict-first keeps z cached
+            wt = w ? static_cast<double>(__ldcs(w + e)) : 1.0;
             k = z[v];
             if (k == static_cast<int32_t>(c) && v < u)
                 valid = false;
