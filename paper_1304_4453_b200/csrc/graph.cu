@@ -499,10 +499,10 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
     std::vector<cudaEvent_t> done(static_cast<size_t>(nchunks));
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
-        CD_CUDA(cudaMemcpyAsync(col_dev + ib, col_host + ib, (ie - ib) * sizeof(int32_t), cudaMemcpyHostToDevice,
+        CD_CUDA(cudaMemcpyAsync(col_dev + ib, col_host + ib, (ie - ib) * sizeof(int32_t), cudaMemcpyDefault,
                                 ctx->copy_stream));
-        if (w_dev)
-            CD_CUDA(cudaMemcpyAsync(w_dev + ib, w_host + ib, (ie - ib) * sizeof(float), cudaMemcpyHostToDevice,
+        if (w_dev)  // (the weights may live anywhere: cudaMemcpyDefault)
+            CD_CUDA(cudaMemcpyAsync(w_dev + ib, w_host + ib, (ie - ib) * sizeof(float), cudaMemcpyDefault,
                                     ctx->copy_stream));
         done[c] = ctx_event(ctx);
         CD_CUDA(cudaEventRecord(done[c], ctx->copy_stream));

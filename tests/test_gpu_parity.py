@@ -295,3 +295,21 @@ def test_end_to_end_with_loops_and_isolated_nodes(dev, ctx, oracle, kind):
         z_ref, k_ref, _ = oracle.louvain_bucketed(og, refine=refine, seed=4)
         z, rep = dev.run_louvain(g, dev.LouvainConfig(refine=refine, seed=4))
         assert np.array_equal(z, z_ref), refine
+
+
+def test_uint64_iteration_caps_saturate(dev, ctx, oracle, e2e_graphs):
+    """The reference's caps are uint64 counts (H/plp.hpp:20, H/louvain.hpp:17):
+    UINT64_MAX means "until converged" -- it saturates, never wraps to -1
+    (zero iterations) or truncates, and the per-pass trace stays bounded."""
+    og = e2e_graphs["lfr"]
+    g = _dev_of(dev, "lfr", og)
+    big = (1 << 64) - 1
+    lab, rep = dev.run_plp(g, dev.PlpConfig(seed=5, max_iterations=big))
+    lab_ref, trace_ref = oracle.plp_bucketed(og, seed=5)
+    assert np.array_equal(lab, lab_ref) and len(rep.iterations) == len(trace_ref)
+    z, rep = dev.run_louvain(g, dev.LouvainConfig(seed=3, max_move_iterations=big, max_levels=big))
+    z_ref, _, _ = oracle.louvain_bucketed(og, seed=3)
+    assert np.array_equal(z, z_ref)
+    # 2^32 + 1 passes is not 1 pass
+    z2, _ = dev.run_louvain(g, dev.LouvainConfig(seed=3, max_move_iterations=(1 << 32) + 1))
+    assert np.array_equal(z2, z_ref)
