@@ -122,17 +122,30 @@ def measured_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons during the timed region."""
+    """nvidia-smi clocks / throttle reasons during the timed region.  Started
+    before the warm-up (nvidia-smi's start-up -- NVML initialisation -- then
+    never overlaps the timed steps); only the samples stamped inside the timed
+    window (mark_begin / mark_end) are reported."""
 
     def __init__(self, device):
         self.device = device
         self.proc = None
         self.path = None
+        self.window = None
+
+    def mark_begin(self):
+        import datetime
+        self.window = [datetime.datetime.now(), None]
+
+    def mark_end(self):
+        import datetime
+        if self.window:
+            self.window[1] = datetime.datetime.now()
 
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
@@ -151,16 +164,23 @@ class ClockSampler:
             self.proc.wait(timeout=5)
         except subprocess.TimeoutExpired:
             self.proc.kill()
+        import datetime
         rows = []
         with open(self.path) as f:
             for line in f:
                 p = [x.strip() for x in line.split(",")]
-                if len(p) >= 8:
+                if len(p) >= 9:
                     try:
-                        rows.append((float(p[0]), float(p[1]), p[4:8]))
+                        ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f")
+                        rows.append((ts, float(p[1]), float(p[2]), p[5:9]))
                     except ValueError:
                         pass
         os.unlink(self.path)
+        if self.window and self.window[1]:
+            pad = datetime.timedelta(milliseconds=250)  # one sampling interval either side
+            inside = [r for r in rows if self.window[0] - pad <= r[0] <= self.window[1] + pad]
+            rows = inside or rows
+        rows = [r[1:] for r in rows]
         if not rows:
             return None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -375,29 +395,40 @@ def bench_b200(args, wl):
     def step():
         run_device(P, g, wl["algo"], out, report=False)
 
+    clocks = ClockSampler(local)
+    clocks.start()  # before the warm-up: its start-up must not overlap the timed steps
     for _ in range(args.warmup):
         step()
     ctx.synchronize()
     # ---- timed region ------------------------------------------------------------
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
+    import gc
+    gc.collect()
+    gc.disable()
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
+    clocks.mark_begin()
     launches0 = ctx.launch_count()
     total_ms = 0.0
+    step_ms, host_ms = [], []
     for _ in range(args.steps):
         flush.fill_(1.0)  # evict L2 (256 MiB > 126 MB) outside the timed step
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
+        h0 = time.perf_counter()
         e0.record(stream)
         step()
         e1.record(stream)
         e1.synchronize()
-        total_ms += e0.elapsed_time(e1)
+        host_ms.append(1e3 * (time.perf_counter() - h0))
+        step_ms.append(e0.elapsed_time(e1))
+        total_ms += step_ms[-1]
     torch.cuda.synchronize()
+    clocks.mark_end()
+    gc.enable()
+    print("timed steps (ms):", " ".join(f"{t:.2f}" for t in step_ms), file=sys.stderr)
+    print("host wall (ms):", " ".join(f"{t:.2f}" for t in host_ms), file=sys.stderr)
     launches = ctx.launch_count() - launches0
     if dist:
         dist.barrier()
