@@ -72,7 +72,8 @@ typedef struct cd_louvain_config {
     uint64_t seed;
     int32_t workers;
     int32_t refine;          /* 0: PLM (run_plm), 1: PLMR (run_plmr)         */
-    int32_t buckets;         /* device: sub-passes per pass (default 4)      */
+    int32_t buckets;         /* device: sub-passes per pass; <= 0 (default): by graph,
+                                8 if its max degree exceeds 4096, else 4     */
     int32_t singleton_guard; /* device: singleton->singleton only to smaller id */
     int64_t move_theta;      /* device: stop a move phase once a pass moves <= this;
                                 <0: floor(n/100000) of the level's graph     */
@@ -84,7 +85,8 @@ typedef struct cd_louvain_config {
                                 input graph's move phases, 2 on every level, 0 never */
     int32_t reserved;
     double move_qtol;        /* device: ... or once a pass's summed gain is <= move_qtol x the
-                                phase's summed gain so far (0 disables; default 2e-3) */
+                                phase's summed gain so far (0 disables; < 0 (default): by
+                                graph, 5e-3 if its max degree exceeds 4096, else 2e-3) */
 } cd_louvain_config;
 
 /* EnsembleConfig (H/ensemble.hpp:19-31), EPP(b, base, final). */

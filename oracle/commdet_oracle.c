@@ -1319,9 +1319,33 @@ int64_t cdo_move_subsweep(const cdo_graph *g, const int32_t *z, const double *vo
     return nm;
 }
 
+/* The device's default schedule (paper_1304_4453_b200/csrc/detect.cu
+ * resolve_louvain_schedule): buckets <= 0 and move_qtol < 0 mean "by graph":
+ * a skewed graph (max degree > 4096: R-MAT-like hubs) takes 8 buckets and
+ * a gain tolerance of 5e-3, anything else 4 and 2e-3.  Resolved once on the
+ * graph a run starts from; every level of the run uses the same values. */
+static cdo_louvain_config resolve_schedule(const cdo_louvain_config *cfg, const cdo_graph *g) {
+    cdo_louvain_config c = *cfg;
+    const int skewed = max_degree(g) > 4096;
+    if (c.buckets <= 0)
+        c.buckets = skewed ? 8 : 4;
+    if (c.move_qtol < 0.0)
+        c.move_qtol = skewed ? 5e-3 : 2e-3;
+    return c;
+}
+
+static int move_phase_impl(const cdo_graph *g, int32_t *z, const cdo_louvain_config *cfg, uint64_t salt,
+                           int32_t *changed_out);
+
 /* Bucketed move phase: the order of paper_1304_4453_b200/csrc/detect.cu move_phase_dev. */
 int cdo_move_phase_bucketed(const cdo_graph *g, int32_t *z, const cdo_louvain_config *cfg, uint64_t salt,
                             int32_t *changed_out) {
+    const cdo_louvain_config c = resolve_schedule(cfg, g);
+    return move_phase_impl(g, z, &c, salt, changed_out);
+}
+
+static int move_phase_impl(const cdo_graph *g, int32_t *z, const cdo_louvain_config *cfg, uint64_t salt,
+                           int32_t *changed_out) {
     const int64_t n = g->n;
     *changed_out = 0;
     if (n == 0 || g->total == 0.0)
@@ -1442,7 +1466,7 @@ static int louvain_recurse(const cdo_graph *g, const cdo_louvain_config *cfg, in
     if (level > 0 && lc.prune < 2)
         lc.prune = 0;
     cfg = &lc;
-    int rc = cdo_move_phase_bucketed(g, z, cfg, louvain_salt(level, 0), &changed);
+    int rc = move_phase_impl(g, z, cfg, louvain_salt(level, 0), &changed);
     if (rc)
         return rc;
     if (changed && level + 1 < cfg->max_levels) {
@@ -1464,7 +1488,7 @@ static int louvain_recurse(const cdo_graph *g, const cdo_louvain_config *cfg, in
             cdo_graph_free(&coarse);
             if (!rc && cfg->refine) {
                 int32_t ch2;
-                rc = cdo_move_phase_bucketed(g, z, cfg, louvain_salt(level, 1), &ch2);
+                rc = move_phase_impl(g, z, cfg, louvain_salt(level, 1), &ch2);
             }
         }
         free(zc);
@@ -1478,7 +1502,8 @@ int cdo_louvain_bucketed(const cdo_graph *g, const cdo_louvain_config *cfg, int3
         return CDO_EDOMAIN;
     int32_t *tmp = (int32_t *)malloc(sizeof(int32_t) * (size_t)(g->n > 0 ? g->n : 1));
     *levels = 0;
-    int rc = louvain_recurse(g, cfg, 0, tmp, levels);
+    const cdo_louvain_config c = resolve_schedule(cfg, g);
+    int rc = louvain_recurse(g, &c, 0, tmp, levels);
     if (!rc)
         *k = cdo_compact(g->n, tmp, z);
     free(tmp);

@@ -451,8 +451,9 @@ def plp_bucketed(g: CSR, theta=-1, max_iterations=100, seed=1, buckets=4, initia
     return labels, trace[: iters.value].copy()
 
 
-def louvain_cfg(gamma=1.0, max_move_iterations=32, max_levels=64, seed=1, buckets=4, refine=False,
-                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True, move_qtol=2e-3):
+def louvain_cfg(gamma=1.0, max_move_iterations=32, max_levels=64, seed=1, buckets=0, refine=False,
+                singleton_guard=True, move_theta=-1, move_tol=1e-3, move_stall=0.95, prune=True, move_qtol=-1.0):
+    """buckets 0 / move_qtol < 0: by graph (8 / 5e-3 when max degree > 4096, else 4 / 2e-3)."""
     return _LouvainCfg(gamma, max_move_iterations, max_levels, seed, buckets, int(refine), int(singleton_guard),
                        move_theta, move_tol, move_stall, int(prune), move_qtol)
 
@@ -475,7 +476,7 @@ def louvain_bucketed(g: CSR, **kw):
 
 def epp_bucketed(g: CSR, ensemble_size=4, seed=1, theta=-1, max_iterations=100, buckets=4, **kw):
     base = _PlpCfg(theta, max_iterations, seed, buckets)
-    fc = louvain_cfg(buckets=buckets, **kw)
+    fc = louvain_cfg(**kw)  # the final solver's own schedule (by the core graph)
     z = np.zeros(g.n, np.int32)
     k = C.c_int64()
     _check(lib().cdo_epp_bucketed(_Borrow(g).ref, ensemble_size, seed, C.byref(base), C.byref(fc), z, C.byref(k)))

@@ -646,13 +646,13 @@ class LouvainConfig:
     seed: int = 1
     workers: int = 1
     refine: bool = False
-    buckets: int = 4
+    buckets: int = 0           # by graph: 8 if its max degree > 4096, else 4
     singleton_guard: bool = True
     move_theta: int = -1
     move_tol: float = 1e-3
     move_stall: float = 0.95
     prune: int = 1
-    move_qtol: float = 2e-3
+    move_qtol: float = -1.0    # by graph: 5e-3 if its max degree > 4096, else 2e-3
 
     @classmethod
     def reference(cls, **kw):

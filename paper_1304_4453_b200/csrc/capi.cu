@@ -138,13 +138,13 @@ void cd_louvain_config_default(cd_louvain_config *c) {
     c->seed = 1;
     c->workers = 1;
     c->refine = 0;
-    c->buckets = 4;
+    c->buckets = 0;  // by graph: 8 if the max degree exceeds 4096, else 4 (resolve_louvain_schedule)
     c->singleton_guard = 1;
     c->move_theta = -1;
     c->move_tol = 1e-3;  // stop a level's passes below 0.1% movers
     c->move_stall = 0.95;  // ... or once the movers stop shrinking (oscillating tail)
     c->prune = 1;          // ... and skip nodes whose neighbourhood did not change
-    c->move_qtol = 2e-3;   // ... or once a pass adds < 0.2% of the phase's modularity gain
+    c->move_qtol = -1.0;   // ... or once a pass adds < 0.5% (skewed) / 0.2% of the phase's gain (by graph)
 }
 
 void cd_louvain_config_reference(cd_louvain_config *c) {
@@ -668,7 +668,8 @@ cd_status cd_move_phase(cd_ctx *ctx, const cd_graph *g, int32_t *z, const cd_lou
             CD_CUDA(cudaMemcpyAsync(dz.d, z, g->n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
         const int64_t mx = max_label_dev(ctx, g->n, dz.d);
         CD_REQUIRE(mx >= 0 && mx <= std::max<int64_t>(g->n, 1), CD_ERANGE, "device move phase needs labels < n");
-        const bool ch = move_phase_dev(ctx, const_cast<cd_graph *>(g), dz.d, *cfg, louvain_salt(0, 0));
+        const bool ch = move_phase_dev(ctx, const_cast<cd_graph *>(g), dz.d, resolve_louvain_schedule(*cfg, g),
+                                       louvain_salt(0, 0));
         dz.finish();
         ctx_sync(ctx);
         if (changed)

@@ -39,6 +39,9 @@ void plp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_plp_config &cfg, const int32
 int64_t plp_sweep_sync_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z_in, int32_t *z_out);
 void move_eval_dev(cd_ctx *ctx, cd_graph *g, const int32_t *z, const double *vols, double gamma, int32_t *best,
                    double *gain);
+// buckets <= 0 / move_qtol < 0 resolved by the graph's degree skew (detect.cu)
+constexpr int64_t SKEWED_MAX_DEGREE = 4096;
+cd_louvain_config resolve_louvain_schedule(const cd_louvain_config &cfg, const cd_graph *g);
 // from_singletons: z holds the node ids (the recursion's every level, H/louvain.hpp:242)
 bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt,
                     int64_t *passes = nullptr, int64_t *moves = nullptr, bool from_singletons = false);
