@@ -47,10 +47,19 @@ int64_t max_label_dev(cd_ctx *ctx, int64_t n, const int32_t *z) {
 }
 
 // ---- first-appearance compaction ------------------------------------------
+// A flooded label (R-MAT PLP: half the nodes share one) would serialise its
+// members on one address: only the warp's smallest member of each label
+// competes, and only while the stored member is larger.
 __global__ void k_first_member(int64_t n, const int32_t *z, int32_t *first) {
-    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
-         u += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        atomicMin(&first[z[u]], static_cast<int32_t>(u));
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t b = static_cast<int64_t>(blockIdx.x) * blockDim.x; b < n; b += stride) {
+        const int64_t u = b + threadIdx.x;
+        const bool in = u < n;
+        const int32_t k = in ? z[u] : -1;
+        const uint32_t peers = __match_any_sync(0xffffffffu, k);
+        if (in && (threadIdx.x & 31) == __ffs(peers) - 1 && __ldcg(&first[k]) > static_cast<int32_t>(u))
+            atomicMin(&first[k], static_cast<int32_t>(u));
+    }
 }
 
 struct FirstFlag {

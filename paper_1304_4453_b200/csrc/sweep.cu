@@ -118,6 +118,18 @@ __device__ __forceinline__ bool better(double a, int32_t ka, double b, int32_t k
     return a > b || (a == b && ka < kb);
 }
 
+// Own-label bypass: entries labelled like the evaluated node itself never go
+// into the tally table.  PLM sums them into w(u, C) (the own community is no
+// candidate, H/louvain.hpp:105-113); PLP with integer tallies counts them in a
+// register and offers the own label as one more candidate after the scan
+// (exact: integer sums are order-free; fp64 PLP tallies keep the lane-order
+// combine).  Converged neighbourhoods are mostly own-labelled, so most
+// shared-memory atomics of the later passes disappear.
+template <int MODE, int VC>
+__host__ __device__ constexpr bool own_bypass() {
+    return MODE == MODE_PLM || VC != VC_REAL;
+}
+
 template <int WIDTH>
 __device__ __forceinline__ void argmax_xor(double &v, int32_t &k) {
 #pragma unroll
@@ -729,8 +741,10 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                 if (MODE == MODE_PLM)
                     valid = valid && vv[c] != u;
                 const double wt = static_cast<double>(ww[c]);
-                if (MODE == MODE_PLM && valid && kk[c] == cur)
+                if (own_bypass<MODE, VC>() && valid && kk[c] == cur) {
                     wc += wt;
+                    valid = false;
+                }
                 bool claimed = false;
                 uint32_t slot = 0;
                 if (VC == VC_REAL) {
@@ -750,7 +764,7 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
             }
             __syncwarp();
             CD_PT(pt, 3);
-            if (MODE == MODE_PLM)
+            if (own_bypass<MODE, VC>())
                 wc = warp_sum(wc);
             double cv = (MODE == MODE_PLP) ? -1.0 : -INFINITY;
             double cs = -1.0;  // PLP margin mode: the runner-up's count
@@ -787,6 +801,14 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                 }
             }
             CD_PT(pt, 4);
+            if (MODE == MODE_PLP && own_bypass<MODE, VC>() && lane == 0 && wc > 0.0) {
+                if (P.chg)
+                    keep2(wc, cur, cv, ck, cs);
+                else if (better(wc, cur, cv, ck)) {
+                    cv = wc;
+                    ck = cur;
+                }
+            }
             double margin = 0.0;
             if (MODE == MODE_PLP && P.chg) {
                 argmax2_xor<32>(cv, ck, cs);
@@ -815,6 +837,272 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
 #endif
         }
     }
+}
+
+// next power of two >= 2*deg, at least 64 (the table size of a node)
+__device__ __forceinline__ uint32_t table_cap(int64_t deg) {
+    const uint32_t want = static_cast<uint32_t>(2 * deg);
+    return want <= 64 ? 64u : (1u << (32 - __clz(want - 1)));
+}
+
+// The selected candidates of one warp's chunks, in list order (warp-uniform).
+struct NodeStream {
+    const int32_t *list;
+    int64_t count, base, step;
+    unsigned long long bkey;
+    int chunk;
+    bool pre;
+    int32_t cand = 0;
+    uint32_t sel = 0;
+
+    // next selected node, or -1 once the warp's chunks are exhausted
+    __device__ __forceinline__ int32_t next(const SweepParams &P) {
+        const int lane = lane_id();
+        while (sel == 0) {
+            if (base >= count)
+                return -1;
+            const bool in = lane < chunk && base + lane < count;
+            cand = in ? list[base + lane] : 0;
+            sel = __ballot_sync(0xffffffffu, in && selected_in(P, bkey, cand, pre));
+            base += step;
+        }
+        const int32_t u = __shfl_sync(0xffffffffu, cand, __ffs(sel) - 1);
+        sel &= sel - 1;
+        return u;
+    }
+};
+
+// PLP, integer tallies: each lane's best (count, label) and runner-up count
+// over its distinct labels -> the warp's winner (ties to the smaller label) and
+// the runner-up's count, by three redux.sync instead of five shuffle rounds
+// of (fp64 value, label, fp64 runner-up).  Every distinct label lives in one
+// lane, so the winner's runner-up is the max of the other lanes' bests and
+// the winning lane's own runner-up -- argmax2_xor's result.
+__device__ __forceinline__ void keep2_u(uint32_t val, int32_t key, uint32_t &v, int32_t &k, uint32_t &s) {
+    if (val > v || (val == v && key < k)) {
+        s = max(s, v);
+        v = val;
+        k = key;
+    } else {
+        s = max(s, val);
+    }
+}
+
+__device__ __forceinline__ void warp_best_u(uint32_t &v, int32_t &k, uint32_t &s) {
+    const uint32_t m = __reduce_max_sync(0xffffffffu, v);
+    const int32_t l = __reduce_min_sync(0xffffffffu, v == m ? k : INT32_MAX);
+    s = __reduce_max_sync(0xffffffffu, (v == m && k == l) ? s : v);
+    v = m;
+    k = l;
+}
+
+// Tier WARP for integer tallies, software-pipelined over the warp's nodes:
+// while node i is tallied, node i+1's label gathers, node i+2's row loads and
+// node i+3's offsets are in flight (a node's off -> col -> z chain is three
+// dependent memory round trips; one node at a time left the SM waiting on
+// them: long-scoreboard stalls, profiles/r02_ncu_c3_plp_k_sweep_warp.txt).
+// Same tally, candidate scan and decision as warp_tier.
+template <int MODE, int VC>
+__device__ __forceinline__ void warp_tier_pipe(const SweepParams &P, int chunk, unsigned long long bkey, int64_t gw,
+                                               int64_t nw, int32_t *keys, TallyT<VC> *vals, uint16_t *dist,
+                                               MoveQueue &q, unsigned long long &st_n, unsigned long long &st_e) {
+    static_assert(VC != VC_REAL, "fp64 tallies keep warp_tier (lane-order combine)");
+    using V = TallyT<VC>;
+    constexpr bool W = VC != VC_COUNT;
+    const int lane = lane_id();
+    NodeStream ns;
+    ns.pre = tier_range(P, TIER_WARP, ns.list, ns.count);
+    ns.base = gw * chunk;
+    ns.step = nw * chunk;
+    ns.bkey = bkey;
+    ns.chunk = chunk;
+    // stage A: offsets; stage B: row ids (+ weights); stage C: labels
+    int32_t uA, uB, uC;
+    int64_t sA = 0, eA = 0, sB = 0, eB = 0;
+    int dC = 0;
+    int32_t vB[SW_WARP_ITEMS], kC[SW_WARP_ITEMS];
+    float wB[SW_WARP_ITEMS], wC[SW_WARP_ITEMS];
+    int32_t curC = 0;
+    double volC = 0.0;
+    auto load_off = [&](int32_t u, int64_t &s, int64_t &e) {
+        if (u >= 0) {
+            s = P.off[u];
+            e = P.off[u + 1];
+        }
+    };
+    auto load_row = [&](int32_t u, int64_t s, int64_t e, int32_t *v, float *w) {
+#pragma unroll
+        for (int c = 0; c < SW_WARP_ITEMS; ++c) {
+            const int64_t f = s + c * 32 + lane;
+            const bool in = u >= 0 && f < e;
+            v[c] = in ? col_at(P, f) : -1;
+            if (MODE == MODE_PLM && v[c] == u)
+                v[c] = -1;  // the self-loop is no candidate (H/louvain.hpp:98)
+            if (W)
+                w[c] = in ? __ldcs(P.w + f) : 0.0f;
+        }
+    };
+    auto gather = [&](int32_t u, const int32_t *v, int32_t *k, int32_t &cur, double &vol) {
+#pragma unroll
+        for (int c = 0; c < SW_WARP_ITEMS; ++c)
+            k[c] = v[c] >= 0 ? P.z[v[c]] : EMPTY_KEY;
+        if (u >= 0) {
+            cur = P.z[u];
+            if (MODE == MODE_PLM)
+                vol = P.vol[u];
+        }
+    };
+    // prime the pipeline
+    uC = ns.next(P);
+    load_off(uC, sA, eA);
+    load_row(uC, sA, eA, vB, wB);
+    dC = static_cast<int>(eA - sA);
+    gather(uC, vB, kC, curC, volC);
+#pragma unroll
+    for (int c = 0; c < SW_WARP_ITEMS; ++c)
+        wC[c] = wB[c];
+    uB = uC >= 0 ? ns.next(P) : -1;
+    load_off(uB, sB, eB);
+    load_row(uB, sB, eB, vB, wB);
+    uA = uB >= 0 ? ns.next(P) : -1;
+    load_off(uA, sA, eA);
+    while (uC >= 0) {
+        // ---- issue the next nodes' loads (consumed one and two iterations later)
+        int32_t kN[SW_WARP_ITEMS];
+        float wN[SW_WARP_ITEMS];
+        int32_t curN = 0;
+        double volN = 0.0;
+        gather(uB, vB, kN, curN, volN);
+        const int dN = static_cast<int>(eB - sB);
+#pragma unroll
+        for (int c = 0; c < SW_WARP_ITEMS; ++c)
+            wN[c] = wB[c];
+        load_row(uA, sA, eA, vB, wB);
+        const int32_t uN2 = uA;
+        const int64_t sN2 = sA, eN2 = eA;
+        uA = uA >= 0 ? ns.next(P) : -1;
+        load_off(uA, sA, eA);
+        // ---- node C: tally its labels
+        const int32_t u = uC, cur = curC;
+        const uint32_t cap = table_cap(dC);
+        const double vols_cur = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
+        double wc = 0.0;
+        uint32_t own = 0;  // PLP: the own label's tally
+        int nd = 0;  // distinct labels so far (warp-uniform)
+#pragma unroll
+        for (int c = 0; c < SW_WARP_ITEMS; ++c) {
+            if (c * 32 >= dC)
+                break;
+            bool valid = kC[c] != EMPTY_KEY;
+            const V wt = W ? static_cast<V>(wC[c]) : V(1);
+            if (valid && kC[c] == cur) {  // own-label bypass
+                if (MODE == MODE_PLM)
+                    wc += static_cast<double>(wt);
+                else
+                    own += static_cast<uint32_t>(wt);
+                valid = false;
+            }
+            uint32_t slot = 0;
+            const bool claimed = valid && tinsert_entry<VC>(keys, vals, cap - 1, kC[c], wt, &slot);
+            const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
+            if (claimed)
+                dist[nd + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
+            nd += __popc(cm);
+        }
+        __syncwarp();
+        // ---- candidate scan over the distinct labels, decision
+        if (MODE == MODE_PLP) {
+            uint32_t bv = 0, sv = 0;
+            int32_t bk = INT32_MAX;
+            for (int j = lane; j < nd; j += 32) {
+                const uint32_t t = dist[j];
+                keep2_u(static_cast<uint32_t>(vals[t]), keys[t], bv, bk, sv);
+            }
+            own = __reduce_add_sync(0xffffffffu, own);
+            if (lane == 0 && own > 0)
+                keep2_u(own, cur, bv, bk, sv);
+            warp_best_u(bv, bk, sv);
+            const double margin = P.chg ? static_cast<double>(bv - sv) : 0.0;
+            decide<MODE>(P, q, lane == 0, u, cur, bk, static_cast<double>(bv), margin);
+        } else {
+            wc = warp_sum(wc);
+            const double vol_c = __dsub_rn(vols_cur, volC);
+            double cv = -INFINITY;
+            int32_t ck = INT32_MAX;
+            for (int j0 = lane; j0 < nd; j0 += 32 * SW_ILP) {
+                int32_t key[SW_ILP];
+                double aff[SW_ILP], vd[SW_ILP];
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    const int j = j0 + 32 * c;
+                    const uint32_t t = j < nd ? dist[j] : 0;
+                    key[c] = j < nd ? keys[t] : EMPTY_KEY;
+                    aff[c] = j < nd ? static_cast<double>(vals[t]) : 0.0;
+                }
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c)
+                    vd[c] = (key[c] != EMPTY_KEY && key[c] != cur) ? P.vols[key[c]] : 0.0;
+#pragma unroll
+                for (int c = 0; c < SW_ILP; ++c) {
+                    if (key[c] == EMPTY_KEY || key[c] == cur)
+                        continue;
+                    const double val = plm_delta(aff[c], wc, vol_c, vd[c], volC, P);
+                    if (better(val, key[c], cv, ck)) {
+                        cv = val;
+                        ck = key[c];
+                    }
+                }
+            }
+            argmax_xor<32>(cv, ck);
+            decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
+        }
+        if (lane == 0) {
+            ++st_n;
+            st_e += static_cast<unsigned long long>(dC);
+        }
+        // leave the table empty for the next node: only the claimed slots
+        for (int j = lane; j < nd; j += 32) {
+            const uint32_t t = dist[j];
+            keys[t] = EMPTY_KEY;
+            vals[t] = tally_empty<VC>();
+        }
+        __syncwarp();
+        // ---- rotate: B -> C, A -> B
+        uC = uB;
+        dC = dN;
+        curC = curN;
+        volC = volN;
+#pragma unroll
+        for (int c = 0; c < SW_WARP_ITEMS; ++c) {
+            kC[c] = kN[c];
+            wC[c] = wN[c];
+        }
+        uB = uN2;
+        sB = sN2;
+        eB = eN2;
+    }
+}
+
+template <int MODE, int VC, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_sweep_warp_pipe(SweepParams P, int chunk) {
+    using V = TallyT<VC>;
+    __shared__ int32_t skeys[4][SW_WARP_CAP];
+    __shared__ V svals[4][SW_WARP_CAP];
+    __shared__ uint16_t sdist[4][SW_WARP_CAP / 2];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    for (int t = lane; t < SW_WARP_CAP; t += 32) {
+        skeys[wid][t] = EMPTY_KEY;
+        svals[wid][t] = tally_empty<VC>();
+    }
+    __syncwarp();
+    const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+    unsigned long long st_n = 0, st_e = 0;
+    MoveQueue q;
+    warp_tier_pipe<MODE, VC>(P, chunk, load_key(P), gw, nw, skeys[wid], svals[wid], sdist[wid], q, st_n, st_e);
+    q.flush(P);
+    q.flush_gain(P);
+    flush_stats(P, TIER_WARP, st_n, st_e);
 }
 
 template <int MODE, int VC>
@@ -860,11 +1148,6 @@ extern "C" __attribute__((visibility("default"))) int cd_debug_phase(unsigned lo
 constexpr int SW_BLOCK_THREADS = 256;
 constexpr int64_t SW_PREBUCKET_MAX = 1 << 16;  // tiers up to this size are pre-bucketed
 
-// next power of two >= 2*deg, at least 64 (the table size of a node)
-__device__ __forceinline__ uint32_t table_cap(int64_t deg) {
-    const uint32_t want = static_cast<uint32_t>(2 * deg);
-    return want <= 64 ? 64u : (1u << (32 - __clz(want - 1)));
-}
 
 // Block-cooperative selection: the block's next SW_BLOCK_THREADS candidates
 // (indices blockIdx.x + k * gridDim.x) are tested in parallel and the
@@ -907,26 +1190,36 @@ struct BlockShared {
 // its neighbours' labels (table of table_cap(deg) slots, claimed slots listed
 // in dlist), Δ / affinity of every distinct label, block argmax, decision.
 // Called by all threads of the block; ends with a block barrier.
-template <int MODE, int VC, int NT = SW_BLOCK_THREADS>
-__device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u, TallyT<VC> *vals, int32_t *keys,
-                                                uint16_t *dlist, BlockShared<NT / 32> &sh, MoveQueue &q,
-                                                unsigned long long &st_n, unsigned long long &st_e) {
+// Where a node's row entries come from (the CSR in global memory).
+struct GlobalRow {
+    const SweepParams *P;
+    int64_t s;
+    __device__ __forceinline__ int32_t col(int64_t f) const { return col_at(*P, s + f); }
+    __device__ __forceinline__ float w(int64_t f) const { return P->w[s + f]; }
+};
+template <int MODE, int VC, int NT, class Row>
+__device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, int64_t d, const Row &row,
+                                               TallyT<VC> *vals, int32_t *keys, uint16_t *dlist,
+                                               BlockShared<NT / 32> &sh, MoveQueue &q, unsigned long long &st_n,
+                                               unsigned long long &st_e) {
     using V = TallyT<VC>;
     const int lane = lane_id(), wid = threadIdx.x >> 5;
-    const int64_t s = P.off[u], e = P.off[u + 1];
     const int32_t cur = P.z[u];
     const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
     const double volsc = (MODE == MODE_PLM) ? P.vols[cur] : 0.0;
-    const uint32_t cap = table_cap(e - s);  // the table is empty on entry (block_table_init)
+    const uint32_t cap = table_cap(d);  // the table is empty on entry (block_table_init)
     double wc = 0.0;
-    for (int64_t f0 = s + wid * 32 * SW_ILP; f0 < e; f0 += NT * SW_ILP) {
+    // round c of a warp covers entries c * NT + wid * 32 + lane: a row spreads
+    // over every warp of the block (the barrier after the tally waits for the
+    // warp with the most entries)
+    for (int64_t f0 = wid * 32; f0 < d; f0 += NT * SW_ILP) {
         int32_t vv[SW_ILP], kk[SW_ILP];
         float ww[SW_ILP];
 #pragma unroll
         for (int c = 0; c < SW_ILP; ++c) {
-            const int64_t f = f0 + c * 32 + lane;
-            vv[c] = f < e ? col_at(P, f) : -1;
-            ww[c] = (VC != VC_COUNT && f < e) ? P.w[f] : 1.0f;
+            const int64_t f = f0 + c * NT + lane;
+            vv[c] = f < d ? row.col(f) : -1;
+            ww[c] = (VC != VC_COUNT && f < d) ? row.w(f) : 1.0f;
         }
 #pragma unroll
         for (int c = 0; c < SW_ILP; ++c)
@@ -937,8 +1230,10 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
             if (MODE == MODE_PLM)
                 valid = valid && vv[c] != u;
             const double wt = static_cast<double>(ww[c]);
-            if (MODE == MODE_PLM && valid && kk[c] == cur)
+            if (own_bypass<MODE, VC>() && valid && kk[c] == cur) {
                 wc += wt;
+                valid = false;
+            }
             bool claimed = false;
             uint32_t slot = 0;
             // integer tallies insert each entry directly (match_any costs about an
@@ -979,13 +1274,13 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
                 dlist[base + __popc(cm & lanemask_lt())] = static_cast<uint16_t>(slot);
         }
     }
-    if (MODE == MODE_PLM) {
+    if (own_bypass<MODE, VC>()) {
         wc = warp_sum(wc);
         if (lane == 0)
             sh.red_wc[wid] = wc;
     }
     __syncthreads();
-    if (MODE == MODE_PLM) {
+    if (own_bypass<MODE, VC>()) {
         wc = 0.0;
 #pragma unroll
         for (int w = 0; w < NT / 32; ++w)
@@ -1026,6 +1321,14 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
         }
     }
     const bool two = MODE == MODE_PLP && P.chg != nullptr;
+    if (MODE == MODE_PLP && own_bypass<MODE, VC>() && threadIdx.x == 0 && wc > 0.0) {
+        if (two)
+            keep2(wc, cur, cv, ck, cs);
+        else if (better(wc, cur, cv, ck)) {
+            cv = wc;
+            ck = cur;
+        }
+    }
     if (two)
         argmax2_xor<32>(cv, ck, cs);
     else
@@ -1050,7 +1353,7 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
         decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
         if (lane == 0) {
             ++st_n;
-            st_e += static_cast<unsigned long long>(e - s);
+            st_e += static_cast<unsigned long long>(d);
         }
     }
     // leave the table empty for the next node: only the claimed slots
@@ -1063,6 +1366,14 @@ __device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u,
     if (threadIdx.x == 0)
         sh.ndist = 0;
     __syncthreads();
+}
+
+template <int MODE, int VC, int NT = SW_BLOCK_THREADS>
+__device__ __forceinline__ void block_eval_node(const SweepParams &P, int32_t u, TallyT<VC> *vals, int32_t *keys,
+                                                uint16_t *dlist, BlockShared<NT / 32> &sh, MoveQueue &q,
+                                                unsigned long long &st_n, unsigned long long &st_e) {
+    const int64_t s = P.off[u], e = P.off[u + 1];
+    block_eval_row<MODE, VC, NT>(P, u, e - s, GlobalRow{&P, s}, vals, keys, dlist, sh, q, st_n, st_e);
 }
 
 // Empties a block evaluator's table once per kernel (nodes then clean up
@@ -1189,8 +1500,10 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                 if (MODE == MODE_PLM)
                     valid = valid && vv[c] != u;
                 const double wt = static_cast<double>(ww[c]);
-                if (MODE == MODE_PLM && valid && kk[c] == cur)
+                if (own_bypass<MODE, VC>() && valid && kk[c] == cur) {
                     wc += wt;
+                    valid = false;
+                }
                 double agg;
                 if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
                     const int owner = cluster_owner<CL>(kk[c]);
@@ -1216,13 +1529,13 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                 }
             }
         }
-        if (MODE == MODE_PLM) {
+        if (own_bypass<MODE, VC>()) {
             wc = warp_sum(wc);
             if (lane == 0)
                 red_wc[wid] = wc;
         }
         __syncthreads();
-        if (threadIdx.x == 0) {
+        if (own_bypass<MODE, VC>() && threadIdx.x == 0) {
             double t = 0.0;
             for (int w = 0; w < NW; ++w)
                 t += red_wc[w];
@@ -1232,7 +1545,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         if (overflow && threadIdx.x == 0 && P.hp_flag)
             *P.hp_flag = 1;
         double wc_all = 0.0;
-        if (MODE == MODE_PLM)
+        if (own_bypass<MODE, VC>())
             for (int r = 0; r < CL; ++r)  // rank order: the same sum on every CTA
                 wc_all += *cluster.map_shared_rank(&part_wc, r);
         const double vol_u = (MODE == MODE_PLM) ? P.vol[u] : 0.0;
@@ -1266,6 +1579,15 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                     cv = val;
                     ck = key[c];
                 }
+            }
+        }
+        // the own label (in no CTA's table): one more candidate, on CTA 0
+        if (MODE == MODE_PLP && own_bypass<MODE, VC>() && rank == 0 && threadIdx.x == 0 && wc_all > 0.0) {
+            if (two)
+                keep2(wc_all, cur, cv, ck, cs);
+            else if (better(wc_all, cur, cv, ck)) {
+                cv = wc_all;
+                ck = cur;
             }
         }
         if (two)
@@ -2457,7 +2779,17 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
     }
     if ((P.tend[TIER_WARP] - P.tbeg[TIER_WARP])) {
         fam = names[MODE][TIER_WARP];
-        auto kfn = k_sweep_warp<MODE, VC>;
+        // integer tallies: the software-pipelined evaluator (CD_WARP_PIPE=0: the plain one)
+        // (value = minimum resident blocks per SM the registers are bounded for)
+        // PLP only by default: PLM's pipelined instance needs 96 registers (5 blocks
+        // per SM) and was measured slower (C3 PLM warp tier 29.3 -> 32.4 ms; C3 PLP
+        // 3.19 -> 2.73 ms)
+        static const int pipe = static_cast<int>(env_i64("CD_WARP_PIPE", MODE == MODE_PLP ? 1 : 0));
+        constexpr int PVC = VC == VC_REAL ? VC_COUNT : VC;
+        auto kfn = VC == VC_REAL || pipe == 0 ? k_sweep_warp<MODE, VC>
+                   : pipe == 8                ? k_sweep_warp_pipe<MODE, PVC, 8>
+                   : pipe == 6                ? k_sweep_warp_pipe<MODE, PVC, 6>
+                                              : k_sweep_warp_pipe<MODE, PVC, 1>;
         const int64_t wave_warps = int64_t(wave(kfn, 128, 0)) * (128 / 32);
         const int64_t cnt = P.tend[TIER_WARP] - P.tbeg[TIER_WARP];
         // pre-bucketed: every listed node is a candidate of this sub-sweep
@@ -2503,19 +2835,9 @@ static void launch_tiers(cd_ctx *ctx, cd_graph *g, const SweepParams &P, bool ca
                        BLOCK2_TABLE_CAP, a256);
     }
     if ((P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3])) {
-        fam = names[MODE][TIER_BLOCK3];
         constexpr int NT3 = 1024;
-        auto kfn = k_sweep_block<MODE, VC, BLOCK3_TABLE_CAP, TIER_BLOCK3, NT3>;
-        const size_t smem = size_t(BLOCK3_TABLE_CAP) * (sizeof(V) + sizeof(int32_t)) +
-                            size_t(BLOCK3_TABLE_CAP / 2) * sizeof(uint16_t);
-        static std::atomic<bool> attr3{false};
-        if (!attr3.load(std::memory_order_acquire)) {
-            set_smem(kfn, smem);
-            attr3.store(true, std::memory_order_release);
-        }
-        const int nb = grid_for(pre_count(P, TIER_BLOCK3, P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK3]), 1,
-                                wave(kfn, NT3, smem));
-        CD_TIER_LAUNCH(kfn, nb, NT3, smem, P);
+        static std::atomic<bool> a3{false};
+        block_tier(k_sweep_block<MODE, VC, BLOCK3_TABLE_CAP, TIER_BLOCK3, NT3>, TIER_BLOCK3, NT3, BLOCK3_TABLE_CAP, a3);
     }
     if ((P.tend[TIER_CLUSTER] - P.tbeg[TIER_CLUSTER])) {
         fam = names[MODE][TIER_CLUSTER];
