@@ -154,6 +154,17 @@ class ClockSampler:
                                          stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        # nvidia-smi's start-up (NVML initialisation) stalls the GPU's work for
+        # tens of ms: wait for its first sample, so that it is over before the
+        # warm-up (a short warm-up alone did not cover it: C3 PLP's first timed
+        # step took 39 ms against 19.6 ms for the others)
+        t0 = time.time()
+        while time.time() - t0 < 10.0 and self.proc.poll() is None:
+            if os.path.getsize(self.path) > 0:
+                break
+            time.sleep(0.02)
+        time.sleep(0.3)
 
     def stop(self):
         if self.proc is None:
@@ -397,9 +408,13 @@ def bench_b200(args, wl):
 
     clocks = ClockSampler(local)
     clocks.start()  # before the warm-up: its start-up must not overlap the timed steps
+    warm_ms = []
     for _ in range(args.warmup):
+        h0 = time.perf_counter()
         step()
-    ctx.synchronize()
+        ctx.synchronize()
+        warm_ms.append(1e3 * (time.perf_counter() - h0))
+    print("warm-up steps, host wall (ms):", " ".join(f"{t:.2f}" for t in warm_ms), file=sys.stderr)
     # ---- timed region ------------------------------------------------------------
     import gc
     gc.collect()
