@@ -20,8 +20,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
-MODE_ARG = {"k_sweep_direct": 1, "k_sweep_warp": 0, "k_sweep_block": 0, "k_hub_pairs": 0, "k_hub_part": 0,
-            "k_hub_decide": 0}
+MODE_ARG = {"k_sweep_direct": 1, "k_sweep_warp": 0, "k_sweep_warp_pipe": 0, "k_sweep_block": 0, "k_sweep_thread": 1,
+            "k_sweep_cluster": 0, "k_hub_pairs": 0, "k_hub_part": 0, "k_hub_decide": 0}
 
 
 def family_of(name):
