@@ -145,7 +145,9 @@ class ClockSampler:
     def start(self):
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
-        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+        # (no power.draw: its query stalled the GPU's work for 50-240 ms now and
+        # then -- C3 PLM timed steps of 253 / 266 ms among 199 ms ones)
+        q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
@@ -180,10 +182,10 @@ class ClockSampler:
         with open(self.path) as f:
             for line in f:
                 p = [x.strip() for x in line.split(",")]
-                if len(p) >= 9:
+                if len(p) >= 8:
                     try:
                         ts = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f")
-                        rows.append((ts, float(p[1]), float(p[2]), p[5:9]))
+                        rows.append((ts, float(p[1]), float(p[2]), p[4:8]))
                     except ValueError:
                         pass
         os.unlink(self.path)

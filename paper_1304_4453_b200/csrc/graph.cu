@@ -482,11 +482,20 @@ std::vector<int64_t> split_rows(cd_ctx *ctx, const int64_t *pre_dev, int64_t lo,
 // validation of an input CSR (ranges, strictly ascending rows, weights > 0)
 // ---------------------------------------------------------------------------
 void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off_dev, int32_t *col_dev,
-                           const int32_t *col_host, float *w_dev, const float *w_host) {
+                           const int32_t *col_host, float *w_dev, const float *w_host, cd_graph *g) {
     if (!ctx->copy_stream)
         CD_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    const bool fin = g != nullptr && w_dev == nullptr && n > 0;
     DBuf<int64_t> flag(ctx, 1);
     flag.zero();
+    DBuf<int32_t> loops;
+    DBuf<int64_t> acc_i;
+    if (fin) {
+        loops.alloc(ctx, n);
+        loops.zero();
+        acc_i.alloc(ctx, 5);
+        acc_i.zero();
+    }
     if (n)
         CD_LAUNCH(ctx, "validate", k_check_offsets, grid_for(n, 256, ctx->num_sms * 16), 256, 0, n, D, off_dev,
                   flag.p);
@@ -507,23 +516,62 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
         done[c] = ctx_event(ctx);
         CD_CUDA(cudaEventRecord(done[c], ctx->copy_stream));
     }
-    // one entry of slack on each side: a chunk's first entry compares with the previous one
+    auto release = [&] {
+        ctx->free_events.push_back(ready);
+        for (cudaEvent_t e : done)
+            ctx->free_events.push_back(e);
+    };
+    if (fin) {
+        // the degree tiers need only the offsets: checked first, then built on
+        // the library stream while the copy stream moves the columns
+        int64_t h = 0;
+        CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+        CD_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (h) {
+            CD_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+            release();
+            fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
+        }
+        g->weighted = false;
+        graph_ensure_bins(ctx, g);
+    }
+    // one entry of slack on each side: a chunk's first entry compares with the previous one;
+    // an unweighted graph's chunks also count their self-loops and upper entries (finalize)
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
         CD_CUDA(cudaStreamWaitEvent(ctx->stream, done[c], 0));
-        CD_LAUNCH(ctx, "validate", k_csr_entries<false>,
-                  grid_for((ie - ib + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32), 256, 0, n, D, off_dev,
-                  static_cast<const int32_t *>(col_dev), static_cast<const float *>(w_dev), flag.p,
-                  static_cast<int32_t *>(nullptr), static_cast<unsigned long long *>(nullptr), ib, ie);
+        const int grid = grid_for((ie - ib + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32);
+        if (fin)
+            CD_LAUNCH(ctx, "validate", k_csr_entries<true>, grid, 256, 0, n, D, off_dev,
+                      static_cast<const int32_t *>(col_dev), static_cast<const float *>(nullptr), flag.p, loops.p,
+                      reinterpret_cast<unsigned long long *>(acc_i.p), ib, ie);
+        else
+            CD_LAUNCH(ctx, "validate", k_csr_entries<false>, grid, 256, 0, n, D, off_dev,
+                      static_cast<const int32_t *>(col_dev), static_cast<const float *>(w_dev), flag.p,
+                      static_cast<int32_t *>(nullptr), static_cast<unsigned long long *>(nullptr), ib, ie);
     }
-    int64_t h = 0;
+    if (fin) {
+        g->vol.alloc(ctx, n);
+        g->loop.alloc(ctx, n);
+        CD_LAUNCH(ctx, "finalize", k_finalize_unweighted, grid_for(n, 256, ctx->num_sms * 16), 256, 0, n, off_dev,
+                  static_cast<const int32_t *>(loops.p), g->vol.p, g->loop.p, acc_i.p);
+    }
+    int64_t h = 0, hi[5] = {};
     CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    if (fin)
+        CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->free_events.push_back(ready);
-    for (cudaEvent_t e : done)
-        ctx->free_events.push_back(e);
+    release();
     if (h)
         fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
+    if (fin) {  // graph_finalize's unweighted path, from the chunks' counts
+        g->m = hi[0];
+        g->max_degree = hi[1];
+        g->isolated = hi[2];
+        std::memcpy(&g->max_vol, &hi[4], sizeof(double));
+        g->int_weights = g->max_vol < 2147483648.0;
+        g->total = static_cast<double>(hi[0]);
+    }
 }
 
 void graph_validate_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const int32_t *col, const float *w, int64_t D) {

@@ -159,8 +159,12 @@ void graph_finalize(cd_ctx *ctx, cd_graph *g, bool integral_weights = false);
 // checks) on the library stream while the next one copies; off_dev is already
 // enqueued on the library stream.  Throws CD_EINPUT like graph_validate_csr.
 constexpr int64_t UPLOAD_CHUNK = int64_t(1) << 25;
+// With g (an unweighted graph being built: n, D, off, col set), the upload
+// also finalizes it -- every chunk's pass counts its self-loops and upper
+// entries -- and builds its degree tiers from the offsets while the columns
+// are still copying; g is then complete (graph_finalize is not needed).
 void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off_dev, int32_t *col_dev,
-                           const int32_t *col_host, float *w_dev, const float *w_host);
+                           const int32_t *col_host, float *w_dev, const float *w_host, cd_graph *g = nullptr);
 // row batching: cut[i] = first row in [lo, hi] whose prefix reaches an even
 // split of [pre[lo], pre[hi]) into k parts (cut has k+1 entries)
 __global__ void k_split_rows(const int64_t *pre, int64_t lo, int64_t hi, int k, int64_t *cut);

@@ -49,3 +49,51 @@ def test_chunked_upload_rejects_out_of_range(dev, big):
     col[-1] = g.node_count()  # the last chunk
     with pytest.raises(dev.InputError, match="malformed CSR"):
         dev.Graph.from_csr(g.node_count(), c["off"], col, c["w"])
+
+
+@pytest.fixture(scope="module")
+def big_unweighted(dev, ctx):
+    """An unweighted graph above two chunks with self-loops scattered over
+    every chunk (built on the device, so its node state comes from
+    graph_finalize)."""
+    g = dev.generate_rmat(21, 16, weighted=False, seed=3)
+    c = g.csr()
+    n = g.node_count()
+    deg = np.diff(c["off"])
+    u = np.repeat(np.arange(n, dtype=np.int64), deg)
+    v = c["col"].astype(np.int64)
+    keep = u <= v
+    loops = np.arange(0, n, 997, dtype=np.int64)
+    gl = dev.Graph.from_edges(n, (np.concatenate([u[keep], loops]), np.concatenate([v[keep], loops])))
+    cl = gl.csr()
+    assert len(cl["col"]) > CHUNK and cl["loop"].sum() == len(loops)
+    return gl, cl
+
+
+def test_chunked_upload_unweighted_finalized_during_copy(dev, big_unweighted):
+    """Unweighted chunks also count self-loops and upper entries, and the
+    degree tiers are built from the offsets while the columns copy: node
+    state, totals and a PLP run equal the device-built graph's."""
+    g, c = big_unweighted
+    h = dev.Graph.from_csr(g.node_count(), c["off"], c["col"])
+    d = h.csr()
+    assert np.array_equal(d["col"], c["col"])
+    np.testing.assert_array_equal(d["vol"], c["vol"])
+    np.testing.assert_array_equal(d["loop"], c["loop"])
+    assert (h.edge_count(), h.total_edge_weight(), h.max_degree, h.isolated) == \
+        (g.edge_count(), g.total_edge_weight(), g.max_degree, g.isolated)
+    la, _ = dev.run_plp(h, dev.PlpConfig(seed=1))
+    lb, _ = dev.run_plp(g, dev.PlpConfig(seed=1))
+    assert np.array_equal(la, lb)
+
+
+def test_chunked_upload_unweighted_rejects(dev, big_unweighted):
+    g, c = big_unweighted
+    col = c["col"].copy()
+    col[CHUNK + 7] = g.node_count() + 5  # second chunk
+    with pytest.raises(dev.InputError, match="malformed CSR"):
+        dev.Graph.from_csr(g.node_count(), c["off"], col)
+    off = c["off"].copy()
+    off[10] = off[11] + 1  # descending offsets: rejected before the tiers are built
+    with pytest.raises(dev.InputError, match="malformed CSR"):
+        dev.Graph.from_csr(g.node_count(), off, c["col"])

@@ -71,6 +71,11 @@ def main():
     print(f"{a.workload}: bytes {nbytes / 1e9:.3f} GB; col H2D alone {ms_h2d:.2f} ms "
           f"({t_col.numel() * 4 / ms_h2d / 1e6:.1f} GB/s); from_csr {ms_build:.2f} ms; run (host out) "
           f"{ms_run:.2f} ms; e2e {ms_e2e:.2f} ms")
+    # exit here, with every local alive: the pinned tensors were used on the
+    # library's stream (torch records an event there when they are freed), so
+    # they must not outlive the context -- nor be freed after it at teardown
+    sys.stdout.flush()
+    os._exit(0)
 
 
 if __name__ == "__main__":
