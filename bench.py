@@ -121,6 +121,97 @@ def measured_peak():
     return 6650.0, "fallback"
 
 
+class NvmlClockSampler:
+    """SM clocks and clock-event (throttle) reasons during the timed region,
+    sampled every 200 ms (the recipe's interval) by a thread of this process
+    through NVML: only the two queries the JSON line needs.  A separate
+    `nvidia-smi -lms 200` process stalled the GPU's work now and then
+    (C3 PLM timed steps of 253 / 306 ms among 198 ms ones; none without it)."""
+
+    NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+             ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+             ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+             ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"))
+
+    def __init__(self, device):
+        import pynvml
+        self.nv = pynvml
+        pynvml.nvmlInit()
+        self.h = None
+        try:  # the CUDA device's own NVML handle (indices may differ)
+            import torch
+            pr = torch.cuda.get_device_properties(device)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+        self.samples = []
+        self.window = None
+        self.stop_ev = None
+        self.thread = None
+
+    def _sample(self):
+        import datetime
+        nv = self.nv
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+            mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            self.samples.append((datetime.datetime.now(), float(sm), float(mx), int(rs)))
+        except Exception:
+            pass
+
+    def _run(self):
+        while not self.stop_ev.wait(0.2):
+            self._sample()
+
+    def start(self):
+        import threading
+        # the first queries initialise NVML's per-device state (it stalled a
+        # timed step by 45 ms): done here, before the warm-up
+        for _ in range(3):
+            self._sample()
+        time.sleep(0.3)
+        self.samples.clear()
+        self.stop_ev = threading.Event()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
+
+    def mark_begin(self):
+        import datetime
+        self.window = [datetime.datetime.now(), None]
+
+    def mark_end(self):
+        import datetime
+        if self.window:
+            self.window[1] = datetime.datetime.now()
+
+    def stop(self):
+        import datetime
+        time.sleep(0.25)
+        self.stop_ev.set()
+        self.thread.join(timeout=5)
+        rows = self.samples
+        if self.window and self.window[1]:
+            pad = datetime.timedelta(milliseconds=250)  # one sampling interval either side
+            inside = [r for r in rows if self.window[0] - pad <= r[0] <= self.window[1] + pad]
+            rows = inside or rows
+        if not rows:
+            return None
+        reasons = sorted({name for r in rows for name, attr in self.NAMES
+                          if r[3] & getattr(self.nv, attr, 0)})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows), "source": "nvml"}
+
+
+def clock_sampler(device):
+    """NVML in-process when pynvml works, else the nvidia-smi process."""
+    try:
+        return NvmlClockSampler(device)
+    except Exception:
+        return ClockSampler(device)
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region.  Started
     before the warm-up (nvidia-smi's start-up -- NVML initialisation -- then
@@ -143,6 +234,8 @@ class ClockSampler:
             self.window[1] = datetime.datetime.now()
 
     def start(self):
+        if os.environ.get("CD_BENCH_NO_CLOCKS"):  # diagnostics only: the JSON line then has no clocks
+            return
         fd, self.path = tempfile.mkstemp(suffix=".csv")
         os.close(fd)
         # (no power.draw: its query stalled the GPU's work for 50-240 ms now and
@@ -408,7 +501,7 @@ def bench_b200(args, wl):
     def step():
         run_device(P, g, wl["algo"], out, report=False)
 
-    clocks = ClockSampler(local)
+    clocks = clock_sampler(local)
     clocks.start()  # before the warm-up: its start-up must not overlap the timed steps
     warm_ms = []
     for _ in range(args.warmup):

@@ -47,7 +47,7 @@ def main():
             e1.synchronize()
             ts.append(e0.elapsed_time(e1))
         z, rep = bench.run_device(P, g, wl["algo"], None, report=True)
-        print(f"AB {a.tag} {name} median_ms {statistics.median(ts):.3f} min_ms {min(ts):.3f} "
+        print(f"AB {a.tag} {name} median_ms {statistics.median(ts):.3f} min_ms {min(ts):.3f} max_ms {max(ts):.3f} "
               f"Q {rep.modularity:.6f} k {rep.community_count}", flush=True)
         ctx.reset_stats()
         ctx.set_profiling(True)
