@@ -566,7 +566,7 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
 // argmax; 8 lanes per node spent most of the round on those collectives.
 // ---------------------------------------------------------------------------
 template <int DM, int MODE, int VC>
-__global__ void __launch_bounds__(256) k_sweep_thread(SweepParams P, int tier) {
+__global__ void __launch_bounds__(256, VC == VC_COUNT ? 4 : 1) k_sweep_thread(SweepParams P, int tier) {
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -576,10 +576,8 @@ __global__ void __launch_bounds__(256) k_sweep_thread(SweepParams P, int tier) {
     const unsigned long long bkey = load_key(P);
     unsigned long long st_n = 0, st_e = 0;
     MoveQueue q;
-    for (int64_t base = gw * 32; base < count; base += nw * 32) {
-        const int64_t i = base + lane;
-        const int32_t u = i < count ? list[i] : 0;
-        const bool act = i < count && selected_in(P, bkey, u, pre);
+    // evaluates node u on this lane (act) and decides; warp-collective
+    auto eval = [&](int32_t u, bool act) {
         int32_t best = INT32_MAX, cur = 0;
         double bv = (MODE == MODE_PLP) ? -1.0 : -INFINITY, sv = -1.0;
         if (act) {
@@ -635,7 +633,41 @@ __global__ void __launch_bounds__(256) k_sweep_thread(SweepParams P, int tier) {
         }
         const double margin = (MODE == MODE_PLP && P.chg) ? bv - fmax(sv, 0.0) : 0.0;
         decide<MODE>(P, q, act, u, cur, best, bv, margin);
+    };
+    // A bucket selects 1/K of the candidates (fewer with margins), so a warp
+    // collects the selected nodes of successive 32-candidate rounds in its
+    // lanes and evaluates 32 at a time: without it 1/K of the lanes worked
+    int32_t pu = 0;
+    int np = 0;  // pending selected nodes, lanes [0, np) (warp-uniform)
+    for (int64_t base = gw * 32; base < count; base += nw * 32) {
+        const int64_t i = base + lane;
+        const int32_t cand = i < count ? list[i] : 0;
+        const bool act = i < count && selected_in(P, bkey, cand, pre);
+        const uint32_t m = __ballot_sync(0xffffffffu, act);
+        const int c = __popc(m);
+        if (c == 0)
+            continue;
+        const int take = min(c, 32 - np);
+        {
+            const int k = lane - np;
+            const bool recv = k >= 0 && k < take;
+            const int32_t v = __shfl_sync(0xffffffffu, cand, recv ? static_cast<int>(__fns(m, 0, k + 1)) : lane);
+            if (recv)
+                pu = v;
+        }
+        np += take;
+        if (np == 32) {
+            eval(pu, true);
+            np = c - take;  // the round's remaining selected nodes start the next batch
+            const bool recv = lane < np;
+            const int32_t v =
+                __shfl_sync(0xffffffffu, cand, recv ? static_cast<int>(__fns(m, 0, take + lane + 1)) : lane);
+            if (recv)
+                pu = v;
+        }
     }
+    if (np)
+        eval(pu, lane < np);
     q.flush(P);
     q.flush_gain(P);
     flush_stats(P, tier, st_n, st_e);
