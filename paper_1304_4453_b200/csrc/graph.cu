@@ -613,17 +613,71 @@ __global__ void k_tiers(int64_t n, const int64_t *off, int64_t cluster_max, uint
         atomicAdd(&counts[threadIdx.x], static_cast<unsigned long long>(sc[threadIdx.x]));
 }
 
-struct TierFlag {
-    const uint8_t *tier;
-    int t;
-    __device__ int32_t operator()(int64_t u) const { return tier[u] == t ? 1 : 0; }
-};
+// Stable partition of the nodes by tier in one pass for all tiers (was one
+// scan + scatter per tier: 18 passes over n per graph, 6 graphs per C3 PLM
+// run): blocks of TP_NODES consecutive nodes count their tiers, one scan over
+// the tier-major (tier, block) counts gives every block's base per tier, and
+// the blocks place their nodes in ascending order.
+constexpr int TP_THREADS = 256, TP_ROUNDS = 8, TP_NODES = TP_THREADS * TP_ROUNDS;
 
-__global__ void k_tier_scatter(int64_t n, const uint8_t *tier, int t, const int32_t *rank, int32_t *out) {
-    for (int64_t u = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
-         u += static_cast<int64_t>(gridDim.x) * blockDim.x)
-        if (tier[u] == t)
-            out[rank[u]] = static_cast<int32_t>(u);
+__global__ void __launch_bounds__(TP_THREADS) k_tier_blockcount(int64_t n, const uint8_t *tier, int64_t nblk,
+                                                                int32_t *bc) {
+    __shared__ int c[NUM_TIERS];
+    if (threadIdx.x < NUM_TIERS)
+        c[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = lane_id();
+    for (int r = 0; r < TP_ROUNDS; ++r) {
+        const int64_t u = static_cast<int64_t>(blockIdx.x) * TP_NODES + r * TP_THREADS + threadIdx.x;
+        const int t = u < n ? tier[u] : TIER_NONE;
+#pragma unroll
+        for (int tt = 0; tt < NUM_TIERS; ++tt) {
+            const uint32_t m = __ballot_sync(0xffffffffu, t == tt);
+            if (lane == 0 && m)
+                atomicAdd(&c[tt], __popc(m));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x < NUM_TIERS)
+        bc[threadIdx.x * nblk + blockIdx.x] = c[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(TP_THREADS) k_tier_place(int64_t n, const uint8_t *tier, int64_t nblk,
+                                                           const int32_t *boff, int32_t *tlist) {
+    __shared__ int base[NUM_TIERS];
+    __shared__ int wcnt[TP_THREADS / 32][NUM_TIERS];
+    const int lane = lane_id(), wid = threadIdx.x >> 5;
+    if (threadIdx.x < NUM_TIERS)
+        base[threadIdx.x] = boff[threadIdx.x * nblk + blockIdx.x];
+    __syncthreads();
+    for (int r = 0; r < TP_ROUNDS; ++r) {
+        const int64_t u = static_cast<int64_t>(blockIdx.x) * TP_NODES + r * TP_THREADS + threadIdx.x;
+        const int t = u < n ? tier[u] : TIER_NONE;
+        int rank = 0;
+#pragma unroll
+        for (int tt = 0; tt < NUM_TIERS; ++tt) {
+            const uint32_t m = __ballot_sync(0xffffffffu, t == tt);
+            if (lane == 0)
+                wcnt[wid][tt] = __popc(m);
+            if (t == tt)
+                rank = __popc(m & lanemask_lt());
+        }
+        __syncthreads();
+        if (t < NUM_TIERS) {
+            int pre = base[t];
+            for (int w = 0; w < wid; ++w)
+                pre += wcnt[w][t];
+            tlist[pre + rank] = static_cast<int32_t>(u);
+        }
+        __syncthreads();
+        if (threadIdx.x < NUM_TIERS) {
+            int add = 0;
+            for (int w = 0; w < TP_THREADS / 32; ++w)
+                add += wcnt[w][threadIdx.x];
+            base[threadIdx.x] += add;
+        }
+        __syncthreads();
+    }
 }
 
 struct HubChunkGen {
@@ -684,17 +738,15 @@ void graph_ensure_bins(cd_ctx *ctx, cd_graph *g) {
     }
     g->tier_start[NUM_TIERS] = s;
     g->tlist.alloc(ctx, std::max<int64_t>(s, 1));
-    {
-        // stable partition by tier: rank within tier = exclusive scan of flags
-        DBuf<int32_t> rank(ctx, n + 1);
-        for (int t = 0; t < NUM_TIERS; ++t) {
-            if (!g->tier_nodes[t])
-                continue;
-            exclusive_scan<int32_t>(ctx, n, TierFlag{g->tier.p, t}, rank.p, rank.p + n);
-            CD_LAUNCH(ctx, "bins", k_tier_scatter, grid_for(n, 256, ctx->num_sms * 8), 256, 0, n,
-                      static_cast<const uint8_t *>(g->tier.p), t, static_cast<const int32_t *>(rank.p),
-                      g->tlist.p + g->tier_start[t]);
-        }
+    if (s > 0) {
+        // stable partition by tier (ascending id within a tier), all tiers at once
+        const int64_t nblk = (n + TP_NODES - 1) / TP_NODES;
+        DBuf<int32_t> bc(ctx, NUM_TIERS * nblk), boff(ctx, NUM_TIERS * nblk + 1);
+        CD_LAUNCH(ctx, "bins", k_tier_blockcount, static_cast<int>(nblk), TP_THREADS, 0, n,
+                  static_cast<const uint8_t *>(g->tier.p), nblk, bc.p);
+        exclusive_scan<int32_t>(ctx, NUM_TIERS * nblk, ArrayGen<int32_t>{bc.p}, boff.p, boff.p + NUM_TIERS * nblk);
+        CD_LAUNCH(ctx, "bins", k_tier_place, static_cast<int>(nblk), TP_THREADS, 0, n,
+                  static_cast<const uint8_t *>(g->tier.p), nblk, static_cast<const int32_t *>(boff.p), g->tlist.p);
     }
     // hubs
     g->n_hubs = g->tier_nodes[TIER_HUB];
