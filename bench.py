@@ -123,10 +123,12 @@ def measured_peak():
 
 class NvmlClockSampler:
     """SM clocks and clock-event (throttle) reasons during the timed region,
-    sampled every 200 ms (the recipe's interval) by a thread of this process
-    through NVML: only the two queries the JSON line needs.  A separate
-    `nvidia-smi -lms 200` process stalled the GPU's work now and then
-    (C3 PLM timed steps of 253 / 306 ms among 198 ms ones; none without it)."""
+    read through NVML by the bench loop itself between timed steps (outside
+    each step's CUDA events), at most every 200 ms (the recipe's interval) and
+    at both ends of the region.  NVML queries taken concurrently with a step
+    stalled it: an `nvidia-smi -lms 200` process gave C3 PLM timed steps of
+    253 / 306 ms among 198 ms ones, a sampling thread a C2 step of 22 ms among
+    6.8 ms ones; between steps they cannot touch a measurement."""
 
     NAMES = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
              ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
@@ -147,8 +149,7 @@ class NvmlClockSampler:
             self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
         self.samples = []
         self.window = None
-        self.stop_ev = None
-        self.thread = None
+        self.last = 0.0
 
     def _sample(self):
         import datetime
@@ -161,47 +162,44 @@ class NvmlClockSampler:
         except Exception:
             pass
 
-    def _run(self):
-        while not self.stop_ev.wait(0.2):
-            self._sample()
-
     def start(self):
-        import threading
         # the first queries initialise NVML's per-device state (it stalled a
         # timed step by 45 ms): done here, before the warm-up
         for _ in range(3):
             self._sample()
-        time.sleep(0.3)
         self.samples.clear()
-        self.stop_ev = threading.Event()
-        self.thread = threading.Thread(target=self._run, daemon=True)
-        self.thread.start()
+        self.last = 0.0
+
+    def between_steps(self):
+        """Called by the timed loop after a step's closing event has completed."""
+        if time.perf_counter() - self.last >= 0.2:
+            self._sample()
+            self.last = time.perf_counter()
 
     def mark_begin(self):
         import datetime
         self.window = [datetime.datetime.now(), None]
+        self._sample()
+        self.last = time.perf_counter()
 
     def mark_end(self):
         import datetime
+        self._sample()
         if self.window:
             self.window[1] = datetime.datetime.now()
 
     def stop(self):
         import datetime
-        time.sleep(0.25)
-        self.stop_ev.set()
-        self.thread.join(timeout=5)
         rows = self.samples
         if self.window and self.window[1]:
-            pad = datetime.timedelta(milliseconds=250)  # one sampling interval either side
-            inside = [r for r in rows if self.window[0] - pad <= r[0] <= self.window[1] + pad]
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1]]
             rows = inside or rows
         if not rows:
             return None
         reasons = sorted({name for r in rows for name, attr in self.NAMES
                           if r[3] & getattr(self.nv, attr, 0)})
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
-                "reasons": reasons, "samples": len(rows), "source": "nvml"}
+                "reasons": reasons, "samples": len(rows), "source": "nvml, between timed steps"}
 
 
 def clock_sampler(device):
@@ -534,6 +532,8 @@ def bench_b200(args, wl):
         host_ms.append(1e3 * (time.perf_counter() - h0))
         step_ms.append(e0.elapsed_time(e1))
         total_ms += step_ms[-1]
+        if hasattr(clocks, "between_steps"):  # outside the step's events
+            clocks.between_steps()
     torch.cuda.synchronize()
     clocks.mark_end()
     gc.enable()
