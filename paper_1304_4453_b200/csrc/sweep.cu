@@ -19,7 +19,7 @@
 // Selection (bucket of this sub-sweep, active flag) is inline: each warp
 // loads up to 32 candidates of its tier's static list and ballots the
 // selected ones; block tiers select 256 candidates cooperatively; short tier
-// lists are pre-bucketed once per pass (k_prebucket).  Small coarse levels run
+// lists are pre-bucketed once per pass (k_prebucket_*).  Small coarse levels run
 // the whole move phase in one cooperative kernel (k_small_move).
 #include "sweep.cuh"
 
@@ -57,13 +57,14 @@ struct SweepParams {
     // one device); nodes outside [own_lo, own_hi) are never evaluated
     int64_t tbeg[NUM_TIERS], tend[NUM_TIERS];
     int32_t own_lo, own_hi;
-    // pre-bucketed tiers (bit t of pre_mask): once per pass k_prebucket
+    // pre-bucketed tiers (bit t of pre_mask): once per pass k_prebucket_*
     // partitions the tier's segment by bucket into blist (same offsets as
     // tlist), bucket b at [boff[9t + b], boff[9t + b + 1]) of the segment
     uint32_t pre_mask;
     int32_t pre_tiers[NUM_TIERS], n_pre;
     int32_t *blist;
     int32_t *boff;
+    int32_t *pb_cnt, *pb_cur;  // k_prebucket_*: per (tier, bucket) counts and cursors
     int32_t *mv_count;  // moves of this bucket
     int2 *mv;           // (node, label) of this bucket's moves
     int32_t *dense_best;
@@ -324,62 +325,63 @@ __device__ __forceinline__ bool selected_in(const SweepParams &P, unsigned long 
     return pre ? is_active(P, u) : selected(P, key, u);
 }
 
-// Once per pass: stable partition of each pre-bucketed tier segment by bucket
-// (one block per tier; ballots per bucket give the in-warp ranks).
-__global__ void __launch_bounds__(1024) k_prebucket(SweepParams P) {
-    const int t = P.pre_tiers[blockIdx.x];
+// Once per pass: each pre-bucketed tier segment partitioned by bucket, on
+// every SM (count, offsets, scatter).  Order within a bucket is irrelevant
+// (a sub-sweep's decisions read frozen labels).  One block per tier took
+// 79 us per pass at C3, serial at every pass's start.
+constexpr int PB_BLOCKS = 16;
+
+__global__ void __launch_bounds__(256) k_prebucket_count(SweepParams P) {
+    const int t = P.pre_tiers[blockIdx.y];
+    const int32_t *list = P.tlist + P.tbeg[t];
+    const int64_t count = P.tend[t] - P.tbeg[t];
+    const unsigned long long key = *P.keyp;
+    __shared__ int c[8];
+    if (threadIdx.x < 8)
+        c[threadIdx.x] = 0;
+    __syncthreads();
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        atomicAdd(&c[bucket_of(key, list[i], P.buckets)], 1);
+    __syncthreads();
+    if (threadIdx.x < P.buckets && c[threadIdx.x])
+        atomicAdd(&P.pb_cnt[9 * t + threadIdx.x], c[threadIdx.x]);
+}
+
+__global__ void k_prebucket_offsets(SweepParams P) {
+    if (static_cast<int>(threadIdx.x) >= P.n_pre)
+        return;
+    const int t = P.pre_tiers[threadIdx.x];
+    int run = 0;
+    for (int b = 0; b < P.buckets; ++b) {
+        P.boff[9 * t + b] = run;
+        P.pb_cur[9 * t + b] = run;
+        run += P.pb_cnt[9 * t + b];
+        P.pb_cnt[9 * t + b] = 0;  // ready for the next pass
+    }
+    P.boff[9 * t + P.buckets] = run;
+}
+
+__global__ void __launch_bounds__(256) k_prebucket_scatter(SweepParams P) {
+    const int t = P.pre_tiers[blockIdx.y];
     const int32_t *list = P.tlist + P.tbeg[t];
     int32_t *out = P.blist + P.tbeg[t];
     const int64_t count = P.tend[t] - P.tbeg[t];
-    const int K = P.buckets;
     const unsigned long long key = *P.keyp;
-    __shared__ int wcnt[32][8];
-    __shared__ int run[8], tot[8];
-    const int lane = lane_id(), wid = threadIdx.x >> 5;
-    if (threadIdx.x < 8)
-        tot[threadIdx.x] = 0;
-    __syncthreads();
-    for (int64_t i = threadIdx.x; i < count; i += blockDim.x)
-        atomicAdd(&tot[bucket_of(key, list[i], K)], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int s = 0;
-        for (int b = 0; b < K; ++b) {
-            run[b] = s;
-            P.boff[9 * t + b] = s;
-            s += tot[b];
-        }
-        P.boff[9 * t + K] = s;
-    }
-    __syncthreads();
-    for (int64_t base = 0; base < count; base += blockDim.x) {
-        const int64_t i = base + threadIdx.x;
-        const bool valid = i < count;
-        const int32_t u = valid ? list[i] : 0;
-        const int b = valid ? bucket_of(key, u, K) : -1;
-        int rank = 0;
-        for (int bb = 0; bb < K; ++bb) {
-            const uint32_t m = __ballot_sync(0xffffffffu, b == bb);
-            if (lane == 0)
-                wcnt[wid][bb] = __popc(m);
-            if (b == bb)
-                rank = __popc(m & lanemask_lt());
-        }
-        __syncthreads();
-        if (valid) {
-            int pre = run[b];
-            for (int w = 0; w < wid; ++w)
-                pre += wcnt[w][b];
-            out[pre + rank] = u;
-        }
-        __syncthreads();
-        if (threadIdx.x < K) {
-            int s = 0;
-            for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w)
-                s += wcnt[w][threadIdx.x];
-            run[threadIdx.x] += s;
-        }
-        __syncthreads();
+    for (int64_t i0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + (threadIdx.x & ~31); i0 < count;
+         i0 += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = i0 + lane_id();
+        const bool in = i < count;
+        const int32_t u = in ? list[i] : 0;
+        const int b = in ? bucket_of(key, u, P.buckets) : -1;
+        const uint32_t peers = __match_any_sync(0xffffffffu, b);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (in && lane_id() == leader)
+            base = atomicAdd(&P.pb_cur[9 * t + b], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (in)
+            out[base + __popc(peers & lanemask_lt())] = u;
     }
 }
 
@@ -2690,6 +2692,9 @@ Sweeper::Sweeper(cd_ctx *ctx, cd_graph *g, const SweepCall &c) : ctx_(ctx), g_(g
         if (n_pre_) {
             blist_.alloc(ctx, std::max<int64_t>(g->tier_start[NUM_TIERS], 1));
             boff_.alloc(ctx, NUM_TIERS * 9);
+            pb_cnt_.alloc(ctx, NUM_TIERS * 9);
+            pb_cur_.alloc(ctx, NUM_TIERS * 9);
+            pb_cnt_.zero();
         }
     }
 }
@@ -2998,6 +3003,8 @@ void Sweeper::enqueue(bool capture, bool recording) {
         P.pre_tiers[i] = pre_tiers_[i];
     P.blist = blist_.p;
     P.boff = boff_.p;
+    P.pb_cnt = pb_cnt_.p;
+    P.pb_cur = pb_cur_.p;
     P.mv = mv_.p;
     P.gain_fx = c_.mode == MODE_PLM ? gain_.p : nullptr;
     P.dense_best = c_.dense_best;
@@ -3029,8 +3036,11 @@ void Sweeper::enqueue(bool capture, bool recording) {
     const bool plp = c_.mode == MODE_PLP;
     if (!c_.dense_best)
         CD_CUDA(cudaMemsetAsync(cnt_.p, 0, 8 * sizeof(int32_t), ctx->stream));
-    if (n_pre_)
-        CD_LAUNCH(ctx, "prebucket", k_prebucket, n_pre_, 1024, 0, P);
+    if (n_pre_) {
+        CD_LAUNCH(ctx, "prebucket", k_prebucket_count, dim3(PB_BLOCKS, n_pre_), 256, 0, P);
+        CD_LAUNCH(ctx, "prebucket", k_prebucket_offsets, 1, 32, 0, P);
+        CD_LAUNCH(ctx, "prebucket", k_prebucket_scatter, dim3(PB_BLOCKS, n_pre_), 256, 0, P);
+    }
     const bool identity = identity_pending_ && !recording;
     if (!recording)
         identity_pending_ = false;

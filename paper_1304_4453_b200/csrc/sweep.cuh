@@ -70,7 +70,7 @@ class Sweeper {
     // sub-sweeps on coarse levels); see k_prebucket
     uint32_t pre_mask_ = 0;
     int pre_tiers_[NUM_TIERS] = {}, n_pre_ = 0;
-    DBuf<int32_t> blist_, boff_;
+    DBuf<int32_t> blist_, boff_, pb_cnt_, pb_cur_;
     DBuf<int32_t> cnt_;     // [8]: [b] moves of bucket b
     DBuf<int2> mv_;         // this rank's moves of the current bucket
     DBuf<int32_t> rcnt_;    // [G] gathered counts
