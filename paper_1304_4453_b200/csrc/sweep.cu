@@ -779,6 +779,8 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                     wc += wt;
                     valid = false;
                 }
+                if (!__any_sync(0xffffffffu, valid))
+                    continue;  // an all-own round: nothing to tally
                 bool claimed = false;
                 uint32_t slot = 0;
                 if (VC == VC_REAL) {
@@ -1036,6 +1038,8 @@ __device__ __forceinline__ void warp_tier_pipe(const SweepParams &P, int chunk, 
                     own += static_cast<uint32_t>(wt);
                 valid = false;
             }
+            if (!__any_sync(0xffffffffu, valid))
+                continue;  // an all-own round: nothing to tally
             uint32_t slot = 0;
             const bool claimed = valid && tinsert_entry<VC>(keys, vals, cap - 1, kC[c], wt, &slot);
             const uint32_t cm = __ballot_sync(0xffffffffu, claimed);
@@ -1268,6 +1272,8 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
                 wc += wt;
                 valid = false;
             }
+            if (!__any_sync(0xffffffffu, valid))
+                continue;  // an all-own round (converged rows): nothing to tally
             bool claimed = false;
             uint32_t slot = 0;
             // integer tallies insert each entry directly (match_any costs about an
@@ -1538,6 +1544,8 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                     wc += wt;
                     valid = false;
                 }
+                if (!__any_sync(0xffffffffu, valid))
+                    continue;  // an all-own round: nothing to tally
                 double agg;
                 if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
                     const int owner = cluster_owner<CL>(kk[c]);
