@@ -488,7 +488,7 @@ __device__ __forceinline__ void flush_stats(const SweepParams &P, int slot, unsi
 // tiers G8 / G16 / G32: one entry per lane, G lanes per node
 // ---------------------------------------------------------------------------
 // One warp's share of a direct tier in one sub-sweep (warps gw of nw).
-template <int G, int MODE, int VC>
+template <int G, int MODE, int VC, bool REDUX = true>
 __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int chunk, unsigned long long bkey,
                                             int64_t gw, int64_t nw, double *scratch_w, MoveQueue &q,
                                             unsigned long long &st_n, unsigned long long &st_e) {
@@ -543,7 +543,19 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
                 }
             }
             double margin = 0.0;
-            if (MODE == MODE_PLP && P.chg) {
+            if (REDUX && MODE == MODE_PLP && VC != VC_REAL) {
+                // integer tallies: each distinct label sits in one leader lane, so the
+                // group's winner (ties to the smaller label) and runner-up are three
+                // redux.sync over (count, label) instead of log2(G) shuffle rounds
+                const uint32_t bv = leader ? static_cast<uint32_t>(agg) : 0u;
+                const int32_t bk = leader ? key : INT32_MAX;
+                const uint32_t mv = __reduce_max_sync(gmask, bv);
+                const int32_t ml = __reduce_min_sync(gmask, bv == mv ? bk : INT32_MAX);
+                const uint32_t sv = __reduce_max_sync(gmask, (bv == mv && bk == ml) ? 0u : bv);
+                cv = static_cast<double>(mv);
+                ck = ml;
+                margin = P.chg ? static_cast<double>(mv - sv) : 0.0;
+            } else if (MODE == MODE_PLP && P.chg) {
                 double cs = -1.0;
                 argmax2_xor<G>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
@@ -1283,8 +1295,10 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
             bool combine = false;
             if (VC != VC_REAL) {
                 const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-                const int32_t k0 = __shfl_sync(0xffffffffu, kk[c], vm ? __ffs(vm) - 1 : 0);
-                combine = __popc(__ballot_sync(0xffffffffu, valid && kk[c] == k0)) >= 16;
+                if (__popc(vm) >= 16) {  // (a flood needs 16 equal labels)
+                    const int32_t k0 = __shfl_sync(0xffffffffu, kk[c], __ffs(vm) - 1);
+                    combine = __popc(__ballot_sync(0xffffffffu, valid && kk[c] == k0)) >= 16;
+                }
             }
             if (VC == VC_REAL) {
                 // fp64: equal labels combined in lane order first (one add per slot per round)
@@ -1764,9 +1778,10 @@ __global__ void __launch_bounds__(FUSED_THREADS, 8) k_fused_phase(SweepParams P,
         for (int b = 0; b < F.K; ++b) {
             P.bucket = b;
             P.mv_count = ctr + b;
-            direct_tier<8, MODE, VC>(P, TIER_G8, F.chunk[0], key, gw, nw, scratch[wid], q, st_n, st_e);
-            direct_tier<16, MODE, VC>(P, TIER_G16, F.chunk[1], key, gw, nw, scratch[wid], q, st_n, st_e);
-            direct_tier<32, MODE, VC>(P, TIER_G32, F.chunk[2], key, gw, nw, scratch[wid], q, st_n, st_e);
+            // (the shuffle argmax: the redux form cost the fused kernel registers, C1 PLP +2 %)
+            direct_tier<8, MODE, VC, false>(P, TIER_G8, F.chunk[0], key, gw, nw, scratch[wid], q, st_n, st_e);
+            direct_tier<16, MODE, VC, false>(P, TIER_G16, F.chunk[1], key, gw, nw, scratch[wid], q, st_n, st_e);
+            direct_tier<32, MODE, VC, false>(P, TIER_G32, F.chunk[2], key, gw, nw, scratch[wid], q, st_n, st_e);
             warp_tier<MODE, VC>(P, F.chunk[3], key, gw, nw, skeys[wid], svals[wid], sdist[wid], scratch[wid], q,
                                 st_n, st_e);
             q.flush(P);
