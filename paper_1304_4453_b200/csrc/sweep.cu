@@ -131,6 +131,31 @@ __host__ __device__ constexpr bool own_bypass() {
     return MODE == MODE_PLM || VC != VC_REAL;
 }
 
+// Group argmax (ties to the smaller key) over WIDTH-lane groups: the value
+// as an order-preserving 64-bit key, reduced by redux.sync on its halves, then
+// the smallest key among the lanes holding the maximum -- three instructions
+// in place of log2(WIDTH) rounds of two fp64 and one int shuffles
+__device__ __forceinline__ unsigned long long f64_order_key(double v) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(v == 0.0 ? 0.0 : v));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+
+__device__ __forceinline__ double f64_from_order_key(unsigned long long key) {
+    return __longlong_as_double(static_cast<long long>((key >> 63) ? (key & 0x7fffffffffffffffull) : ~key));
+}
+
+template <int WIDTH>
+__device__ __forceinline__ void argmax_redux(double &v, int32_t &k) {
+    const uint32_t mask =
+        WIDTH == 32 ? 0xffffffffu : (((1u << WIDTH) - 1u) << ((threadIdx.x & 31) & ~(WIDTH - 1)));
+    const unsigned long long key = f64_order_key(v);
+    const uint32_t hi = static_cast<uint32_t>(key >> 32), lo = static_cast<uint32_t>(key);
+    const uint32_t mh = __reduce_max_sync(mask, hi);
+    const uint32_t ml = __reduce_max_sync(mask, hi == mh ? lo : 0u);
+    k = static_cast<int32_t>(__reduce_min_sync(mask, (hi == mh && lo == ml) ? k : INT32_MAX));
+    v = f64_from_order_key((static_cast<unsigned long long>(mh) << 32) | ml);
+}
+
 template <int WIDTH>
 __device__ __forceinline__ void argmax_xor(double &v, int32_t &k) {
 #pragma unroll
@@ -142,6 +167,16 @@ __device__ __forceinline__ void argmax_xor(double &v, int32_t &k) {
             k = ok;
         }
     }
+}
+
+// PLM: the redux form (C3 PLM -1.5 %, C2 -1.8 %); PLP keeps the shuffles (its
+// kernels grew registers with the redux form: C3 PLP +13 %)
+template <int MODE, int WIDTH>
+__device__ __forceinline__ void argmax_m(double &v, int32_t &k) {
+    if (MODE == MODE_PLM)
+        argmax_redux<WIDTH>(v, k);
+    else
+        argmax_xor<WIDTH>(v, k);
 }
 
 // argmax that also keeps the runner-up's value s (over all other keys)
@@ -560,7 +595,7 @@ __device__ __forceinline__ void direct_tier(const SweepParams &P, int tier, int 
                 argmax2_xor<G>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
             } else {
-                argmax_xor<G>(cv, ck);
+                argmax_m<MODE, G>(cv, ck);
             }
             const bool act = has && k == 0;
             decide<MODE>(P, q, act, u, cur, ck, cv, margin);
@@ -862,7 +897,7 @@ __device__ __forceinline__ void warp_tier(const SweepParams &P, int chunk, unsig
                 argmax2_xor<32>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
             } else {
-                argmax_xor<32>(cv, ck);
+                argmax_m<MODE, 32>(cv, ck);
             }
             decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
@@ -1103,7 +1138,7 @@ __device__ __forceinline__ void warp_tier_pipe(const SweepParams &P, int chunk, 
                     }
                 }
             }
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE, 32>(cv, ck);
             decide<MODE>(P, q, lane == 0, u, cur, ck, cv);
         }
         if (lane == 0) {
@@ -1386,7 +1421,7 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
     if (two)
         argmax2_xor<32>(cv, ck, cs);
     else
-        argmax_xor<32>(cv, ck);
+        argmax_m<MODE, 32>(cv, ck);
     if (lane == 0) {
         sh.red_v[wid] = cv;
         sh.red_k[wid] = ck;
@@ -1402,7 +1437,7 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
             argmax2_xor<32>(cv, ck, cs);
             margin = cv - fmax(cs, 0.0);
         } else {
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE, 32>(cv, ck);
         }
         decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
         if (lane == 0) {
@@ -1649,7 +1684,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         if (two)
             argmax2_xor<32>(cv, ck, cs);
         else
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE, 32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
@@ -1663,7 +1698,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
             if (two)
                 argmax2_xor<32>(cv, ck, cs);
             else
-                argmax_xor<32>(cv, ck);
+                argmax_m<MODE, 32>(cv, ck);
             if (lane == 0) {
                 best_v = cv;
                 best_k = ck;
@@ -1680,7 +1715,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
                 argmax2_xor<32>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
             } else {
-                argmax_xor<32>(cv, ck);
+                argmax_m<MODE, 32>(cv, ck);
             }
             decide<MODE>(P, q, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
@@ -2247,7 +2282,7 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
         if (two)
             argmax2_xor<32>(cv, ck, cs);
         else
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE, 32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
@@ -2309,7 +2344,7 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
         if (two)
             argmax2_xor<32>(cv, ck, cs);
         else
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE, 32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
@@ -2325,7 +2360,7 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
                 argmax2_xor<32>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
             } else {
-                argmax_xor<32>(cv, ck);
+                argmax_m<MODE, 32>(cv, ck);
             }
             const int32_t cur = P.z[u];
             decide<MODE>(P, mq, lane == 0, u, cur, ck, cv, margin);
@@ -2433,7 +2468,7 @@ __global__ void __launch_bounds__(256) k_plm_identity_warp(SweepParams P) {
         double cv = -INFINITY;
         int32_t ck = INT32_MAX;
         plm_identity_scan(P, u, s, e, vol_u, vol_c, 32, lane, cv, ck);
-        argmax_xor<32>(cv, ck);
+        argmax_m<MODE_PLM, 32>(cv, ck);
         decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
     }
     q.flush(P);
@@ -2458,7 +2493,7 @@ __global__ void __launch_bounds__(256) k_plm_identity_block(SweepParams P) {
         double cv = -INFINITY;
         int32_t ck = INT32_MAX;
         plm_identity_scan(P, u, s, e, vol_u, vol_c, 256, threadIdx.x, cv, ck);
-        argmax_xor<32>(cv, ck);
+        argmax_m<MODE_PLM, 32>(cv, ck);
         if (lane == 0) {
             red_v[wid] = cv;
             red_k[wid] = ck;
@@ -2467,7 +2502,7 @@ __global__ void __launch_bounds__(256) k_plm_identity_block(SweepParams P) {
         if (wid == 0) {
             cv = lane < 8 ? red_v[lane] : -INFINITY;
             ck = lane < 8 ? red_k[lane] : INT32_MAX;
-            argmax_xor<32>(cv, ck);
+            argmax_m<MODE_PLM, 32>(cv, ck);
             decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
         }
         __syncthreads();
@@ -2560,11 +2595,11 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
 
 __device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                int64_t count, uint8_t *active, const int64_t *toff,
-                                               const int32_t *tcol, int64_t n) {
+                                               const int32_t *tcol, int64_t n, int64_t dense_at) {
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    if (count > n / 16) {
+    if (count > dense_at) {
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < (n + 15) / 16;
              i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
             if (16 * i + 16 <= n)
@@ -2589,7 +2624,7 @@ __device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *co
 __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, double *vols, int32_t *csize, const double *vol,
                                                    uint8_t *active, const int64_t *toff, const int32_t *tcol,
-                                                   int64_t n, long long *total) {
+                                                   int64_t n, long long *total, int64_t dense_at) {
     __shared__ double scratch[8][32];
     const int lane = lane_id(), wid = threadIdx.x >> 5;
     const int64_t count_all = seg_total(counts, nseg);
@@ -2597,7 +2632,7 @@ __global__ void __launch_bounds__(256) k_apply_plm(const int2 *mv, const int32_t
         atomicAdd(reinterpret_cast<unsigned long long *>(total), static_cast<unsigned long long>(count_all));
     // pruning: the movers' neighbours wake up (same rule as PLP's active set)
     if (active)
-        activate_moved(mv, counts, nseg, stride, count_all, active, toff, tcol, n);
+        activate_moved(mv, counts, nseg, stride, count_all, active, toff, tcol, n, dense_at);
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t count = counts[sg];
@@ -3129,6 +3164,13 @@ static int64_t plp_dense_at(int64_t n) {
     return n / div;
 }
 
+// PLM pruning: movers in one sub-sweep beyond which every node wakes up
+// (CD_PLM_DENSE_DIV: n / div, default 16; ported as cdo_activate's rule)
+static int64_t plm_dense_at(int64_t n) {
+    static const int64_t div = std::max<int64_t>(1, env_i64("CD_PLM_DENSE_DIV", 16));
+    return n / div;
+}
+
 void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride) {
     cd_ctx *ctx = ctx_;
     cd_graph *g = g_;
@@ -3141,7 +3183,7 @@ void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t str
         CD_LAUNCH(ctx, "plm_apply", k_apply_plm, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
                   c_.vols, c_.csize, static_cast<const double *>(g->vol.p), c_.active,
                   c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
-                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), g->n, total_.p);
+                  c_.tcol ? c_.tcol : static_cast<const int32_t *>(g->col.p), g->n, total_.p, plm_dense_at(g->n));
 }
 
 // Sharded sub-sweep exchange: allgather the per-rank move counts, then the
