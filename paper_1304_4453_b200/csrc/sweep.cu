@@ -979,6 +979,19 @@ __device__ __forceinline__ void warp_best_u(uint32_t &v, int32_t &k, uint32_t &s
     k = l;
 }
 
+// argmax2_xor<32> for integer tallies held as doubles (-1: none): warp_best_u
+template <int VC>
+__device__ __forceinline__ void argmax2_w(double &v, int32_t &k, double &s) {
+    if (VC == VC_REAL) {
+        argmax2_xor<32>(v, k, s);
+        return;
+    }
+    uint32_t bv = v > 0.0 ? static_cast<uint32_t>(v) : 0u, sv = s > 0.0 ? static_cast<uint32_t>(s) : 0u;
+    warp_best_u(bv, k, sv);
+    v = bv ? static_cast<double>(bv) : -1.0;
+    s = sv ? static_cast<double>(sv) : -1.0;
+}
+
 // Tier WARP for integer tallies, software-pipelined over the warp's nodes:
 // while node i is tallied, node i+1's label gathers, node i+2's row loads and
 // node i+3's offsets are in flight (a node's off -> col -> z chain is three
@@ -1419,7 +1432,7 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
         }
     }
     if (two)
-        argmax2_xor<32>(cv, ck, cs);
+        argmax2_w<VC>(cv, ck, cs);
     else
         argmax_m<MODE, 32>(cv, ck);
     if (lane == 0) {
@@ -1434,7 +1447,7 @@ __device__ __forceinline__ void block_eval_row(const SweepParams &P, int32_t u, 
         cs = lane < NT / 32 ? sh.red_s[lane] : -1.0;
         double margin = 0.0;
         if (two) {
-            argmax2_xor<32>(cv, ck, cs);
+            argmax2_w<VC>(cv, ck, cs);
             margin = cv - fmax(cs, 0.0);
         } else {
             argmax_m<MODE, 32>(cv, ck);
