@@ -1695,7 +1695,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
             }
         }
         if (two)
-            argmax2_xor<32>(cv, ck, cs);
+            argmax2_w<VC>(cv, ck, cs);
         else
             argmax_m<MODE, 32>(cv, ck);
         if (lane == 0) {
@@ -1709,7 +1709,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
             ck = lane < NW ? red_k[lane] : INT32_MAX;
             cs = lane < NW ? red_s[lane] : -1.0;
             if (two)
-                argmax2_xor<32>(cv, ck, cs);
+                argmax2_w<VC>(cv, ck, cs);
             else
                 argmax_m<MODE, 32>(cv, ck);
             if (lane == 0) {
@@ -1725,7 +1725,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
             cs = lane < CL ? *cluster.map_shared_rank(&best_s, lane < CL ? lane : 0) : -1.0;
             double margin = 0.0;
             if (two) {
-                argmax2_xor<32>(cv, ck, cs);
+                argmax2_w<VC>(cv, ck, cs);
                 margin = cv - fmax(cs, 0.0);
             } else {
                 argmax_m<MODE, 32>(cv, ck);
@@ -2293,7 +2293,7 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 8 : 1) k_hub_part(SweepP
             }
         }
         if (two)
-            argmax2_xor<32>(cv, ck, cs);
+            argmax2_w<VC>(cv, ck, cs);
         else
             argmax_m<MODE, 32>(cv, ck);
         if (lane == 0) {
