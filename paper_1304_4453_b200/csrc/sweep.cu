@@ -688,9 +688,14 @@ __global__ void __launch_bounds__(256, VC == VC_COUNT ? 4 : 1) k_sweep_thread(Sw
     // lanes and evaluates 32 at a time: without it 1/K of the lanes worked
     int32_t pu = 0;
     int np = 0;  // pending selected nodes, lanes [0, np) (warp-uniform)
+    // the next round's candidates load while this round's selection (bucket,
+    // then the changes / active flag) runs: a sparse sub-sweep is all scan
+    int32_t cand_next = gw * 32 + lane < count ? list[gw * 32 + lane] : 0;
     for (int64_t base = gw * 32; base < count; base += nw * 32) {
         const int64_t i = base + lane;
-        const int32_t cand = i < count ? list[i] : 0;
+        const int32_t cand = cand_next;
+        const int64_t inext = i + nw * 32;
+        cand_next = inext < count ? list[inext] : 0;
         const bool act = i < count && selected_in(P, bkey, cand, pre);
         const uint32_t m = __ballot_sync(0xffffffffu, act);
         const int c = __popc(m);
