@@ -2131,14 +2131,17 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
             if (MODE == MODE_PLM)
                 valid = valid && vv[c] != u;
             const double wt = static_cast<double>(ww[c]);
-            if (MODE == MODE_PLM && valid && kk[c] == cur)
+            // the own label gets no pairs (it was the hottest key of every hub
+            // partition table): PLM sums it into w_c, PLP's integer tallies into
+            // the own label's count (both in hub_aux; k_hub_decide)
+            if (own_bypass<MODE, VC>() && valid && kk[c] == cur) {
                 wc += wt;
+                valid = false;
+            }
+            if (!__any_sync(0xffffffffu, valid))
+                continue;
             double agg;
-            // PLM: the own community is never a candidate (its weight w_c is
-            // summed into hub_aux), so it gets no pairs -- it was the hottest
-            // key of every hub partition table
-            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg) &&
-                !(MODE == MODE_PLM && kk[c] == cur)) {
+            if (aggregate<VC>(kk[c], wt, valid, 0xffffffffu, scratch[wid], agg)) {
                 atomicAdd(&hist[hub_part(kk[c], pbits)], 1);
                 const int64_t at = static_cast<int64_t>(blockIdx.x) * HUB_CHUNK + atomicAdd(&npairs, 1);
                 P.st_key[at] = kk[c];
@@ -2152,7 +2155,7 @@ __global__ void __launch_bounds__(256) k_hub_pairs(SweepParams P) {
     for (int q = threadIdx.x; q < np; q += blockDim.x)
         if (hist[q])
             atomicAdd(&P.hp_cnt[pbase + q], hist[q]);
-    if (MODE == MODE_PLM) {
+    if (own_bypass<MODE, VC>()) {
         wc = warp_sum(wc);
         if (lane == 0)
             red_wc[wid] = wc;
@@ -2359,6 +2362,19 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
                 ck = k;
             }
         }
+        const int32_t cur = P.z[u];
+        if (MODE == MODE_PLP && threadIdx.x == 0) {
+            // PLP integer tallies: the own label's count (no pairs, k_hub_pairs)
+            const double own = P.hub_aux[h];
+            if (own > 0.0) {
+                if (two)
+                    keep2(own, cur, cv, ck, cs);
+                else if (better(own, cur, cv, ck)) {
+                    cv = own;
+                    ck = cur;
+                }
+            }
+        }
         if (two)
             argmax2_xor<32>(cv, ck, cs);
         else
@@ -2380,11 +2396,9 @@ __global__ void __launch_bounds__(256) k_hub_decide(SweepParams P) {
             } else {
                 argmax_m<MODE, 32>(cv, ck);
             }
-            const int32_t cur = P.z[u];
             decide<MODE>(P, mq, lane == 0, u, cur, ck, cv, margin);
             if (lane == 0) {
-                if (MODE == MODE_PLM)
-                    P.hub_aux[h] = 0.0;
+                P.hub_aux[h] = 0.0;
                 atomicAdd(&P.stats[3 * TIER_HUB], 1ULL);
             }
         }
