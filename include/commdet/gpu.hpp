@@ -17,18 +17,22 @@
 //   * node ids / labels must fit int32 (std::out_of_range otherwise);
 //   * stored edge weights are fp32 (decisions and sums are fp64);
 //   * PLP/PLM update order is the device's seeded bucket schedule, so
-//     `workers` and `randomize_order` do not change the result, and
-//     MoveObserver / EnsembleConfig::base_override are not supported.
+//     `workers` and `randomize_order` do not change the result;
+//   * move_phase with a MoveObserver runs the reference's one-worker order
+//     (cd_move_phase_sequential), whose move sequence the reference defines
+//     only for workers == 1 (H/louvain.hpp:58-60).
 #pragma once
 
 #include <algorithm>
 #include <charconv>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
 #include <cctype>
 #include <cstdio>
 #include <fstream>
 #include <cstring>
+#include <exception>
 #include <functional>
 #include <map>
 #include <memory>
@@ -373,6 +377,8 @@ struct EnsembleConfig {
     int workers = 1;
     PlpConfig base_plp{.randomize_order = true};
     LouvainConfig final_louvain;
+    /// Test hook (H/ensemble.hpp:30): replaces the base algorithm when set; called as f(g, seed).
+    std::function<Partition(const Graph &, std::uint64_t)> base_override;
 };
 
 struct LevelTiming {
@@ -774,9 +780,47 @@ inline double delta_mod(const Graph &g, const Partition &z, const CommunityVolum
     return (w_d - w_c) / total + gamma * ((vols[c] - vol_u) - vols[target]) * vol_u / (2.0 * total * total);
 }
 
-/// move_phase (H/louvain.hpp:65-141) with the device's bucketed order.
-inline bool move_phase(const Graph &g, Partition &z, const LouvainConfig &cfg) {
+/// Called after each applied move: (node, source, target, predicted gain) (H/louvain.hpp:58-60).
+using MoveObserver = std::function<void(node, index, index, double)>;
+
+namespace detail {
+struct ObserverCall {
+    Partition *z;
+    const MoveObserver *observer;
+    std::exception_ptr error;
+};
+inline void observer_trampoline(void *user, int32_t u, int32_t c, int32_t d, double gain) {
+    auto *oc = static_cast<ObserverCall *>(user);
+    if (oc->error)
+        return;
+    try {
+        (*oc->z)[static_cast<node>(u)] = static_cast<index>(d);  // the partition after this move
+        (*oc->observer)(static_cast<node>(u), static_cast<index>(c), static_cast<index>(d), gain);
+    } catch (...) {
+        oc->error = std::current_exception();
+    }
+}
+}  // namespace detail
+
+/// move_phase (H/louvain.hpp:65-141) with the device's bucketed order, or,
+/// given an observer, in the reference's one-worker order with every move
+/// reported as it is applied to z.
+inline bool move_phase(const Graph &g, Partition &z, const LouvainConfig &cfg, const MoveObserver &observer = {}) {
     detail::check_cover(g, z);
+    if (observer) {
+        auto l = z.to_device_labels();
+        cd_louvain_config c = detail::louvain_c(cfg);
+        const index ub = z.upper_bound();
+        detail::ObserverCall oc{&z, &observer, nullptr};
+        int32_t changed = 0;
+        detail::check(cd_move_phase_sequential(Context::instance().get(), g.handle(), l.data(),
+                                               static_cast<int64_t>(std::max<index>(ub, 1)), &c,
+                                               &detail::observer_trampoline, &oc, &changed));
+        if (oc.error)
+            std::rethrow_exception(oc.error);
+        z = Partition::from_device_labels(l, ub);
+        return changed != 0;
+    }
     auto l = z.to_device_labels();
     cd_louvain_config c = detail::louvain_c(cfg);
     int32_t changed = 0;
@@ -872,8 +916,31 @@ inline std::pair<Partition, RunReport> run_epp(const Graph &g, const EnsembleCon
     c.final_louvain = detail::louvain_c(cfg.final_louvain);
     std::vector<int32_t> z(g.node_count());
     auto rep = std::make_unique<cd_report>();
-    detail::check(cd_epp_run(Context::instance().get(), g.handle(), &c, z.data(), rep.get()));
-    return {Partition::from_device_labels(z), detail::report_of(*rep)};
+    if (!cfg.base_override) {
+        detail::check(cd_epp_run(Context::instance().get(), g.handle(), &c, z.data(), rep.get()));
+        return {Partition::from_device_labels(z), detail::report_of(*rep)};
+    }
+    // base_override (H/ensemble.hpp:127-128): the hook's partitions replace the base runs
+    if (cfg.ensemble_size < 1)
+        throw std::invalid_argument("ensemble size must be >= 1");
+    const auto t0 = std::chrono::steady_clock::now();
+    std::vector<std::vector<int32_t>> bases;
+    for (count i = 0; i < cfg.ensemble_size; ++i) {
+        Partition p = cfg.base_override(g, cfg.seed + static_cast<std::uint64_t>(i));
+        if (!bases.empty() && p.size() != bases.front().size())
+            throw std::invalid_argument("ensemble partitions cover different node sets");  // :33-39
+        detail::check_cover(g, p);
+        bases.push_back(p.to_device_labels());
+    }
+    const double base_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<const int32_t *> ptrs;
+    for (auto &b : bases)
+        ptrs.push_back(b.data());
+    detail::check(cd_epp_run_bases(Context::instance().get(), g.handle(), &c, ptrs.data(), z.data(), rep.get()));
+    RunReport r = detail::report_of(*rep);
+    r.base_ms = base_ms;
+    r.total_ms += base_ms;
+    return {Partition::from_device_labels(z), std::move(r)};
 }
 
 // ---- generator (H/generator.hpp) ------------------------------------------------------

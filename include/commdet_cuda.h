@@ -250,6 +250,19 @@ CD_API cd_status cd_move_eval(cd_ctx *ctx, const cd_graph *g, const int32_t *z, 
 /* move_phase (H/louvain.hpp:65-141) with the device's bucketed order. */
 CD_API cd_status cd_move_phase(cd_ctx *ctx, const cd_graph *g, int32_t *z, const cd_louvain_config *cfg,
                                int32_t *changed);
+/* MoveObserver (H/louvain.hpp:60): called after each applied move with
+ * (node, source community, target community, predicted gain). */
+typedef void (*cd_move_observer)(void *user, int32_t node, int32_t source, int32_t target, double gain);
+/* move_phase (H/louvain.hpp:65-141) in the reference's one-worker order:
+ * u = 0..n-1, each move applied before the next node is evaluated; a pass
+ * without moves or cfg->max_move_iterations passes end it (cfg->gamma and
+ * the pass cap are the only fields read).  Labels in [0, ub).  observer
+ * (nullable) receives every applied move in order; the calls of a pass
+ * arrive when that pass has finished on the device.  z is written when the
+ * phase ends.  A serial test / debugging path (one warp walks the nodes). */
+CD_API cd_status cd_move_phase_sequential(cd_ctx *ctx, const cd_graph *g, int32_t *z, int64_t ub,
+                                          const cd_louvain_config *cfg, cd_move_observer observer, void *user,
+                                          int32_t *changed);
 
 /* ---- detectors (H/plp.hpp:67, H/louvain.hpp:290/297, H/ensemble.hpp:111) -- */
 /* run_plp: labels raw (not compacted), like the reference (H/plp.hpp:148). */
@@ -261,6 +274,12 @@ CD_API cd_status cd_louvain_run(cd_ctx *ctx, const cd_graph *g, const cd_louvain
 /* run_epp; z compacted. */
 CD_API cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *cfg, int32_t *z,
                             cd_report *report);
+/* run_epp with EnsembleConfig::base_override (H/ensemble.hpp:30, :127-128):
+ * bases[i] (i < cfg->ensemble_size; n labels each, host or device memory)
+ * replace the base detector's runs; combine, coarsen, final solver and
+ * prolongation are run_epp's. */
+CD_API cd_status cd_epp_run_bases(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *cfg,
+                                  const int32_t *const *bases, int32_t *z, cd_report *report);
 
 /* ---- text ingest (H/io.hpp) ------------------------------------------------
  * The file's bytes (host or device memory) are parsed on the device with the

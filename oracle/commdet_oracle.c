@@ -1004,6 +1004,63 @@ void cdo_move_eval(const cdo_graph *g, const int32_t *z, const double *vols, int
     scratch_free(&s);
 }
 
+/* move_phase (H/louvain.hpp:65-141) with one worker: passes over u = 0..n-1,
+ * each move applied in place (z, vols) before the next node is evaluated;
+ * stops after a pass without moves or max_passes.  Every applied move is
+ * appended to the log (H/louvain.hpp:127-128's observer arguments). */
+int cdo_move_phase_sequential(const cdo_graph *g, int32_t *z, int64_t ub, double gamma, int64_t max_passes,
+                              cdo_move_log *log, int32_t *changed_out) {
+    *changed_out = 0;
+    if (log)
+        log->count = 0;
+    if (g->n == 0 || g->total == 0.0)
+        return 0;
+    for (int64_t u = 0; u < g->n; ++u)
+        if (z[u] < 0 || z[u] >= ub)
+            return CDO_ERANGE;
+    scratch_t s;
+    if (scratch_init(&s, ub, max_degree(g)))
+        return CDO_ENOMEM;
+    double *vols = (double *)calloc((size_t)ub, sizeof(double));
+    if (!vols) {
+        scratch_free(&s);
+        return CDO_ENOMEM;
+    }
+    cdo_community_volumes(g, z, ub, vols);
+    const double inv_total = 1.0 / g->total;
+    const double inv_sq2 = 1.0 / (2.0 * g->total * g->total);
+    for (int64_t pass = 0; pass < max_passes; ++pass) {
+        int moved = 0;
+        for (int64_t u = 0; u < g->n; ++u) {
+            if (g->off[u + 1] == g->off[u])
+                continue;
+            const int32_t c = z[u];
+            double gain = 0.0;
+            const int32_t best = move_best(g, z, vols, gamma, inv_total, inv_sq2, (int32_t)u, &s, &gain);
+            if (best != c && gain > 0.0) {
+                vols[c] -= g->vol[u];
+                vols[best] += g->vol[u];
+                z[u] = best;
+                moved = 1;
+                if (log && log->count < log->capacity) {
+                    log->node[log->count] = (int32_t)u;
+                    log->source[log->count] = c;
+                    log->target[log->count] = best;
+                    log->gain[log->count] = gain;
+                }
+                if (log)
+                    log->count++;
+            }
+        }
+        if (!moved)
+            break;
+        *changed_out = 1;
+    }
+    free(vols);
+    scratch_free(&s);
+    return 0;
+}
+
 /* H/louvain.hpp:154-220.  Single worker: rows accumulate in (fine u asc,
  * row position asc) order; coarse rows sorted ascending; pi = z. */
 int cdo_coarsen(const cdo_graph *g, const int32_t *z, cdo_graph *coarse) {

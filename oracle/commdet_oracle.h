@@ -108,6 +108,16 @@ double cdo_delta_mod(const cdo_graph *g, const int32_t *z, const double *vols, i
  * nodes and non-movers return best = z[u], gain 0. */
 void cdo_move_eval(const cdo_graph *g, const int32_t *z, const double *vols, int64_t ub, double gamma,
                    int32_t *best, double *gain);
+/* Applied moves of a sequential move phase, in order (the MoveObserver's
+ * arguments, H/louvain.hpp:60, :127-128).  count may exceed capacity. */
+typedef struct {
+    int32_t *node, *source, *target;
+    double *gain;
+    int64_t capacity, count;
+} cdo_move_log;
+/* move_phase (H/louvain.hpp:65-141) with workers == 1: u = 0..n-1 in place. */
+int cdo_move_phase_sequential(const cdo_graph *g, int32_t *z, int64_t ub, double gamma, int64_t max_passes,
+                              cdo_move_log *log, int32_t *changed);
 /* H/louvain.hpp:154-220 (coarse weights double). Returns CDO_EINVAL if z is
  * not compact. */
 int cdo_coarsen(const cdo_graph *g, const int32_t *z, cdo_graph *coarse);

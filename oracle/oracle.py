@@ -127,6 +127,8 @@ def lib():
         L.cdo_move_eval.argtypes = [gp, i32p, f64p, C.c_int64, C.c_double, i32p, f64p]
         L.cdo_move_eval.restype = None
         L.cdo_coarsen.argtypes = [gp, i32p, gp]
+        L.cdo_move_phase_sequential.argtypes = [gp, i32p, C.c_int64, C.c_double, C.c_int64, C.c_void_p,
+                                                C.POINTER(C.c_int32)]
         L.cdo_prolong.argtypes = [C.c_int64, i32p, C.c_int64, i32p, i32p]
         L.cdo_djb2.argtypes = [C.c_char_p, C.c_uint64]
         L.cdo_djb2.restype = C.c_uint64
@@ -184,6 +186,9 @@ def ref():
                                       i32p, C.POINTER(_RefReport)]
         R.ref_move_phase.argtypes = [C.c_void_p, i32p, C.c_int64, C.c_double, C.c_int64, C.c_int,
                                      C.POINTER(C.c_int)]
+        R.ref_move_phase_log.argtypes = [C.c_void_p, i32p, C.c_int64, C.c_double, C.c_int64, C.c_int, i32p, i32p,
+                                         i32p, f64p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64),
+                                         C.POINTER(C.c_int)]
         R.ref_delta_mod.argtypes = [C.c_void_p, i32p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                     C.POINTER(C.c_double)]
         R.ref_coarsen.argtypes = [C.c_void_p, i32p, C.c_int, vpp, i32p]
@@ -396,6 +401,26 @@ def move_eval(g: CSR, z, vols, gamma=1.0):
     gain = np.zeros(len(z), np.float64)
     lib().cdo_move_eval(_Borrow(g).ref, z, vols, len(vols), gamma, best, gain)
     return best, gain
+
+
+class _MoveLog(C.Structure):
+    _fields_ = [("node", C.c_void_p), ("source", C.c_void_p), ("target", C.c_void_p), ("gain", C.c_void_p),
+                ("capacity", C.c_int64), ("count", C.c_int64)]
+
+
+def move_phase_sequential(g: CSR, z, gamma=1.0, max_move_iterations=32, ub=None):
+    """move_phase with one worker (H/louvain.hpp:65-141): (z, changed, moves[(u, c, d, gain)])."""
+    z = _i32(z).copy()
+    ub = int(ub) if ub is not None else max(int(z.max()) + 1 if len(z) else 1, 1)
+    cap = max(len(z), 1) * max(int(max_move_iterations), 1)
+    lu, lc, ld = (np.zeros(cap, np.int32) for _ in range(3))
+    lg = np.zeros(cap, np.float64)
+    log = _MoveLog(lu.ctypes.data, lc.ctypes.data, ld.ctypes.data, lg.ctypes.data, cap, 0)
+    ch = C.c_int32()
+    _check(lib().cdo_move_phase_sequential(_Borrow(g).ref, z, ub, gamma, max_move_iterations, C.byref(log),
+                                           C.byref(ch)))
+    k = min(log.count, cap)
+    return z, bool(ch.value), list(zip(lu[:k].tolist(), lc[:k].tolist(), ld[:k].tolist(), lg[:k].tolist()))
 
 
 def coarsen(g: CSR, z) -> CSR:
@@ -636,6 +661,20 @@ class RefGraph:
         ch = C.c_int()
         _rcheck(ref().ref_move_phase(self.h, z, ub, gamma, max_move_iterations, workers, C.byref(ch)))
         return z, bool(ch.value)
+
+    def move_phase_log(self, z, gamma=1.0, max_move_iterations=32, workers=1, ub=0, with_q=False):
+        """move_phase with a MoveObserver: (z, changed, moves[(u, c, d, gain)], q after each move)."""
+        z = _i32(z).copy()
+        cap = max(len(z), 1) * max(int(max_move_iterations), 1)
+        lu, lc, ld = (np.zeros(cap, np.int32) for _ in range(3))
+        lg = np.zeros(cap, np.float64)
+        lq = np.zeros(cap, np.float64) if with_q else None
+        cnt, ch = C.c_int64(), C.c_int()
+        _rcheck(ref().ref_move_phase_log(self.h, z, ub, gamma, max_move_iterations, workers, lu, lc, ld, lg,
+                                         None if lq is None else lq.ctypes.data, cap, C.byref(cnt), C.byref(ch)))
+        k = min(cnt.value, cap)
+        moves = list(zip(lu[:k].tolist(), lc[:k].tolist(), ld[:k].tolist(), lg[:k].tolist()))
+        return z, bool(ch.value), moves, (lq[:k].copy() if with_q else None)
 
     def delta_mod(self, z, u, target, gamma=1.0, ub=0):
         out = C.c_double()

@@ -242,6 +242,38 @@ int ref_move_phase(const void *gp, int32_t *z, int64_t ub, double gamma, int64_t
     });
 }
 
+// move_phase with a MoveObserver (H/louvain.hpp:60, :127-128) that logs every
+// applied move and the modularity of the partition right after it
+int ref_move_phase_log(const void *gp, int32_t *z, int64_t ub, double gamma, int64_t max_move_iterations,
+                       int workers, int32_t *lu, int32_t *lc, int32_t *ld, double *lgain, double *lq, int64_t cap,
+                       int64_t *count, int *changed) {
+    return guarded([&] {
+        const auto &g = *static_cast<const cd::Graph *>(gp);
+        cd::Partition p = to_partition(static_cast<int64_t>(g.node_count()), z, ub);
+        cd::LouvainConfig cfg;
+        cfg.gamma = gamma;
+        cfg.max_move_iterations = static_cast<cd::count>(max_move_iterations);
+        cfg.workers = workers;
+        int64_t k = 0;
+        *changed = cd::move_phase(g, p, cfg,
+                                  [&](cd::node u, cd::index c, cd::index d, double gain) {
+                                      if (k < cap) {
+                                          lu[k] = static_cast<int32_t>(u);
+                                          lc[k] = static_cast<int32_t>(c);
+                                          ld[k] = static_cast<int32_t>(d);
+                                          lgain[k] = gain;
+                                          if (lq)
+                                              lq[k] = cd::modularity(g, p);
+                                      }
+                                      ++k;
+                                  })
+                       ? 1
+                       : 0;
+        *count = k;
+        from_partition(p, z);
+    });
+}
+
 // delta_mod (H/louvain.hpp:37-56)
 int ref_delta_mod(const void *gp, const int32_t *z, int64_t ub, int64_t u, int64_t target, double gamma,
                   double *out) {

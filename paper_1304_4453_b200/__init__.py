@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import time
 import weakref
 from dataclasses import dataclass, field
 
@@ -37,7 +38,8 @@ __all__ = [
     "InputError", "InvalidArgument", "DomainError", "OutOfRange", "CudaError",
     "generate_planted", "generate_rmat", "generate_lfr", "run_plp", "run_plm", "run_plmr", "run_epp",
     "run_louvain", "modularity", "coverage", "community_volumes", "coarsen", "prolong", "compacted",
-    "community_count", "combine_hashed", "plp_sweep_sync", "move_eval", "move_phase", "dominant_label",
+    "community_count", "combine_hashed", "plp_sweep_sync", "move_eval", "move_phase", "move_phase_sequential",
+    "dominant_label",
     "is_stable", "library_path", "load_library", "default_context", "ALGO_PLP", "ALGO_PLM", "ALGO_PLMR",
     "LoopbackGroup", "nccl_unique_id", "shard_bounds", "read_metis", "read_edge_list", "graph_rand_index",
 ]
@@ -140,12 +142,17 @@ EXPORTS = [
     "cd_graph_generate_rmat_shard",
     "cd_graph_generate_lfr", "cd_graph_get_info", "cd_graph_download", "cd_graph_destroy", "cd_modularity",
     "cd_community_volumes", "cd_compact", "cd_community_count", "cd_coarsen", "cd_prolong", "cd_combine_hashed",
-    "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_plp_run", "cd_louvain_run", "cd_epp_run",
+    "cd_plp_sweep_sync", "cd_move_eval", "cd_move_phase", "cd_move_phase_sequential", "cd_plp_run", "cd_louvain_run",
+    "cd_epp_run", "cd_epp_run_bases",
     "cd_nccl_unique_id", "cd_ctx_attach_nccl", "cd_loopback_create", "cd_loopback_destroy",
     "cd_ctx_attach_loopback", "cd_ctx_detach", "cd_ctx_world", "cd_shard_bounds", "cd_graph_shard", "cd_graph_from_csr_rows",
     "cd_graph_read_metis", "cd_graph_read_edge_list", "cd_graph_load_metis", "cd_graph_load_edge_list",
     "cd_graph_original_ids", "cd_rand_index",
 ]
+
+
+# MoveObserver (H/louvain.hpp:60) as the C ABI's cd_move_observer
+_MoveObserver = C.CFUNCTYPE(None, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_double)
 
 
 def library_path() -> str:
@@ -189,6 +196,9 @@ def load_library():
         "cd_plp_run": [vp, vp, C.POINTER(_PlpConfig), vp, vp, C.POINTER(_Report)],
         "cd_louvain_run": [vp, vp, C.POINTER(_LouvainConfig), vp, C.POINTER(_Report)],
         "cd_epp_run": [vp, vp, C.POINTER(_EnsembleConfig), vp, C.POINTER(_Report)],
+        "cd_epp_run_bases": [vp, vp, C.POINTER(_EnsembleConfig), vp, vp, C.POINTER(_Report)],
+        "cd_move_phase_sequential": [vp, vp, vp, i64, C.POINTER(_LouvainConfig), _MoveObserver, vp,
+                                     C.POINTER(i32)],
         "cd_nccl_unique_id": [vp], "cd_ctx_attach_nccl": [vp, i32, i32, vp],
         "cd_loopback_create": [i32, vpp], "cd_loopback_destroy": [vp], "cd_ctx_attach_loopback": [vp, vp, i32],
         "cd_ctx_detach": [vp], "cd_ctx_world": [vp, C.POINTER(i32), C.POINTER(i32)],
@@ -677,6 +687,8 @@ class EnsembleConfig:
     workers: int = 1
     base_plp: PlpConfig = field(default_factory=lambda: PlpConfig(randomize_order=True))
     final_louvain: LouvainConfig = field(default_factory=LouvainConfig)
+    # test hook (H/ensemble.hpp:30): f(g, seed) -> labels, replaces the base detector
+    base_override: object = None
 
     def _c(self):
         return _EnsembleConfig(self.ensemble_size, self.base, self.final_algo, self.seed, self.workers, 0,
@@ -780,13 +792,33 @@ def run_plmr(g: Graph, cfg: LouvainConfig = None, out=None):
 
 
 def run_epp(g: Graph, cfg: EnsembleConfig = None, out=None):
-    """run_epp (H/ensemble.hpp:111-199)."""
+    """run_epp (H/ensemble.hpp:111-199).  cfg.base_override, when set, is
+    called as f(g, seed + i) for each base (H/ensemble.hpp:30, :127-128) and
+    its partitions replace the base detector's runs."""
     cfg = cfg or EnsembleConfig()
     z, zp = _labels_out(g, out)
     rep = _Report()
     c = cfg._c()
-    _check(load_library().cd_epp_run(g.ctx.h, g.h, C.byref(c), zp, C.byref(rep)))
-    return _trim(g, z), RunReport._from(rep)
+    if cfg.base_override is None:
+        _check(load_library().cd_epp_run(g.ctx.h, g.h, C.byref(c), zp, C.byref(rep)))
+        return _trim(g, z), RunReport._from(rep)
+    if cfg.ensemble_size < 1:
+        raise InvalidArgument("ensemble size must be >= 1")
+    t0 = time.perf_counter()
+    bases = [cfg.base_override(g, cfg.seed + i) for i in range(cfg.ensemble_size)]
+    base_ms = 1e3 * (time.perf_counter() - t0)
+    keep = []
+    for b in bases:
+        if len(b) != len(bases[0]):
+            raise InvalidArgument("ensemble partitions cover different node sets")  # H/ensemble.hpp:33-39
+        _check_cover(g, b)
+        keep.append(b if _is_dev(b) else np.ascontiguousarray(b, np.int32))
+    ptrs = (C.c_void_p * len(keep))(*[b.data_ptr() if _is_dev(b) else b.ctypes.data for b in keep])
+    _check(load_library().cd_epp_run_bases(g.ctx.h, g.h, C.byref(c), ptrs, zp, C.byref(rep)))
+    r = RunReport._from(rep)
+    r.base_ms = base_ms
+    r.total_ms += base_ms
+    return _trim(g, z), r
 
 
 # ---------------------------------------------------------------------------
@@ -933,6 +965,42 @@ def move_phase(g: Graph, z, cfg: LouvainConfig = None):
     c = cfg._c()
     _check(load_library().cd_move_phase(g.ctx.h, g.h, z.ctypes.data if len(z) else None, C.byref(c),
                                         C.byref(ch)))
+    return z, bool(ch.value)
+
+
+def move_phase_sequential(g: Graph, z, cfg: LouvainConfig = None, observer=None, ub=None):
+    """move_phase (H/louvain.hpp:65-141) in the reference's one-worker order
+    (u = 0..n-1, each move applied before the next node): returns (z, changed).
+    Like the reference's ``Partition &z``, a contiguous int32 numpy ``z`` is
+    updated in place.  observer(u, source, target, gain) is the MoveObserver
+    (:60, :127-128): each call comes after ``z[u] = target``, so an observer
+    holding ``z`` sees the partition right after that move.  Only cfg.gamma
+    and cfg.max_move_iterations are read."""
+    cfg = cfg or LouvainConfig()
+    _check_cover(g, z)
+    if not (isinstance(z, np.ndarray) and z.dtype == np.int32 and z.flags.c_contiguous and z.flags.writeable):
+        z = np.array(z, np.int32, copy=True)
+    ub = int(ub) if ub is not None else max(int(z.max()) + 1 if len(z) else 1, 1)
+    dz = z.copy()  # the device's in/out copy; z itself follows the replayed moves
+    err = []
+
+    def trampoline(_user, u, c, d, gain):
+        if err:
+            return
+        try:
+            z[u] = d
+            observer(u, c, d, gain)
+        except BaseException as e:  # noqa: BLE001 -- re-raised after the call
+            err.append(e)
+
+    cb = _MoveObserver(trampoline) if observer is not None else _MoveObserver()
+    ch = C.c_int32()
+    c = cfg._c()
+    _check(load_library().cd_move_phase_sequential(g.ctx.h, g.h, dz.ctypes.data if len(dz) else None, ub,
+                                                   C.byref(c), cb, None, C.byref(ch)))
+    if err:
+        raise err[0]
+    z[:] = dz
     return z, bool(ch.value)
 
 

@@ -4,6 +4,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <new>
 
 #include "comm.cuh"
@@ -682,6 +683,25 @@ cd_status cd_move_phase(cd_ctx *ctx, const cd_graph *g, int32_t *z, const cd_lou
     })
 }
 
+cd_status cd_move_phase_sequential(cd_ctx *ctx, const cd_graph *g, int32_t *z, int64_t ub, const cd_louvain_config *cfg,
+                                   cd_move_observer observer, void *user, int32_t *changed) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && g && cfg && (g->n == 0 || z) && ub >= 1, CD_EINVAL, "invalid argument");
+        CD_REQUIRE(!g->rows_local || g->shard_size == 1, CD_EINVAL, "sub-kernel needs a whole graph, not a row shard");
+        OutArr<int32_t> dz(ctx, z, g->n);
+        if (dz.host && g->n)
+            CD_CUDA(cudaMemcpyAsync(dz.d, z, g->n * sizeof(int32_t), cudaMemcpyHostToDevice, ctx->stream));
+        const int64_t mx = max_label_dev(ctx, g->n, dz.d);
+        CD_REQUIRE(mx >= 0 && mx <= ub, CD_ERANGE, "community id outside [0, ub)");
+        const bool ch = move_phase_sequential_dev(ctx, const_cast<cd_graph *>(g), dz.d, ub, cfg->gamma,
+                                                  cfg->max_move_iterations, observer, user);
+        dz.finish();
+        ctx_sync(ctx);
+        if (changed)
+            *changed = ch ? 1 : 0;
+    })
+}
+
 // ---- detectors -------------------------------------------------------------------
 
 cd_status cd_plp_run(cd_ctx *ctx, const cd_graph *g, const cd_plp_config *cfg, const int32_t *initial,
@@ -748,6 +768,38 @@ cd_status cd_epp_run(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *c
         DevTimer t(ctx);
         t.start();
         const int64_t k = epp_run_dev(ctx, gg, *cfg, dz.d, Report{report});
+        const double ms = t.stop_ms();
+        if (report) {
+            report->total_ms = ms;
+            report_quality(ctx, gg, dz.d, std::max<int64_t>(k, 1), 1.0, report);
+            report->community_count = k;
+            report->kernel_launches = ctx->launches - launches0;
+        }
+        dz.finish();
+        ctx_sync(ctx);
+    })
+}
+
+cd_status cd_epp_run_bases(cd_ctx *ctx, const cd_graph *g, const cd_ensemble_config *cfg,
+                           const int32_t *const *bases, int32_t *z, cd_report *report) {
+    CD_GUARD(ctx, {
+        CD_REQUIRE(ctx && g && cfg && (g->n == 0 || z), CD_EINVAL, "invalid argument");
+        CD_REQUIRE(cfg->ensemble_size >= 1, CD_EINVAL, "ensemble size must be >= 1");  // H/ensemble.hpp:113-114
+        CD_REQUIRE(bases, CD_EINVAL, "empty ensemble");
+        cd_graph *gg = const_cast<cd_graph *>(g);
+        const int64_t launches0 = ctx->launches, b = cfg->ensemble_size;
+        report_begin(report, "epp", cfg->workers, cfg->seed);
+        std::vector<std::unique_ptr<InArr<int32_t>>> ins;
+        std::vector<const int32_t *> ptrs;
+        for (int64_t i = 0; i < b; ++i) {
+            CD_REQUIRE(g->n == 0 || bases[i], CD_EINVAL, "invalid argument");
+            ins.emplace_back(new InArr<int32_t>(ctx, bases[i], g->n));
+            ptrs.push_back(ins.back()->d);
+        }
+        OutArr<int32_t> dz(ctx, z, g->n);
+        DevTimer t(ctx);
+        t.start();
+        const int64_t k = epp_run_dev(ctx, gg, *cfg, dz.d, Report{report}, ptrs.data());
         const double ms = t.stop_ms();
         if (report) {
             report->total_ms = ms;

@@ -381,7 +381,8 @@ int64_t louvain_run_dev(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg_i
 // ---------------------------------------------------------------------------
 // EPP
 // ---------------------------------------------------------------------------
-int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep) {
+int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep,
+                    const int32_t *const *given_bases) {
     if (cfg.ensemble_size < 1)
         fail(CD_EINVAL, "ensemble size must be >= 1");  // H/ensemble.hpp:113-114
     if (g->total == 0.0)
@@ -394,9 +395,9 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     // ensemble parallelism: with a replicated graph, rank r computes bases
     // r, r+G, ... alone and the bases are allgathered; a row shard computes
     // every base cooperatively
-    const bool base_parallel = G > 1 && !g->rows_local;
+    const bool base_parallel = G > 1 && !g->rows_local && !given_bases;
     const int64_t slots = base_parallel ? (b + G - 1) / G * G : b;
-    DBuf<int32_t> bases(ctx, std::max<int64_t>(n * slots, 1));
+    DBuf<int32_t> bases(ctx, given_bases ? 1 : std::max<int64_t>(n * slots, 1));
     auto run_base_on = [&](cd_ctx *c, int64_t i, int32_t *zi) {
         if (cfg.base == CD_ALGO_PLP) {
             cd_plp_config pc = cfg.base_plp;
@@ -418,9 +419,11 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     // the small PLM levels -- each want the whole GPU); not under profiling
     // (per-launch timing wants the kernels serialised) nor for graphs that
     // drop their bins between phases (BIG_GRAPH_ENTRIES).
-    const bool concurrent = G == 1 && b > 1 && cfg.base == CD_ALGO_PLP && g->max_degree > 256 &&
+    const bool concurrent = !given_bases && G == 1 && b > 1 && cfg.base == CD_ALGO_PLP && g->max_degree > 256 &&
                             !ctx->profiling && g->D < BIG_GRAPH_ENTRIES && env_i64("CD_EPP_CONCURRENT", 1) != 0;
-    if (base_parallel) {
+    if (given_bases) {
+        // EnsembleConfig::base_override (H/ensemble.hpp:127-128): the caller's partitions
+    } else if (base_parallel) {
         for (int64_t j = 0; j < slots; j += G) {
             const int64_t i = j + rank;
             int32_t *zi = bases.p + i * n;
@@ -472,7 +475,7 @@ int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int
     t.start();
     std::vector<const int32_t *> hp(b);
     for (int64_t i = 0; i < b; ++i)
-        hp[i] = bases.p + i * n;
+        hp[i] = given_bases ? given_bases[i] : bases.p + i * n;
     DBuf<const int32_t *> dp(ctx, b);
     CD_CUDA(cudaMemcpyAsync(dp.p, hp.data(), b * sizeof(int32_t *), cudaMemcpyHostToDevice, ctx->stream));
     DBuf<int32_t> core(ctx, std::max<int64_t>(n, 1));

@@ -45,8 +45,15 @@ cd_louvain_config resolve_louvain_schedule(const cd_louvain_config &cfg, const c
 // from_singletons: z holds the node ids (the recursion's every level, H/louvain.hpp:242)
 bool move_phase_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, const cd_louvain_config &cfg, uint64_t salt,
                     int64_t *passes = nullptr, int64_t *moves = nullptr, bool from_singletons = false);
+// the reference's one-worker move phase (sequential.cu): u = 0..n-1 in place,
+// every applied move replayed to `observer` (may be null) after its pass
+bool move_phase_sequential_dev(cd_ctx *ctx, cd_graph *g, int32_t *z, int64_t ub, double gamma, int64_t max_passes,
+                               cd_move_observer observer, void *user);
 int64_t louvain_run_dev(cd_ctx *ctx, cd_graph *g, const cd_louvain_config &cfg, int32_t *z, Report rep);
-int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep);
+// given_bases: caller-supplied base partitions (ensemble_size device arrays of
+// n labels) instead of running the base detector (EnsembleConfig::base_override)
+int64_t epp_run_dev(cd_ctx *ctx, cd_graph *g, const cd_ensemble_config &cfg, int32_t *z, Report rep,
+                    const int32_t *const *given_bases = nullptr);
 
 bool is_compact_dev(cd_ctx *ctx, int64_t n, const int32_t *z, int64_t nc);
 

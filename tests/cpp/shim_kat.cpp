@@ -6,6 +6,8 @@
 
 #include <cmath>
 #include <cstdio>
+#include <random>
+#include <stdexcept>
 
 using namespace commdet;
 
@@ -154,6 +156,66 @@ int main() {
         std::remove(mp);
         std::remove(bad);
         std::remove(ep);
+    }
+
+    {
+        // sequential moves strictly increase modularity (T/test_louvain.cpp:85-98 with a MoveObserver)
+        std::mt19937_64 rng(404);
+        std::uniform_real_distribution<double> coin(0.0, 1.0);
+        int observed = 0;
+        for (int i = 0; i < 20; ++i) {
+            const count n = 8 + i % 12;
+            EdgeList edges;
+            for (node u = 0; u < n; ++u)
+                for (node v = u + 1; v < n; ++v)
+                    if (coin(rng) < 0.35)
+                        edges.push_back({u, v, 1.0});
+            if (edges.empty())
+                edges.push_back({0, 1, 1.0});
+            Graph rg = Graph::from_edges(n, edges);
+            Partition z = singleton_partition(rg);
+            double last = modularity(rg, z);
+            LouvainConfig cfg;
+            cfg.workers = 1;
+            move_phase(rg, z, cfg, [&](node u, commdet::index c, commdet::index d, double gain) {
+                const double now = modularity(rg, z);
+                CHECK(now > last);
+                CHECK(z[u] == d && c != d && gain > 0.0);
+                last = now;
+                ++observed;
+            });
+        }
+        CHECK(observed > 0);
+        // no moves on the optimum; an observer that throws propagates
+        Partition zt = triangles();
+        CHECK(!move_phase(two_triangles(), zt, LouvainConfig{}, [](node, commdet::index, commdet::index, double) {}));
+        Partition zs = singleton_partition(g);
+        CHECK_THROWS_AS(move_phase(g, zs, LouvainConfig{},
+                                   [](node, commdet::index, commdet::index, double) { throw std::runtime_error("x"); }),
+                        std::runtime_error);
+    }
+    {
+        // epp with singleton base stub equals plain plm (T/test_ensemble.cpp:101-113)
+        EnsembleConfig cfg;
+        cfg.ensemble_size = 1;
+        cfg.final_algo = Algo::plm;
+        cfg.workers = 1;
+        int calls = 0;
+        cfg.base_override = [&](const Graph &graph, std::uint64_t) {
+            ++calls;
+            return singleton_partition(graph);
+        };
+        auto [ze, re] = run_epp(g, cfg);
+        LouvainConfig lc;
+        lc.workers = 1;
+        auto [zp, rp] = run_plm(g, lc);
+        CHECK(calls == 1);
+        CHECK(ze == zp.compacted());
+        CHECK(std::abs(re.modularity - rp.modularity) < 1e-12);
+        // the hook's partitions must cover the graph
+        cfg.ensemble_size = 2;
+        cfg.base_override = [](const Graph &, std::uint64_t s) { return Partition::singletons(s == 1 ? 6 : 5); };
+        CHECK_THROWS_AS(run_epp(g, cfg), std::invalid_argument);
     }
 
     std::printf("%s: %d failure(s)\n", failures ? "FAIL" : "PASS", failures);
