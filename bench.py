@@ -622,6 +622,7 @@ def bench_b200(args, wl):
     h_out = torch.empty(max(n, 1), dtype=torch.int32).pin_memory().numpy()
     e2e_ms = 0.0
     e2e_steps = max(1, min(args.steps, 5))
+    e2e_step_ms = []
     for i in range(e2e_steps + 1):
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
@@ -635,9 +636,11 @@ def bench_b200(args, wl):
         e1.record(stream)
         e1.synchronize()
         if i > 0:  # first iteration is a warm-up
-            e2e_ms += e0.elapsed_time(e1)
+            e2e_step_ms.append(e0.elapsed_time(e1))
+            e2e_ms += e2e_step_ms[-1]
         del gh
     e2e_ms /= e2e_steps
+    print("e2e steps (ms):", " ".join(f"{t:.2f}" for t in e2e_step_ms), file=sys.stderr)
     h2d = h_off.nbytes + h_col.nbytes + (h_w.nbytes if h_w is not None else 0)
     if dist:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=f"cuda:{local}")
@@ -645,6 +648,7 @@ def bench_b200(args, wl):
         e2e_ms = float(t.item())
     e2e = {"value": units * m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(4 * n), "ms_per_step": e2e_ms,
+           "steps_ms": [round(t, 3) for t in e2e_step_ms],
            "path": "pinned host CSR -> cd_graph_from_csr" + ("_rows (own rows)" if mode == "rows" else "")
                    + " -> detector -> host labels"}
 
@@ -691,7 +695,8 @@ def bench_b200(args, wl):
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "steps_ms": [round(t, 3) for t in step_ms], "higher_is_better": True,
             "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "int32+f64",
             "data": "synthetic",
             "config": workload_config(args, wl, n, m, entries),

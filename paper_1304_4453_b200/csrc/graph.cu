@@ -485,6 +485,10 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
                            const int32_t *col_host, float *w_dev, const float *w_host, cd_graph *g) {
     if (!ctx->copy_stream)
         CD_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    // one copy stream: chunks alternating over two streams do not interleave (the copy
+    // engine drains one stream's chunks first, CD_UPLOAD_TRACE), so chunk 0 would land
+    // half-way through and the validation overlap would be lost
+    const cudaStream_t cs[2] = {ctx->copy_stream, ctx->copy_stream};
     const bool fin = g != nullptr && w_dev == nullptr && n > 0;
     DBuf<int64_t> flag(ctx, 1);
     flag.zero();
@@ -503,18 +507,18 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
     // library stream (stream-ordered pool allocations)
     cudaEvent_t ready = ctx_event(ctx);
     CD_CUDA(cudaEventRecord(ready, ctx->stream));
-    CD_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ready, 0));
+    CD_CUDA(cudaStreamWaitEvent(cs[0], ready, 0));
     const int64_t nchunks = (D + UPLOAD_CHUNK - 1) / UPLOAD_CHUNK;
     std::vector<cudaEvent_t> done(static_cast<size_t>(nchunks));
     for (int64_t c = 0; c < nchunks; ++c) {
         const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
         CD_CUDA(cudaMemcpyAsync(col_dev + ib, col_host + ib, (ie - ib) * sizeof(int32_t), cudaMemcpyDefault,
-                                ctx->copy_stream));
+                                cs[c & 1]));
         if (w_dev)  // (the weights may live anywhere: cudaMemcpyDefault)
             CD_CUDA(cudaMemcpyAsync(w_dev + ib, w_host + ib, (ie - ib) * sizeof(float), cudaMemcpyDefault,
-                                    ctx->copy_stream));
+                                    cs[c & 1]));
         done[c] = ctx_event(ctx);
-        CD_CUDA(cudaEventRecord(done[c], ctx->copy_stream));
+        CD_CUDA(cudaEventRecord(done[c], cs[c & 1]));
     }
     auto release = [&] {
         ctx->free_events.push_back(ready);
@@ -528,7 +532,7 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
         CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
         CD_CUDA(cudaStreamSynchronize(ctx->stream));
         if (h) {
-            CD_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+            CD_CUDA(cudaStreamSynchronize(cs[0]));
             release();
             fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
         }
@@ -560,7 +564,25 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
     CD_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
     if (fin)
         CD_CUDA(cudaMemcpyAsync(hi, acc_i.p, sizeof(hi), cudaMemcpyDeviceToHost, ctx->stream));
+    cudaEvent_t fin_ev = nullptr;
+    static const bool trace = std::getenv("CD_UPLOAD_TRACE") != nullptr;
+    if (trace) {
+        fin_ev = ctx_event(ctx);
+        CD_CUDA(cudaEventRecord(fin_ev, ctx->stream));
+    }
     CD_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (trace) {  // diagnostic: when each chunk landed and when the graph was ready, ms after `ready`
+        std::fprintf(stderr, "[cd upload] chunks landed (ms after the offsets check):");
+        for (cudaEvent_t e : done) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ready, e);
+            std::fprintf(stderr, " %.2f", ms);
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ready, fin_ev);
+        std::fprintf(stderr, "; ready %.2f\n", ms);
+        ctx->free_events.push_back(fin_ev);
+    }
     release();
     if (h)
         fail(CD_EINPUT, "malformed CSR (offsets, out-of-range or unsorted neighbours, or nonpositive weight)");
