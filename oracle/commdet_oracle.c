@@ -1178,7 +1178,7 @@ uint64_t cdo_djb2(const uint8_t *data, uint64_t len) {
 int64_t cdo_combine_hashed(int64_t b, int64_t n, const int32_t *const *solutions, int32_t *out) {
     if (b < 1)
         return CDO_EINVAL;
-    uint64_t *h = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
+    uint64_t *h = (uint64_t *)calloc((size_t)(n > 0 ? n : 1), sizeof(uint64_t));
     uint64_t *idx = (uint64_t *)malloc(sizeof(uint64_t) * (size_t)(n > 0 ? n : 1));
     for (int64_t v = 0; v < n; ++v) {
         uint64_t x = 5381;

@@ -8,8 +8,8 @@
  *
  * Two kinds of functions live here:
  *
- *  (1) Restatements of the reference algorithm (/root/reference/proj/include/
- *      commdet/*.hpp, abbreviated H/ below).  Each cites the file:line it
+ *  (1) Restatements of the reference algorithm (the headers under
+ *      /root/reference/proj/include/commdet, abbreviated H/ below).  Each cites the file:line it
  *      follows.  These are pinned against the reference itself (compiled into
  *      oracle/_ref/ by oracle/Makefile) and against the reference's own KATs
  *      (tests/golden/, tests/test_oracle_*.py).
