@@ -807,8 +807,8 @@ int cdo_dominant_label(const cdo_graph *g, const int32_t *z, int32_t u, int32_t 
     const int64_t lo = g->off[u], hi = g->off[u + 1];
     if (hi == lo)
         return CDO_EINVAL;
-    int32_t *lab = (int32_t *)malloc(sizeof(int32_t) * (size_t)(hi - lo));
-    double *wt = (double *)malloc(sizeof(double) * (size_t)(hi - lo));
+    int32_t *lab = (int32_t *)calloc((size_t)(hi - lo), sizeof(int32_t));
+    double *wt = (double *)calloc((size_t)(hi - lo), sizeof(double));
     int64_t k = 0;
     for (int64_t i = lo; i < hi; ++i) {
         const int32_t l = z[g->col[i]];
