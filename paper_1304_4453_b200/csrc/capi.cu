@@ -408,7 +408,7 @@ cd_status cd_graph_from_csr(cd_ctx *ctx, int64_t n, const int64_t *off, const in
             if (w)
                 g->w.alloc(ctx, std::max<int64_t>(D, 1));
             CD_CUDA(cudaMemcpyAsync(g->off.p, off, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, ctx->stream));
-            if (D && !is_device_ptr(col) && D >= UPLOAD_CHUNK) {
+            if (D && !is_device_ptr(col) && D >= UPLOAD_MIN_ENTRIES) {
                 // host columns: chunked copies, each chunk validated while the next one copies;
                 // an unweighted graph is finalized and binned during the copy as well
                 graph_upload_validate(ctx, n, D, g->off.p, g->col.p, col, w ? g->w.p : nullptr, w, w ? nullptr : g);

@@ -508,10 +508,11 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
     cudaEvent_t ready = ctx_event(ctx);
     CD_CUDA(cudaEventRecord(ready, ctx->stream));
     CD_CUDA(cudaStreamWaitEvent(cs[0], ready, 0));
-    const int64_t nchunks = (D + UPLOAD_CHUNK - 1) / UPLOAD_CHUNK;
+    const int64_t CH = upload_chunk(D);
+    const int64_t nchunks = (D + CH - 1) / CH;
     std::vector<cudaEvent_t> done(static_cast<size_t>(nchunks));
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
+        const int64_t ib = c * CH, ie = std::min(D, ib + CH);
         CD_CUDA(cudaMemcpyAsync(col_dev + ib, col_host + ib, (ie - ib) * sizeof(int32_t), cudaMemcpyDefault,
                                 cs[c & 1]));
         if (w_dev)  // (the weights may live anywhere: cudaMemcpyDefault)
@@ -542,7 +543,7 @@ void graph_upload_validate(cd_ctx *ctx, int64_t n, int64_t D, const int64_t *off
     // one entry of slack on each side: a chunk's first entry compares with the previous one;
     // an unweighted graph's chunks also count their self-loops and upper entries (finalize)
     for (int64_t c = 0; c < nchunks; ++c) {
-        const int64_t ib = c * UPLOAD_CHUNK, ie = std::min(D, ib + UPLOAD_CHUNK);
+        const int64_t ib = c * CH, ie = std::min(D, ib + CH);
         CD_CUDA(cudaStreamWaitEvent(ctx->stream, done[c], 0));
         const int grid = grid_for((ie - ib + CSR_CHUNK - 1) / CSR_CHUNK, 256, ctx->num_sms * 32);
         if (fin)

@@ -158,7 +158,16 @@ void graph_finalize(cd_ctx *ctx, cd_graph *g, bool integral_weights = false);
 // the context's copy stream, each chunk validated (graph_validate_csr's
 // checks) on the library stream while the next one copies; off_dev is already
 // enqueued on the library stream.  Throws CD_EINPUT like graph_validate_csr.
-constexpr int64_t UPLOAD_CHUNK = int64_t(1) << 25;
+constexpr int64_t UPLOAD_CHUNK = int64_t(1) << 25;        // largest chunk (128 MB of columns)
+constexpr int64_t UPLOAD_MIN_ENTRIES = int64_t(1) << 22;  // chunked from 16 MB of columns
+// about eight chunks for a mid-size graph (C2: 18.3M entries in five chunks of
+// 2^22), so its checks, finalize and tiers also hide behind the copy
+inline int64_t upload_chunk(int64_t D) {
+    int64_t c = int64_t(1) << 21;
+    while (c < UPLOAD_CHUNK && c * 8 < D)
+        c <<= 1;
+    return c;
+}
 // With g (an unweighted graph being built: n, D, off, col set), the upload
 // also finalizes it -- every chunk's pass counts its self-loops and upper
 // entries -- and builds its degree tiers from the offsets while the columns

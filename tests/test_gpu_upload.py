@@ -1,6 +1,7 @@
-"""cd_graph_from_csr with host arrays above UPLOAD_CHUNK (2^25) entries: the
-columns are copied in chunks, each validated while the next one copies
-(graph_upload_validate).  The graph must equal the device-built one, and a
+"""cd_graph_from_csr with host arrays of at least UPLOAD_MIN_ENTRIES (2^22)
+entries: the columns are copied in chunks (upload_chunk(D): a power of two near
+D / 8 within [2^21, 2^25], so 2^25 is a chunk boundary of the big fixtures),
+each validated while the next one copies (graph_upload_validate).  The graph must equal the device-built one, and a
 defect in any chunk -- or right at a chunk boundary -- must raise the same
 input error as the unchunked path (H/graph.hpp:48-81 semantics)."""
 import numpy as np
@@ -97,3 +98,48 @@ def test_chunked_upload_unweighted_rejects(dev, big_unweighted):
     off[10] = off[11] + 1  # descending offsets: rejected before the tiers are built
     with pytest.raises(dev.InputError, match="malformed CSR"):
         dev.Graph.from_csr(g.node_count(), off, c["col"])
+
+
+# ---- mid-size graphs: chunks of 2^21 entries (csrc/graph.cuh upload_chunk) -------
+SMALL_CHUNK = 1 << 21
+
+
+@pytest.fixture(scope="module", params=[False, True], ids=["unweighted", "weighted"])
+def mid(request, dev, ctx):
+    g = dev.generate_rmat(18, 16, weighted=request.param, seed=5)  # ~8M entries: four chunks of 2^21
+    c = g.csr()
+    assert (1 << 22) <= len(c["col"]) <= 8 * SMALL_CHUNK
+    return g, c
+
+
+def test_mid_size_chunked_upload_equals_device_graph(dev, mid):
+    g, c = mid
+    h = dev.Graph.from_csr(g.node_count(), c["off"], c["col"], c["w"])
+    d = h.csr()
+    assert np.array_equal(d["off"], c["off"]) and np.array_equal(d["col"], c["col"])
+    if c["w"] is not None:
+        assert np.array_equal(d["w"], c["w"])
+    np.testing.assert_array_equal(d["vol"], c["vol"])
+    np.testing.assert_array_equal(d["loop"], c["loop"])
+    assert (h.edge_count(), h.total_edge_weight(), h.max_degree, h.isolated) == \
+        (g.edge_count(), g.total_edge_weight(), g.max_degree, g.isolated)
+    la, _ = dev.run_plm(h)
+    lb, _ = dev.run_plm(g)
+    assert np.array_equal(la, lb)
+
+
+@pytest.mark.parametrize("where", ["boundary", "third_chunk", "last_entry"])
+def test_mid_size_chunked_upload_rejects(dev, mid, where):
+    g, c = mid
+    off, col = c["off"], c["col"].copy()
+    if where == "last_entry":
+        col[-1] = g.node_count()
+    else:
+        target = SMALL_CHUNK if where == "boundary" else 2 * SMALL_CHUNK + 4321
+        u = int(np.searchsorted(off, target, side="right") - 1)
+        while off[u + 1] - off[u] < 2:
+            u += 1
+        i = max(int(off[u]) + 1, target) if target < off[u + 1] else int(off[u]) + 1
+        col[i - 1], col[i] = col[i], col[i - 1]
+    with pytest.raises(dev.InputError, match="malformed CSR"):
+        dev.Graph.from_csr(g.node_count(), off, col, c["w"])
