@@ -109,14 +109,19 @@ cd_graph *graph_from_rows_dev(cd_ctx *ctx, int64_t n, const int64_t *off, int64_
                   static_cast<const int64_t *>(full.p), lo, hi, g->off.p);
         full.release();
         g->col.alloc(ctx, std::max<int64_t>(D, 1));
-        if (D)
-            CD_CUDA(cudaMemcpyAsync(g->col.p, col, D * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
-        if (w) {
+        if (w)
             g->w.alloc(ctx, std::max<int64_t>(D, 1));
+        if (D >= UPLOAD_MIN_ENTRIES && !is_device_ptr(col)) {
+            // host rows: chunked copies, each chunk checked while the next one copies
+            // (as cd_graph_from_csr; the shard's node state needs the finalize below)
+            graph_upload_validate(ctx, n, D, g->off.p, g->col.p, col, w ? g->w.p : nullptr, w);
+        } else {
             if (D)
+                CD_CUDA(cudaMemcpyAsync(g->col.p, col, D * sizeof(int32_t), cudaMemcpyDefault, ctx->stream));
+            if (w && D)
                 CD_CUDA(cudaMemcpyAsync(g->w.p, w, D * sizeof(float), cudaMemcpyDefault, ctx->stream));
+            graph_validate_csr(ctx, n, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, D);
         }
-        graph_validate_csr(ctx, n, g->off.p, g->col.p, g->weighted ? g->w.p : nullptr, D);
         graph_finalize(ctx, g);  // over the owned rows: each edge counted once, by its smaller endpoint's owner
         if (G > 1)
             shard_globalize(ctx, g, lo, hi);

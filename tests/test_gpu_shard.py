@@ -356,6 +356,47 @@ def test_row_shard_from_own_rows(dev, G, kind):
         assert np.array_equal(z, z1) and np.array_equal(p, p1)
 
 
+@pytest.mark.parametrize("weighted", [False, True])
+def test_row_shard_from_own_rows_chunked(dev, weighted):
+    """Row shards of at least 2^22 entries take the chunked upload (each
+    chunk checked while the next one copies): same shard as the cut one, same
+    labels as one device, and a defect inside a later chunk is an input error."""
+    G = 2
+    ctx0 = dev.Context(0)
+    g1 = dev.generate_rmat(19, 16, weighted=weighted, seed=4, ctx=ctx0)
+    full = g1.csr()
+    n, m, total = g1.node_count(), g1.edge_count(), g1.total_edge_weight()
+    p1, _ = detect(dev, "plp", g1)
+    ctx0.close()
+    bounds = dev.shard_bounds(full["off"], G)
+    assert all(int(full["off"][bounds[r + 1]] - full["off"][bounds[r]]) >= (1 << 22) for r in range(G))
+
+    def fn(ctx, r):
+        lo, hi = int(bounds[r]), int(bounds[r + 1])
+        e0, e1 = int(full["off"][lo]), int(full["off"][hi])
+        w = None if full["w"] is None else full["w"][e0:e1]
+        g = dev.Graph.from_csr_rows(n, full["off"], lo, hi, full["col"][e0:e1], w, ctx=ctx)
+        ref = dev.generate_rmat(19, 16, weighted=weighted, seed=4, ctx=ctx).shard(ctx)
+        a, b = g.csr(), ref.csr()
+        for key in ("off", "col", "vol", "loop"):
+            np.testing.assert_array_equal(a[key], b[key])
+        assert (g.edge_count(), g.total_edge_weight()) == (m, total)
+        return detect(dev, "plp", g)[0]
+
+    for p in run_ranks(dev, G, fn):
+        assert np.array_equal(p, p1)
+    # a neighbour out of range inside a later chunk (world size 1: the one rank's rows
+    # are the whole graph)
+    ctx = dev.Context(0)
+    try:
+        bad = full["col"].copy()
+        bad[2 * (1 << 21) + 99] = n
+        with pytest.raises(dev.InputError, match="malformed CSR"):
+            dev.Graph.from_csr_rows(n, full["off"], 0, n, bad, full["w"], ctx=ctx)
+    finally:
+        ctx.close()
+
+
 def test_row_shard_from_own_rows_checks_range(dev):
     """Every rank must pass exactly its cd_shard_bounds range (checked
     before any collective, so a wrong range fails on each rank alone)."""
