@@ -2564,6 +2564,52 @@ __device__ __forceinline__ int64_t seg_total(const int32_t *counts, int nseg) {
     return t;
 }
 
+// One mover's row walked by a warp, APPLY_UNROLL loads in flight per lane before
+// their updates: with one load per iteration every update waited for its own
+// load (ncu: 95 % long-scoreboard stalls, and C3 PLM's first apply -- 1M movers,
+// hubs among them -- took 3.3 ms of the phase's 14 ms).
+constexpr int APPLY_UNROLL = 8;
+template <class F>
+__device__ __forceinline__ void for_row_entries(const int32_t *tcol, int64_t s, int64_t t, int lane, F &&f) {
+    for (int64_t e0 = s + lane; e0 < t; e0 += 32 * APPLY_UNROLL) {
+        int32_t v[APPLY_UNROLL];
+#pragma unroll
+        for (int c = 0; c < APPLY_UNROLL; ++c)
+            v[c] = e0 + 32 * c < t ? __ldcs(tcol + e0 + 32 * c) : -1;
+#pragma unroll
+        for (int c = 0; c < APPLY_UNROLL; ++c)
+            if (v[c] >= 0)
+                f(v[c]);
+    }
+}
+
+// A warp's movers i = gw, gw + nw, ... of one segment: the next mover and its
+// row bounds load while the current row is walked (move -> offsets -> entries
+// were three dependent loads per mover; C3 PLM's first pass applies ~770 k
+// sparse movers per sub-sweep, ~160 in sequence per warp).  f(move, s, t).
+template <class F>
+__device__ __forceinline__ void for_movers(const int2 *m, int64_t cnt, int64_t gw, int64_t nw, const int64_t *toff,
+                                           F &&f) {
+    if (gw >= cnt)
+        return;
+    int2 cur = m[gw];
+    int64_t s = toff[cur.x], t = toff[cur.x + 1];
+    for (int64_t i = gw; i < cnt; i += nw) {
+        const int64_t in = i + nw;
+        int2 nxt = cur;
+        int64_t sn = 0, tn = 0;
+        if (in < cnt) {
+            nxt = m[in];
+            sn = toff[nxt.x];
+            tn = toff[nxt.x + 1];
+        }
+        f(cur, s, t);
+        cur = nxt;
+        s = sn;
+        t = tn;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t *counts, int nseg, int64_t stride,
                                                    int32_t *z, uint8_t *active, int2 *chg, const int64_t *toff,
                                                    const int32_t *tcol, long long *total, int64_t n,
@@ -2611,17 +2657,14 @@ __global__ void __launch_bounds__(256) k_apply_plp(const int2 *mv, const int32_t
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t cnt = counts[sg];
-        for (int64_t i = gw; i < cnt; i += nw) {
-            const int2 e2 = m[i];
+        for_movers(m, cnt, gw, nw, toff, [&](int2 e2, int64_t rs, int64_t rt) {
             if (lane == 0)
                 z[e2.x] = e2.y;
             if (chg)
-                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
-                    atomicAdd(&chg[tcol[e]].x, 1);
+                for_row_entries(tcol, rs, rt, lane, [&](int32_t v) { atomicAdd(&chg[v].x, 1); });
             else
-                for (int64_t e = toff[e2.x] + lane; e < toff[e2.x + 1]; e += 32)
-                    active[tcol[e]] = 1;
-        }
+                for_row_entries(tcol, rs, rt, lane, [&](int32_t v) { active[v] = 1; });
+        });
     }
 }
 
@@ -2645,11 +2688,9 @@ __device__ __forceinline__ void activate_moved(const int2 *mv, const int32_t *co
     for (int sg = 0; sg < nseg; ++sg) {
         const int2 *m = mv + sg * stride;
         const int64_t cnt = counts[sg];
-        for (int64_t i = gw; i < cnt; i += nw) {
-            const int32_t u = m[i].x;
-            for (int64_t e = toff[u] + lane; e < toff[u + 1]; e += 32)
-                active[tcol[e]] = 1;
-        }
+        for_movers(m, cnt, gw, nw, toff, [&](int2, int64_t rs, int64_t rt) {
+            for_row_entries(tcol, rs, rt, lane, [&](int32_t v) { active[v] = 1; });
+        });
     }
 }
 
@@ -3206,7 +3247,10 @@ static int64_t plm_dense_at(int64_t n) {
 void Sweeper::apply(const int2 *mv, const int32_t *counts, int nseg, int64_t stride) {
     cd_ctx *ctx = ctx_;
     cd_graph *g = g_;
-    const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, ctx->num_sms * 4));
+    // 8 blocks of 256 per SM (30 registers): every resident warp walks movers' rows
+    // (C3 PLM apply 10.4 -> 9.5 ms, C3 PLP apply 1.71 -> 1.42 ms against 4 per SM)
+    static const int64_t per_sm = std::max<int64_t>(1, env_i64("CD_APPLY_BLOCKS_PER_SM", 8));
+    const int64_t napply = std::max<int64_t>(1, std::min<int64_t>((g->n + 255) / 256, ctx->num_sms * per_sm));
     if (c_.mode == MODE_PLP)
         CD_LAUNCH(ctx, "plp_apply", k_apply_plp, static_cast<int>(napply), 256, 0, mv, counts, nseg, stride, c_.z,
                   c_.active, c_.chg, c_.toff ? c_.toff : static_cast<const int64_t *>(g->off.p),
