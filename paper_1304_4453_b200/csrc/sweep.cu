@@ -2482,26 +2482,65 @@ __device__ __forceinline__ void plm_identity_scan(const SweepParams &P, int32_t 
     }
 }
 
+// SCAN32: the short-row tiers (G8 .. WARP); the block tiers' rows (up to 8192 entries)
+// keep a candidate per warp iteration, which spreads the long rows over the warps
+template <bool SCAN32>
 __global__ void __launch_bounds__(256) k_plm_identity_warp(SweepParams P) {
     const int lane = lane_id();
     const int64_t gw = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
     const unsigned long long key = load_key(P);
-    const int32_t *list = P.tlist + P.tbeg[TIER_G8];
-    const int64_t count = P.tend[TIER_BLOCK3] - P.tbeg[TIER_G8];
+    const int32_t *list = P.tlist + (SCAN32 ? P.tbeg[TIER_G8] : P.tbeg[TIER_BLOCK]);
+    const int64_t count = SCAN32 ? P.tend[TIER_WARP] - P.tbeg[TIER_G8] : P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK];
     MoveQueue q;
-    for (int64_t i = gw; i < count; i += nw) {
-        const int32_t u = list[i];
-        if (!selected(P, key, u))
-            continue;
-        const int64_t s = P.off[u], e = P.off[u + 1];
-        const double vol_u = P.vol[u];
-        const double vol_c = __dsub_rn(P.vols[u], vol_u);
-        double cv = -INFINITY;
-        int32_t ck = INT32_MAX;
-        plm_identity_scan(P, u, s, e, vol_u, vol_c, 32, lane, cv, ck);
-        argmax_m<MODE_PLM, 32>(cv, ck);
-        decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
+    if (!SCAN32) {
+        for (int64_t i = gw; i < count; i += nw) {
+            const int32_t u = list[i];
+            if (!selected(P, key, u))
+                continue;
+            const int64_t s = P.off[u], e = P.off[u + 1];
+            const double vol_u = P.vol[u];
+            const double vol_c = __dsub_rn(P.vols[u], vol_u);
+            double cv = -INFINITY;
+            int32_t ck = INT32_MAX;
+            plm_identity_scan(P, u, s, e, vol_u, vol_c, 32, lane, cv, ck);
+            argmax_m<MODE_PLM, 32>(cv, ck);
+            decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
+        }
+        q.flush(P);
+        q.flush_gain(P);
+        return;
+    }
+    // 32 candidates per round, the bucket test once per lane (a candidate per warp
+    // iteration spent most iterations on the K - 1 other buckets' nodes); each
+    // selected node's row bounds and volumes are loaded by its lane before the
+    // warp evaluates the selected nodes one after the other
+    for (int64_t base = gw * 32; base < count; base += nw * 32) {
+        const int64_t i = base + lane;
+        const int32_t cand = i < count ? list[i] : 0;
+        const bool sel = i < count && selected(P, key, cand);
+        int64_t ls = 0, le = 0;
+        double lvol = 0.0, lvols = 0.0;
+        if (sel) {
+            ls = P.off[cand];
+            le = P.off[cand + 1];
+            lvol = P.vol[cand];
+            lvols = P.vols[cand];
+        }
+        uint32_t m = __ballot_sync(0xffffffffu, sel);
+        while (m) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int32_t u = __shfl_sync(0xffffffffu, cand, src);
+            const int64_t s = __shfl_sync(0xffffffffu, ls, src), e = __shfl_sync(0xffffffffu, le, src);
+            const double vol_u = __shfl_sync(0xffffffffu, lvol, src);
+            const double vol_c = __dsub_rn(__shfl_sync(0xffffffffu, lvols, src), vol_u);
+            double cv = -INFINITY;
+            int32_t ck = INT32_MAX;
+            plm_identity_scan(P, u, s, e, vol_u, vol_c, 32, lane, cv, ck);
+            argmax_m<MODE_PLM, 32>(cv, ck);
+            decide<MODE_PLM>(P, q, lane == 0, u, u, ck, cv);
+        }
     }
     q.flush(P);
     q.flush_gain(P);
@@ -3187,10 +3226,15 @@ void Sweeper::enqueue(bool capture, bool recording) {
                           0, P);
             } else {
                 // singletons: every neighbour is its own community
-                const int64_t nw = P.tend[TIER_BLOCK3] - P.tbeg[TIER_G8];
+                const int64_t nw = P.tend[TIER_WARP] - P.tbeg[TIER_G8];
+                const int64_t nw2 = P.tend[TIER_BLOCK3] - P.tbeg[TIER_BLOCK];
                 const int64_t nb = P.tend[TIER_HUB] - P.tbeg[TIER_CLUSTER];
                 if (nw > 0)
-                    CD_LAUNCH(ctx, "plm_first", k_plm_identity_warp, grid_for(nw, 8, ctx->num_sms * 16), 256, 0, P);
+                    CD_LAUNCH(ctx, "plm_first", k_plm_identity_warp<true>, grid_for((nw + 31) / 32, 8, ctx->num_sms * 16),
+                              256, 0, P);
+                if (nw2 > 0)
+                    CD_LAUNCH(ctx, "plm_first", k_plm_identity_warp<false>, grid_for(nw2, 8, ctx->num_sms * 16), 256, 0,
+                              P);
                 if (nb > 0)
                     CD_LAUNCH(ctx, "plm_first", k_plm_identity_block, grid_for(nb, 1, ctx->num_sms * 8), 256, 0, P);
             }
