@@ -1581,10 +1581,17 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         overflow = 0;
     }
     cluster.sync();
-    for (int64_t i = cid; i < count; i += ncl) {
-        const int32_t u = list[i];
-        if (!selected_in(P, bkey, u, pre))  // uniform across the cluster
-            continue;
+    // 32 of the cluster's candidates per round, the bucket / activity test once per
+    // lane: one candidate per iteration cost a dependent load chain (list, flags) for
+    // every node of the other K - 1 buckets.  Every warp of the cluster computes the
+    // same mask (a node's flags change only when the node itself is decided)
+    for (int64_t r0 = 0; cid + r0 * ncl < count; r0 += 32) {
+      const int64_t ci = cid + (r0 + lane) * ncl;
+      const int32_t cand = ci < count ? list[ci] : 0;
+      uint32_t selm = __ballot_sync(0xffffffffu, ci < count && selected_in(P, bkey, cand, pre));
+      while (selm) {
+        const int32_t u = __shfl_sync(0xffffffffu, cand, __ffs(selm) - 1);
+        selm &= selm - 1;
         const int64_t s = P.off[u], e = P.off[u + 1];
         const int32_t cur = P.z[u];
         double wc = 0.0;
@@ -1751,6 +1758,7 @@ __global__ void __cluster_dims__(CL, 1, 1) __launch_bounds__(CL_THREADS) k_sweep
         if (threadIdx.x == 0)
             ndist = 0;
         cluster.sync();  // nobody inserts before every table is clean
+      }
     }
     if (rank == 0 && wid == 0) {
         q.flush(P);
